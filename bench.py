@@ -1,0 +1,517 @@
+#!/usr/bin/env python
+"""Benchmark of the DynaSpec dynamic drafter head on B200 (BASELINE.json metric:
+"draft-head tokens/s & us/step (V=128k, d=4096); % HBM peak; speedup vs dense").
+
+A bench "step" is one draft cycle: `positions` consecutive DynaSpec draft steps (Alg. 1 lines
+7-11 for t = 0..gamma-1 with the position-aware budget 32,32,8,...) over one batch of B
+synthetic rows per GPU: router (S_m stream) -> select -> gathered head + fused epilogue (S_d).
+value = draft tokens (rows x positions, all ranks) per second of device time (max over ranks).
+
+Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--config llama3] [--batch B]
+       python bench.py --impl reference ...   (the CPU oracle, timed on the host cores)
+"""
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from synth import inputs as S  # noqa: E402
+
+L2_FLUSH_BYTES = 512 << 20  # 4x the 126 MB L2
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="llama3", choices=list(S.CONFIGS))
+    ap.add_argument("--batch", type=int, default=None)
+    ap.add_argument("--dtype", default="bf16", choices=["bf16", "f32"])
+    ap.add_argument("--partition", default="kmeans", choices=["kmeans", "random"])
+    ap.add_argument("--kmeans-iters", type=int, default=8)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--no-graph", action="store_true")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------------------- distributed
+
+def dist_setup(args):
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1:
+        import torch.distributed as dist
+        backend = "nccl" if torch.cuda.is_available() else "gloo"
+        if torch.cuda.is_available():
+            torch.cuda.set_device(local)
+        dist.init_process_group(backend)
+    elif torch.cuda.is_available():
+        torch.cuda.set_device(0)
+    return ws, rank, local
+
+
+def barrier(ws):
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(x, ws):
+    if ws == 1:
+        return x
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda" if torch.cuda.is_available() else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ----------------------------------------------------------------------------- clocks
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.idx = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 9:
+                continue
+            try:
+                sm.append(float(p[1]))
+                smax = float(p[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, p[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- helpers
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        j = json.load(open(p))
+        return j.get("hbm_gbs"), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def committed_traffic(config, batch):
+    """dram bytes per head launch from the committed ncu --set full summary (profiles/), or None."""
+    p = os.path.join(ROOT, "profiles", "head_traffic.json")
+    if not os.path.exists(p):
+        return None
+    j = json.load(open(p))
+    return j.get(f"{config}_B{batch}")
+
+
+class HostRows:
+    """fp64 row access to a host bf16 head for the oracle."""
+
+    def __init__(self, W):
+        self.W = W
+        self.shape = tuple(W.shape)
+
+    def __getitem__(self, idx):
+        return self.W[torch.as_tensor(np.asarray(idx), dtype=torch.long)].to(torch.float64).numpy()
+
+
+# ----------------------------------------------------------------------------- oracle (CPU) arm
+
+def oracle_cycles(C, B, dtype, seconds, W_host, rt_host, part):
+    """Run whole oracle draft cycles (all positions) on the host until `seconds` elapse."""
+    from oracle import dynaspec_oracle as O
+    W = HostRows(W_host)
+    ro = tuple(None if x is None else x.to(torch.float64).numpy() for x in rt_host)
+    rows, t0, cycles = 0, time.perf_counter(), 0
+    while True:
+        for t in range(C.positions):
+            hp, e, hn = S.step_inputs(B, C.d, t, dtype)
+            f = lambda x: x.to(torch.float64).numpy()
+            O.draft_step(part, ro, W, f(hp), f(e), f(hn), t, C.k_max, C.k_min, C.k_t, shared=C.shared)
+            rows += B
+        cycles += 1
+        el = time.perf_counter() - t0
+        if el >= seconds:
+            break
+    threads = os.cpu_count()
+    try:
+        from threadpoolctl import threadpool_info
+        threads = max(i.get("num_threads", 1) for i in threadpool_info()) or threads
+    except Exception:
+        pass
+    return rows / el, el, cycles, threads
+
+
+def run_reference(args, ws, rank):
+    """--impl reference: the CPU oracle as it stands, on this box's host cores.  Each step is a
+    bounded sample of the workload: one whole draft cycle (all positions) of B rows."""
+    if rank != 0:
+        return
+    from oracle import dynaspec_oracle as O
+    C = S.CONFIGS[args.config]
+    B = args.batch or C.B
+    unit = "draft tokens/s"
+    W_host = S.lm_head(C.V, C.d, 0, args.dtype)
+    rt_host = S.router(C.d, C.h_r, C.M, 1, args.dtype)
+    perm, off = O.layout(S.random_partition(C.V, C.M, 2), C.M)
+    part = {"perm": perm, "offsets": off}
+    total_rows, total_t, thr = 0.0, 0.0, 1
+    for i in range(args.warmup + args.steps):
+        r, el, cyc, thr = oracle_cycles(C, B, args.dtype, 0.0, W_host, rt_host, part)
+        if i >= args.warmup:
+            total_rows += r * el
+            total_t += el
+    value = total_rows / total_t
+    line = {"impl": "reference", "metric": "draft-head tokens/s & us/step (V=128k,d=4096); % HBM peak; speedup vs dense",
+            "value": value, "unit": unit, "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1000.0 * total_t / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded random-init weights and hidden states)",
+            "config": {"workload": C.name, "V": C.V, "d": C.d, "M": C.M, "batch_per_gpu": B,
+                       "positions": C.positions, "k_schedule": [budget_of(t, C) for t in range(C.positions)],
+                       "k_t": C.k_t},
+            "cpu_baseline": {"value": value, "unit": unit, "cores": thr, "kind": "oracle",
+                             "sample": f"{args.steps} whole draft cycles ({C.positions} positions x B={B}) of the "
+                                       "numpy fp64 oracle on the host"},
+            "e2e": {"value": value, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+def budget_of(t, C):
+    """k_c(t) with the k_min clamp (R1) — the schedule the bench drives (for reporting only)."""
+    return C.k_max if t < 2 else max(C.k_min, C.k_max // ((t + 1) * 2))
+
+
+# ----------------------------------------------------------------------------- GPU arm
+
+def run_ours(args, ws, rank, local):
+    from paper_2510_13847_b200 import dynaspec as D
+    dev = torch.device("cuda", torch.cuda.current_device())
+    C = S.CONFIGS[args.config]
+    B = args.batch or C.B
+    tdt = S.TORCH_DTYPES[args.dtype]
+    # ---- setup (untimed): weights, router, offline partition (S0)
+    W = S.lm_head(C.V, C.d, 0, args.dtype, device=dev)
+    rt = [None if x is None else x.to(dev) for x in S.router(C.d, C.h_r, C.M, 1, args.dtype)]
+    t0 = time.perf_counter()
+    if args.partition == "kmeans":
+        try:
+            clusters = D.Clusters.build(W, C.M, seed=2, max_iters=args.kmeans_iters)
+            part_info = {"partition": "spherical k-means (GPU, integer-exact)", "kmeans_iters": clusters.iters}
+        except D.DynaspecError as ex:
+            if ex.name != "DS_ERR_UNSUPPORTED":
+                raise
+            args.partition = "random"
+    if args.partition == "random":
+        tau = torch.as_tensor(S.random_partition(C.V, C.M, 2), dtype=torch.int32, device=dev)
+        clusters = D.Clusters.from_tau(W, tau, C.M)
+        part_info = {"partition": "seeded random (Zipf sizes)"}
+    torch.cuda.synchronize()
+    part_info["build_s"] = round(time.perf_counter() - t0, 3)
+    part_info["cluster_size_min_max"] = [clusters.min_size, clusters.max_size]
+    router = D.Router(*rt)
+    W_host = W.cpu() if (rank == 0 and ws == 1 and not args.no_cpu_baseline) else None
+    del W  # the drafter-side copy W_perm is what the head reads (R21)
+    torch.cuda.empty_cache()
+
+    # ---- input pool: 64 distinct (h_prev, e, h_new) per position so touched clusters vary
+    pool = 16
+    inputs = [[tuple(x.to(dev) for x in S.step_inputs(B, C.d, 64 * t + i, args.dtype, sibling_eps=0.1 if C.shared
+                                                      else None, base_seed=1000 + 977 * rank))
+               for t in range(C.positions)] for i in range(pool)]
+    steppers = [D.DraftStep(clusters, router, B, C.k_t, shared=C.shared, two_streams=True, device=dev)
+                for _ in range(C.positions)]
+    kb = [budget_of(t, C) for t in range(C.positions)]
+    flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
+    head_ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                for _ in range(C.positions)] for _ in range(pool)]
+    for lst in head_ev:
+        for a, b in lst:
+            a.record(); b.record()
+
+    def cycle(i, timed_heads=True):
+        for t in range(C.positions):
+            hp, e, hn = inputs[i][t]
+            steppers[t](hp, e, hn, t, C.k_max, C.k_min, head_events=head_ev[i][t] if timed_heads else None)
+
+    use_graph = not args.no_graph
+    graphs = []
+    if use_graph:
+        s = torch.cuda.Stream(device=dev)
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            for i in range(pool):   # warm the library (attributes, first launches) outside capture
+                cycle(i)
+        torch.cuda.current_stream().wait_stream(s)
+        torch.cuda.synchronize()
+        for i in range(pool):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                cycle(i)
+            graphs.append(g)
+        torch.cuda.synchronize()
+
+    def run(i):
+        if use_graph:
+            graphs[i % pool].replay()
+        else:
+            cycle(i % pool)
+
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    for i in range(args.warmup):
+        flush.zero_()
+        run(i)
+    torch.cuda.synchronize()
+    barrier(ws)
+    clk = ClockSampler(local)
+    clk.start()
+    torch.cuda.synchronize()
+    barrier(ws)
+    head_ms, head_bytes = [], []
+    for i in range(args.steps):
+        flush.zero_()                       # cold L2 between steps, outside the event pair
+        ev[i][0].record()
+        run(args.warmup + i)
+        ev[i][1].record()
+    torch.cuda.synchronize()
+    barrier(ws)
+    clocks = clk.stop()
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    # head-kernel durations (events around each head launch, recorded on S_d inside the graph)
+    for i in range(args.steps):
+        j = (args.warmup + i) % pool
+        for t in range(C.positions):
+            try:
+                head_ms.append(head_ev[j][t][0].elapsed_time(head_ev[j][t][1]))
+            except RuntimeError:
+                head_ms.append(float("nan"))
+    # algorithmic bytes per head launch: shortlist rows x d x b_w + h_new + perm ids + outputs
+    bw = 2 if args.dtype == "bf16" else 4
+    vs_sizes = []
+    # replay each pool entry once more (untimed) to read back its shortlist sizes
+    sizes_by_pool = {}
+    for j in sorted({(args.warmup + i) % pool for i in range(args.steps)}):
+        run(j)
+        torch.cuda.synchronize()
+        per_t = []
+        for t in range(C.positions):
+            st = steppers[t]
+            cnt = st.sel_count.cpu()
+            offs = st.sl_offsets.cpu()
+            per_t.append([int(offs[r, cnt[r]]) for r in range(cnt.numel())])
+        sizes_by_pool[j] = per_t
+    for i in range(args.steps):
+        j = (args.warmup + i) % pool
+        for t in range(C.positions):
+            n_rows = sizes_by_pool[j][t]
+            vs = sum(n_rows)
+            vs_sizes.append(vs / len(n_rows))
+            head_bytes.append(vs * C.d * bw + 4 * vs + B * C.d * bw + B * (C.k_t * 12 + 4))
+    total_ms = sum(step_ms)
+    tot_ms_max = max_over_ranks(total_ms, ws)
+    rows_all = B * C.positions * args.steps * ws
+    value = rows_all / (tot_ms_max / 1e3)
+    ms_per_step = tot_ms_max / args.steps
+    hb = np.array(head_bytes)
+    hm = np.array(head_ms)
+    good = np.isfinite(hm)
+    peak, peak_src = measured_peaks()
+    achieved = float(hb[good].sum() / (hm[good].sum() / 1e3) / 1e9) if good.any() else None
+    head_share = float(hm[good].sum() / total_ms) if good.any() else None
+
+    # ---- dense comparator (untimed above): full-V head + log-softmax + top-k_t
+    dense = dense_baseline(D, clusters, inputs, B, C, dev, flush)
+    dyn_us_per_pos = 1e3 * ms_per_step / C.positions
+    e2e = e2e_run(D, steppers, clusters, router, C, B, args, dev, flush, ws)
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        from oracle import dynaspec_oracle as O
+        perm_h, off_h = O.layout(clusters.tau.cpu().numpy().astype(np.int64), C.M)
+        rate, el, cyc, thr = oracle_cycles(C, B, args.dtype, args.cpu_seconds, W_host,
+                                           [None if x is None else x.cpu() for x in rt],
+                                           {"perm": perm_h, "offsets": off_h})
+        cpu = {"value": rate, "unit": "draft tokens/s", "cores": thr, "kind": "oracle",
+               "sample": f"{cyc} whole draft cycle(s) ({C.positions} positions x B={B}, {el:.1f} s) of the numpy "
+                         "fp64 oracle on the same partition/router/W"}
+    launches = sum(s.launches for s in steppers) * args.steps
+    if rank == 0:
+        line = {
+            "metric": "draft-head tokens/s & us/step (V=128k,d=4096); % HBM peak; speedup vs dense",
+            "value": value, "unit": "draft tokens/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": args.dtype, "data": "synthetic (seeded random-init weights, router and hidden states)",
+            "config": {"workload": C.name, "V": C.V, "d": C.d, "M": C.M, "h_r": C.h_r, "batch_per_gpu": B,
+                       "positions": C.positions, "k_schedule": kb, "k_t": C.k_t, "shared": C.shared,
+                       "parallelism": f"request-sharded x{ws} (no data-path collective)",
+                       "us_per_draft_step": dyn_us_per_pos,
+                       "mean_shortlist_rows": float(np.mean(vs_sizes)),
+                       "l2": "flushed (512 MB write) before every step, outside the timed event pair",
+                       "cuda_graph": use_graph, **part_info,
+                       "dense_us_per_draft_step": dense["best_us"], "dense_detail": dense,
+                       "speedup_vs_dense": dense["best_us"] / dyn_us_per_pos if dyn_us_per_pos else None,
+                       "head_share_of_step": head_share},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak if achieved else None,
+                         "traffic": committed_traffic(C.name, B), "kernel": "ds::head_kernel (S5+S6)",
+                         "peak_source": peak_src, "frac_of_8TBps": achieved / 8000.0 if achieved else None},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": clocks,
+        }
+        print(json.dumps(line))
+
+
+def dense_baseline(D, clusters, inputs, B, C, dev, flush, reps=20):
+    """Dense full-vocabulary head with the same epilogue: (a) our kernel with k = M (all clusters),
+    (b) torch/cuBLAS matmul + logsumexp + topk.  Cold L2 before each rep."""
+    M = clusters.M
+    sel = torch.arange(M, dtype=torch.int32, device=dev).repeat(B, 1).contiguous()
+    cnt = torch.full((B,), M, dtype=torch.int32, device=dev)
+    off = clusters.offsets.repeat(B, 1).contiguous()
+    ws = D.Workspace(D.lib().dynaspec_head_forward_ws(clusters.struct(), B, C.k_t), dev)
+    hn = inputs[0][2][2]
+    res = {}
+    times = []
+    for i in range(reps + 3):
+        flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        D.head_forward(clusters, hn, sel, cnt, off, C.k_t, ws=ws)
+        b.record()
+        torch.cuda.synchronize()
+        if i >= 3:
+            times.append(a.elapsed_time(b))
+    res["ours_k_eq_M_us"] = 1e3 * statistics.median(times)
+    Wp = clusters.W_perm
+    times = []
+    for i in range(reps + 3):
+        flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        z = torch.matmul(hn, Wp.t()).float()
+        lse = torch.logsumexp(z, dim=-1)
+        v, idx = torch.topk(z, C.k_t, dim=-1)
+        b.record()
+        torch.cuda.synchronize()
+        if i >= 3:
+            times.append(a.elapsed_time(b))
+    res["torch_cublas_us"] = 1e3 * statistics.median(times)
+    res["best_us"] = min(res["ours_k_eq_M_us"], res["torch_cublas_us"])
+    return res
+
+
+def e2e_run(D, steppers, clusters, router, C, B, args, dev, flush, ws, reps=None):
+    """End to end through the public API: every step copies its inputs from pinned host memory
+    (H2D), runs the draft cycle, and reads the step's results (top ids + log-probs) back (D2H)."""
+    reps = reps or args.steps
+    bw = 2 if args.dtype == "bf16" else 4
+    host_in = [[tuple(x.pin_memory() for x in S.step_inputs(B, C.d, 64 * t + 5000 + i, args.dtype))
+                for t in range(C.positions)] for i in range(2)]
+    dev_in = [tuple(torch.empty((B, C.d), dtype=S.TORCH_DTYPES[args.dtype], device=dev) for _ in range(3))
+              for _ in range(C.positions)]
+    out_ids = torch.empty((C.positions, B, C.k_t), dtype=torch.int32).pin_memory()
+    out_lp = torch.empty((C.positions, B, C.k_t), dtype=torch.float32).pin_memory()
+
+    def step(i):
+        src = host_in[i % 2]
+        for t in range(C.positions):
+            for dst, s in zip(dev_in[t], src[t]):
+                dst.copy_(s, non_blocking=True)
+        for t in range(C.positions):
+            steppers[t](*dev_in[t], t, C.k_max, C.k_min)
+            out_ids[t].copy_(steppers[t].top_ids, non_blocking=True)
+            out_lp[t].copy_(steppers[t].top_logp, non_blocking=True)
+
+    g = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream(device=dev)
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        step(0)
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    with torch.cuda.graph(g):
+        step(0)
+    for _ in range(3):
+        g.replay()
+    torch.cuda.synchronize()
+    tot = 0.0
+    for i in range(reps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        g.replay()
+        torch.cuda.synchronize()   # the host has the step's results
+        tot += time.perf_counter() - t0
+    tot = max_over_ranks(tot, ws)
+    h2d = C.positions * 3 * B * C.d * bw
+    d2h = C.positions * B * C.k_t * 8
+    return {"value": B * C.positions * reps * ws / tot, "unit": "draft tokens/s", "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h, "timing": "host wall clock around graph replay + synchronize",
+            "ms_per_step": 1e3 * tot / reps}
+
+
+def main():
+    args = parse()
+    ws, rank, local = dist_setup(args)
+    if args.impl == "reference":
+        run_reference(args, ws, rank)
+    else:
+        run_ours(args, ws, rank, local)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,244 @@
+/*
+ * dynaspec.h — C ABI of the B200-native DynaSpec dynamic drafter LM head.
+ *
+ * Paper: "DynaSpec: Context-aware Dynamic Speculative Sampling for Large-Vocabulary
+ * Language Models", arXiv 2510.13847.  Citations are PAPER.md line numbers (P:n) with
+ * the section / equation / Algorithm-1 line they fall in; R<n> are the readings of
+ * ambiguous passages listed in DESIGN.md §2.
+ *
+ * One draft step of Algorithm 1 for one position t is
+ *   k   = k_c(t)                                   (line 7)   dynaspec_budget
+ *   s   = r_theta([h_prev || e])                   (line 8)       dynaspec_meta_score
+ *   K   = TopK_k(s);  I = indices(U_{m in K} C_m)  (line 8)   dynaspec_select
+ *   z   = FUSED_INDEX_GEMM(h_new, W_LM, I)         (line 10)      dynaspec_head_forward
+ *   p   = log_softmax(z); T, TopP = TopK_{k_t}(p); T~ = remap2realid(T)
+ *                                                  (line 11)  (fused into head_forward)
+ * and dynaspec_draft_step runs the whole step on two streams (S_m and S_d).
+ * The clusters C_m come from dynaspec_build_clusters (offline spherical k-means).
+ *
+ * ------------------------------------------------------------------------------------
+ * Conventions (all calls)
+ *  - Tensor pointers are DEVICE pointers unless the name ends in _host.  They are owned by
+ *    the caller, row-major and contiguous, and must stay alive until the enqueued work has
+ *    completed on the given stream(s).  16-byte alignment is required for weights and
+ *    hidden states.
+ *  - Every call validates its arguments synchronously (on the host, before any launch)
+ *    and returns a ds_status; on any error nothing is enqueued and no output is written.
+ *    Calls only ENQUEUE work and return (except dynaspec_build_clusters, which
+ *    synchronises its stream once per k-means iteration and documents it).
+ *  - No call allocates device memory.  Scratch comes from a caller-provided workspace
+ *    whose size is queried with the matching *_ws() function and which must be
+ *    zero-filled once by dynaspec_ws_init() before its first use (the library leaves the
+ *    counters it uses back at zero after each call).  One workspace must not be used by
+ *    two calls that may run concurrently.
+ *  - Precision: weights and activations are bf16 (DS_BF16) or fp32 (DS_F32), one dtype per
+ *    call; every dot product accumulates in fp32; all floating outputs are fp32.
+ *  - Determinism: no floating-point atomics; every reduction has a fixed order, so two
+ *    runs with the same inputs and launch configuration produce identical bytes.
+ *  - Total orders (R7, R23): clusters by (score desc, cluster id asc); tokens by
+ *    (logit desc, vocabulary id asc); -0.0 and +0.0 compare equal.  NaN/Inf inputs are a
+ *    precondition violation (not checked on the hot path).
+ *  - CUDA errors raised while launching are returned as DS_ERR_CUDA.
+ * ------------------------------------------------------------------------------------
+ */
+#ifndef DYNASPEC_H
+#define DYNASPEC_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* ds_stream_t; /* == cudaStream_t (NULL = legacy default stream) */
+typedef struct CUevent_st* ds_event_t;   /* == cudaEvent_t */
+
+typedef enum {
+  DS_OK = 0,
+  DS_ERR_SHAPE = 1,                 /* inconsistent d / M / V / B / h_r, or a required pointer is NULL */
+  DS_ERR_DTYPE = 2,                 /* dtype not DS_BF16 / DS_F32, or mixed dtypes */
+  DS_ERR_INVALID_BUDGET = 3,        /* k < 1, k > M, k_min > k_max, k_t < 1 or k_t > 64 (SPEC InvalidBudget) */
+  DS_ERR_INVALID_CLUSTER_COUNT = 4, /* M < 1, M > V or M > 1024 (SPEC InvalidClusterCount) */
+  DS_ERR_INVALID_CLUSTER_ID = 5,    /* a cluster id outside [0, M) (SPEC InvalidClusterId) */
+  DS_ERR_INVALID_TOKEN = 6,         /* a token id outside [0, V) (SPEC InvalidToken) */
+  DS_ERR_DEGENERATE_COLUMN = 7,     /* a zero-norm token vector in build_clusters (SPEC DegenerateColumn) */
+  DS_ERR_EMPTY_SHORTLIST = 8,       /* a cluster would be empty (SPEC EmptyShortlist) */
+  DS_ERR_WORKSPACE = 9,             /* workspace NULL or smaller than the *_ws() size */
+  DS_ERR_CUDA = 10,                 /* a CUDA runtime error while launching */
+  DS_ERR_UNSUPPORTED = 11           /* shape outside what the kernels support (e.g. d % 8 != 0) */
+} ds_status;
+
+typedef enum { DS_BF16 = 0, DS_F32 = 1 } ds_dtype;
+
+/* Vocabulary partition Pi = {C_1..C_M}, tau: V -> [M], in the cluster-permuted
+ * layout: cluster m occupies rows [offsets[m], offsets[m+1]) of W_perm, tokens ascending
+ * inside a cluster; perm[i] is the vocabulary id of row i of W_perm (remap2realid).
+ * Filled by dynaspec_build_clusters or dynaspec_layout. */
+typedef struct {
+  int64_t V;               /* vocabulary size |V| */
+  int32_t d;               /* hidden size */
+  int32_t M;               /* number of clusters, 1 <= M <= min(V, 1024) */
+  int32_t dtype;           /* ds_dtype of W_perm */
+  int32_t min_size;        /* HOST: smallest |C_m| (>= 1) */
+  int32_t max_size;        /* HOST: largest |C_m| */
+  const int32_t* tau;      /* device [V]   cluster of each token (may be NULL on the hot path) */
+  const int32_t* perm;     /* device [V]   W_perm row -> vocabulary id */
+  const int32_t* offsets;  /* device [M+1] exclusive scan of cluster sizes */
+  const void* W_perm;      /* device [V][d] LM-head rows (W_LM columns) in cluster order */
+} ds_clusters;
+
+/* Router r_theta: R^{2d} -> R^M, input x = [h_prev || e] (R4).
+ * h_r > 0: s = W2 * ReLU(W1 x + b1) + b2, W1 [h_r][2d], b1 [h_r], W2 [M][h_r], b2 [M]  (R5).
+ * h_r == 0: linear router s = W1 x + b1 with W1 [M][2d], b1 [M]; W2, b2 unused.
+ * Biases are fp32; W1/W2 have the router dtype.  Scores are pre-sigmoid logits (R6). */
+typedef struct {
+  int32_t d;
+  int32_t h_r;
+  int32_t M;
+  int32_t dtype;
+  const void* W1;
+  const float* b1;
+  const void* W2;
+  const float* b2;
+} ds_router;
+
+/* Outputs of one draft step (all device pointers).  B_sel = 1 in shared mode, else B. */
+typedef struct {
+  float* scores;       /* [B][M]       router scores s (may be NULL: then the workspace holds them) */
+  int32_t* sel;        /* [B_sel][M]   selected cluster ids, ascending, first sel_count[r] valid */
+  int32_t* sel_count;  /* [B_sel]      |K| */
+  int32_t* sl_offsets; /* [B_sel][M+1] exclusive scan of |C_m| over sel; |V_S| = sl_offsets[r][sel_count[r]] */
+  int32_t* top_ids;    /* [B][k_t]     vocabulary ids of TopK_{k_t}, (logit desc, id asc); -1 padding */
+  float* top_logits;   /* [B][k_t]     z at those ids; -inf padding */
+  float* top_logp;     /* [B][k_t]     log_softmax(z) at those ids = z - lse; -inf padding */
+  float* lse;          /* [B]          log sum_{v in V_S} exp(z_v) */
+  float* z_out;        /* nullable [B][z_stride]: z over V_S in shortlist order (tau(v), v) (R8) */
+  int64_t z_stride;    /* >= dynaspec_max_shortlist(c, k) when z_out != NULL */
+} ds_step_outputs;
+
+/* ---------------------------------------------------------------- helpers (host only) */
+
+const char* dynaspec_status_string(ds_status s);
+
+/* k_c(t) = k_max for t in {0,1}, floor(k_max / ((t+1)*2)) for t >= 2 (Alg. 1
+ * line 7, with i read as the step index, R2), clamped below by k_min (R1).
+ * Returns -1 if t < 0, k_min < 1 or k_max < k_min. */
+int32_t dynaspec_budget(int32_t t, int32_t k_max, int32_t k_min);
+
+/* Upper bound on |V_S| for k selected clusters of one row: min(V, k * max_size). */
+int64_t dynaspec_max_shortlist(const ds_clusters* c, int32_t k);
+
+/* Zero-fill a workspace (once, before its first use). */
+ds_status dynaspec_ws_init(void* ws, size_t ws_bytes, ds_stream_t stream);
+
+/* ---------------------------------------------------------------- S0: offline partition */
+
+/* Workspace bytes for dynaspec_build_clusters. */
+size_t dynaspec_build_clusters_ws(int64_t V, int32_t d, int32_t M);
+
+/* Spherical k-means on column-normalised W_LM columns, no balance constraint,
+ * in the integer-exact reading R12: u_v = rint(2^14 w_v/||w_v||) with the
+ * norm a sequential fp64 sum; Forgy init from splitmix64(seed) (or init_ids_host);
+ * assignment argmax_m <u_v, c_m> in exact integers (ties -> lower m); centroids
+ * rint(2^14 S_m/||S_m||); empty clusters reseeded in ascending m with the lowest-similarity
+ * token of a cluster of size > 1; stop when tau repeats or after max_iters assignment
+ * passes; clusters relabelled by their smallest token id; then the layout of ds_clusters.
+ *   W        device [V][d] (dtype)                  input LM-head rows (W_LM columns)
+ *   init_ids_host  NULL or host [M] distinct token ids (replaces the Forgy draw)
+ *   tau      device [V] out;  perm device [V] out;  offsets device [M+1] out
+ *   W_perm   device [V][d] out (dtype), W_perm[i] = W[perm[i]]  (a drafter-side copy, R21)
+ *   iters_run_host   host out: assignment passes run;  sizes_host: host [2] out (min, max |C_m|), nullable
+ * SYNCHRONISES `stream` once per iteration (one 4-byte D->H copy).  Errors:
+ * DS_ERR_INVALID_CLUSTER_COUNT, DS_ERR_DEGENERATE_COLUMN, DS_ERR_SHAPE, DS_ERR_WORKSPACE. */
+ds_status dynaspec_build_clusters(const void* W, int32_t dtype, int64_t V, int32_t d, int32_t M,
+                                  uint64_t seed, int32_t max_iters, const int32_t* init_ids_host,
+                                  int32_t* tau, int32_t* perm, int32_t* offsets, void* W_perm,
+                                  int32_t* iters_run_host, int32_t* sizes_host,
+                                  void* ws, size_t ws_bytes, ds_stream_t stream);
+
+/* Layout from a given partition tau (device [V], values in [0,M), every cluster non-empty):
+ * perm = stable sort of token ids by tau, offsets = exclusive scan of sizes, W_perm[i] =
+ * W[perm[i]] (R12 step 9).  SYNCHRONISES `stream` once (to validate and to return sizes).
+ * Errors: DS_ERR_INVALID_CLUSTER_ID (tau out of range), DS_ERR_EMPTY_SHORTLIST (empty cluster). */
+size_t dynaspec_layout_ws(int64_t V, int32_t M);
+ds_status dynaspec_layout(const int32_t* tau, const void* W, int32_t dtype, int64_t V, int32_t d, int32_t M,
+                          int32_t* perm, int32_t* offsets, void* W_perm, int32_t* sizes_host,
+                          void* ws, size_t ws_bytes, ds_stream_t stream);
+
+/* ---------------------------------------------------------------- S1: meta-classifier */
+
+/* Workspace bytes for dynaspec_meta_score with B rows. */
+size_t dynaspec_meta_score_ws(const ds_router* r, int32_t B);
+
+/* s = r_theta([h_prev || e]) for B independent rows (Alg. 1 line 3 / line 8).
+ *   h_prev  device [B][d]  drafter hidden of the previous position (h_{c[-1]} at j = 0, R11)
+ *   e       device [B][d]  embedding E(x_t) of the current input token (R10)
+ *   scores  device [B][M]  out, fp32 */
+ds_status dynaspec_meta_score(const ds_router* r, const void* h_prev, const void* e, int32_t B,
+                              float* scores, void* ws, size_t ws_bytes, ds_stream_t stream);
+
+/* ---------------------------------------------------------------- S3/S4: selection */
+
+/* K_r = TopK_k(s_r) under (score desc, id asc), emitted in ascending id (R7, R8),
+ * and sl_offsets_r = exclusive scan of |C_m| over K_r (|V_S| = sum |C_m|).
+ * shared = 0: one selection per row (independent requests).  shared = 1: ONE output row, the
+ * ascending union over the B rows of their TopK sets (tree depth, one I for all rows, R9).
+ * k_per_row: nullable device [B] per-row budgets (each in [1, M]); else every row uses k.
+ *   scores device [B][M]; sel device [B_sel][M] out; sel_count device [B_sel] out;
+ *   sl_offsets device [B_sel][M+1] out.  Errors: DS_ERR_INVALID_BUDGET. */
+ds_status dynaspec_select(const float* scores, int32_t B, const ds_clusters* c, int32_t k,
+                          const int32_t* k_per_row, int32_t shared, int32_t* sel, int32_t* sel_count,
+                          int32_t* sl_offsets, ds_stream_t stream);
+
+/* ---------------------------------------------------------------- S5/S6: head + epilogue */
+
+/* Workspace bytes for dynaspec_head_forward with B rows and token budget k_t. */
+size_t dynaspec_head_forward_ws(const ds_clusters* c, int32_t B, int32_t k_t);
+
+/* z_r[j] = <h_new_r, W_LM[:, V_S,r[j]]> over the shortlist only (Alg. 1 line 10),
+ * fp32 accumulation, then log_softmax over V_S (R14), TopK_{k_t} by (z desc, id asc) and
+ * remap2realid through perm (line 11) — one fused pass.
+ *   h_new        device [B][d]          head input (as-is, no norm/bias/temperature, R22)
+ *   sel, sel_count, sl_offsets          as produced by dynaspec_select (shared: one row)
+ *   max_shortlist  upper bound on every row's |V_S| (0 => V); sizes the on-chip buffers
+ *   outputs      as in ds_step_outputs (top_*: [B][k_t]; lse: [B]; z_out nullable)
+ * Rows whose |V_S| < k_t get -1 / -inf padding.  A row whose |V_S| exceeds max_shortlist
+ * is not computed: its top_ids are -1 and lse is NaN.  Errors: DS_ERR_INVALID_BUDGET
+ * (k_t < 1 or > 64), DS_ERR_SHAPE, DS_ERR_WORKSPACE, DS_ERR_UNSUPPORTED (d % 8 != 0). */
+ds_status dynaspec_head_forward(const ds_clusters* c, const void* h_new, int32_t B, const int32_t* sel,
+                                const int32_t* sel_count, const int32_t* sl_offsets, int32_t shared,
+                                int32_t k_t, int64_t max_shortlist, int32_t* top_ids, float* top_logits,
+                                float* top_logp, float* lse, float* z_out, int64_t z_stride,
+                                void* ws, size_t ws_bytes, ds_stream_t stream);
+
+/* ---------------------------------------------------------------- S7: one draft step */
+
+/* Workspace bytes for dynaspec_draft_step. */
+size_t dynaspec_draft_step_ws(const ds_clusters* c, const ds_router* r, int32_t B, int32_t k_t);
+
+/* One DynaSpec draft position t (Alg. 1 lines 7-11):
+ *   host:   k = dynaspec_budget(t, k_max, k_min)                     (line 7)
+ *   s_meta: meta_score(h_prev, e) -> select(k)                       (line 8, stream S_m)
+ *   s_draft: [caller's drafter core already enqueued]                (line 9, stream S_d)
+ *            wait(meta) -> head_forward(h_new)                       (lines 10-11, after "sync S_m,S_d")
+ * ev_fork / ev_join: caller-owned events used to fork s_meta off s_draft and join it back
+ * (both required when s_meta != s_draft; ignored otherwise).  head_begin / head_end:
+ * nullable events recorded on s_draft around the head kernel (for measurement).
+ * On return all work is enqueued; the outputs are complete when s_draft reaches this point.
+ * Errors: as the individual calls, plus DS_ERR_INVALID_BUDGET if k_t > k * min_size. */
+ds_status dynaspec_draft_step(const ds_clusters* c, const ds_router* r, const void* h_prev, const void* e,
+                              const void* h_new, int32_t B, int32_t t, int32_t k_max, int32_t k_min,
+                              int32_t k_t, int32_t shared, const ds_step_outputs* out,
+                              void* ws, size_t ws_bytes, ds_stream_t s_draft, ds_stream_t s_meta,
+                              ds_event_t ev_fork, ds_event_t ev_join, ds_event_t head_begin,
+                              ds_event_t head_end);
+
+/* Number of kernel launches one dynaspec_draft_step enqueues (for launch accounting). */
+int32_t dynaspec_draft_step_launches(const ds_clusters* c, const ds_router* r, int32_t B, int32_t k_t,
+                                     int32_t shared);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DYNASPEC_H */

@@ -1,0 +1,274 @@
+// api.cu — the C ABI (include/dynaspec.h): synchronous validation, workspace carving, launches.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <mutex>
+
+#include "../../include/dynaspec.h"
+#include "internal.h"
+
+namespace ds {
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+int num_sms() {
+  static int cache[64] = {0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
+  if (cache[dev] == 0) {
+    int n = 0;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    cache[dev] = n > 0 ? n : 148;
+  }
+  return cache[dev];
+}
+
+static bool dtype_ok(int dt) { return dt == DS_BF16 || dt == DS_F32; }
+
+static ds_status check_clusters(const ds_clusters* c) {
+  if (!c || !c->perm || !c->offsets || !c->W_perm) return DS_ERR_SHAPE;
+  if (!dtype_ok(c->dtype)) return DS_ERR_DTYPE;
+  if (c->V < 1 || c->V > INT32_MAX || c->d < 1) return DS_ERR_SHAPE;
+  if (c->M < 1 || c->M > c->V || c->M > kMaxMHost) return DS_ERR_INVALID_CLUSTER_COUNT;
+  if (c->d % 8 != 0) return DS_ERR_UNSUPPORTED;
+  if (c->min_size < 1 || c->max_size < c->min_size) return DS_ERR_SHAPE;
+  return DS_OK;
+}
+
+static ds_status check_router(const ds_router* r) {
+  if (!r || !r->W1 || !r->b1) return DS_ERR_SHAPE;
+  if (!dtype_ok(r->dtype)) return DS_ERR_DTYPE;
+  if (r->d < 1 || r->d % 8 != 0) return r->d < 1 ? DS_ERR_SHAPE : DS_ERR_UNSUPPORTED;
+  if (r->M < 1 || r->M > kMaxMHost) return DS_ERR_INVALID_CLUSTER_COUNT;
+  if (r->h_r < 0 || r->h_r > kMaxMHost) return DS_ERR_SHAPE;
+  if (r->h_r > 0 && (!r->W2 || !r->b2)) return DS_ERR_SHAPE;
+  return DS_OK;
+}
+
+// Workspace carving: [counters 256 B][meta partials][head partials]
+struct WsLayout {
+  size_t counters, meta, head, total;
+};
+static WsLayout ws_layout(size_t meta_bytes, size_t head_bytes) {
+  WsLayout L;
+  L.counters = 0;
+  L.meta = 256;
+  L.head = align_up(L.meta + meta_bytes, 256);
+  L.total = align_up(L.head + head_bytes, 256);
+  return L;
+}
+
+}  // namespace ds
+
+using namespace ds;
+
+extern "C" {
+
+const char* dynaspec_status_string(ds_status s) {
+  switch (s) {
+    case DS_OK: return "ok";
+    case DS_ERR_SHAPE: return "shape error: inconsistent sizes or NULL required pointer";
+    case DS_ERR_DTYPE: return "dtype error";
+    case DS_ERR_INVALID_BUDGET: return "invalid budget (k or k_t out of range)";
+    case DS_ERR_INVALID_CLUSTER_COUNT: return "invalid cluster count";
+    case DS_ERR_INVALID_CLUSTER_ID: return "invalid cluster id";
+    case DS_ERR_INVALID_TOKEN: return "invalid token id";
+    case DS_ERR_DEGENERATE_COLUMN: return "degenerate (zero-norm) LM-head column";
+    case DS_ERR_EMPTY_SHORTLIST: return "empty cluster / shortlist";
+    case DS_ERR_WORKSPACE: return "workspace missing or too small";
+    case DS_ERR_CUDA: return "CUDA error";
+    case DS_ERR_UNSUPPORTED: return "unsupported shape";
+  }
+  return "unknown status";
+}
+
+int32_t dynaspec_budget(int32_t t, int32_t k_max, int32_t k_min) {
+  if (t < 0 || k_min < 1 || k_max < k_min) return -1;
+  if (t <= 1) return k_max;
+  const int32_t k = k_max / ((t + 1) * 2);
+  return k > k_min ? k : k_min;
+}
+
+int64_t dynaspec_max_shortlist(const ds_clusters* c, int32_t k) {
+  if (!c || k < 1) return 0;
+  const int64_t b = (int64_t)k * c->max_size;
+  return b < c->V ? b : c->V;
+}
+
+ds_status dynaspec_ws_init(void* ws, size_t ws_bytes, ds_stream_t stream) {
+  if (!ws || ws_bytes < 256) return DS_ERR_WORKSPACE;
+  return cudaMemsetAsync(ws, 0, ws_bytes, (cudaStream_t)stream) == cudaSuccess ? DS_OK : DS_ERR_CUDA;
+}
+
+size_t dynaspec_layout_ws(int64_t V, int32_t M) { return layout_ws_bytes(V, M); }
+
+ds_status dynaspec_layout(const int32_t* tau, const void* W, int32_t dtype, int64_t V, int32_t d, int32_t M,
+                          int32_t* perm, int32_t* offsets, void* W_perm, int32_t* sizes_host, void* ws,
+                          size_t ws_bytes, ds_stream_t stream) {
+  if (!tau || !perm || !offsets) return DS_ERR_SHAPE;
+  if ((W == nullptr) != (W_perm == nullptr)) return DS_ERR_SHAPE;
+  if (!dtype_ok(dtype)) return DS_ERR_DTYPE;
+  if (V < 1 || V > INT32_MAX || d < 1) return DS_ERR_SHAPE;
+  if (M < 1 || M > V || M > kMaxMHost) return DS_ERR_INVALID_CLUSTER_COUNT;
+  if (d % 8 != 0) return DS_ERR_UNSUPPORTED;
+  if (!ws || ws_bytes < layout_ws_bytes(V, M)) return DS_ERR_WORKSPACE;
+  return run_layout(tau, W, dtype, V, d, M, perm, offsets, W_perm, sizes_host, ws, (cudaStream_t)stream);
+}
+
+size_t dynaspec_build_clusters_ws(int64_t V, int32_t d, int32_t M) { return build_ws_bytes(V, d, M); }
+
+ds_status dynaspec_build_clusters(const void* W, int32_t dtype, int64_t V, int32_t d, int32_t M, uint64_t seed,
+                                  int32_t max_iters, const int32_t* init_ids_host, int32_t* tau, int32_t* perm,
+                                  int32_t* offsets, void* W_perm, int32_t* iters_run_host, int32_t* sizes_host,
+                                  void* ws, size_t ws_bytes, ds_stream_t stream) {
+  if (!W || !tau || !perm || !offsets || !W_perm) return DS_ERR_SHAPE;
+  if (!dtype_ok(dtype)) return DS_ERR_DTYPE;
+  if (V < 1 || V > INT32_MAX || d < 1 || max_iters < 1) return DS_ERR_SHAPE;
+  if (M < 1 || M > V || M > kMaxMHost) return DS_ERR_INVALID_CLUSTER_COUNT;
+  if (d % 8 != 0) return DS_ERR_UNSUPPORTED;
+  if (!ws || ws_bytes < build_ws_bytes(V, d, M)) return DS_ERR_WORKSPACE;
+  if (init_ids_host) {
+    for (int m = 0; m < M; ++m)
+      if (init_ids_host[m] < 0 || init_ids_host[m] >= V) return DS_ERR_INVALID_TOKEN;
+  }
+  return run_build(W, dtype, V, d, M, seed, max_iters, init_ids_host, tau, perm, offsets, W_perm, iters_run_host,
+                   sizes_host, ws, (cudaStream_t)stream);
+}
+
+size_t dynaspec_meta_score_ws(const ds_router* r, int32_t B) {
+  if (!r || B < 1) return 0;
+  return ws_layout(meta_plan(r, B).part_bytes, 0).total;
+}
+
+ds_status dynaspec_meta_score(const ds_router* r, const void* h_prev, const void* e, int32_t B, float* scores,
+                              void* ws, size_t ws_bytes, ds_stream_t stream) {
+  ds_status s = check_router(r);
+  if (s != DS_OK) return s;
+  if (!h_prev || !e || !scores || B < 1) return DS_ERR_SHAPE;
+  const WsLayout L = ws_layout(meta_plan(r, B).part_bytes, 0);
+  if (!ws || ws_bytes < L.total) return DS_ERR_WORKSPACE;
+  uint8_t* w8 = static_cast<uint8_t*>(ws);
+  cudaError_t err = launch_meta(r, h_prev, e, B, scores, reinterpret_cast<float*>(w8 + L.meta),
+                                reinterpret_cast<unsigned*>(w8 + L.counters), nullptr, 0, nullptr, 0, nullptr,
+                                nullptr, nullptr, (cudaStream_t)stream, false);
+  return err == cudaSuccess ? DS_OK : DS_ERR_CUDA;
+}
+
+ds_status dynaspec_select(const float* scores, int32_t B, const ds_clusters* c, int32_t k, const int32_t* k_per_row,
+                          int32_t shared, int32_t* sel, int32_t* sel_count, int32_t* sl_offsets,
+                          ds_stream_t stream) {
+  if (!c || !c->offsets) return DS_ERR_SHAPE;
+  if (c->M < 1 || c->M > kMaxMHost || c->M > c->V) return DS_ERR_INVALID_CLUSTER_COUNT;
+  if (!scores || !sel || !sel_count || !sl_offsets || B < 1) return DS_ERR_SHAPE;
+  if (!k_per_row && (k < 1 || k > c->M)) return DS_ERR_INVALID_BUDGET;
+  cudaError_t err = launch_select(scores, B, c->M, c->offsets, k, k_per_row, shared ? 1 : 0, sel, sel_count,
+                                  sl_offsets, nullptr, (cudaStream_t)stream);
+  return err == cudaSuccess ? DS_OK : DS_ERR_CUDA;
+}
+
+size_t dynaspec_head_forward_ws(const ds_clusters* c, int32_t B, int32_t k_t) {
+  HeadPlan p;
+  if (!c || B < 1 || k_t < 1 || k_t > kMaxKt) return 0;
+  if (!head_plan(c, B, k_t, 0, &p)) return 0;
+  return ws_layout(0, p.part_bytes).total;
+}
+
+ds_status dynaspec_head_forward(const ds_clusters* c, const void* h_new, int32_t B, const int32_t* sel,
+                                const int32_t* sel_count, const int32_t* sl_offsets, int32_t shared, int32_t k_t,
+                                int64_t max_shortlist, int32_t* top_ids, float* top_logits, float* top_logp,
+                                float* lse, float* z_out, int64_t z_stride, void* ws, size_t ws_bytes,
+                                ds_stream_t stream) {
+  ds_status s = check_clusters(c);
+  if (s != DS_OK) return s;
+  if (!h_new || !sel || !sel_count || !sl_offsets || !top_ids || !top_logits || !top_logp || !lse || B < 1)
+    return DS_ERR_SHAPE;
+  if (k_t < 1 || k_t > kMaxKt) return DS_ERR_INVALID_BUDGET;
+  if (max_shortlist < 0) return DS_ERR_SHAPE;
+  if (z_out && z_stride < (max_shortlist > 0 ? std::min<int64_t>(max_shortlist, c->V) : c->V)) return DS_ERR_SHAPE;
+  HeadPlan p;
+  if (!head_plan(c, B, k_t, max_shortlist, &p)) return DS_ERR_UNSUPPORTED;
+  // the workspace is sized for the largest plan (max_shortlist = V); smaller bounds need less
+  const WsLayout L = ws_layout(0, p.part_bytes);
+  if (!ws || ws_bytes < L.total) return DS_ERR_WORKSPACE;
+  uint8_t* w8 = static_cast<uint8_t*>(ws);
+  cudaError_t err = launch_head(c, p, h_new, B, sel, sel_count, sl_offsets, shared ? 1 : 0, k_t, max_shortlist,
+                                top_ids, top_logits, top_logp, lse, z_out, z_stride,
+                                reinterpret_cast<float*>(w8 + L.head), reinterpret_cast<unsigned*>(w8 + L.counters),
+                                (cudaStream_t)stream, false);
+  return err == cudaSuccess ? DS_OK : DS_ERR_CUDA;
+}
+
+size_t dynaspec_draft_step_ws(const ds_clusters* c, const ds_router* r, int32_t B, int32_t k_t) {
+  HeadPlan p;
+  if (!c || !r || B < 1 || k_t < 1 || k_t > kMaxKt) return 0;
+  if (!head_plan(c, B, k_t, 0, &p)) return 0;
+  const size_t meta = meta_plan(r, B).part_bytes;
+  const size_t scores = (size_t)B * r->M * sizeof(float);
+  return ws_layout(align_up(meta, 256) + align_up(scores, 256), p.part_bytes).total;
+}
+
+int32_t dynaspec_draft_step_launches(const ds_clusters* c, const ds_router* r, int32_t B, int32_t k_t,
+                                     int32_t shared) {
+  HeadPlan p;
+  if (!c || !r || !head_plan(c, B, k_t, 0, &p)) return 0;
+  (void)shared;
+  return 2 + p.launches;  // meta layer 1, meta layer 2 (+select), head chunks
+}
+
+ds_status dynaspec_draft_step(const ds_clusters* c, const ds_router* r, const void* h_prev, const void* e,
+                              const void* h_new, int32_t B, int32_t t, int32_t k_max, int32_t k_min, int32_t k_t,
+                              int32_t shared, const ds_step_outputs* out, void* ws, size_t ws_bytes,
+                              ds_stream_t s_draft, ds_stream_t s_meta, ds_event_t ev_fork, ds_event_t ev_join,
+                              ds_event_t head_begin, ds_event_t head_end) {
+  ds_status s = check_clusters(c);
+  if (s != DS_OK) return s;
+  if ((s = check_router(r)) != DS_OK) return s;
+  if (r->M != c->M || r->d != c->d) return DS_ERR_SHAPE;
+  if (r->dtype != c->dtype) return DS_ERR_DTYPE;
+  if (!h_prev || !e || !h_new || !out || B < 1) return DS_ERR_SHAPE;
+  if (!out->sel || !out->sel_count || !out->sl_offsets || !out->top_ids || !out->top_logits || !out->top_logp ||
+      !out->lse)
+    return DS_ERR_SHAPE;
+  const int32_t k = dynaspec_budget(t, k_max, k_min);
+  if (k < 1 || k_max > c->M) return DS_ERR_INVALID_BUDGET;
+  if (k_t < 1 || k_t > kMaxKt || (int64_t)k_t > (int64_t)k * c->min_size) return DS_ERR_INVALID_BUDGET;
+  const int64_t ms = shared ? c->V : dynaspec_max_shortlist(c, k);
+  if (out->z_out && out->z_stride < ms) return DS_ERR_SHAPE;
+  const bool two_streams = s_meta != nullptr && s_meta != s_draft;
+  if (two_streams && (!ev_fork || !ev_join)) return DS_ERR_SHAPE;
+  HeadPlan p;
+  if (!head_plan(c, B, k_t, ms, &p)) return DS_ERR_UNSUPPORTED;
+  HeadPlan pmax;
+  if (!head_plan(c, B, k_t, 0, &pmax)) return DS_ERR_UNSUPPORTED;
+  const size_t meta_bytes = meta_plan(r, B).part_bytes;
+  const size_t score_bytes = (size_t)B * r->M * sizeof(float);
+  const WsLayout L = ws_layout(align_up(meta_bytes, 256) + align_up(score_bytes, 256), pmax.part_bytes);
+  if (!ws || ws_bytes < L.total) return DS_ERR_WORKSPACE;
+  uint8_t* w8 = static_cast<uint8_t*>(ws);
+  unsigned* counters = reinterpret_cast<unsigned*>(w8 + L.counters);
+  float* meta_part = reinterpret_cast<float*>(w8 + L.meta);
+  float* scores = out->scores ? out->scores : reinterpret_cast<float*>(w8 + L.meta + align_up(meta_bytes, 256));
+
+  cudaStream_t sd = (cudaStream_t)s_draft;
+  cudaStream_t sm = two_streams ? (cudaStream_t)s_meta : sd;
+  if (two_streams) {  // S_m forks off S_d (its inputs h_prev, e were produced upstream on S_d)
+    if (cudaEventRecord((cudaEvent_t)ev_fork, sd) != cudaSuccess) return DS_ERR_CUDA;
+    if (cudaStreamWaitEvent(sm, (cudaEvent_t)ev_fork, 0) != cudaSuccess) return DS_ERR_CUDA;
+  }
+  cudaError_t err = launch_meta(r, h_prev, e, B, scores, meta_part, counters + 1, c->offsets, k, nullptr,
+                                shared ? 1 : 0, out->sel, out->sel_count, out->sl_offsets, sm, !two_streams);
+  if (err != cudaSuccess) return DS_ERR_CUDA;
+  if (two_streams) {  // Alg. 1 line 10: "sync S_m, S_d"
+    if (cudaEventRecord((cudaEvent_t)ev_join, sm) != cudaSuccess) return DS_ERR_CUDA;
+    if (cudaStreamWaitEvent(sd, (cudaEvent_t)ev_join, 0) != cudaSuccess) return DS_ERR_CUDA;
+  }
+  if (head_begin && cudaEventRecord((cudaEvent_t)head_begin, sd) != cudaSuccess) return DS_ERR_CUDA;
+  err = launch_head(c, p, h_new, B, out->sel, out->sel_count, out->sl_offsets, shared ? 1 : 0, k_t, ms, out->top_ids,
+                    out->top_logits, out->top_logp, out->lse, out->z_out, out->z_stride,
+                    reinterpret_cast<float*>(w8 + L.head), counters, sd, !two_streams && head_begin == nullptr);
+  if (err != cudaSuccess) return DS_ERR_CUDA;
+  if (head_end && cudaEventRecord((cudaEvent_t)head_end, sd) != cudaSuccess) return DS_ERR_CUDA;
+  return DS_OK;
+}
+
+}  // extern "C"

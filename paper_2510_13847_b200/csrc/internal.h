@@ -1,0 +1,62 @@
+// internal.h — launchers shared between the kernel translation units and the C-ABI layer.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/dynaspec.h"
+
+namespace ds {
+
+constexpr int kMaxM = 1024;      // largest cluster count the select kernels support
+constexpr int kMaxMHost = kMaxM;
+constexpr int kMaxKt = 64;       // largest token budget k_t
+
+int num_sms();                 // SM count of the current device (cached per device)
+size_t align_up(size_t x, size_t a);
+
+// ---- meta-classifier (meta.cu)
+struct MetaPlan {
+  int KC;       // K-chunk per split (elements of the 2d input)
+  int KS;       // number of K splits
+  int rows1;    // layer-1 output rows (h_r, or M for a linear router)
+  size_t part_bytes;
+};
+MetaPlan meta_plan(const ds_router* r, int B);
+// Enqueue layer 1 (split-K partials) and layer 2 + (optionally) selection.
+// sel == nullptr => scores only.
+cudaError_t launch_meta(const ds_router* r, const void* h_prev, const void* e, int B, float* scores,
+                        float* part, unsigned* counter, const int32_t* offsets, int k,
+                        const int32_t* k_per_row, int shared, int32_t* sel, int32_t* sel_count,
+                        int32_t* sl_offsets, cudaStream_t st, bool pdl);
+cudaError_t launch_select(const float* scores, int B, int M, const int32_t* offsets, int k,
+                          const int32_t* k_per_row, int shared, int32_t* sel, int32_t* sel_count,
+                          int32_t* sl_offsets, unsigned* counter, cudaStream_t st);
+
+// ---- head (head.cu)
+struct HeadPlan {
+  int G;               // CTAs per launch
+  int rows_per_launch; // rows (per-row mode) / rows sharing the list (shared) per launch
+  int lcap;            // logits capacity per row per CTA
+  int rec;             // floats per partial record (2 + 2*k_t)
+  int stage_rows;
+  size_t smem;
+  size_t part_bytes;   // workspace bytes for partials
+  int launches;        // number of launches for B rows
+};
+bool head_plan(const ds_clusters* c, int B, int k_t, int64_t max_shortlist, HeadPlan* p);
+cudaError_t launch_head(const ds_clusters* c, const HeadPlan& p, const void* h_new, int B, const int32_t* sel,
+                        const int32_t* sel_count, const int32_t* sl_offsets, int shared, int k_t,
+                        int64_t max_shortlist, int32_t* top_ids, float* top_logits, float* top_logp,
+                        float* lse, float* z_out, int64_t z_stride, float* part, unsigned* counter,
+                        cudaStream_t st, bool pdl);
+
+// ---- offline partition (build.cu)
+size_t build_ws_bytes(int64_t V, int d, int M);
+size_t layout_ws_bytes(int64_t V, int M);
+ds_status run_layout(const int32_t* tau, const void* W, int dtype, int64_t V, int d, int M, int32_t* perm,
+                     int32_t* offsets, void* W_perm, int32_t* sizes_host, void* ws, cudaStream_t st);
+ds_status run_build(const void* W, int dtype, int64_t V, int d, int M, uint64_t seed, int max_iters,
+                    const int32_t* init_ids_host, int32_t* tau, int32_t* perm, int32_t* offsets, void* W_perm,
+                    int32_t* iters_host, int32_t* sizes_host, void* ws, cudaStream_t st);
+
+}  // namespace ds

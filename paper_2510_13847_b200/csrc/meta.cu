@@ -1,0 +1,290 @@
+// meta.cu — S1 meta-classifier r_theta and S3/S4 cluster selection (stream S_m).
+//
+// s = W2 ReLU(W1 [h_prev || e] + b1) + b2          (§4.2 "Low-cost router"; R4, R5)
+// K = TopK_k(s), ascending ids; sl_offsets = scan  (Alg. 1 line 8)
+//
+// Layer 1 is a skinny GEMV (h_r x 2d weights, 2 MB at Llama-3) and is HBM/latency bound:
+// it is split over (h_r / 8) x KS CTAs, each warp owning one hidden unit and one K-chunk,
+// holding its W1 slice in registers and reusing it for all B rows; x = [h_prev||e] is
+// staged in shared memory.  Partials go to the workspace (no float atomics) and layer 2
+// (one CTA per row) reduces them in fixed split order, applies b1 + ReLU, computes the M
+// scores (warp per score) and then selects in the same CTA — selection never leaves the
+// chip.  Shared (tree) mode: the last row-CTA (atomic ticket) forms the union selection.
+#include <limits.h>
+
+#include <algorithm>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace ds {
+
+constexpr int kMetaThreads = 256;
+constexpr int kMetaUnitsPerCTA = kMetaThreads / 32;
+constexpr int kSelThreads = 256;
+
+// ------------------------------------------------------------------ selection (block of 256)
+
+// flags[m] |= rank(m) < k, rank under (score desc, id asc); scores staged in smem `s`.
+__device__ void rank_select(const float* s, int M, int k, uint8_t* flags) {
+  for (int m = threadIdx.x; m < M; m += blockDim.x) {
+    const float key = s[m] + 0.0f;
+    int rank = 0;
+    for (int j = 0; j < M; ++j) {
+      const float o = s[j] + 0.0f;
+      rank += (o > key) || (o == key && j < m);
+    }
+    if (rank < k) flags[m] = 1;
+  }
+}
+
+// Compact flags into ascending ids + exclusive scan of cluster sizes (sl_offsets).
+__device__ void emit_selection(const uint8_t* flags, int M, const int32_t* offsets, int32_t* sel,
+                               int32_t* sel_count, int32_t* sl_off, int* scratch) {
+  // each thread owns up to 4 consecutive cluster ids (M <= 1024)
+  const int per = (M + kSelThreads - 1) / kSelThreads;
+  const int m0 = threadIdx.x * per;
+  int cnt = 0, sz = 0;
+  for (int j = 0; j < per; ++j) {
+    const int m = m0 + j;
+    if (m < M && flags[m]) {
+      ++cnt;
+      sz += offsets[m + 1] - offsets[m];
+    }
+  }
+  int tot_cnt, tot_sz;
+  int pos = block_excl_scan<kSelThreads>(cnt, scratch, tot_cnt);
+  int off = block_excl_scan<kSelThreads>(sz, scratch, tot_sz);
+  for (int j = 0; j < per; ++j) {
+    const int m = m0 + j;
+    if (m < M && flags[m]) {
+      sel[pos] = m;
+      sl_off[pos] = off;
+      ++pos;
+      off += offsets[m + 1] - offsets[m];
+    }
+  }
+  if (threadIdx.x == 0) {
+    *sel_count = tot_cnt;
+    sl_off[tot_cnt] = tot_sz;
+  }
+}
+
+__global__ void __launch_bounds__(kSelThreads) select_kernel(const float* __restrict__ scores, int B, int M,
+                                                             const int32_t* __restrict__ offsets, int k,
+                                                             const int32_t* __restrict__ k_per_row, int shared,
+                                                             int32_t* sel, int32_t* sel_count, int32_t* sl_off) {
+  __shared__ float s[kMaxM];
+  __shared__ uint8_t flags[kMaxM];
+  __shared__ int scratch[kSelThreads / 32 + 1];
+  for (int m = threadIdx.x; m < M; m += blockDim.x) flags[m] = 0;
+  const int r_lo = shared ? 0 : blockIdx.x, r_hi = shared ? B : blockIdx.x + 1;
+  for (int r = r_lo; r < r_hi; ++r) {
+    __syncthreads();
+    for (int m = threadIdx.x; m < M; m += blockDim.x) s[m] = scores[(size_t)r * M + m];
+    __syncthreads();
+    rank_select(s, M, k_per_row ? k_per_row[r] : k, flags);
+  }
+  __syncthreads();
+  const int o = shared ? 0 : blockIdx.x;
+  emit_selection(flags, M, offsets, sel + (size_t)o * M, sel_count + o, sl_off + (size_t)o * (M + 1), scratch);
+}
+
+// ------------------------------------------------------------------ layer 1: split-K partials
+
+template <typename T>
+__global__ void __launch_bounds__(kMetaThreads) meta_l1_kernel(const T* __restrict__ W1, const T* __restrict__ h_prev,
+                                                               const T* __restrict__ e, int B, int d, int rows1,
+                                                               int KC, float* __restrict__ part, int pdl) {
+  constexpr int E = Elem<T>::kPer16B;
+  extern __shared__ __align__(16) uint8_t msm[];
+  T* xs = reinterpret_cast<T*>(msm);  // [B][KC]
+  const int dr = 2 * d;
+  const int k0 = blockIdx.y * KC;
+  const int kn = min(KC, dr - k0);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int u = blockIdx.x * kMetaUnitsPerCTA + warp;
+
+  // W1 slice of this warp -> registers (independent of upstream kernels: load before the PDL wait)
+  constexpr int kMaxChunks = 4;  // KC <= 32 * E * kMaxChunks
+  uint4 wv[kMaxChunks];
+#pragma unroll
+  for (int i = 0; i < kMaxChunks; ++i) {
+    const int c = lane * E + i * 32 * E;
+    wv[i] = (u < rows1 && c < kn) ? __ldg(reinterpret_cast<const uint4*>(W1 + (size_t)u * dr + k0 + c))
+                                  : make_uint4(0, 0, 0, 0);
+  }
+  if (pdl) pdl_wait();
+  // stage x = [h_prev || e][:, k0:k0+kn]; a 16-byte chunk never straddles h/e since d % E == 0
+  const int cpr = kn / E;
+  for (int idx = threadIdx.x; idx < B * cpr; idx += blockDim.x) {
+    const int b = idx / cpr, c = (idx - b * cpr) * E;
+    const int k = k0 + c;
+    const T* src = k < d ? h_prev + (size_t)b * d + k : e + (size_t)b * d + (k - d);
+    *reinterpret_cast<uint4*>(xs + (size_t)b * KC + c) = *reinterpret_cast<const uint4*>(src);
+  }
+  __syncthreads();
+  if (pdl) pdl_launch_dependents();
+  if (u >= rows1) return;
+  for (int b = 0; b < B; ++b) {
+    float acc = 0.f;
+#pragma unroll
+    for (int i = 0; i < kMaxChunks; ++i) {
+      const int c = lane * E + i * 32 * E;
+      if (c < kn) {
+        float wf[E], xf[E];
+        widen16(wv[i], wf, W1);
+        widen16(*reinterpret_cast<const uint4*>(xs + (size_t)b * KC + c), xf, W1);
+#pragma unroll
+        for (int j = 0; j < E; ++j) acc = fmaf(wf[j], xf[j], acc);
+      }
+    }
+    acc = warp_sum(acc);
+    if (lane == 0) part[((size_t)blockIdx.y * B + b) * rows1 + u] = acc;
+  }
+}
+
+// ------------------------------------------------------------------ layer 2 + select (CTA per row)
+
+template <typename T>
+__global__ void __launch_bounds__(kMetaThreads) meta_l2_kernel(const float* __restrict__ part, int KS, int B,
+                                                               int rows1, const float* __restrict__ b1,
+                                                               const T* __restrict__ W2, const float* __restrict__ b2,
+                                                               int h_r, int M, float* __restrict__ scores,
+                                                               const int32_t* __restrict__ offsets, int k,
+                                                               const int32_t* __restrict__ k_per_row, int shared,
+                                                               int32_t* sel, int32_t* sel_count, int32_t* sl_off,
+                                                               unsigned* counter, int pdl) {
+  __shared__ float a1[kMaxM];
+  __shared__ float s[kMaxM];
+  __shared__ uint8_t flags[kMaxM];
+  __shared__ int scratch[kMetaThreads / 32 + 1];
+  __shared__ int is_last;
+  const int b = blockIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (pdl) pdl_wait();
+  // a = ReLU(sum_splits part + b1): fixed split order
+  for (int u = threadIdx.x; u < rows1; u += blockDim.x) {
+    float acc = 0.f;
+    for (int ks = 0; ks < KS; ++ks) acc += part[((size_t)ks * B + b) * rows1 + u];
+    acc += b1[u];
+    a1[u] = h_r > 0 ? fmaxf(acc, 0.f) : acc;
+  }
+  __syncthreads();
+  if (h_r > 0) {
+    for (int m = warp; m < M; m += kMetaThreads / 32) {
+      const T* w = W2 + (size_t)m * h_r;
+      float acc = 0.f;
+      for (int u = lane; u < h_r; u += 32) acc = fmaf(static_cast<float>(w[u]), a1[u], acc);
+      acc = warp_sum(acc) + b2[m];
+      if (lane == 0) s[m] = acc;
+    }
+  } else {
+    for (int m = threadIdx.x; m < M; m += blockDim.x) s[m] = a1[m];
+  }
+  __syncthreads();
+  for (int m = threadIdx.x; m < M; m += blockDim.x) {
+    scores[(size_t)b * M + m] = s[m];
+    flags[m] = 0;
+  }
+  if (sel == nullptr) return;
+  __syncthreads();
+  if (pdl) pdl_launch_dependents();
+  if (!shared) {
+    rank_select(s, M, k_per_row ? k_per_row[b] : k, flags);
+    __syncthreads();
+    emit_selection(flags, M, offsets, sel + (size_t)b * M, sel_count + b, sl_off + (size_t)b * (M + 1), scratch);
+    return;
+  }
+  // shared mode: the last row-CTA forms the union of every row's TopK
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) is_last = atomicAdd(counter, 1u) == (unsigned)(gridDim.x - 1);
+  __syncthreads();
+  if (!is_last) return;
+  __threadfence();
+  for (int r = 0; r < B; ++r) {
+    __syncthreads();
+    for (int m = threadIdx.x; m < M; m += blockDim.x) s[m] = __ldcg(scores + (size_t)r * M + m);
+    __syncthreads();
+    rank_select(s, M, k_per_row ? k_per_row[r] : k, flags);
+  }
+  __syncthreads();
+  emit_selection(flags, M, offsets, sel, sel_count, sl_off, scratch);
+  if (threadIdx.x == 0) *counter = 0u;
+}
+
+// ------------------------------------------------------------------ host side
+
+MetaPlan meta_plan(const ds_router* r, int B) {
+  MetaPlan p;
+  const int E = r->dtype == DS_BF16 ? 8 : 4;
+  p.rows1 = r->h_r > 0 ? r->h_r : r->M;
+  const int dr = 2 * r->d;
+  // K-chunk: up to 4 x 16-byte chunks per lane; keep x staging <= 96 KB
+  int KC = 4 * 32 * E;
+  const int esz = r->dtype == DS_BF16 ? 2 : 4;
+  while (KC > 32 * E && (size_t)B * KC * esz > 96 * 1024) KC /= 2;
+  if (KC > dr) KC = ((dr + E - 1) / E) * E;
+  p.KC = KC;
+  p.KS = (dr + KC - 1) / KC;
+  p.part_bytes = (size_t)p.KS * B * p.rows1 * sizeof(float);
+  return p;
+}
+
+template <typename T>
+static cudaError_t launch_meta_t(const ds_router* r, const void* h_prev, const void* e, int B, float* scores,
+                                 float* part, unsigned* counter, const int32_t* offsets, int k,
+                                 const int32_t* k_per_row, int shared, int32_t* sel, int32_t* sel_count,
+                                 int32_t* sl_offsets, cudaStream_t st, bool pdl) {
+  const MetaPlan p = meta_plan(r, B);
+  const size_t smem1 = (size_t)B * p.KC * sizeof(T);
+  if (smem1 > 48 * 1024) {
+    cudaError_t ea = cudaFuncSetAttribute(meta_l1_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1);
+    if (ea != cudaSuccess) return ea;
+  }
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+
+  cudaLaunchConfig_t c1 = {};
+  c1.gridDim = dim3((p.rows1 + kMetaUnitsPerCTA - 1) / kMetaUnitsPerCTA, p.KS);
+  c1.blockDim = dim3(kMetaThreads);
+  c1.dynamicSmemBytes = smem1;
+  c1.stream = st;
+  c1.attrs = attr;
+  c1.numAttrs = pdl ? 1 : 0;
+  cudaError_t err = cudaLaunchKernelEx(&c1, meta_l1_kernel<T>, static_cast<const T*>(r->W1),
+                                       static_cast<const T*>(h_prev), static_cast<const T*>(e), B, r->d, p.rows1,
+                                       p.KC, part, pdl ? 1 : 0);
+  if (err != cudaSuccess) return err;
+  cudaLaunchConfig_t c2 = {};
+  c2.gridDim = dim3(B);
+  c2.blockDim = dim3(kMetaThreads);
+  c2.stream = st;
+  c2.attrs = attr;
+  c2.numAttrs = 1;  // layer 2 always follows layer 1 in-stream
+  return cudaLaunchKernelEx(&c2, meta_l2_kernel<T>, (const float*)part, p.KS, B, p.rows1, r->b1,
+                            static_cast<const T*>(r->W2), r->b2, r->h_r, r->M, scores, offsets, k, k_per_row,
+                            shared, sel, sel_count, sl_offsets, counter, 1);
+}
+
+cudaError_t launch_meta(const ds_router* r, const void* h_prev, const void* e, int B, float* scores, float* part,
+                        unsigned* counter, const int32_t* offsets, int k, const int32_t* k_per_row, int shared,
+                        int32_t* sel, int32_t* sel_count, int32_t* sl_offsets, cudaStream_t st, bool pdl) {
+  if (r->dtype == DS_BF16)
+    return launch_meta_t<__nv_bfloat16>(r, h_prev, e, B, scores, part, counter, offsets, k, k_per_row, shared, sel,
+                                        sel_count, sl_offsets, st, pdl);
+  return launch_meta_t<float>(r, h_prev, e, B, scores, part, counter, offsets, k, k_per_row, shared, sel,
+                              sel_count, sl_offsets, st, pdl);
+}
+
+cudaError_t launch_select(const float* scores, int B, int M, const int32_t* offsets, int k, const int32_t* k_per_row,
+                          int shared, int32_t* sel, int32_t* sel_count, int32_t* sl_offsets, unsigned* /*counter*/,
+                          cudaStream_t st) {
+  select_kernel<<<shared ? 1 : B, kSelThreads, 0, st>>>(scores, B, M, offsets, k, k_per_row, shared, sel, sel_count,
+                                                        sl_offsets);
+  return cudaGetLastError();
+}
+
+}  // namespace ds

@@ -1,0 +1,329 @@
+"""Thin ctypes binding of libdynaspec.so (include/dynaspec.h).
+
+Argument marshalling only: every step of the DynaSpec head runs in the CUDA library.
+PyTorch provides device memory, streams and events.  There is no CPU fallback: if the
+library is missing, importing this module raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from ctypes import c_int32, c_int64, c_size_t, c_uint64, c_void_p, POINTER
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libdynaspec.so")
+
+DS_BF16, DS_F32 = 0, 1
+_DTYPE = {torch.bfloat16: DS_BF16, torch.float32: DS_F32}
+
+STATUS = {
+    0: "DS_OK", 1: "DS_ERR_SHAPE", 2: "DS_ERR_DTYPE", 3: "DS_ERR_INVALID_BUDGET",
+    4: "DS_ERR_INVALID_CLUSTER_COUNT", 5: "DS_ERR_INVALID_CLUSTER_ID", 6: "DS_ERR_INVALID_TOKEN",
+    7: "DS_ERR_DEGENERATE_COLUMN", 8: "DS_ERR_EMPTY_SHORTLIST", 9: "DS_ERR_WORKSPACE", 10: "DS_ERR_CUDA",
+    11: "DS_ERR_UNSUPPORTED",
+}
+
+
+class DynaspecError(RuntimeError):
+    def __init__(self, code, what=""):
+        self.code = code
+        self.name = STATUS.get(code, str(code))
+        super().__init__(f"{what}: {self.name} ({_lib.dynaspec_status_string(code).decode()})")
+
+
+class DsClusters(ctypes.Structure):
+    _fields_ = [("V", c_int64), ("d", c_int32), ("M", c_int32), ("dtype", c_int32), ("min_size", c_int32),
+                ("max_size", c_int32), ("tau", c_void_p), ("perm", c_void_p), ("offsets", c_void_p),
+                ("W_perm", c_void_p)]
+
+
+class DsRouter(ctypes.Structure):
+    _fields_ = [("d", c_int32), ("h_r", c_int32), ("M", c_int32), ("dtype", c_int32), ("W1", c_void_p),
+                ("b1", c_void_p), ("W2", c_void_p), ("b2", c_void_p)]
+
+
+class DsStepOutputs(ctypes.Structure):
+    _fields_ = [("scores", c_void_p), ("sel", c_void_p), ("sel_count", c_void_p), ("sl_offsets", c_void_p),
+                ("top_ids", c_void_p), ("top_logits", c_void_p), ("top_logp", c_void_p), ("lse", c_void_p),
+                ("z_out", c_void_p), ("z_stride", c_int64)]
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is not built; run `python -c 'import __graft_entry__ as g; g.build()'`. "
+                          "There is no CPU fallback for the DynaSpec head.")
+    lib = ctypes.CDLL(LIB_PATH)
+    P = c_void_p
+    sig = {
+        "dynaspec_status_string": (ctypes.c_char_p, [c_int32]),
+        "dynaspec_budget": (c_int32, [c_int32, c_int32, c_int32]),
+        "dynaspec_max_shortlist": (c_int64, [POINTER(DsClusters), c_int32]),
+        "dynaspec_ws_init": (c_int32, [P, c_size_t, P]),
+        "dynaspec_build_clusters_ws": (c_size_t, [c_int64, c_int32, c_int32]),
+        "dynaspec_build_clusters": (c_int32, [P, c_int32, c_int64, c_int32, c_int32, c_uint64, c_int32, P, P, P, P,
+                                              P, P, P, P, c_size_t, P]),
+        "dynaspec_layout_ws": (c_size_t, [c_int64, c_int32]),
+        "dynaspec_layout": (c_int32, [P, P, c_int32, c_int64, c_int32, c_int32, P, P, P, P, P, c_size_t, P]),
+        "dynaspec_meta_score_ws": (c_size_t, [POINTER(DsRouter), c_int32]),
+        "dynaspec_meta_score": (c_int32, [POINTER(DsRouter), P, P, c_int32, P, P, c_size_t, P]),
+        "dynaspec_select": (c_int32, [P, c_int32, POINTER(DsClusters), c_int32, P, c_int32, P, P, P, P]),
+        "dynaspec_head_forward_ws": (c_size_t, [POINTER(DsClusters), c_int32, c_int32]),
+        "dynaspec_head_forward": (c_int32, [POINTER(DsClusters), P, c_int32, P, P, P, c_int32, c_int32, c_int64, P,
+                                            P, P, P, P, c_int64, P, c_size_t, P]),
+        "dynaspec_draft_step_ws": (c_size_t, [POINTER(DsClusters), POINTER(DsRouter), c_int32, c_int32]),
+        "dynaspec_draft_step": (c_int32, [POINTER(DsClusters), POINTER(DsRouter), P, P, P, c_int32, c_int32,
+                                          c_int32, c_int32, c_int32, c_int32, POINTER(DsStepOutputs), P, c_size_t,
+                                          P, P, P, P, P, P]),
+        "dynaspec_draft_step_launches": (c_int32, [POINTER(DsClusters), POINTER(DsRouter), c_int32, c_int32,
+                                                   c_int32]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    return lib
+
+
+_lib = _load()
+
+EXPORTED = [
+    "dynaspec_status_string", "dynaspec_budget", "dynaspec_max_shortlist", "dynaspec_ws_init",
+    "dynaspec_build_clusters_ws", "dynaspec_build_clusters", "dynaspec_layout_ws", "dynaspec_layout",
+    "dynaspec_meta_score_ws", "dynaspec_meta_score", "dynaspec_select", "dynaspec_head_forward_ws",
+    "dynaspec_head_forward", "dynaspec_draft_step_ws", "dynaspec_draft_step", "dynaspec_draft_step_launches",
+]
+
+
+def lib():
+    return _lib
+
+
+def _check(code, what):
+    if code != 0:
+        raise DynaspecError(code, what)
+
+
+def _ptr(t):
+    return None if t is None else c_void_p(t.data_ptr())
+
+
+def _stream(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return c_void_p(s.cuda_stream)
+
+
+def _need_cuda(*ts):
+    for t in ts:
+        if t is not None:
+            if not t.is_cuda:
+                raise ValueError("DynaSpec head tensors must be CUDA tensors (no CPU path)")
+            if not t.is_contiguous():
+                raise ValueError("DynaSpec head tensors must be contiguous")
+
+
+# ---------------------------------------------------------------------------- host helpers
+
+def budget(t, k_max, k_min=1):
+    """k_c(t) (R1).  Returns -1 on invalid arguments."""
+    return _lib.dynaspec_budget(t, k_max, k_min)
+
+
+class Workspace:
+    """Caller-provided scratch (zero-filled once, reused across calls on one stream)."""
+
+    def __init__(self, nbytes, device="cuda"):
+        self.nbytes = max(int(nbytes), 256)
+        self.buf = torch.empty(self.nbytes, dtype=torch.uint8, device=device)
+        _check(_lib.dynaspec_ws_init(_ptr(self.buf), self.nbytes, _stream()), "ws_init")
+
+    def ptr(self):
+        return _ptr(self.buf)
+
+    def ensure(self, nbytes):
+        if nbytes > self.nbytes:
+            self.__init__(nbytes, self.buf.device)
+        return self
+
+
+# ---------------------------------------------------------------------------- S0 partition
+
+class Clusters:
+    """Cluster-permuted LM head (ds_clusters)."""
+
+    def __init__(self, tau, perm, offsets, W_perm, min_size, max_size):
+        self.tau, self.perm, self.offsets, self.W_perm = tau, perm, offsets, W_perm
+        self.min_size, self.max_size = int(min_size), int(max_size)
+        self.V, self.d = W_perm.shape
+        self.M = offsets.numel() - 1
+        self.dtype = W_perm.dtype
+        self._s = DsClusters(self.V, self.d, self.M, _DTYPE[self.dtype], self.min_size, self.max_size,
+                             _ptr(tau), _ptr(perm), _ptr(offsets), _ptr(W_perm))
+
+    def struct(self):
+        return ctypes.byref(self._s)
+
+    def max_shortlist(self, k):
+        return _lib.dynaspec_max_shortlist(self.struct(), k)
+
+    @classmethod
+    def from_tau(cls, W, tau, M):
+        """dynaspec_layout: perm / offsets / W_perm from a given partition tau."""
+        _need_cuda(W, tau)
+        V, d = W.shape
+        tau = tau.to(torch.int32).contiguous()
+        perm = torch.empty(V, dtype=torch.int32, device=W.device)
+        offsets = torch.empty(M + 1, dtype=torch.int32, device=W.device)
+        W_perm = torch.empty_like(W)
+        sizes = (c_int32 * 2)()
+        ws = Workspace(_lib.dynaspec_layout_ws(V, M), W.device)
+        _check(_lib.dynaspec_layout(_ptr(tau), _ptr(W), _DTYPE[W.dtype], V, d, M, _ptr(perm), _ptr(offsets),
+                                    _ptr(W_perm), ctypes.cast(sizes, c_void_p), ws.ptr(), ws.nbytes, _stream()),
+               "dynaspec_layout")
+        return cls(tau, perm, offsets, W_perm, sizes[0], sizes[1])
+
+    @classmethod
+    def build(cls, W, M, seed=2, max_iters=20, init_ids=None):
+        """dynaspec_build_clusters: offline spherical k-means (R12) + layout."""
+        _need_cuda(W)
+        V, d = W.shape
+        tau = torch.empty(V, dtype=torch.int32, device=W.device)
+        perm = torch.empty(V, dtype=torch.int32, device=W.device)
+        offsets = torch.empty(M + 1, dtype=torch.int32, device=W.device)
+        W_perm = torch.empty_like(W)
+        iters = c_int32(0)
+        sizes = (c_int32 * 2)()
+        init = None
+        if init_ids is not None:
+            init = (c_int32 * M)(*[int(x) for x in init_ids])
+        ws = Workspace(_lib.dynaspec_build_clusters_ws(V, d, M), W.device)
+        _check(_lib.dynaspec_build_clusters(_ptr(W), _DTYPE[W.dtype], V, d, M, seed, max_iters,
+                                            None if init is None else ctypes.cast(init, c_void_p),
+                                            _ptr(tau), _ptr(perm), _ptr(offsets), _ptr(W_perm),
+                                            ctypes.cast(ctypes.pointer(iters), c_void_p),
+                                            ctypes.cast(sizes, c_void_p), ws.ptr(), ws.nbytes, _stream()),
+               "dynaspec_build_clusters")
+        c = cls(tau, perm, offsets, W_perm, sizes[0], sizes[1])
+        c.iters = iters.value
+        return c
+
+
+# ---------------------------------------------------------------------------- S1 router
+
+class Router:
+    def __init__(self, W1, b1, W2=None, b2=None):
+        _need_cuda(W1, b1, W2, b2)
+        self.W1, self.b1, self.W2, self.b2 = W1, b1, W2, b2
+        self.h_r = 0 if W2 is None else W1.shape[0]
+        self.M = W1.shape[0] if W2 is None else W2.shape[0]
+        self.d = W1.shape[1] // 2
+        self._s = DsRouter(self.d, self.h_r, self.M, _DTYPE[W1.dtype], _ptr(W1), _ptr(b1), _ptr(W2), _ptr(b2))
+
+    def struct(self):
+        return ctypes.byref(self._s)
+
+
+def meta_score(router, h_prev, e, ws=None):
+    _need_cuda(h_prev, e)
+    B = h_prev.shape[0]
+    scores = torch.empty((B, router.M), dtype=torch.float32, device=h_prev.device)
+    ws = (ws or Workspace(256, h_prev.device)).ensure(_lib.dynaspec_meta_score_ws(router.struct(), B))
+    _check(_lib.dynaspec_meta_score(router.struct(), _ptr(h_prev), _ptr(e), B, _ptr(scores), ws.ptr(), ws.nbytes,
+                                    _stream()), "dynaspec_meta_score")
+    return scores
+
+
+# ---------------------------------------------------------------------------- S3/S4 select
+
+def select(scores, clusters, k, shared=False, k_per_row=None):
+    _need_cuda(scores, k_per_row)
+    B, M = scores.shape
+    rows = 1 if shared else B
+    dev = scores.device
+    sel = torch.empty((rows, M), dtype=torch.int32, device=dev)
+    cnt = torch.empty(rows, dtype=torch.int32, device=dev)
+    off = torch.empty((rows, M + 1), dtype=torch.int32, device=dev)
+    _check(_lib.dynaspec_select(_ptr(scores), B, clusters.struct(), k, _ptr(k_per_row), int(shared), _ptr(sel),
+                                _ptr(cnt), _ptr(off), _stream()), "dynaspec_select")
+    return sel, cnt, off
+
+
+# ---------------------------------------------------------------------------- S5/S6 head
+
+def head_forward(clusters, h_new, sel, sel_count, sl_offsets, k_t, shared=False, max_shortlist=0, z_out=False,
+                 ws=None):
+    _need_cuda(h_new, sel, sel_count, sl_offsets)
+    B = h_new.shape[0]
+    dev = h_new.device
+    out = {
+        "top_ids": torch.empty((B, k_t), dtype=torch.int32, device=dev),
+        "top_logits": torch.empty((B, k_t), dtype=torch.float32, device=dev),
+        "top_logp": torch.empty((B, k_t), dtype=torch.float32, device=dev),
+        "lse": torch.empty(B, dtype=torch.float32, device=dev),
+    }
+    zs = 0
+    z = None
+    if z_out:
+        zs = max_shortlist if max_shortlist > 0 else clusters.V
+        z = torch.full((B, zs), float("nan"), dtype=torch.float32, device=dev)
+    ws = (ws or Workspace(256, dev)).ensure(_lib.dynaspec_head_forward_ws(clusters.struct(), B, k_t))
+    _check(_lib.dynaspec_head_forward(clusters.struct(), _ptr(h_new), B, _ptr(sel), _ptr(sel_count),
+                                      _ptr(sl_offsets), int(shared), k_t, max_shortlist, _ptr(out["top_ids"]),
+                                      _ptr(out["top_logits"]), _ptr(out["top_logp"]), _ptr(out["lse"]), _ptr(z), zs,
+                                      ws.ptr(), ws.nbytes, _stream()), "dynaspec_head_forward")
+    out["z"] = z
+    return out
+
+
+# ---------------------------------------------------------------------------- S7 draft step
+
+def make_event(enable_timing=False):
+    """torch.cuda.Event created eagerly (torch creates the CUDA event lazily on first record)."""
+    ev = torch.cuda.Event(enable_timing=enable_timing)
+    ev.record()
+    return ev
+
+
+class DraftStep:
+    """Pre-allocated outputs + workspace + events for repeated dynaspec_draft_step calls
+    (graph-capturable: no allocation, no host sync inside __call__)."""
+
+    def __init__(self, clusters, router, B, k_t, shared=False, z_out=False, two_streams=True, device="cuda"):
+        self.c, self.r, self.B, self.k_t, self.shared = clusters, router, B, k_t, bool(shared)
+        M = clusters.M
+        rows = 1 if shared else B
+        dev = device
+        self.scores = torch.empty((B, M), dtype=torch.float32, device=dev)
+        self.sel = torch.empty((rows, M), dtype=torch.int32, device=dev)
+        self.sel_count = torch.empty(rows, dtype=torch.int32, device=dev)
+        self.sl_offsets = torch.empty((rows, M + 1), dtype=torch.int32, device=dev)
+        self.top_ids = torch.empty((B, k_t), dtype=torch.int32, device=dev)
+        self.top_logits = torch.empty((B, k_t), dtype=torch.float32, device=dev)
+        self.top_logp = torch.empty((B, k_t), dtype=torch.float32, device=dev)
+        self.lse = torch.empty(B, dtype=torch.float32, device=dev)
+        self.z_stride = clusters.V if z_out else 0
+        self.z = torch.full((B, clusters.V), float("nan"), dtype=torch.float32, device=dev) if z_out else None
+        self._o = DsStepOutputs(_ptr(self.scores), _ptr(self.sel), _ptr(self.sel_count), _ptr(self.sl_offsets),
+                                _ptr(self.top_ids), _ptr(self.top_logits), _ptr(self.top_logp), _ptr(self.lse),
+                                _ptr(self.z), self.z_stride)
+        self.ws = Workspace(_lib.dynaspec_draft_step_ws(clusters.struct(), router.struct(), B, k_t), dev)
+        self.two_streams = two_streams
+        self.s_meta = torch.cuda.Stream(device=dev) if two_streams else None
+        self.ev_fork = make_event() if two_streams else None
+        self.ev_join = make_event() if two_streams else None
+        self.launches = _lib.dynaspec_draft_step_launches(clusters.struct(), router.struct(), B, k_t, int(shared))
+
+    def __call__(self, h_prev, e, h_new, t, k_max, k_min, head_events=None, stream=None):
+        sd = _stream(stream)
+        hb, he = (head_events if head_events is not None else (None, None))
+        _check(_lib.dynaspec_draft_step(self.c.struct(), self.r.struct(), _ptr(h_prev), _ptr(e), _ptr(h_new), self.B,
+                                        t, k_max, k_min, self.k_t, int(self.shared), ctypes.byref(self._o),
+                                        self.ws.ptr(), self.ws.nbytes, sd,
+                                        c_void_p(self.s_meta.cuda_stream) if self.s_meta is not None else None,
+                                        self.ev_fork, self.ev_join, hb, he), "dynaspec_draft_step")
+        return self
+
+    def outputs(self):
+        return {k: getattr(self, k) for k in ("scores", "sel", "sel_count", "sl_offsets", "top_ids", "top_logits",
+                                               "top_logp", "lse", "z")}

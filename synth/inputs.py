@@ -123,8 +123,8 @@ def router_q(d, h_r, qb=16):
     """Exact-regime grid bound for router inputs and W1: every partial sum of both layers
     stays within 2^24 units (SURVEY §8(c) 'The 2-layer router is much tighter')."""
     if h_r == 0:
-        return max(1, int(math.isqrt((1 << 24) // (2 * d))))
-    return max(1, int(math.isqrt(((1 << 24) // h_r - qb) // (2 * d))))
+        return max(1, min(127, int(math.isqrt((1 << 24) // (2 * d)))))
+    return max(1, min(127, int(math.isqrt(((1 << 24) // h_r - qb) // (2 * d)))))
 
 
 def step_inputs(B, d, t, dtype="bf16", regime="random", pool=64, q=None, device="cpu", base_seed=1000,

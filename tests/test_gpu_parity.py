@@ -1,0 +1,374 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle on the same seeded inputs.
+
+Bar (task rule ③, BASELINE.json north star): bit-exact for cluster ids, selections,
+offsets and token ids; logits within 2e-2 (bf16) / 1e-5 relative (fp32); in the exact
+regime (integer-grid inputs) scores and logits are bit-exact too.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import dynaspec_oracle as O
+from synth import inputs as S
+from tests.parity import Rows, check_topk, f64, selection_certified
+
+pytestmark = pytest.mark.gpu
+
+D = None
+
+
+def _dyn():
+    global D
+    if D is None:
+        from paper_2510_13847_b200 import dynaspec
+        D = dynaspec
+    return D
+
+
+DEV = "cuda"
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "e2e1.json")))
+
+
+def _partition(V, M, seed=2):
+    tau = S.random_partition(V, M, seed)
+    perm, off = O.layout(tau, M)
+    return tau, {"perm": perm, "offsets": off}
+
+
+def _setup(V, d, M, h_r, dtype, regime, seed_part=2):
+    W = S.lm_head(V, d, 0, dtype, regime)
+    rt = S.router(d, h_r, M, 1, dtype, regime)
+    tau, part = _partition(V, M, seed_part)
+    c = _dyn().Clusters.from_tau(W.to(DEV), torch.as_tensor(tau, dtype=torch.int32, device=DEV), M)
+    r = _dyn().Router(*[None if x is None else x.to(DEV) for x in rt])
+    return W, rt, tau, part, c, r
+
+
+def _oracle_router(rt):
+    return tuple(f64(x) for x in rt)
+
+
+# ------------------------------------------------------------------ golden worked example
+
+def test_e2e1_golden_on_gpu():
+    Dy = _dyn()
+    d = 8  # pad the 2-D example with zero dimensions (kernels need d % 8 == 0); dot products unchanged
+    W = torch.zeros((6, d), dtype=torch.float32)
+    W[:, :2] = torch.tensor(GOLD["W_rows"], dtype=torch.float32)
+    tau = torch.tensor(GOLD["partition"]["tau"], dtype=torch.int32)
+    c = Dy.Clusters.from_tau(W.to(DEV), tau.to(DEV), 3)
+    assert c.perm.cpu().tolist() == GOLD["partition"]["perm"]
+    assert c.offsets.cpu().tolist() == GOLD["partition"]["offsets"]
+    R = torch.zeros((3, 2 * d))
+    rows = torch.tensor(GOLD["router_linear_rows"], dtype=torch.float32)
+    R[:, 0:2] = rows[:, 0:2]            # acts on h_prev
+    R[:, d:d + 2] = rows[:, 2:4]        # acts on e
+    r = Dy.Router(R.to(DEV), torch.zeros(3, device=DEV))
+    hp = torch.zeros((1, d)); hp[0, :2] = torch.tensor(GOLD["h_prev"], dtype=torch.float32)
+    e = torch.zeros((1, d)); e[0, :2] = torch.tensor(GOLD["e"], dtype=torch.float32)
+    hn = torch.zeros((1, d)); hn[0, :2] = torch.tensor(GOLD["h_new"], dtype=torch.float32)
+    s = Dy.meta_score(r, hp.to(DEV), e.to(DEV))
+    assert s.cpu()[0].tolist() == GOLD["scores"]
+    for case in GOLD["cases"]:
+        k = case["k"]
+        sel, cnt, off = Dy.select(s, c, k)
+        assert cnt.item() == k and sel.cpu()[0, :k].tolist() == case["sel"]
+        assert off.cpu()[0, :k + 1].tolist() == case["sl_offsets"]
+        kt = len(case["V_S"])
+        out = Dy.head_forward(c, hn.to(DEV), sel, cnt, off, kt, z_out=True)
+        assert out["z"].cpu()[0, :kt].tolist() == case["z"]
+        assert out["top_ids"].cpu()[0].tolist() == case["top_ids"]
+        assert abs(out["lse"].item() - case["lse"]) < 1e-6
+        # draft_step (both streams) reproduces the same step
+        st = Dy.DraftStep(c, r, 1, kt)
+        st(hp.to(DEV), e.to(DEV), hn.to(DEV), t=0, k_max=k, k_min=1)
+        torch.cuda.synchronize()
+        assert st.top_ids.cpu()[0].tolist() == case["top_ids"]
+        assert st.sel.cpu()[0, :k].tolist() == case["sel"]
+    # tie variants: lower cluster id / lower token id win (R7)
+    R2 = R.clone(); R2[0, 0] = 2.0
+    s2 = Dy.meta_score(Dy.Router(R2.to(DEV), torch.zeros(3, device=DEV)), hp.to(DEV), e.to(DEV))
+    sel, cnt, _ = Dy.select(s2, c, 1)
+    assert sel.cpu()[0, 0].item() == 0
+    tv = GOLD["tie_variants"]["h_new_3_2"]
+    hn2 = torch.zeros((1, d)); hn2[0, :2] = torch.tensor(tv["h_new"], dtype=torch.float32)
+    sel, cnt, off = Dy.select(s, c, 2)
+    out = Dy.head_forward(c, hn2.to(DEV), sel, cnt, off, 4, z_out=True)
+    assert out["z"].cpu()[0, :4].tolist() == tv["z"]
+    assert out["top_ids"].cpu()[0].tolist() == tv["top_ids"]
+
+
+# ------------------------------------------------------------------ exact regime: bit-exact
+
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+@pytest.mark.parametrize("shared", [False, True])
+def test_exact_regime_pipeline(dtype, shared):
+    Dy = _dyn()
+    V, d, M, h_r, B = 5003, 256, 24, 16, 3   # ragged V (prime), several tiles, ragged clusters
+    W, rt, tau, part, c, r = _setup(V, d, M, h_r, dtype, "exact")
+    Wo = Rows(W)
+    ro = _oracle_router(rt)
+    k_t = 8
+    st = Dy.DraftStep(c, r, B, k_t, shared=shared, z_out=True)
+    for t in range(4):
+        hp, e, hn = S.step_inputs(B, d, t, dtype, "exact", h_r=h_r)
+        st(hp.to(DEV), e.to(DEV), hn.to(DEV), t=t, k_max=8, k_min=2)
+        torch.cuda.synchronize()
+        ref = O.draft_step(part, ro, Wo, f64(hp), f64(e), f64(hn), t, 8, 2, k_t, shared=shared)
+        scores = st.scores.cpu().numpy()
+        for b in range(B):
+            assert np.array_equal(scores[b], ref[b]["scores"].astype(np.float32)), "scores not bit-exact"
+        rows = 1 if shared else B
+        for b in range(rows):
+            cnt = st.sel_count[b].item()
+            assert st.sel[b, :cnt].cpu().tolist() == ref[b]["sel"].tolist()
+            assert st.sl_offsets[b, :cnt + 1].cpu().tolist() == ref[b]["sl_offsets"].tolist()
+        for b in range(B):
+            n = len(ref[b]["V_S"])
+            z = st.z[b, :n].cpu().numpy()
+            assert np.array_equal(z, ref[b]["z"].astype(np.float32)), "logits not bit-exact"
+            check_topk(st.top_ids[b].cpu().numpy(), st.top_logits[b].cpu().numpy(), st.top_logp[b].cpu().numpy(),
+                       st.lse[b].item(), ref[b]["z"], ref[b]["V_S"], k_t, torch.float32, exact=True)
+
+
+def test_exact_ties_injected():
+    """Duplicated router rows (score ties -> lower cluster id) and duplicated W rows
+    (logit ties -> lower token id), exact regime."""
+    Dy = _dyn()
+    V, d, M = 2000, 64, 10
+    W = S.lm_head(V, d, 0, "bf16", "exact")
+    hn0 = S.step_inputs(2, d, 0, "bf16", "exact", h_r=0)[2]
+    top = (torch.sign(hn0[0].float()) * 127 * 2.0 ** -6).to(torch.bfloat16)
+    W[7] = top; W[901] = top; W[1500] = top   # the maximal logit for row 0 at t=0, tied 3 ways
+    rt = list(S.router(d, 0, M, 1, "bf16", "exact"))
+    rt[0][6] = rt[0][2]; rt[1][6] = rt[1][2]   # clusters 2 and 6: identical scores
+    tau, part = _partition(V, M)
+    c = Dy.Clusters.from_tau(W.to(DEV), torch.as_tensor(tau, dtype=torch.int32, device=DEV), M)
+    r = Dy.Router(rt[0].to(DEV), rt[1].to(DEV))
+    for t in range(6):
+        hp, e, hn = S.step_inputs(2, d, t, "bf16", "exact", h_r=0)
+        hn = hn.clone()
+        for kk in range(1, M + 1):
+            s = Dy.meta_score(r, hp.to(DEV), e.to(DEV))
+            sel, cnt, off = Dy.select(s, c, kk)
+            ref_s = O.meta_score(f64(rt[0]), f64(rt[1]), None, None, f64(hp), f64(e))
+            for b in range(2):
+                assert sel[b, :kk].cpu().tolist() == O.select(ref_s[b], kk).tolist()
+        sel_all = torch.arange(M, dtype=torch.int32, device=DEV).repeat(2, 1)
+        cnt_all = torch.full((2,), M, dtype=torch.int32, device=DEV)
+        off_all = c.offsets.repeat(2, 1)
+        out = Dy.head_forward(c, hn.to(DEV), sel_all, cnt_all, off_all, 64)
+        dense = O.dense_head(f64(hn), f64(W), 64)
+        for b in range(2):
+            assert out["top_ids"][b].cpu().tolist() == dense[b]["top_ids"].tolist()
+        if t == 0:
+            assert out["top_ids"][0, :3].cpu().tolist() == [7, 901, 1500]
+
+
+# ------------------------------------------------------------------ random regime
+
+@pytest.mark.parametrize("cfg,dtype,B", [("tiny", "bf16", 1), ("tiny", "f32", 1), ("llama2", "bf16", 1),
+                                         ("tiny", "bf16", 8)])
+def test_random_regime_config(cfg, dtype, B):
+    Dy = _dyn()
+    C = S.CONFIGS[cfg]
+    W, rt, tau, part, c, r = _setup(C.V, C.d, C.M, C.h_r, dtype, "random")
+    Wo, ro = Rows(W), _oracle_router(rt)
+    k_t = C.k_t
+    st = Dy.DraftStep(c, r, B, k_t, z_out=True)
+    tdt = S.TORCH_DTYPES[dtype]
+    for t in range(min(C.positions, 4)):
+        hp, e, hn = S.step_inputs(B, C.d, t, dtype)
+        st(hp.to(DEV), e.to(DEV), hn.to(DEV), t=t, k_max=C.k_max, k_min=C.k_min)
+        torch.cuda.synchronize()
+        ref = O.draft_step(part, ro, Wo, f64(hp), f64(e), f64(hn), t, C.k_max, C.k_min, k_t)
+        s_gpu = st.scores.cpu().numpy()
+        for b in range(B):
+            s_ref = ref[b]["scores"]
+            assert np.max(np.abs(s_gpu[b] - s_ref)) < 1e-3 * max(1.0, np.sqrt(np.mean(s_ref ** 2)))
+            cnt = st.sel_count[b].item()
+            sel_gpu = np.array(st.sel[b, :cnt].cpu().tolist())
+            if selection_certified(s_ref, ref[b]["k"]):
+                assert sel_gpu.tolist() == ref[b]["sel"].tolist()
+                rb = ref[b]
+            else:   # conditional parity: feed the GPU's selection back to the oracle
+                rb = O.draft_step(part, ro, Wo, f64(hp[b:b + 1]), f64(e[b:b + 1]), f64(hn[b:b + 1]), t, C.k_max,
+                                  C.k_min, k_t, sel_override=[sel_gpu])[0]
+            assert st.sl_offsets[b, :cnt + 1].cpu().tolist() == rb["sl_offsets"].tolist()
+            n = len(rb["V_S"])
+            z = st.z[b, :n].cpu().numpy().astype(np.float64)
+            if tdt == torch.bfloat16:
+                assert np.max(np.abs(z - rb["z"])) <= 2e-2
+            else:
+                rms = np.sqrt(np.mean(rb["z"] ** 2))
+                assert np.all(np.abs(z - rb["z"]) <= 1e-5 * np.maximum(np.abs(rb["z"]), rms))
+            check_topk(st.top_ids[b].cpu().numpy(), st.top_logits[b].cpu().numpy(), st.top_logp[b].cpu().numpy(),
+                       st.lse[b].item(), rb["z"], rb["V_S"], k_t, tdt)
+
+
+@pytest.mark.parametrize("positions", [(0, 2)])
+def test_llama3_full_size(positions):
+    """BASELINE configs[2] at full size (V=128256, d=4096, M=256, bf16), the bench's launch
+    configuration (two streams, B=1); every logit of V_S compared with the oracle."""
+    Dy = _dyn()
+    C = S.CONFIGS["llama3"]
+    W, rt, tau, part, c, r = _setup(C.V, C.d, C.M, C.h_r, "bf16", "random")
+    Wo, ro = Rows(W), _oracle_router(rt)
+    st = Dy.DraftStep(c, r, 1, C.k_t, z_out=True)
+    for t in positions:
+        hp, e, hn = S.step_inputs(1, C.d, t, "bf16")
+        st(hp.to(DEV), e.to(DEV), hn.to(DEV), t=t, k_max=C.k_max, k_min=C.k_min)
+        torch.cuda.synchronize()
+        ref = O.draft_step(part, ro, Wo, f64(hp), f64(e), f64(hn), t, C.k_max, C.k_min, C.k_t)[0]
+        cnt = st.sel_count[0].item()
+        assert cnt == ref["k"]
+        sel_gpu = st.sel[0, :cnt].cpu().numpy()
+        if not selection_certified(ref["scores"], ref["k"]):
+            ref = O.draft_step(part, ro, Wo, f64(hp), f64(e), f64(hn), t, C.k_max, C.k_min, C.k_t,
+                               sel_override=[sel_gpu])[0]
+        assert sel_gpu.tolist() == ref["sel"].tolist()
+        n = len(ref["V_S"])
+        assert st.sl_offsets[0, cnt].item() == n
+        z = st.z[0, :n].cpu().numpy().astype(np.float64)
+        assert np.max(np.abs(z - ref["z"])) <= 2e-2
+        check_topk(st.top_ids[0].cpu().numpy(), st.top_logits[0].cpu().numpy(), st.top_logp[0].cpu().numpy(),
+                   st.lse[0].item(), ref["z"], ref["V_S"], C.k_t, torch.bfloat16)
+
+
+def test_shared_tree_mode_qwen_shape():
+    """Tree mode (R9): R=10 sibling rows share the union shortlist (Qwen-2.5 head shape)."""
+    Dy = _dyn()
+    C = S.CONFIGS["qwen25"]
+    W, rt, tau, part, c, r = _setup(C.V, C.d, C.M, C.h_r, "bf16", "random")
+    Wo, ro = Rows(W), _oracle_router(rt)
+    st = Dy.DraftStep(c, r, C.B, C.k_t, shared=True, z_out=True)
+    t = 2
+    hp, e, hn = S.step_inputs(C.B, C.d, t, "bf16", sibling_eps=0.1)
+    st(hp.to(DEV), e.to(DEV), hn.to(DEV), t=t, k_max=C.k_max, k_min=C.k_min)
+    torch.cuda.synchronize()
+    cnt = st.sel_count[0].item()
+    sel_gpu = st.sel[0, :cnt].cpu().numpy()
+    ref = O.draft_step(part, ro, Wo, f64(hp), f64(e), f64(hn), t, C.k_max, C.k_min, C.k_t, shared=True,
+                       sel_override=[sel_gpu] * C.B)
+    scores_ref = ref[0]["scores"]
+    ok = all(selection_certified(O.meta_score(*ro, f64(hp), f64(e))[b], ref[0]["k"]) for b in range(C.B))
+    if ok:
+        assert sel_gpu.tolist() == O.select_shared(O.meta_score(*ro, f64(hp), f64(e)), ref[0]["k"]).tolist()
+    for b in range(C.B):
+        n = len(ref[b]["V_S"])
+        z = st.z[b, :n].cpu().numpy().astype(np.float64)
+        assert np.max(np.abs(z - ref[b]["z"])) <= 2e-2
+        check_topk(st.top_ids[b].cpu().numpy(), st.top_logits[b].cpu().numpy(), st.top_logp[b].cpu().numpy(),
+                   st.lse[b].item(), ref[b]["z"], ref[b]["V_S"], C.k_t, torch.bfloat16)
+    del scores_ref
+
+
+# ------------------------------------------------------------------ invariants / edge cases
+
+def test_k_equals_M_is_dense():
+    Dy = _dyn()
+    V, d, M = 7001, 512, 16
+    W, rt, tau, part, c, r = _setup(V, d, M, 8, "bf16", "random")
+    hn = S.hidden(2, d, 77, "bf16")
+    sel = torch.arange(M, dtype=torch.int32, device=DEV).repeat(2, 1)
+    cnt = torch.full((2,), M, dtype=torch.int32, device=DEV)
+    off = c.offsets.repeat(2, 1)
+    out = Dy.head_forward(c, hn.to(DEV), sel, cnt, off, 16, z_out=True)
+    dense = O.dense_head(f64(hn), f64(W), 16)
+    perm = c.perm.cpu().numpy()
+    for b in range(2):
+        z = out["z"][b].cpu().numpy().astype(np.float64)
+        assert np.max(np.abs(z - dense[b]["z"][perm])) <= 2e-2     # shortlist logits == dense logits at ids
+        assert out["top_ids"][b, 0].item() == dense[b]["top_ids"][0]
+        assert abs(out["lse"][b].item() - dense[b]["lse"]) <= 2e-2
+
+
+def test_edge_cases_small_clusters_padding_and_singletons():
+    Dy = _dyn()
+    V, d, M = 40, 8, 20
+    W = S.lm_head(V, d, 3, "f32", "exact")
+    tau = np.arange(V) % M
+    tau[0] = 5                                    # cluster 0 = {20}, size 1 ... sizes 1..3
+    part_perm, part_off = O.layout(tau, M)
+    c = Dy.Clusters.from_tau(W.to(DEV), torch.as_tensor(tau, dtype=torch.int32, device=DEV), M)
+    assert c.min_size == 1
+    hn = S.hidden(1, d, 5, "f32", "exact")
+    for m in range(M):
+        sel = torch.tensor([[m] + [0] * (M - 1)], dtype=torch.int32, device=DEV)
+        cnt = torch.tensor([1], dtype=torch.int32, device=DEV)
+        off = torch.zeros((1, M + 1), dtype=torch.int32, device=DEV)
+        size = int(part_off[m + 1] - part_off[m])
+        off[0, 1] = size
+        out = Dy.head_forward(c, hn.to(DEV), sel, cnt, off, 5, z_out=True)
+        V_S = O.shortlist([m], part_perm, part_off)
+        z = O.head(f64(hn)[0], f64(W), V_S)[0]
+        check_topk(out["top_ids"][0].cpu().numpy(), out["top_logits"][0].cpu().numpy(),
+                   out["top_logp"][0].cpu().numpy(), out["lse"][0].item(), z, V_S, 5, torch.float32, exact=True)
+        if size == 1:
+            assert out["top_logp"][0, 0].item() == 0.0          # |V_S| = 1 => p = 1
+
+
+def test_single_cluster_M1_and_d8():
+    Dy = _dyn()
+    V, d = 333, 8
+    W = S.lm_head(V, d, 4, "bf16", "random")
+    c = Dy.Clusters.from_tau(W.to(DEV), torch.zeros(V, dtype=torch.int32, device=DEV), 1)
+    hn = S.hidden(1, d, 9, "bf16")
+    sel, cnt, off = Dy.select(torch.zeros((1, 1), device=DEV), c, 1)
+    out = Dy.head_forward(c, hn.to(DEV), sel, cnt, off, 64, z_out=True)
+    dense = O.dense_head(f64(hn), f64(W), 64)[0]
+    assert out["top_ids"][0].cpu().tolist()[:3] == dense["top_ids"][:3].tolist()
+
+
+def test_determinism_bytes():
+    Dy = _dyn()
+    C = S.CONFIGS["tiny"]
+    W, rt, tau, part, c, r = _setup(C.V, C.d, C.M, C.h_r, "bf16", "random")
+    hp, e, hn = S.step_inputs(4, C.d, 0, "bf16")
+    outs = []
+    for _ in range(2):
+        st = Dy.DraftStep(c, r, 4, 16, z_out=True)
+        st(hp.to(DEV), e.to(DEV), hn.to(DEV), t=0, k_max=8, k_min=8)
+        torch.cuda.synchronize()
+        outs.append({k: v.clone() for k, v in st.outputs().items() if v is not None})
+    for k in outs[0]:
+        assert torch.equal(outs[0][k].view(torch.uint8), outs[1][k].view(torch.uint8)), k
+
+
+def test_error_codes():
+    Dy = _dyn()
+    V, d, M = 100, 16, 4
+    W = S.lm_head(V, d, 0, "bf16").to(DEV)
+    tau = torch.as_tensor(np.arange(V) % M, dtype=torch.int32, device=DEV)
+    c = Dy.Clusters.from_tau(W, tau, M)
+    r = Dy.Router(*[x.to(DEV) for x in S.router(d, 4, M, 1, "bf16")])
+    s = torch.zeros((1, M), device=DEV)
+    with pytest.raises(Dy.DynaspecError) as ei:
+        Dy.select(s, c, M + 1)
+    assert ei.value.name == "DS_ERR_INVALID_BUDGET"
+    with pytest.raises(Dy.DynaspecError) as ei:
+        Dy.select(s, c, 0)
+    assert ei.value.name == "DS_ERR_INVALID_BUDGET"
+    sel, cnt, off = Dy.select(s, c, 1)
+    with pytest.raises(Dy.DynaspecError) as ei:
+        Dy.head_forward(c, torch.zeros((1, d), dtype=torch.bfloat16, device=DEV), sel, cnt, off, 65)
+    assert ei.value.name == "DS_ERR_INVALID_BUDGET"
+    bad = torch.full((V,), M, dtype=torch.int32, device=DEV)
+    with pytest.raises(Dy.DynaspecError) as ei:
+        Dy.Clusters.from_tau(W, bad, M)
+    assert ei.value.name == "DS_ERR_INVALID_CLUSTER_ID"
+    gap = torch.zeros(V, dtype=torch.int32, device=DEV)
+    with pytest.raises(Dy.DynaspecError) as ei:
+        Dy.Clusters.from_tau(W, gap, M)
+    assert ei.value.name == "DS_ERR_EMPTY_SHORTLIST"
+    st = Dy.DraftStep(c, r, 1, 8)
+    z = torch.zeros((1, d), dtype=torch.bfloat16, device=DEV)
+    with pytest.raises(Dy.DynaspecError) as ei:
+        st(z, z, z, t=0, k_max=M + 1, k_min=1)
+    assert ei.value.name == "DS_ERR_INVALID_BUDGET"
+    with pytest.raises(Dy.DynaspecError) as ei:   # k_t > k * min_size
+        Dy.DraftStep(c, r, 1, 64)(z, z, z, t=0, k_max=1, k_min=1)
+    assert ei.value.name == "DS_ERR_INVALID_BUDGET"
