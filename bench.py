@@ -45,6 +45,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--profile", action="store_true", help="timed steps only (for ncu): no dense/e2e/cpu legs")
     return ap.parse_args()
 
 
@@ -369,9 +370,13 @@ def run_ours(args, ws, rank, local):
     head_share = float(hm[good].sum() / total_ms) if good.any() else None
 
     # ---- dense comparator (untimed above): full-V head + log-softmax + top-k_t
-    dense = dense_baseline(D, clusters, inputs, B, C, dev, flush)
     dyn_us_per_pos = 1e3 * ms_per_step / C.positions
-    e2e = e2e_run(D, steppers, clusters, router, C, B, args, dev, flush, ws)
+    if args.profile:
+        dense, e2e = {"best_us": float("nan")}, None
+        args.no_cpu_baseline = True
+    else:
+        dense = dense_baseline(D, clusters, inputs, B, C, dev, flush)
+        e2e = e2e_run(D, steppers, clusters, router, C, B, args, dev, flush, ws)
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:

@@ -262,12 +262,16 @@ ds_status dynaspec_draft_step(const ds_clusters* c, const ds_router* r, const vo
     if (cudaEventRecord((cudaEvent_t)ev_join, sm) != cudaSuccess) return DS_ERR_CUDA;
     if (cudaStreamWaitEvent(sd, (cudaEvent_t)ev_join, 0) != cudaSuccess) return DS_ERR_CUDA;
   }
-  if (head_begin && cudaEventRecord((cudaEvent_t)head_begin, sd) != cudaSuccess) return DS_ERR_CUDA;
+  // measurement events: recorded as real event nodes when the stream is being captured into a graph
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(sd, &cap);
+  const unsigned evflags = cap == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : cudaEventRecordDefault;
+  if (head_begin && cudaEventRecordWithFlags((cudaEvent_t)head_begin, sd, evflags) != cudaSuccess) return DS_ERR_CUDA;
   err = launch_head(c, p, h_new, B, out->sel, out->sel_count, out->sl_offsets, shared ? 1 : 0, k_t, ms, out->top_ids,
                     out->top_logits, out->top_logp, out->lse, out->z_out, out->z_stride,
                     reinterpret_cast<float*>(w8 + L.head), counters, sd, !two_streams && head_begin == nullptr);
   if (err != cudaSuccess) return DS_ERR_CUDA;
-  if (head_end && cudaEventRecord((cudaEvent_t)head_end, sd) != cudaSuccess) return DS_ERR_CUDA;
+  if (head_end && cudaEventRecordWithFlags((cudaEvent_t)head_end, sd, evflags) != cudaSuccess) return DS_ERR_CUDA;
   return DS_OK;
 }
 

@@ -294,10 +294,10 @@ class DraftStep:
         M = clusters.M
         rows = 1 if shared else B
         dev = device
-        self.scores = torch.empty((B, M), dtype=torch.float32, device=dev)
-        self.sel = torch.empty((rows, M), dtype=torch.int32, device=dev)
-        self.sel_count = torch.empty(rows, dtype=torch.int32, device=dev)
-        self.sl_offsets = torch.empty((rows, M + 1), dtype=torch.int32, device=dev)
+        self.scores = torch.zeros((B, M), dtype=torch.float32, device=dev)
+        self.sel = torch.zeros((rows, M), dtype=torch.int32, device=dev)
+        self.sel_count = torch.zeros(rows, dtype=torch.int32, device=dev)
+        self.sl_offsets = torch.zeros((rows, M + 1), dtype=torch.int32, device=dev)
         self.top_ids = torch.empty((B, k_t), dtype=torch.int32, device=dev)
         self.top_logits = torch.empty((B, k_t), dtype=torch.float32, device=dev)
         self.top_logp = torch.empty((B, k_t), dtype=torch.float32, device=dev)
