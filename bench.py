@@ -269,8 +269,9 @@ def run_ours(args, ws, rank, local):
     inputs = [[tuple(x.to(dev) for x in S.step_inputs(B, C.d, 64 * t + i, args.dtype, sibling_eps=0.1 if C.shared
                                                       else None, base_seed=1000 + 977 * rank))
                for t in range(C.positions)] for i in range(pool)]
-    steppers = [D.DraftStep(clusters, router, B, C.k_t, shared=C.shared, two_streams=True, device=dev)
+    steppers = [D.DraftStep(clusters, router, B, C.k_t, shared=C.shared, two_streams=False, device=dev)
                 for _ in range(C.positions)]
+    fused = steppers[0].launches == 1
     kb = [budget_of(t, C) for t in range(C.positions)]
     flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
     head_ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
@@ -356,7 +357,10 @@ def run_ours(args, ws, rank, local):
             n_rows = sizes_by_pool[j][t]
             vs = sum(n_rows)
             vs_sizes.append(vs / len(n_rows))
-            head_bytes.append(vs * C.d * bw + 4 * vs + B * C.d * bw + B * (C.k_t * 12 + 4))
+            hb_ = vs * C.d * bw + 4 * vs + B * C.d * bw + B * (C.k_t * 12 + 4)
+            if fused:  # the fused kernel also streams the router: W1, W2, x = [h_prev || e]
+                hb_ += (max(C.h_r, 0) or C.M) * 2 * C.d * bw + C.M * C.h_r * bw + B * 2 * C.d * bw + B * C.M * 4
+            head_bytes.append(hb_)
     total_ms = sum(step_ms)
     tot_ms_max = max_over_ranks(total_ms, ws)
     rows_all = B * C.positions * args.steps * ws
@@ -377,6 +381,7 @@ def run_ours(args, ws, rank, local):
     else:
         dense = dense_baseline(D, clusters, inputs, B, C, dev, flush)
         e2e = e2e_run(D, steppers, clusters, router, C, B, args, dev, flush, ws)
+        two = two_stream_run(D, clusters, router, inputs, C, B, args, dev, flush)
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
@@ -404,10 +409,13 @@ def run_ours(args, ws, rank, local):
                        "cuda_graph": use_graph, **part_info,
                        "dense_us_per_draft_step": dense["best_us"], "dense_detail": dense,
                        "speedup_vs_dense": dense["best_us"] / dyn_us_per_pos if dyn_us_per_pos else None,
-                       "head_share_of_step": head_share},
+                       "head_share_of_step": head_share,
+                       "step_mode": "fused one-launch step" if fused else "two kernels per step",
+                       "two_stream_mode": None if args.profile else two},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak if achieved else None,
-                         "traffic": committed_traffic(C.name, B), "kernel": "ds::head_kernel (S5+S6)",
+                         "traffic": committed_traffic(C.name, B), "kernel": ("ds::step_kernel (router + select + gathered head + epilogue, one launch)" if fused
+                                    else "ds::head_kernel (S5+S6)"),
                          "peak_source": peak_src, "frac_of_8TBps": achieved / 8000.0 if achieved else None},
             "cpu_baseline": cpu,
             "e2e": e2e,
@@ -454,6 +462,38 @@ def dense_baseline(D, clusters, inputs, B, C, dev, flush, reps=20):
     res["torch_cublas_us"] = 1e3 * statistics.median(times)
     res["best_us"] = min(res["ours_k_eq_M_us"], res["torch_cublas_us"])
     return res
+
+
+def two_stream_run(D, clusters, router, inputs, C, B, args, dev, flush):
+    """The paper's stream layout (router + select on S_m, joined before the head on S_d), one CUDA
+    graph per cycle, same inputs and cold-L2 protocol: us per draft step (serialized, no core)."""
+    st = [D.DraftStep(clusters, router, B, C.k_t, shared=C.shared, two_streams=True, device=dev)
+          for _ in range(C.positions)]
+
+    def cyc(i):
+        for t in range(C.positions):
+            st[t](*inputs[i][t], t, C.k_max, C.k_min)
+
+    s = torch.cuda.Stream(device=dev)
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        cyc(0)
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        cyc(0)
+    times = []
+    for i in range(args.steps + 3):
+        flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        g.replay()
+        b.record()
+        torch.cuda.synchronize()
+        if i >= 3:
+            times.append(a.elapsed_time(b))
+    return {"us_per_draft_step": 1e3 * statistics.mean(times) / C.positions, "launches_per_step": st[0].launches}
 
 
 def e2e_run(D, steppers, clusters, router, C, B, args, dev, flush, ws, reps=None):

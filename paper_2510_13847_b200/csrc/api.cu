@@ -42,6 +42,7 @@ static ds_status check_router(const ds_router* r) {
   if (r->M < 1 || r->M > kMaxMHost) return DS_ERR_INVALID_CLUSTER_COUNT;
   if (r->h_r < 0 || r->h_r > kMaxMHost) return DS_ERR_SHAPE;
   if (r->h_r > 0 && (!r->W2 || !r->b2)) return DS_ERR_SHAPE;
+  if (r->h_r % 8 != 0) return DS_ERR_UNSUPPORTED;
   return DS_OK;
 }
 
@@ -204,14 +205,15 @@ size_t dynaspec_draft_step_ws(const ds_clusters* c, const ds_router* r, int32_t 
   if (!head_plan(c, B, k_t, 0, &p)) return 0;
   const size_t meta = meta_plan(r, B).part_bytes;
   const size_t scores = (size_t)B * r->M * sizeof(float);
-  return ws_layout(align_up(meta, 256) + align_up(scores, 256), p.part_bytes).total;
+  return std::max(ws_layout(align_up(meta, 256) + align_up(scores, 256), p.part_bytes).total,
+                  step_ws_bytes(c, r, B, k_t));
 }
 
 int32_t dynaspec_draft_step_launches(const ds_clusters* c, const ds_router* r, int32_t B, int32_t k_t,
                                      int32_t shared) {
   HeadPlan p;
   if (!c || !r || !head_plan(c, B, k_t, 0, &p)) return 0;
-  (void)shared;
+  if (step_supported(c, r, B, k_t, shared, 0)) return 1;  // fused single-stream step
   return 2 + p.launches;  // meta layer 1, meta layer 2 (+select), head chunks
 }
 
@@ -236,6 +238,23 @@ ds_status dynaspec_draft_step(const ds_clusters* c, const ds_router* r, const vo
   if (out->z_out && out->z_stride < ms) return DS_ERR_SHAPE;
   const bool two_streams = s_meta != nullptr && s_meta != s_draft;
   if (two_streams && (!ev_fork || !ev_join)) return DS_ERR_SHAPE;
+  const bool fused = !two_streams && step_supported(c, r, B, k_t, shared, ms);
+  if (fused) {  // one persistent launch: router + select + head + epilogue (step.cu)
+    const size_t need = step_ws_bytes(c, r, B, k_t);
+    if (!ws || need == 0 || ws_bytes < need) return DS_ERR_WORKSPACE;
+    cudaStream_t sd = (cudaStream_t)s_draft;
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(sd, &cap);
+    const unsigned evflags = cap == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : cudaEventRecordDefault;
+    if (head_begin && cudaEventRecordWithFlags((cudaEvent_t)head_begin, sd, evflags) != cudaSuccess)
+      return DS_ERR_CUDA;
+    cudaError_t err = launch_step(c, r, h_prev, e, h_new, B, k, k_t, shared ? 1 : 0, ms, out->scores, out->sel,
+                                  out->sel_count, out->sl_offsets, out->top_ids, out->top_logits, out->top_logp,
+                                  out->lse, out->z_out, out->z_stride, ws, sd, head_begin == nullptr);
+    if (err != cudaSuccess) return DS_ERR_CUDA;
+    if (head_end && cudaEventRecordWithFlags((cudaEvent_t)head_end, sd, evflags) != cudaSuccess) return DS_ERR_CUDA;
+    return DS_OK;
+  }
   HeadPlan p;
   if (!head_plan(c, B, k_t, ms, &p)) return DS_ERR_UNSUPPORTED;
   HeadPlan pmax;

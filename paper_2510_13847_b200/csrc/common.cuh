@@ -119,7 +119,50 @@ __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
 }
 __device__ __forceinline__ float ld_cg_f32(const float* p) { return __ldcg(p); }
 
-// ------------------------------------------------------------------ block scan (int), blockDim = 256
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ unsigned ld_volatile_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.volatile.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+// Spin (one thread) until *ctr >= target, then acquire.
+__device__ __forceinline__ void spin_until_geq(const unsigned* ctr, unsigned target) {
+  while (ld_volatile_u32(ctr) < target) {
+    __nanosleep(20);
+  }
+  __threadfence();
+}
+
+// Exclusive scan of one int per thread over the whole block (any blockDim multiple of 32, <= 1024).
+__device__ __forceinline__ int block_excl_scan_dyn(int v, int* scratch /* >= 33 ints */, int& total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) scratch[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    int w = (lane < nw) ? scratch[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int y = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += y;
+    }
+    if (lane < nw) scratch[lane] = w;
+  }
+  __syncthreads();
+  const int base = warp > 0 ? scratch[warp - 1] : 0;
+  total = scratch[nw - 1];
+  __syncthreads();
+  return base + x - v;
+}
+
+// ------------------------------------------------------------------ block scan (int), blockDim = NT
 // Exclusive scan of one value per thread; returns the exclusive prefix, writes the total.
 template <int NT>
 __device__ __forceinline__ int block_excl_scan(int v, int* scratch /* >= NT/32 + 1 ints */, int& total) {

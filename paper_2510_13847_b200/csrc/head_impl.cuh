@@ -1,0 +1,413 @@
+// head_impl.cuh — building blocks of the gathered head (S5) + fused epilogue (S6), shared by the
+// standalone head kernel (head.cu) and the fused one-launch draft-step kernel (step.cu).
+//
+// Per CTA: a ring of `stages` shared-memory slots (16 KB each), filled by ONE producer lane with
+// TMA 1D bulk copies of contiguous W_perm row runs (a selected cluster is one contiguous block,
+// R12 layout) and drained by one consumer warp per slot, which dots two staged rows at a time with
+// h_new (staged once in shared memory) in fp32.  Logits stay on chip; each CTA emits a
+// (max, sum exp, top-k_t) partial per row and the last CTA merges the partials in CTA order.
+#pragma once
+#include <float.h>
+#include <limits.h>
+
+#include "common.cuh"
+
+namespace ds {
+
+constexpr int kMaxStages = 12;
+constexpr int kStageTarget = 16384;          // bytes per ring slot (rounded to whole rows)
+constexpr int kRingMax = kMaxStages * kStageTarget;
+constexpr int kMaxGroups = 64;               // rows per launch
+constexpr int kStepExtra = 4096 * 2 + 1024 + 256;  // fused step: a1 + scores + flags + scan scratch
+
+struct HeadArgs {
+  const void* W;             // W_perm [V][d]
+  const int32_t* perm;       // [V]
+  const int32_t* offsets;    // [M+1]
+  const int32_t* sel;        // [groups][M]
+  const int32_t* sel_count;  // [groups]
+  const int32_t* sl_off;     // [groups][M+1]
+  const void* h;             // [nrows][d]
+  int32_t M, nrows, d, k_t, shared, lcap, pdl;
+  int32_t stages, stage_bytes, stage_rows;
+  int64_t max_shortlist;
+  int32_t* top_ids;
+  float* top_logits;
+  float* top_logp;
+  float* lse;
+  float* z_out;
+  int64_t z_stride;
+  float* part;               // [G][nrows][2 + 2 k_t]
+  unsigned* counter;         // [0] = merge ticket (the fused step also uses [1], [2])
+};
+
+void fill_head_args(HeadArgs& a, const ds_clusters* c, const HeadPlan& p, const void* h_new, int r0, int nr,
+                    const int32_t* sel, const int32_t* sel_count, const int32_t* sl_offsets, int shared, int k_t,
+                    int64_t max_shortlist, int32_t* top_ids, float* top_logits, float* top_logp, float* lse,
+                    float* z_out, int64_t z_stride, float* part, unsigned* counter, bool pdl);
+
+struct HeadSmem {
+  uint32_t ring, bars, info, misc, sega, segn, h, zl, zid, extra, total;
+};
+
+__host__ __device__ inline HeadSmem head_smem(int stages, int stage_bytes, int rows, int d, int esz, int lcap,
+                                              int extra) {
+  HeadSmem L;
+  uint32_t o = 0;
+  L.ring = o;
+  o += (uint32_t)stages * stage_bytes;
+  L.bars = o;
+  o += (2 * kMaxStages + 2) * 8;
+  L.info = o;
+  o += kMaxStages * 16;
+  L.misc = o;
+  o += 16 * 4;
+  L.sega = o;
+  o += kMaxGroups * 8;
+  L.segn = o;
+  o += kMaxGroups * 4;
+  o = (o + 127u) & ~127u;
+  L.h = o;
+  o += (uint32_t)rows * d * esz;
+  o = (o + 15u) & ~15u;
+  L.zl = o;
+  o += (uint32_t)rows * lcap * 4;
+  L.zid = o;
+  o += (uint32_t)rows * lcap * 4;
+  o = (o + 15u) & ~15u;
+  L.extra = o;
+  o += extra;
+  L.total = o;
+  return L;
+}
+
+struct HeadCtx {
+  uint8_t* ring;
+  uint64_t* full;
+  uint64_t* empty;
+  int4* info;
+  int* misc;
+  long long* sega;
+  int* segn;
+  void* hs;
+  float* zl;
+  int* zid;
+  uint8_t* extra;
+};
+
+__device__ __forceinline__ HeadCtx head_ctx(uint8_t* smem, const HeadSmem& L) {
+  HeadCtx c;
+  c.ring = smem + L.ring;
+  c.full = reinterpret_cast<uint64_t*>(smem + L.bars);
+  c.empty = c.full + kMaxStages;
+  c.info = reinterpret_cast<int4*>(smem + L.info);
+  c.misc = reinterpret_cast<int*>(smem + L.misc);
+  c.sega = reinterpret_cast<long long*>(smem + L.sega);
+  c.segn = reinterpret_cast<int*>(smem + L.segn);
+  c.hs = smem + L.h;
+  c.zl = reinterpret_cast<float*>(smem + L.zl);
+  c.zid = reinterpret_cast<int*>(smem + L.zid);
+  c.extra = smem + L.extra;
+  return c;
+}
+
+__device__ __forceinline__ void head_init_barriers(const HeadCtx& c, int stages) {
+  for (int s = 0; s < stages; ++s) {
+    mbar_init(&c.full[s], 1);
+    mbar_init(&c.empty[s], 1);
+  }
+  fence_mbar_init();
+}
+
+__device__ __forceinline__ long long shortlist_len(const HeadArgs& a, int gi) {
+  const int cnt = __ldcg(a.sel_count + gi);
+  if (cnt < 1 || cnt > a.M) return -1;
+  const long long N = __ldcg(a.sl_off + (size_t)gi * (a.M + 1) + cnt);
+  return (N >= 1 && N <= a.max_shortlist) ? N : -1;
+}
+
+// Segment [N*g/G, N*(g+1)/G) of each group's virtual shortlist (even split by rows).
+__device__ __forceinline__ void head_segments(const HeadArgs& a, const HeadCtx& c) {
+  const int G = gridDim.x, g = blockIdx.x;
+  const int ngroups = a.shared ? 1 : a.nrows;
+  for (int gi = threadIdx.x; gi < ngroups; gi += blockDim.x) {
+    const long long N = shortlist_len(a, gi);
+    if (N < 0) {
+      c.sega[gi] = 0;
+      c.segn[gi] = -1;
+    } else {
+      const long long s0 = N * g / G, s1 = N * (g + 1) / G;
+      c.sega[gi] = s0;
+      c.segn[gi] = (int)(s1 - s0);
+    }
+  }
+}
+
+// Producer (one lane): stream every segment as runs of whole rows, slot it % stages.
+template <typename T>
+__device__ void head_produce(const HeadArgs& a, const HeadCtx& c) {
+  const uint64_t pol = policy_evict_first();
+  const uint32_t rowbytes = (uint32_t)a.d * (uint32_t)sizeof(T);
+  const uint8_t* W = static_cast<const uint8_t*>(a.W);
+  const int ngroups = a.shared ? 1 : a.nrows;
+  const uint32_t S = (uint32_t)a.stages;
+  uint32_t it = 0;
+  for (int gi = 0; gi < ngroups; ++gi) {
+    const int nseg = c.segn[gi];
+    if (nseg <= 0) continue;
+    const long long s0 = c.sega[gi], s1 = s0 + nseg;
+    const int32_t* so = a.sl_off + (size_t)gi * (a.M + 1);
+    const int32_t* sl = a.sel + (size_t)gi * a.M;
+    int i = 0;
+    while (__ldcg(so + i + 1) <= s0) ++i;  // cluster holding virtual position s0
+    long long pos = s0;
+    long long cl_beg = __ldcg(so + i), cl_end = __ldcg(so + i + 1);
+    long long base = __ldg(a.offsets + __ldcg(sl + i));
+    while (pos < s1) {
+      const long long lim = cl_end < s1 ? cl_end : s1;
+      const int n = (int)min((long long)a.stage_rows, lim - pos);
+      const long long wrow = base + (pos - cl_beg);
+      const uint32_t s = it % S;
+      mbar_wait(&c.empty[s], ((it / S) & 1u) ^ 1u);
+      c.info[s] = make_int4(gi, (int)(pos - s0), n, (int)wrow);
+      mbar_arrive_expect_tx(&c.full[s], (uint32_t)n * rowbytes);
+      bulk_g2s(c.ring + (size_t)s * a.stage_bytes, W + (size_t)wrow * rowbytes, (uint32_t)n * rowbytes, &c.full[s],
+               pol);
+      ++it;
+      pos += n;
+      if (pos == cl_end && pos < s1) {
+        ++i;
+        cl_beg = cl_end;
+        cl_end = __ldcg(so + i + 1);
+        base = __ldg(a.offsets + __ldcg(sl + i));
+      }
+    }
+  }
+  for (uint32_t j = 0; j < S; ++j, ++it) {  // one end-of-stream marker per slot
+    const uint32_t s = it % S;
+    mbar_wait(&c.empty[s], ((it / S) & 1u) ^ 1u);
+    c.info[s] = make_int4(-1, 0, -1, 0);
+    mbar_arrive(&c.full[s]);
+  }
+}
+
+// Two staged rows at once against one h row: 4 independent fp32 FMA chains per lane, then warp
+// trees (R18: lane-parallel partials).  `two == false` duplicates row 0 (result ignored).
+template <typename T>
+__device__ __forceinline__ void dot2(const T* __restrict__ w0, const T* __restrict__ w1, const T* __restrict__ h,
+                                     int d, int lane, float& z0, float& z1) {
+  constexpr int E = Elem<T>::kPer16B;
+  float a0 = 0.f, a1 = 0.f, b0 = 0.f, b1 = 0.f;
+#pragma unroll 2
+  for (int c = lane * E; c < d; c += 32 * E) {
+    const uint4 hv = *reinterpret_cast<const uint4*>(h + c);
+    const uint4 xv = *reinterpret_cast<const uint4*>(w0 + c);
+    const uint4 yv = *reinterpret_cast<const uint4*>(w1 + c);
+    float hf[E], xf[E], yf[E];
+    widen16(hv, hf, h);
+    widen16(xv, xf, h);
+    widen16(yv, yf, h);
+#pragma unroll
+    for (int j = 0; j < E; j += 2) {
+      a0 = fmaf(xf[j], hf[j], a0);
+      b0 = fmaf(yf[j], hf[j], b0);
+      a1 = fmaf(xf[j + 1], hf[j + 1], a1);
+      b1 = fmaf(yf[j + 1], hf[j + 1], b1);
+    }
+  }
+  z0 = warp_sum(a0 + a1) + 0.0f;  // + 0.0f: -0 -> +0 (R23)
+  z1 = warp_sum(b0 + b1) + 0.0f;
+}
+
+// Consumer warp `w` owns ring slot `w`.
+template <typename T>
+__device__ void head_consume(const HeadArgs& a, const HeadCtx& c, int w, int lane) {
+  const T* hs = static_cast<const T*>(c.hs);
+  for (uint32_t k = 0;; ++k) {
+    mbar_wait(&c.full[w], k & 1u);
+    const int4 inf = c.info[w];
+    if (inf.z < 0) break;
+    const T* st = reinterpret_cast<const T*>(c.ring + (size_t)w * a.stage_bytes);
+    const int gi = inf.x;
+    const int r_lo = a.shared ? 0 : gi, r_hi = a.shared ? a.nrows : gi + 1;
+    const long long zbase = c.sega[gi] + inf.y;
+    for (int rr = 0; rr < inf.z; rr += 2) {
+      const bool two = rr + 1 < inf.z;
+      const T* w0 = st + (size_t)rr * a.d;
+      const T* w1 = two ? w0 + a.d : w0;
+      int tok0 = 0, tok1 = 0;
+      if (lane == 0) {
+        tok0 = __ldg(a.perm + inf.w + rr);
+        tok1 = two ? __ldg(a.perm + inf.w + rr + 1) : 0;
+      }
+      for (int r = r_lo; r < r_hi; ++r) {
+        float z0, z1;
+        dot2<T>(w0, w1, hs + (size_t)r * a.d, a.d, lane, z0, z1);
+        if (lane == 0) {
+          const int li = inf.y + rr;
+          c.zl[r * a.lcap + li] = z0;
+          c.zid[r * a.lcap + li] = tok0;
+          if (a.z_out) a.z_out[(size_t)r * a.z_stride + zbase + rr] = z0;
+          if (two) {
+            c.zl[r * a.lcap + li + 1] = z1;
+            c.zid[r * a.lcap + li + 1] = tok1;
+            if (a.z_out) a.z_out[(size_t)r * a.z_stride + zbase + rr + 1] = z1;
+          }
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&c.empty[w]);
+  }
+}
+
+// Stage h_new rows into shared memory (16-byte vectors).
+__device__ __forceinline__ void head_load_h(const HeadArgs& a, const HeadCtx& c, int esz, int t0, int nt) {
+  const size_t nvec = (size_t)a.nrows * a.d * esz / 16;
+  const uint4* src = static_cast<const uint4*>(a.h);
+  uint4* dst = reinterpret_cast<uint4*>(c.hs);
+  for (size_t i = t0; i < nvec; i += nt) dst[i] = src[i];
+}
+
+// Per-CTA partial per row: top-k_t by (logit desc, id asc), max, sum exp(z - max).
+__device__ inline void head_partials(const HeadArgs& a, const HeadCtx& c) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const int rec = 2 + 2 * a.k_t;
+  for (int r = warp; r < a.nrows; r += nw) {
+    const int gi = a.shared ? 0 : r;
+    const int n = c.segn[gi];
+    float* P = a.part + ((size_t)blockIdx.x * a.nrows + r) * rec;
+    const float* zr = c.zl + r * a.lcap;
+    const int* ir = c.zid + r * a.lcap;
+    float pv = INFINITY, mx = -INFINITY;
+    int pid = -1;
+    for (int qq = 0; qq < a.k_t; ++qq) {
+      float bv = -INFINITY;
+      int bid = INT_MAX, aux = 0;
+      for (int j = lane; j < n; j += 32) {
+        const float v = zr[j];
+        const int id = ir[j];
+        if (beats(pv, pid, v, id) && beats(v, id, bv, bid)) {
+          bv = v;
+          bid = id;
+        }
+      }
+      warp_best(bv, bid, aux);
+      if (qq == 0) mx = bv;
+      if (lane == 0) {
+        P[2 + 2 * qq] = bv;
+        P[3 + 2 * qq] = __int_as_float(bid);
+      }
+      pv = bv;
+      pid = bid;
+      if (bv == -INFINITY) {  // exhausted: pad the rest
+        for (int q2 = qq + 1 + lane; q2 < a.k_t; q2 += 32) {
+          P[2 + 2 * q2] = -INFINITY;
+          P[3 + 2 * q2] = __int_as_float(INT_MAX);
+        }
+        break;
+      }
+    }
+    float se = 0.f;
+    for (int j = lane; j < n; j += 32) se += expf(zr[j] - mx);
+    se = warp_sum(se);
+    if (lane == 0) {
+      P[0] = mx;
+      P[1] = se;
+    }
+  }
+}
+
+// Ticket: returns true in the last CTA to finish (all partials visible).
+__device__ __forceinline__ bool head_ticket(const HeadArgs& a, const HeadCtx& c) {
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) c.misc[0] = (atomicAdd(a.counter, 1u) == (unsigned)(gridDim.x - 1)) ? 1 : 0;
+  __syncthreads();
+  const bool last = c.misc[0] != 0;
+  if (last) __threadfence();
+  return last;
+}
+
+// Last CTA: merge the G partials of every row in CTA order -> lse, top ids (remapped), logp.
+__device__ inline void head_merge(const HeadArgs& a, const HeadCtx& c, int ring_bytes) {
+  const int G = gridDim.x;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, nw = blockDim.x >> 5;
+  const int rec = 2 + 2 * a.k_t;
+  const int per_row = G * rec;
+  int batch = ring_bytes / (per_row * 4 + G);
+  batch = batch < 1 ? 1 : (batch > nw ? nw : batch);
+  float* mbuf = reinterpret_cast<float*>(c.ring);
+  uint8_t* ptr_base = c.ring + (size_t)batch * per_row * 4;
+  for (int r0 = 0; r0 < a.nrows; r0 += batch) {
+    const int nb = min(batch, a.nrows - r0);
+    for (int rb = 0; rb < nb; ++rb) {
+      const float* src = a.part + (size_t)(r0 + rb) * rec;
+      float* dst = mbuf + (size_t)rb * per_row;
+      for (int idx = tid; idx < per_row; idx += blockDim.x) {
+        const int gg = idx / rec, f = idx - gg * rec;
+        dst[idx] = __ldcg(src + (size_t)gg * a.nrows * rec + f);
+      }
+    }
+    __syncthreads();
+    if (warp < nb) {
+      const int r = r0 + warp;
+      const float* R = mbuf + (size_t)warp * per_row;
+      uint8_t* ptr = ptr_base + (size_t)warp * G;
+      const bool ok = shortlist_len(a, a.shared ? 0 : r) >= 0;
+      float mx = -INFINITY;
+      for (int gg = lane; gg < G; gg += 32) {
+        mx = fmaxf(mx, R[gg * rec]);
+        ptr[gg] = 0;
+      }
+      mx = warp_max(mx);
+      float S = 0.f;
+      for (int gg = lane; gg < G; gg += 32) {
+        const float m = R[gg * rec];
+        if (m > -INFINITY) S += R[gg * rec + 1] * expf(m - mx);
+      }
+      S = warp_sum(S);
+      const float lse = ok ? mx + logf(S) : __int_as_float(0x7fc00000);
+      __syncwarp();
+      float bv;
+      int bid, bl;
+      auto lane_best = [&]() {
+        bv = -INFINITY;
+        bid = INT_MAX;
+        bl = -1;
+        for (int gg = lane; gg < G; gg += 32) {
+          const int p = ptr[gg];
+          if (p >= a.k_t) continue;
+          const float v = R[gg * rec + 2 + 2 * p];
+          const int id = __float_as_int(R[gg * rec + 3 + 2 * p]);
+          if (beats(v, id, bv, bid)) {
+            bv = v;
+            bid = id;
+            bl = gg;
+          }
+        }
+      };
+      lane_best();
+      for (int qq = 0; qq < a.k_t; ++qq) {
+        float wv = bv;
+        int wid = bid, wl = bl;
+        warp_best(wv, wid, wl);
+        if (lane == 0) {
+          const bool valid = ok && wv > -INFINITY;
+          a.top_ids[(size_t)r * a.k_t + qq] = valid ? wid : -1;
+          a.top_logits[(size_t)r * a.k_t + qq] = valid ? wv : -INFINITY;
+          a.top_logp[(size_t)r * a.k_t + qq] = valid ? wv - lse : -INFINITY;
+        }
+        if (wl >= 0 && (wl & 31) == lane) {
+          ptr[wl] = (uint8_t)(ptr[wl] + 1);
+          lane_best();
+        }
+        __syncwarp();
+      }
+      if (lane == 0) a.lse[r] = lse;
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace ds

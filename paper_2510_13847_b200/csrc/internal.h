@@ -39,16 +39,30 @@ struct HeadPlan {
   int lcap;            // logits capacity per row per CTA
   int rec;             // floats per partial record (2 + 2*k_t)
   int stage_rows;
+  int stages;          // ring slots (= consumer warps)
+  int stage_bytes;
   size_t smem;
   size_t part_bytes;   // workspace bytes for partials
   int launches;        // number of launches for B rows
 };
 bool head_plan(const ds_clusters* c, int B, int k_t, int64_t max_shortlist, HeadPlan* p);
+bool head_plan_ex(const ds_clusters* c, int B, int k_t, int64_t max_shortlist, int extra_smem, int max_rows,
+                  HeadPlan* p);
+int max_smem_optin();
 cudaError_t launch_head(const ds_clusters* c, const HeadPlan& p, const void* h_new, int B, const int32_t* sel,
                         const int32_t* sel_count, const int32_t* sl_offsets, int shared, int k_t,
                         int64_t max_shortlist, int32_t* top_ids, float* top_logits, float* top_logp,
                         float* lse, float* z_out, int64_t z_stride, float* part, unsigned* counter,
                         cudaStream_t st, bool pdl);
+
+// ---- fused one-launch draft step (step.cu): router + select + head + epilogue
+bool step_supported(const ds_clusters* c, const ds_router* r, int B, int k_t, int shared, int64_t max_shortlist);
+size_t step_ws_bytes(const ds_clusters* c, const ds_router* r, int B, int k_t);
+cudaError_t launch_step(const ds_clusters* c, const ds_router* r, const void* h_prev, const void* e,
+                        const void* h_new, int B, int k, int k_t, int shared, int64_t max_shortlist, float* scores,
+                        int32_t* sel, int32_t* sel_count, int32_t* sl_offsets, int32_t* top_ids, float* top_logits,
+                        float* top_logp, float* lse, float* z_out, int64_t z_stride, void* ws, cudaStream_t st,
+                        bool pdl);
 
 // ---- offline partition (build.cu)
 size_t build_ws_bytes(int64_t V, int d, int M);

@@ -16,6 +16,7 @@
 
 #include "common.cuh"
 #include "internal.h"
+#include "select_impl.cuh"
 
 namespace ds {
 
@@ -23,60 +24,13 @@ constexpr int kMetaThreads = 256;
 constexpr int kMetaUnitsPerCTA = kMetaThreads / 32;
 constexpr int kSelThreads = 256;
 
-// ------------------------------------------------------------------ selection (block of 256)
-
-// flags[m] |= rank(m) < k, rank under (score desc, id asc); scores staged in smem `s`.
-__device__ void rank_select(const float* s, int M, int k, uint8_t* flags) {
-  for (int m = threadIdx.x; m < M; m += blockDim.x) {
-    const float key = s[m] + 0.0f;
-    int rank = 0;
-    for (int j = 0; j < M; ++j) {
-      const float o = s[j] + 0.0f;
-      rank += (o > key) || (o == key && j < m);
-    }
-    if (rank < k) flags[m] = 1;
-  }
-}
-
-// Compact flags into ascending ids + exclusive scan of cluster sizes (sl_offsets).
-__device__ void emit_selection(const uint8_t* flags, int M, const int32_t* offsets, int32_t* sel,
-                               int32_t* sel_count, int32_t* sl_off, int* scratch) {
-  // each thread owns up to 4 consecutive cluster ids (M <= 1024)
-  const int per = (M + kSelThreads - 1) / kSelThreads;
-  const int m0 = threadIdx.x * per;
-  int cnt = 0, sz = 0;
-  for (int j = 0; j < per; ++j) {
-    const int m = m0 + j;
-    if (m < M && flags[m]) {
-      ++cnt;
-      sz += offsets[m + 1] - offsets[m];
-    }
-  }
-  int tot_cnt, tot_sz;
-  int pos = block_excl_scan<kSelThreads>(cnt, scratch, tot_cnt);
-  int off = block_excl_scan<kSelThreads>(sz, scratch, tot_sz);
-  for (int j = 0; j < per; ++j) {
-    const int m = m0 + j;
-    if (m < M && flags[m]) {
-      sel[pos] = m;
-      sl_off[pos] = off;
-      ++pos;
-      off += offsets[m + 1] - offsets[m];
-    }
-  }
-  if (threadIdx.x == 0) {
-    *sel_count = tot_cnt;
-    sl_off[tot_cnt] = tot_sz;
-  }
-}
-
 __global__ void __launch_bounds__(kSelThreads) select_kernel(const float* __restrict__ scores, int B, int M,
                                                              const int32_t* __restrict__ offsets, int k,
                                                              const int32_t* __restrict__ k_per_row, int shared,
                                                              int32_t* sel, int32_t* sel_count, int32_t* sl_off) {
-  __shared__ float s[kMaxM];
+  __shared__ __align__(16) float s[kMaxM];
   __shared__ uint8_t flags[kMaxM];
-  __shared__ int scratch[kSelThreads / 32 + 1];
+  __shared__ int scratch[33];
   for (int m = threadIdx.x; m < M; m += blockDim.x) flags[m] = 0;
   const int r_lo = shared ? 0 : blockIdx.x, r_hi = shared ? B : blockIdx.x + 1;
   for (int r = r_lo; r < r_hi; ++r) {
@@ -155,30 +109,17 @@ __global__ void __launch_bounds__(kMetaThreads) meta_l2_kernel(const float* __re
                                                                const int32_t* __restrict__ k_per_row, int shared,
                                                                int32_t* sel, int32_t* sel_count, int32_t* sl_off,
                                                                unsigned* counter, int pdl) {
-  __shared__ float a1[kMaxM];
-  __shared__ float s[kMaxM];
+  __shared__ __align__(16) float a1[kMaxM];
+  __shared__ __align__(16) float s[kMaxM];
   __shared__ uint8_t flags[kMaxM];
-  __shared__ int scratch[kMetaThreads / 32 + 1];
+  __shared__ int scratch[33];
   __shared__ int is_last;
   const int b = blockIdx.x;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (pdl) pdl_wait();
-  // a = ReLU(sum_splits part + b1): fixed split order
-  for (int u = threadIdx.x; u < rows1; u += blockDim.x) {
-    float acc = 0.f;
-    for (int ks = 0; ks < KS; ++ks) acc += part[((size_t)ks * B + b) * rows1 + u];
-    acc += b1[u];
-    a1[u] = h_r > 0 ? fmaxf(acc, 0.f) : acc;
-  }
+  router_hidden(part, KS, B, b, rows1, b1, h_r > 0, a1);
   __syncthreads();
   if (h_r > 0) {
-    for (int m = warp; m < M; m += kMetaThreads / 32) {
-      const T* w = W2 + (size_t)m * h_r;
-      float acc = 0.f;
-      for (int u = lane; u < h_r; u += 32) acc = fmaf(static_cast<float>(w[u]), a1[u], acc);
-      acc = warp_sum(acc) + b2[m];
-      if (lane == 0) s[m] = acc;
-    }
+    router_out<T>(W2, a1, b2, M, h_r, s);
   } else {
     for (int m = threadIdx.x; m < M; m += blockDim.x) s[m] = a1[m];
   }

@@ -289,7 +289,9 @@ class DraftStep:
     """Pre-allocated outputs + workspace + events for repeated dynaspec_draft_step calls
     (graph-capturable: no allocation, no host sync inside __call__)."""
 
-    def __init__(self, clusters, router, B, k_t, shared=False, z_out=False, two_streams=True, device="cuda"):
+    def __init__(self, clusters, router, B, k_t, shared=False, z_out=False, two_streams=False, device="cuda"):
+        """two_streams=False: one fused launch per step (router + select + head + epilogue);
+        two_streams=True: router + select on a side stream S_m joined before the head."""
         self.c, self.r, self.B, self.k_t, self.shared = clusters, router, B, k_t, bool(shared)
         M = clusters.M
         rows = 1 if shared else B

@@ -82,12 +82,14 @@ def test_e2e1_golden_on_gpu():
         assert out["z"].cpu()[0, :kt].tolist() == case["z"]
         assert out["top_ids"].cpu()[0].tolist() == case["top_ids"]
         assert abs(out["lse"].item() - case["lse"]) < 1e-6
-        # draft_step (both streams) reproduces the same step
-        st = Dy.DraftStep(c, r, 1, kt)
-        st(hp.to(DEV), e.to(DEV), hn.to(DEV), t=0, k_max=k, k_min=1)
-        torch.cuda.synchronize()
-        assert st.top_ids.cpu()[0].tolist() == case["top_ids"]
-        assert st.sel.cpu()[0, :k].tolist() == case["sel"]
+        # draft_step (two streams, and the fused one-launch step) reproduces the same step
+        for two in (True, False):
+            st = Dy.DraftStep(c, r, 1, kt, two_streams=two)
+            st(hp.to(DEV), e.to(DEV), hn.to(DEV), t=0, k_max=k, k_min=1)
+            torch.cuda.synchronize()
+            assert st.top_ids.cpu()[0].tolist() == case["top_ids"]
+            assert st.sel.cpu()[0, :k].tolist() == case["sel"]
+            assert abs(st.lse.item() - case["lse"]) < 1e-6
     # tie variants: lower cluster id / lower token id win (R7)
     R2 = R.clone(); R2[0, 0] = 2.0
     s2 = Dy.meta_score(Dy.Router(R2.to(DEV), torch.zeros(3, device=DEV)), hp.to(DEV), e.to(DEV))
@@ -103,16 +105,18 @@ def test_e2e1_golden_on_gpu():
 
 # ------------------------------------------------------------------ exact regime: bit-exact
 
+@pytest.mark.parametrize("fused", [True, False])
 @pytest.mark.parametrize("dtype", ["bf16", "f32"])
 @pytest.mark.parametrize("shared", [False, True])
-def test_exact_regime_pipeline(dtype, shared):
+def test_exact_regime_pipeline(dtype, shared, fused):
     Dy = _dyn()
     V, d, M, h_r, B = 5003, 256, 24, 16, 3   # ragged V (prime), several tiles, ragged clusters
     W, rt, tau, part, c, r = _setup(V, d, M, h_r, dtype, "exact")
     Wo = Rows(W)
     ro = _oracle_router(rt)
     k_t = 8
-    st = Dy.DraftStep(c, r, B, k_t, shared=shared, z_out=True)
+    st = Dy.DraftStep(c, r, B, k_t, shared=shared, z_out=True, two_streams=not fused)
+    assert (st.launches == 1) == fused
     for t in range(4):
         hp, e, hn = S.step_inputs(B, d, t, dtype, "exact", h_r=h_r)
         st(hp.to(DEV), e.to(DEV), hn.to(DEV), t=t, k_max=8, k_min=2)
@@ -170,15 +174,16 @@ def test_exact_ties_injected():
 
 # ------------------------------------------------------------------ random regime
 
+@pytest.mark.parametrize("fused", [True, False])
 @pytest.mark.parametrize("cfg,dtype,B", [("tiny", "bf16", 1), ("tiny", "f32", 1), ("llama2", "bf16", 1),
-                                         ("tiny", "bf16", 8)])
-def test_random_regime_config(cfg, dtype, B):
+                                         ("tiny", "bf16", 8), ("llama3", "bf16", 4)])
+def test_random_regime_config(cfg, dtype, B, fused):
     Dy = _dyn()
     C = S.CONFIGS[cfg]
     W, rt, tau, part, c, r = _setup(C.V, C.d, C.M, C.h_r, dtype, "random")
     Wo, ro = Rows(W), _oracle_router(rt)
     k_t = C.k_t
-    st = Dy.DraftStep(c, r, B, k_t, z_out=True)
+    st = Dy.DraftStep(c, r, B, k_t, z_out=True, two_streams=not fused)
     tdt = S.TORCH_DTYPES[dtype]
     for t in range(min(C.positions, 4)):
         hp, e, hn = S.step_inputs(B, C.d, t, dtype)
@@ -209,15 +214,16 @@ def test_random_regime_config(cfg, dtype, B):
                        st.lse[b].item(), rb["z"], rb["V_S"], k_t, tdt)
 
 
+@pytest.mark.parametrize("fused", [True, False])
 @pytest.mark.parametrize("positions", [(0, 2)])
-def test_llama3_full_size(positions):
+def test_llama3_full_size(positions, fused):
     """BASELINE configs[2] at full size (V=128256, d=4096, M=256, bf16), the bench's launch
     configuration (two streams, B=1); every logit of V_S compared with the oracle."""
     Dy = _dyn()
     C = S.CONFIGS["llama3"]
     W, rt, tau, part, c, r = _setup(C.V, C.d, C.M, C.h_r, "bf16", "random")
     Wo, ro = Rows(W), _oracle_router(rt)
-    st = Dy.DraftStep(c, r, 1, C.k_t, z_out=True)
+    st = Dy.DraftStep(c, r, 1, C.k_t, z_out=True, two_streams=not fused)
     for t in positions:
         hp, e, hn = S.step_inputs(1, C.d, t, "bf16")
         st(hp.to(DEV), e.to(DEV), hn.to(DEV), t=t, k_max=C.k_max, k_min=C.k_min)
@@ -238,13 +244,14 @@ def test_llama3_full_size(positions):
                    st.lse[0].item(), ref["z"], ref["V_S"], C.k_t, torch.bfloat16)
 
 
-def test_shared_tree_mode_qwen_shape():
+@pytest.mark.parametrize("fused", [True, False])
+def test_shared_tree_mode_qwen_shape(fused):
     """Tree mode (R9): R=10 sibling rows share the union shortlist (Qwen-2.5 head shape)."""
     Dy = _dyn()
     C = S.CONFIGS["qwen25"]
     W, rt, tau, part, c, r = _setup(C.V, C.d, C.M, C.h_r, "bf16", "random")
     Wo, ro = Rows(W), _oracle_router(rt)
-    st = Dy.DraftStep(c, r, C.B, C.k_t, shared=True, z_out=True)
+    st = Dy.DraftStep(c, r, C.B, C.k_t, shared=True, z_out=True, two_streams=not fused)
     t = 2
     hp, e, hn = S.step_inputs(C.B, C.d, t, "bf16", sibling_eps=0.1)
     st(hp.to(DEV), e.to(DEV), hn.to(DEV), t=t, k_max=C.k_max, k_min=C.k_min)
@@ -329,13 +336,14 @@ def test_determinism_bytes():
     W, rt, tau, part, c, r = _setup(C.V, C.d, C.M, C.h_r, "bf16", "random")
     hp, e, hn = S.step_inputs(4, C.d, 0, "bf16")
     outs = []
-    for _ in range(2):
-        st = Dy.DraftStep(c, r, 4, 16, z_out=True)
+    for two in (True, True, False, False):
+        st = Dy.DraftStep(c, r, 4, 16, z_out=True, two_streams=two)
         st(hp.to(DEV), e.to(DEV), hn.to(DEV), t=0, k_max=8, k_min=8)
         torch.cuda.synchronize()
         outs.append({k: v.clone() for k, v in st.outputs().items() if v is not None})
     for k in outs[0]:
         assert torch.equal(outs[0][k].view(torch.uint8), outs[1][k].view(torch.uint8)), k
+        assert torch.equal(outs[2][k].view(torch.uint8), outs[3][k].view(torch.uint8)), k
 
 
 def test_error_codes():
