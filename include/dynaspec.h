@@ -234,9 +234,10 @@ ds_status dynaspec_draft_step(const ds_clusters* c, const ds_router* r, const vo
                               ds_event_t ev_fork, ds_event_t ev_join, ds_event_t head_begin,
                               ds_event_t head_end);
 
-/* Number of kernel launches one dynaspec_draft_step enqueues (for launch accounting). */
+/* Number of kernel launches one dynaspec_draft_step enqueues (for launch accounting):
+ * 1 for the fused single-stream step, 2 + head chunks for the two-stream path. */
 int32_t dynaspec_draft_step_launches(const ds_clusters* c, const ds_router* r, int32_t B, int32_t k_t,
-                                     int32_t shared);
+                                     int32_t shared, int32_t two_streams);
 
 #ifdef __cplusplus
 }

@@ -210,10 +210,10 @@ size_t dynaspec_draft_step_ws(const ds_clusters* c, const ds_router* r, int32_t 
 }
 
 int32_t dynaspec_draft_step_launches(const ds_clusters* c, const ds_router* r, int32_t B, int32_t k_t,
-                                     int32_t shared) {
+                                     int32_t shared, int32_t two_streams) {
   HeadPlan p;
   if (!c || !r || !head_plan(c, B, k_t, 0, &p)) return 0;
-  if (step_supported(c, r, B, k_t, shared, 0)) return 1;  // fused single-stream step
+  if (!two_streams && step_supported(c, r, B, k_t, shared, 0)) return 1;  // fused single-stream step
   return 2 + p.launches;  // meta layer 1, meta layer 2 (+select), head chunks
 }
 

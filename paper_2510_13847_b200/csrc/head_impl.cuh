@@ -18,7 +18,8 @@ constexpr int kMaxStages = 12;
 constexpr int kStageTarget = 16384;          // bytes per ring slot (rounded to whole rows)
 constexpr int kRingMax = kMaxStages * kStageTarget;
 constexpr int kMaxGroups = 64;               // rows per launch
-constexpr int kStepExtra = 4096 * 2 + 1024 + 256;  // fused step: a1 + scores + flags + scan scratch
+// fused step: a1, scores, b1, b2 (fp32, <= 1024 each) + offsets (<= 1025 ints) + flags + scan scratch
+constexpr int kStepExtra = 4096 * 4 + 4112 + 1024 + 256;
 
 struct HeadArgs {
   const void* W;             // W_perm [V][d]
@@ -47,7 +48,7 @@ void fill_head_args(HeadArgs& a, const ds_clusters* c, const HeadPlan& p, const 
                     float* z_out, int64_t z_stride, float* part, unsigned* counter, bool pdl);
 
 struct HeadSmem {
-  uint32_t ring, bars, info, misc, sega, segn, h, zl, zid, extra, total;
+  uint32_t ring, bars, info, misc, sega, segn, segi, h, zl, zid, extra, total;
 };
 
 __host__ __device__ inline HeadSmem head_smem(int stages, int stage_bytes, int rows, int d, int esz, int lcap,
@@ -65,6 +66,8 @@ __host__ __device__ inline HeadSmem head_smem(int stages, int stage_bytes, int r
   L.sega = o;
   o += kMaxGroups * 8;
   L.segn = o;
+  o += kMaxGroups * 4;
+  L.segi = o;
   o += kMaxGroups * 4;
   o = (o + 127u) & ~127u;
   L.h = o;
@@ -89,6 +92,7 @@ struct HeadCtx {
   int* misc;
   long long* sega;
   int* segn;
+  int* segi;   // index (into the group's selection) of the cluster holding the segment start
   void* hs;
   float* zl;
   int* zid;
@@ -104,6 +108,7 @@ __device__ __forceinline__ HeadCtx head_ctx(uint8_t* smem, const HeadSmem& L) {
   c.misc = reinterpret_cast<int*>(smem + L.misc);
   c.sega = reinterpret_cast<long long*>(smem + L.sega);
   c.segn = reinterpret_cast<int*>(smem + L.segn);
+  c.segi = reinterpret_cast<int*>(smem + L.segi);
   c.hs = smem + L.h;
   c.zl = reinterpret_cast<float*>(smem + L.zl);
   c.zid = reinterpret_cast<int*>(smem + L.zid);
@@ -126,19 +131,33 @@ __device__ __forceinline__ long long shortlist_len(const HeadArgs& a, int gi) {
   return (N >= 1 && N <= a.max_shortlist) ? N : -1;
 }
 
-// Segment [N*g/G, N*(g+1)/G) of each group's virtual shortlist (even split by rows).
+// Segment [N*g/G, N*(g+1)/G) of each group's virtual shortlist (even split by rows), and
+// the selected cluster holding its first row (warp-parallel search: one L2 round trip per 32
+// selected clusters instead of a dependent chain).  Warp w handles groups w, w + nwarps, ...
 __device__ __forceinline__ void head_segments(const HeadArgs& a, const HeadCtx& c) {
   const int G = gridDim.x, g = blockIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   const int ngroups = a.shared ? 1 : a.nrows;
-  for (int gi = threadIdx.x; gi < ngroups; gi += blockDim.x) {
+  for (int gi = warp; gi < ngroups; gi += nw) {
     const long long N = shortlist_len(a, gi);
-    if (N < 0) {
-      c.sega[gi] = 0;
-      c.segn[gi] = -1;
-    } else {
-      const long long s0 = N * g / G, s1 = N * (g + 1) / G;
+    long long s0 = 0;
+    int n = -1, idx = 0;
+    if (N >= 0) {
+      s0 = N * g / G;
+      n = (int)(N * (g + 1) / G - s0);
+      const int cnt = __ldcg(a.sel_count + gi);
+      const int32_t* so = a.sl_off + (size_t)gi * (a.M + 1);
+      // idx = number of i in [1, cnt) with so[i] <= s0  (so[0] = 0 <= s0 always)
+      for (int i0 = 1; i0 < cnt; i0 += 32) {
+        const int i = i0 + lane;
+        const bool le = i < cnt && __ldcg(so + i) <= s0;
+        idx += __popc(__ballot_sync(0xffffffffu, le));
+      }
+    }
+    if (lane == 0) {
       c.sega[gi] = s0;
-      c.segn[gi] = (int)(s1 - s0);
+      c.segn[gi] = n;
+      c.segi[gi] = idx;
     }
   }
 }
@@ -158,8 +177,7 @@ __device__ void head_produce(const HeadArgs& a, const HeadCtx& c) {
     const long long s0 = c.sega[gi], s1 = s0 + nseg;
     const int32_t* so = a.sl_off + (size_t)gi * (a.M + 1);
     const int32_t* sl = a.sel + (size_t)gi * a.M;
-    int i = 0;
-    while (__ldcg(so + i + 1) <= s0) ++i;  // cluster holding virtual position s0
+    int i = c.segi[gi];  // cluster holding virtual position s0
     long long pos = s0;
     long long cl_beg = __ldcg(so + i), cl_end = __ldcg(so + i + 1);
     long long base = __ldg(a.offsets + __ldcg(sl + i));

@@ -31,6 +31,8 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(const float* __rest
   __shared__ __align__(16) float s[kMaxM];
   __shared__ uint8_t flags[kMaxM];
   __shared__ int scratch[33];
+  __shared__ int32_t offs[kMaxM + 1];
+  for (int m = threadIdx.x; m <= M; m += blockDim.x) offs[m] = offsets[m];
   for (int m = threadIdx.x; m < M; m += blockDim.x) flags[m] = 0;
   const int r_lo = shared ? 0 : blockIdx.x, r_hi = shared ? B : blockIdx.x + 1;
   for (int r = r_lo; r < r_hi; ++r) {
@@ -41,7 +43,7 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(const float* __rest
   }
   __syncthreads();
   const int o = shared ? 0 : blockIdx.x;
-  emit_selection(flags, M, offsets, sel + (size_t)o * M, sel_count + o, sl_off + (size_t)o * (M + 1), scratch);
+  emit_selection(flags, M, offs, sel + (size_t)o * M, sel_count + o, sl_off + (size_t)o * (M + 1), scratch);
 }
 
 // ------------------------------------------------------------------ layer 1: split-K partials
@@ -114,12 +116,21 @@ __global__ void __launch_bounds__(kMetaThreads) meta_l2_kernel(const float* __re
   __shared__ uint8_t flags[kMaxM];
   __shared__ int scratch[33];
   __shared__ int is_last;
+  __shared__ float b1s[kMaxM];
+  __shared__ float b2s[kMaxM];
+  __shared__ int32_t offs[kMaxM + 1];
   const int b = blockIdx.x;
+  // constants first (they do not depend on the upstream kernel)
+  for (int u = threadIdx.x; u < rows1; u += blockDim.x) b1s[u] = b1[u];
+  for (int m = threadIdx.x; m < M; m += blockDim.x) b2s[m] = h_r > 0 ? b2[m] : 0.f;
+  if (offsets)
+    for (int m = threadIdx.x; m <= M; m += blockDim.x) offs[m] = offsets[m];
   if (pdl) pdl_wait();
-  router_hidden(part, KS, B, b, rows1, b1, h_r > 0, a1);
+  __syncthreads();
+  router_hidden(part, KS, B, b, rows1, b1s, h_r > 0, a1);
   __syncthreads();
   if (h_r > 0) {
-    router_out<T>(W2, a1, b2, M, h_r, s);
+    router_out<T>(W2, a1, b2s, M, h_r, s);
   } else {
     for (int m = threadIdx.x; m < M; m += blockDim.x) s[m] = a1[m];
   }
@@ -134,7 +145,7 @@ __global__ void __launch_bounds__(kMetaThreads) meta_l2_kernel(const float* __re
   if (!shared) {
     rank_select(s, M, k_per_row ? k_per_row[b] : k, flags);
     __syncthreads();
-    emit_selection(flags, M, offsets, sel + (size_t)b * M, sel_count + b, sl_off + (size_t)b * (M + 1), scratch);
+    emit_selection(flags, M, offs, sel + (size_t)b * M, sel_count + b, sl_off + (size_t)b * (M + 1), scratch);
     return;
   }
   // shared mode: the last row-CTA forms the union of every row's TopK
@@ -151,7 +162,7 @@ __global__ void __launch_bounds__(kMetaThreads) meta_l2_kernel(const float* __re
     rank_select(s, M, k_per_row ? k_per_row[r] : k, flags);
   }
   __syncthreads();
-  emit_selection(flags, M, offsets, sel, sel_count, sl_off, scratch);
+  emit_selection(flags, M, offs, sel, sel_count, sl_off, scratch);
   if (threadIdx.x == 0) *counter = 0u;
 }
 

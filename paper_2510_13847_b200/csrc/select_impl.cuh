@@ -39,7 +39,7 @@ __device__ __forceinline__ void emit_selection(const uint8_t* flags, int M, cons
     const int m = m0 + j;
     if (m < M && flags[m]) {
       ++cnt;
-      sz += __ldg(offsets + m + 1) - __ldg(offsets + m);
+      sz += offsets[m + 1] - offsets[m];
     }
   }
   int tot_cnt, tot_sz;
@@ -51,7 +51,7 @@ __device__ __forceinline__ void emit_selection(const uint8_t* flags, int M, cons
       sel[pos] = m;
       sl_off[pos] = off;
       ++pos;
-      off += __ldg(offsets + m + 1) - __ldg(offsets + m);
+      off += offsets[m + 1] - offsets[m];
     }
   }
   if (threadIdx.x == 0) {
@@ -66,12 +66,13 @@ __device__ __forceinline__ void router_hidden(const float* part, int KS, int B, 
   for (int u = threadIdx.x; u < rows1; u += blockDim.x) {
     float acc = 0.f;
     for (int ks = 0; ks < KS; ++ks) acc += __ldcg(part + ((size_t)ks * B + b) * rows1 + u);
-    acc += __ldg(b1 + u);
+    acc += b1[u];
     a1[u] = relu ? fmaxf(acc, 0.f) : acc;
   }
 }
 
 // s[m] = sum_u W2[m][u] a1[u] + b2[m]: warp per score, 16-byte loads of W2 (smem or global).
+// b2 must already be staged (smem or registers-resident): no dependent global load per score.
 template <typename T>
 __device__ __forceinline__ void router_out(const T* W2, const float* a1, const float* b2, int M, int h_r, float* s) {
   constexpr int E = Elem<T>::kPer16B;
@@ -85,7 +86,7 @@ __device__ __forceinline__ void router_out(const T* W2, const float* a1, const f
 #pragma unroll
       for (int j = 0; j < E; ++j) acc = fmaf(wf[j], a1[c + j], acc);
     }
-    acc = warp_sum(acc) + __ldg(b2 + m);
+    acc = warp_sum(acc) + b2[m];
     if (lane == 0) s[m] = acc;
   }
 }

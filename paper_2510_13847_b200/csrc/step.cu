@@ -80,7 +80,10 @@ __device__ void step_phase_b(const StepArgs& s, const HeadCtx& c, uint64_t* w2ba
   const int M = s.h.M;
   float* a1 = reinterpret_cast<float*>(c.extra);
   float* sc = a1 + 1024;
-  uint8_t* flags = reinterpret_cast<uint8_t*>(sc + 1024);
+  float* b1s = sc + 1024;
+  float* b2s = b1s + 1024;
+  int32_t* offs = reinterpret_cast<int32_t*>(b2s + 1024);
+  uint8_t* flags = reinterpret_cast<uint8_t*>(offs + 1028);
   int* scratch = reinterpret_cast<int*>(flags + 1024);
   const T* W2 = s.w2_prefetch ? reinterpret_cast<const T*>(c.ring) : static_cast<const T*>(s.W2);
   if (threadIdx.x == 0) spin_until_geq(s.ctr + 1, gridDim.x);  // all layer-1 partials visible
@@ -93,10 +96,10 @@ __device__ void step_phase_b(const StepArgs& s, const HeadCtx& c, uint64_t* w2ba
   int published = 0;
   for (int b = b_lo; b < s.B; b += b_step) {
     __syncthreads();
-    router_hidden(s.mpart, s.KS, s.B, b, s.rows1, s.b1, s.h_r > 0, a1);
+    router_hidden(s.mpart, s.KS, s.B, b, s.rows1, b1s, s.h_r > 0, a1);
     __syncthreads();
     if (s.h_r > 0) {
-      router_out<T>(W2, a1, s.b2, M, s.h_r, sc);
+      router_out<T>(W2, a1, b2s, M, s.h_r, sc);
     } else {
       for (int m = threadIdx.x; m < M; m += blockDim.x) sc[m] = a1[m];
     }
@@ -105,7 +108,7 @@ __device__ void step_phase_b(const StepArgs& s, const HeadCtx& c, uint64_t* w2ba
     rank_select(sc, M, s.k, flags);
     if (!shared) {
       __syncthreads();
-      emit_selection(flags, M, s.h.offsets, const_cast<int32_t*>(s.h.sel) + (size_t)b * M,
+      emit_selection(flags, M, offs, const_cast<int32_t*>(s.h.sel) + (size_t)b * M,
                      const_cast<int32_t*>(s.h.sel_count) + b, const_cast<int32_t*>(s.h.sl_off) + (size_t)b * (M + 1),
                      scratch);
       __syncthreads();
@@ -115,7 +118,7 @@ __device__ void step_phase_b(const StepArgs& s, const HeadCtx& c, uint64_t* w2ba
   }
   if (shared) {
     __syncthreads();
-    emit_selection(flags, M, s.h.offsets, const_cast<int32_t*>(s.h.sel), const_cast<int32_t*>(s.h.sel_count),
+    emit_selection(flags, M, offs, const_cast<int32_t*>(s.h.sel), const_cast<int32_t*>(s.h.sel_count),
                    const_cast<int32_t*>(s.h.sl_off), scratch);
     published = 1;
   }
@@ -143,10 +146,19 @@ __global__ void __launch_bounds__((kMaxStages + 1) * 32, 1) step_kernel(const St
     }
   }
   __syncthreads();
-  // W2 does not depend on upstream work: prefetch it before waiting on the previous kernel
-  if (selector && s.w2_prefetch && threadIdx.x == 0) {
-    mbar_arrive_expect_tx(w2bar, (uint32_t)s.w2_prefetch);
-    bulk_g2s(c.ring, s.W2, (uint32_t)s.w2_prefetch, w2bar, policy_evict_last());
+  // Router constants do not depend on upstream work: stage them before waiting on the previous
+  // kernel (W2 by TMA into the idle ring; b1, b2, offsets by plain loads into `extra`).
+  if (selector) {
+    if (s.w2_prefetch && threadIdx.x == 0) {
+      mbar_arrive_expect_tx(w2bar, (uint32_t)s.w2_prefetch);
+      bulk_g2s(c.ring, s.W2, (uint32_t)s.w2_prefetch, w2bar, policy_evict_last());
+    }
+    float* b1s = reinterpret_cast<float*>(c.extra) + 2048;
+    float* b2s = b1s + 1024;
+    int32_t* offs = reinterpret_cast<int32_t*>(b2s + 1024);
+    for (int u = threadIdx.x; u < s.rows1; u += blockDim.x) b1s[u] = __ldg(s.b1 + u);
+    for (int m = threadIdx.x; m < a.M; m += blockDim.x) b2s[m] = s.h_r > 0 ? __ldg(s.b2 + m) : 0.f;
+    for (int m = threadIdx.x; m <= a.M; m += blockDim.x) offs[m] = __ldg(a.offsets + m);
   }
   if (a.pdl) pdl_wait();  // h_prev / e / h_new come from upstream kernels
   // h_new -> smem (consumer warps), layer-1 partials (all warps)

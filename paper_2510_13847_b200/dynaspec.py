@@ -77,7 +77,7 @@ def _load():
                                           c_int32, c_int32, c_int32, c_int32, POINTER(DsStepOutputs), P, c_size_t,
                                           P, P, P, P, P, P]),
         "dynaspec_draft_step_launches": (c_int32, [POINTER(DsClusters), POINTER(DsRouter), c_int32, c_int32,
-                                                   c_int32]),
+                                                   c_int32, c_int32]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -314,7 +314,8 @@ class DraftStep:
         self.s_meta = torch.cuda.Stream(device=dev) if two_streams else None
         self.ev_fork = make_event() if two_streams else None
         self.ev_join = make_event() if two_streams else None
-        self.launches = _lib.dynaspec_draft_step_launches(clusters.struct(), router.struct(), B, k_t, int(shared))
+        self.launches = _lib.dynaspec_draft_step_launches(clusters.struct(), router.struct(), B, k_t, int(shared),
+                                                          int(two_streams))
 
     def __call__(self, h_prev, e, h_new, t, k_max, k_min, head_events=None, stream=None):
         sd = _stream(stream)
