@@ -9,6 +9,8 @@
 
 namespace ds {
 
+__device__ unsigned long long* g_ds_trace = nullptr;
+
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 int num_sms() {
@@ -81,6 +83,11 @@ const char* dynaspec_status_string(ds_status s) {
     case DS_ERR_UNSUPPORTED: return "unsupported shape";
   }
   return "unknown status";
+}
+
+ds_status dynaspec_debug_set_trace(void* dev_buf) {
+  unsigned long long* p = static_cast<unsigned long long*>(dev_buf);
+  return cudaMemcpyToSymbol(g_ds_trace, &p, sizeof(p)) == cudaSuccess ? DS_OK : DS_ERR_CUDA;
 }
 
 int32_t dynaspec_budget(int32_t t, int32_t k_max, int32_t k_min) {

@@ -127,6 +127,18 @@ __device__ __forceinline__ unsigned ld_volatile_u32(const unsigned* p) {
   asm volatile("ld.volatile.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+// Opt-in phase trace (dynaspec_debug_set_trace): [cta][slot] nanosecond timestamps.
+extern __device__ unsigned long long* g_ds_trace;
+__device__ __forceinline__ void trace_mark(int slot) {
+  unsigned long long* t = g_ds_trace;
+  if (t != nullptr && threadIdx.x == 0) t[blockIdx.x * 16 + slot] = globaltimer_ns();
+}
+
 // Spin (one thread) until *ctr >= target, then acquire.
 __device__ __forceinline__ void spin_until_geq(const unsigned* ctr, unsigned target) {
   while (ld_volatile_u32(ctr) < target) {

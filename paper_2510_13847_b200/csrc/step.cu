@@ -87,8 +87,10 @@ __device__ void step_phase_b(const StepArgs& s, const HeadCtx& c, uint64_t* w2ba
   int* scratch = reinterpret_cast<int*>(flags + 1024);
   const T* W2 = s.w2_prefetch ? reinterpret_cast<const T*>(c.ring) : static_cast<const T*>(s.W2);
   if (threadIdx.x == 0) spin_until_geq(s.ctr + 1, gridDim.x);  // all layer-1 partials visible
+  trace_mark(8);
   if (s.w2_prefetch) mbar_wait(w2bar, 0);
   __syncthreads();
+  trace_mark(9);
   for (int m = threadIdx.x; m < M; m += blockDim.x) flags[m] = 0;
   const bool shared = s.h.shared != 0;
   const int b_lo = shared ? 0 : blockIdx.x;
@@ -124,6 +126,7 @@ __device__ void step_phase_b(const StepArgs& s, const HeadCtx& c, uint64_t* w2ba
   }
   __threadfence();
   __syncthreads();
+  trace_mark(10);
   if (threadIdx.x == 0 && published) atomicAdd(s.ctr + 2, (unsigned)published);
 }
 
@@ -160,29 +163,37 @@ __global__ void __launch_bounds__((kMaxStages + 1) * 32, 1) step_kernel(const St
     for (int m = threadIdx.x; m < a.M; m += blockDim.x) b2s[m] = s.h_r > 0 ? __ldg(s.b2 + m) : 0.f;
     for (int m = threadIdx.x; m <= a.M; m += blockDim.x) offs[m] = __ldg(a.offsets + m);
   }
+  trace_mark(0);
   if (a.pdl) pdl_wait();  // h_prev / e / h_new come from upstream kernels
+  trace_mark(1);
   // h_new -> smem (consumer warps), layer-1 partials (all warps)
   head_load_h(a, c, (int)sizeof(T), threadIdx.x, blockDim.x);
   step_phase_a<T>(s);
   __threadfence();
   __syncthreads();
+  trace_mark(2);
   if (threadIdx.x == 0) atomicAdd(s.ctr + 1, 1u);
   if (selector) step_phase_b<T>(s, c, w2bar);
   if (threadIdx.x == 0) spin_until_geq(s.ctr + 2, (unsigned)nsel_rows);  // selections published
   __syncthreads();
+  trace_mark(3);
   if (selector && s.w2_prefetch) fence_proxy_async_smem();  // generic reads of W2 before TMA reuse
   head_segments(a, c);
   __syncthreads();
+  trace_mark(4);
   if (warp == a.stages) {
     if (lane == 0) head_produce<T>(a, c);
   } else {
     head_consume<T>(a, c, warp, lane);
   }
   __syncthreads();
+  trace_mark(5);
   if (a.pdl) pdl_launch_dependents();
   head_partials(a, c);
+  trace_mark(6);
   if (!head_ticket(a, c)) return;
   head_merge(a, c, a.stages * a.stage_bytes);
+  trace_mark(7);
   if (threadIdx.x == 0) {
     s.ctr[0] = 0u;
     s.ctr[1] = 0u;

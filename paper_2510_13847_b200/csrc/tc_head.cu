@@ -1,0 +1,405 @@
+// tc_head.cu — S5' shared-shortlist head on the 5th-generation tensor cores (tcgen05 + TMEM).
+//
+// Tree drafting (R9, Alg. 1 line 8/10: one index set I for all k_t beam rows of a depth) makes the
+// head a dense contraction Z[R x |V_S|] = H[R x d] W_S^T with R rows sharing V_S (P:262, P:286
+// "computes on Tensor Cores").  Swap-AB so the vocabulary dimension is MMA-M = 128 and the rows
+// are MMA-N (R padded to 16):  D[128 tokens x N] (fp32, TMEM) += A[128 x 64] (W_perm rows, smem)
+// * B[N x 64]^T (h rows, smem), K = 16 per instruction (kind::f16, bf16 inputs).
+//
+// Per CTA (one per SM) the even segment of the shortlist (split rows, not clusters) is cut
+// into 16-row boxes that never cross a cluster run; 8 boxes form one 128-row MMA tile.  Roles:
+//   warp 0 lane 0   TMA producer: per (tile, 64-wide K chunk) 8 x 2-D boxes of W_perm (128B
+//                   swizzle, evict_first) + one box of H into a ring slot (mbarrier tx count)
+//   warp 1 lane 0   MMA issuer: 4 x tcgen05.mma per K chunk into a double-buffered TMEM
+//                   accumulator; tcgen05.commit frees the slot / publishes the tile
+//   warps 2..5      epilogue: tcgen05.ld 32x32b (one token per thread, R logits), remap via perm,
+//                   logits to shared memory; then the shared per-CTA partial + last-CTA merge.
+// Exactness: bf16 x bf16 products are exact in fp32; the exact-regime tests keep every partial
+// sum an integer below 2^24, so any accumulation order reproduces the oracle bit for bit.
+#include <cuda.h>
+
+#include <algorithm>
+
+#include "head_impl.cuh"
+#include "internal.h"
+
+namespace ds {
+
+constexpr int kTcBoxRows = 16;
+constexpr int kTcBoxes = 8;              // boxes per 128-row tile
+constexpr int kTcK = 64;                 // K elements per stage (128 bytes: one swizzle span)
+constexpr int kTcABytes = 128 * kTcK * 2;
+constexpr int kTcThreads = 6 * 32;
+constexpr int kTcMaxBoxes = 2048;
+
+struct TcArgs {
+  HeadArgs h;
+  int32_t N;        // MMA N (rows padded to 16)
+  int32_t S;        // ring stages
+  int32_t kchunks;  // ceil(d / 64)
+  int32_t tmem_cols;
+};
+
+struct TcSmem {
+  uint32_t a, b, bars, slot, misc, sega, segn, segi, boxes, zl, zid, total;
+};
+
+__host__ __device__ inline TcSmem tc_smem(int S, int N, int rows, int lcap) {
+  TcSmem L;
+  uint32_t o = 0;
+  L.a = o;
+  o += (uint32_t)S * kTcABytes;
+  L.b = o;
+  o += (uint32_t)S * N * 128;
+  o = (o + 1023u) & ~1023u;
+  L.bars = o;
+  o += (2 * 16 + 4) * 8;
+  L.slot = o;
+  o += 16;
+  L.misc = o;
+  o += 16 * 4;
+  L.sega = o;
+  o += kMaxGroups * 8;
+  L.segn = o;
+  o += kMaxGroups * 4;
+  L.segi = o;
+  o += kMaxGroups * 4;
+  o = (o + 15u) & ~15u;
+  L.boxes = o;
+  o += kTcMaxBoxes * 16;
+  L.zl = o;
+  o += (uint32_t)rows * lcap * 4;
+  L.zid = o;
+  o += (uint32_t)rows * lcap * 4;
+  L.total = o;
+  return L;
+}
+
+// ------------------------------------------------------------------ tcgen05 / TMA PTX
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar,
+                                            uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint "
+      "[%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tc_mma_bf16(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                            uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// Shared-memory matrix descriptor: K-major, 128-byte swizzle, 8-row groups 1024 B apart.
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// ------------------------------------------------------------------ kernel
+__global__ void __launch_bounds__(kTcThreads, 1) tc_head_kernel(const __grid_constant__ CUtensorMap tmW,
+                                                                const __grid_constant__ CUtensorMap tmH,
+                                                                const TcArgs t) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const HeadArgs& a = t.h;
+  const TcSmem L = tc_smem(t.S, t.N, a.nrows, a.lcap);
+  uint8_t* sa = smem + L.a;
+  uint8_t* sb = smem + L.b;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.bars);
+  uint64_t* empty = full + 16;
+  uint64_t* tfull = empty + 16;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* slot = reinterpret_cast<uint32_t*>(smem + L.slot);
+  int4* boxes = reinterpret_cast<int4*>(smem + L.boxes);
+  HeadCtx c;
+  c.ring = sa;
+  c.full = full;
+  c.empty = empty;
+  c.info = nullptr;
+  c.misc = reinterpret_cast<int*>(smem + L.misc);
+  c.sega = reinterpret_cast<long long*>(smem + L.sega);
+  c.segn = reinterpret_cast<int*>(smem + L.segn);
+  c.segi = reinterpret_cast<int*>(smem + L.segi);
+  c.hs = nullptr;
+  c.zl = reinterpret_cast<float*>(smem + L.zl);
+  c.zid = reinterpret_cast<int*>(smem + L.zid);
+  c.extra = nullptr;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < t.S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 4);
+    }
+    fence_mbar_init();
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmW)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmH)) : "memory");
+  }
+  if (warp == 1) {  // TMEM accumulators: 2 x N fp32 columns, owned (and freed) by warp 1
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(slot)),
+                 "r"(t.tmem_cols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  if (a.pdl) pdl_wait();
+  head_segments(a, c);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *slot;
+
+  // boxes of <= 16 rows covering the segment, never crossing a cluster boundary
+  if (threadIdx.x == 0) {
+    int nb = 0;
+    const int n = c.segn[0];
+    if (n > 0) {
+      const long long s0 = c.sega[0], s1 = s0 + n;
+      const int32_t* so = a.sl_off;
+      int i = c.segi[0];
+      long long cl_beg = __ldcg(so + i), cl_end = __ldcg(so + i + 1);
+      long long base = __ldg(a.offsets + __ldcg(a.sel + i));
+      long long pos = s0;
+      while (pos < s1 && nb < kTcMaxBoxes) {
+        const long long lim = cl_end < s1 ? cl_end : s1;
+        const int m = (int)min((long long)kTcBoxRows, lim - pos);
+        boxes[nb++] = make_int4((int)(base + (pos - cl_beg)), (int)(pos - s0), m, 0);
+        pos += m;
+        if (pos == cl_end && pos < s1) {
+          ++i;
+          cl_beg = cl_end;
+          cl_end = __ldcg(so + i + 1);
+          base = __ldg(a.offsets + __ldcg(a.sel + i));
+        }
+      }
+      if (pos < s1) nb = -1;  // segment too long for the box table: flag (host sizes lcap to avoid)
+    }
+    c.misc[1] = nb;
+  }
+  __syncthreads();
+  const int nboxes = c.misc[1];
+  const int ntiles = nboxes > 0 ? (nboxes + kTcBoxes - 1) / kTcBoxes : 0;
+  const uint32_t S = (uint32_t)t.S;
+
+  if (warp == 0) {
+    if (lane == 0 && ntiles > 0) {
+      const uint64_t pol_w = policy_evict_first(), pol_h = policy_evict_last();
+      uint32_t it = 0;
+      for (int tile = 0; tile < ntiles; ++tile) {
+        const int b0 = tile * kTcBoxes, b1 = min(nboxes, b0 + kTcBoxes);
+        const uint32_t bytes = (uint32_t)(b1 - b0) * kTcBoxRows * kTcK * 2 + (uint32_t)t.N * kTcK * 2;
+        for (int kc = 0; kc < t.kchunks; ++kc, ++it) {
+          const uint32_t s = it % S;
+          mbar_wait(&empty[s], ((it / S) & 1u) ^ 1u);
+          mbar_arrive_expect_tx(&full[s], bytes);
+          for (int b = b0; b < b1; ++b)
+            tma_load_2d(sa + (size_t)s * kTcABytes + (size_t)(b - b0) * kTcBoxRows * 128, &tmW, kc * kTcK,
+                        boxes[b].x, &full[s], pol_w);
+          tma_load_2d(sb + (size_t)s * t.N * 128, &tmH, kc * kTcK, 0, &full[s], pol_h);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && ntiles > 0) {
+      // instruction descriptor: D f32, A/B bf16, K-major both, N >> 3, M = 128 >> 4
+      const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(t.N >> 3) << 17) | (8u << 24);
+      uint32_t it = 0;
+      for (int tile = 0; tile < ntiles; ++tile) {
+        const int buf = tile & 1;
+        mbar_wait(&tempty[buf], (((uint32_t)tile >> 1) & 1u) ^ 1u);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem + (uint32_t)(buf * t.N);
+        for (int kc = 0; kc < t.kchunks; ++kc, ++it) {
+          const uint32_t s = it % S;
+          mbar_wait(&full[s], (it / S) & 1u);
+          tc_fence_after();
+          const uint32_t abase = smem_u32(sa + (size_t)s * kTcABytes);
+          const uint32_t bbase = smem_u32(sb + (size_t)s * t.N * 128);
+#pragma unroll
+          for (int k = 0; k < kTcK / 16; ++k)
+            tc_mma_bf16(d_tmem, sw128_desc(abase + k * 32), sw128_desc(bbase + k * 32), idesc,
+                        (kc | k) != 0 ? 1u : 0u);
+          tc_commit(&empty[s]);  // slot reusable once these MMAs have read it
+        }
+        tc_commit(&tfull[buf]);  // accumulator complete
+      }
+    }
+    __syncwarp();
+  } else {
+    // epilogue warps 2..5: TMEM lane quarter q = warp % 4 holds tokens 32q .. 32q + 31 of a tile
+    const int q = warp & 3;
+    const int row = 32 * q + lane;
+    const int nr = a.nrows;
+    for (int tile = 0; tile < ntiles; ++tile) {
+      const int buf = tile & 1;
+      mbar_wait(&tfull[buf], ((uint32_t)tile >> 1) & 1u);
+      tc_fence_after();
+      float v[64];
+      const uint32_t taddr = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(buf * t.N);
+      for (int c0 = 0; c0 < t.N; c0 += 16) tmem_ld16(taddr + c0, v + c0);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[buf]);
+      const int bi = tile * kTcBoxes + row / kTcBoxRows, r = row % kTcBoxRows;
+      if (bi < nboxes) {
+        const int4 bx = boxes[bi];
+        if (r < bx.z) {
+          const int local = bx.y + r;
+          const int tok = __ldg(a.perm + bx.x + r);
+          const long long vpos = c.sega[0] + local;
+          for (int rr = 0; rr < nr; ++rr) {
+            const float z = v[rr] + 0.0f;
+            c.zl[rr * a.lcap + local] = z;
+            c.zid[rr * a.lcap + local] = tok;
+            if (a.z_out) a.z_out[(size_t)rr * a.z_stride + vpos] = z;
+          }
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(t.tmem_cols) : "memory");
+  }
+  if (a.pdl) pdl_launch_dependents();
+  head_partials(a, c);
+  if (!head_ticket(a, c)) return;
+  head_merge(a, c, t.S * kTcABytes);
+  if (threadIdx.x == 0) *a.counter = 0u;
+}
+
+// ------------------------------------------------------------------ host side
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+static bool make_map(CUtensorMap* m, const void* base, uint64_t rows, uint64_t d, uint32_t box_rows) {
+  EncodeTiledFn f = encode_fn();
+  if (!f) return false;
+  const cuuint64_t dims[2] = {d, rows};
+  const cuuint64_t strides[1] = {d * 2};
+  const cuuint32_t box[2] = {(cuuint32_t)kTcK, box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  return f(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+struct TcPlan {
+  HeadPlan hp;  // G, lcap, rec, part_bytes
+  int N, S, tmem_cols;
+  size_t smem;
+};
+
+static bool tc_plan(const ds_clusters* c, int R, int k_t, int64_t max_shortlist, TcPlan* p) {
+  if (c->dtype != DS_BF16 || R < 1 || R > 64 || (c->d % 8) != 0) return false;
+  p->N = ((R + 15) / 16) * 16;
+  p->tmem_cols = 32;
+  while (p->tmem_cols < 2 * p->N) p->tmem_cols *= 2;
+  p->hp.G = num_sms();
+  const int64_t ms = (max_shortlist > 0 && max_shortlist < c->V) ? max_shortlist : c->V;
+  p->hp.lcap = (int)((ms + p->hp.G - 1) / p->hp.G);
+  if ((p->hp.lcap + kTcBoxRows - 1) / kTcBoxRows + c->M > kTcMaxBoxes) return false;
+  p->hp.rec = 2 + 2 * k_t;
+  p->hp.rows_per_launch = R;
+  p->hp.launches = 1;
+  p->hp.part_bytes = (size_t)p->hp.G * R * p->hp.rec * sizeof(float);
+  const int smax = max_smem_optin();
+  p->S = 0;
+  for (int S = 8; S >= 3; --S) {
+    if ((int64_t)S * kTcABytes < (int64_t)p->hp.G * p->hp.rec * 4 + p->hp.G) break;
+    if ((int)tc_smem(S, p->N, R, p->hp.lcap).total <= smax) {
+      p->S = S;
+      break;
+    }
+  }
+  if (p->S == 0) return false;
+  p->smem = tc_smem(p->S, p->N, R, p->hp.lcap).total;
+  return encode_fn() != nullptr;
+}
+
+bool tc_head_supported(const ds_clusters* c, int R, int k_t, int64_t max_shortlist) {
+  TcPlan p;
+  return tc_plan(c, R, k_t, max_shortlist, &p);
+}
+
+size_t tc_head_part_bytes(const ds_clusters* c, int R, int k_t) {
+  TcPlan p;
+  return tc_plan(c, R, k_t, 0, &p) ? p.hp.part_bytes : 0;
+}
+
+cudaError_t launch_tc_head(const ds_clusters* c, const void* h_new, int R, const int32_t* sel,
+                           const int32_t* sel_count, const int32_t* sl_offsets, int k_t, int64_t max_shortlist,
+                           int32_t* top_ids, float* top_logits, float* top_logp, float* lse, float* z_out,
+                           int64_t z_stride, float* part, unsigned* counter, cudaStream_t st, bool pdl) {
+  TcPlan p;
+  if (!tc_plan(c, R, k_t, max_shortlist, &p)) return cudaErrorInvalidValue;
+  CUtensorMap mw, mh;
+  if (!make_map(&mw, c->W_perm, (uint64_t)c->V, (uint64_t)c->d, kTcBoxRows)) return cudaErrorInvalidValue;
+  if (!make_map(&mh, h_new, (uint64_t)R, (uint64_t)c->d, (uint32_t)p.N)) return cudaErrorInvalidValue;
+  TcArgs t;
+  fill_head_args(t.h, c, p.hp, h_new, 0, R, sel, sel_count, sl_offsets, 1, k_t, max_shortlist, top_ids, top_logits,
+                 top_logp, lse, z_out, z_stride, part, counter, pdl);
+  t.N = p.N;
+  t.S = p.S;
+  t.kchunks = (c->d + kTcK - 1) / kTcK;
+  t.tmem_cols = p.tmem_cols;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(tc_head_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem_optin());
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(p.hp.G);
+  cfg.blockDim = dim3(kTcThreads);
+  cfg.dynamicSmemBytes = p.smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, tc_head_kernel, mw, mh, t);
+}
+
+}  // namespace ds

@@ -76,6 +76,7 @@ def _load():
         "dynaspec_draft_step": (c_int32, [POINTER(DsClusters), POINTER(DsRouter), P, P, P, c_int32, c_int32,
                                           c_int32, c_int32, c_int32, c_int32, POINTER(DsStepOutputs), P, c_size_t,
                                           P, P, P, P, P, P]),
+        "dynaspec_debug_set_trace": (c_int32, [P]),
         "dynaspec_draft_step_launches": (c_int32, [POINTER(DsClusters), POINTER(DsRouter), c_int32, c_int32,
                                                    c_int32, c_int32]),
     }
@@ -93,6 +94,7 @@ EXPORTED = [
     "dynaspec_build_clusters_ws", "dynaspec_build_clusters", "dynaspec_layout_ws", "dynaspec_layout",
     "dynaspec_meta_score_ws", "dynaspec_meta_score", "dynaspec_select", "dynaspec_head_forward_ws",
     "dynaspec_head_forward", "dynaspec_draft_step_ws", "dynaspec_draft_step", "dynaspec_draft_step_launches",
+    "dynaspec_debug_set_trace",
 ]
 
 
@@ -124,6 +126,11 @@ def _need_cuda(*ts):
 
 
 # ---------------------------------------------------------------------------- host helpers
+
+def debug_set_trace(buf):
+    """buf: int64 CUDA tensor of >= #SM*16 entries, or None (fused-step phase timestamps)."""
+    _check(_lib.dynaspec_debug_set_trace(_ptr(buf)), "dynaspec_debug_set_trace")
+
 
 def budget(t, k_max, k_min=1):
     """k_c(t) (R1).  Returns -1 on invalid arguments."""
