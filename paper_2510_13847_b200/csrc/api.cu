@@ -9,7 +9,8 @@
 
 namespace ds {
 
-__device__ unsigned long long* g_ds_trace = nullptr;
+static unsigned long long* g_trace = nullptr;
+unsigned long long* debug_trace() { return g_trace; }
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
@@ -86,8 +87,8 @@ const char* dynaspec_status_string(ds_status s) {
 }
 
 ds_status dynaspec_debug_set_trace(void* dev_buf) {
-  unsigned long long* p = static_cast<unsigned long long*>(dev_buf);
-  return cudaMemcpyToSymbol(g_ds_trace, &p, sizeof(p)) == cudaSuccess ? DS_OK : DS_ERR_CUDA;
+  g_trace = static_cast<unsigned long long*>(dev_buf);
+  return DS_OK;
 }
 
 int32_t dynaspec_budget(int32_t t, int32_t k_max, int32_t k_min) {

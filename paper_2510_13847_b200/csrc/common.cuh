@@ -133,9 +133,7 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
   return t;
 }
 // Opt-in phase trace (dynaspec_debug_set_trace): [cta][slot] nanosecond timestamps.
-extern __device__ unsigned long long* g_ds_trace;
-__device__ __forceinline__ void trace_mark(int slot) {
-  unsigned long long* t = g_ds_trace;
+__device__ __forceinline__ void trace_mark(unsigned long long* t, int slot) {
   if (t != nullptr && threadIdx.x == 0) t[blockIdx.x * 16 + slot] = globaltimer_ns();
 }
 

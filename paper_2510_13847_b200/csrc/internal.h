@@ -11,7 +11,8 @@ constexpr int kMaxM = 1024;      // largest cluster count the select kernels sup
 constexpr int kMaxMHost = kMaxM;
 constexpr int kMaxKt = 64;       // largest token budget k_t
 
-int num_sms();                 // SM count of the current device (cached per device)
+int num_sms();
+unsigned long long* debug_trace();   // device buffer set by dynaspec_debug_set_trace, or nullptr                 // SM count of the current device (cached per device)
 size_t align_up(size_t x, size_t a);
 
 // ---- meta-classifier (meta.cu)

@@ -33,6 +33,7 @@ struct StepArgs {
   float* mpart;             // [KS][B][rows1]
   int32_t B, h_r, rows1, KC, KS, k, w2_prefetch;
   unsigned* ctr;            // [0] merge ticket, [1] phase-A count, [2] selections published
+  unsigned long long* trace;  // opt-in phase timestamps (nullptr)
 };
 
 template <typename T>
@@ -87,10 +88,10 @@ __device__ void step_phase_b(const StepArgs& s, const HeadCtx& c, uint64_t* w2ba
   int* scratch = reinterpret_cast<int*>(flags + 1024);
   const T* W2 = s.w2_prefetch ? reinterpret_cast<const T*>(c.ring) : static_cast<const T*>(s.W2);
   if (threadIdx.x == 0) spin_until_geq(s.ctr + 1, gridDim.x);  // all layer-1 partials visible
-  trace_mark(8);
+  trace_mark(s.trace, 8);
   if (s.w2_prefetch) mbar_wait(w2bar, 0);
   __syncthreads();
-  trace_mark(9);
+  trace_mark(s.trace, 9);
   for (int m = threadIdx.x; m < M; m += blockDim.x) flags[m] = 0;
   const bool shared = s.h.shared != 0;
   const int b_lo = shared ? 0 : blockIdx.x;
@@ -126,7 +127,7 @@ __device__ void step_phase_b(const StepArgs& s, const HeadCtx& c, uint64_t* w2ba
   }
   __threadfence();
   __syncthreads();
-  trace_mark(10);
+  trace_mark(s.trace, 10);
   if (threadIdx.x == 0 && published) atomicAdd(s.ctr + 2, (unsigned)published);
 }
 
@@ -163,37 +164,37 @@ __global__ void __launch_bounds__((kMaxStages + 1) * 32, 1) step_kernel(const St
     for (int m = threadIdx.x; m < a.M; m += blockDim.x) b2s[m] = s.h_r > 0 ? __ldg(s.b2 + m) : 0.f;
     for (int m = threadIdx.x; m <= a.M; m += blockDim.x) offs[m] = __ldg(a.offsets + m);
   }
-  trace_mark(0);
+  trace_mark(s.trace, 0);
   if (a.pdl) pdl_wait();  // h_prev / e / h_new come from upstream kernels
-  trace_mark(1);
+  trace_mark(s.trace, 1);
   // h_new -> smem (consumer warps), layer-1 partials (all warps)
   head_load_h(a, c, (int)sizeof(T), threadIdx.x, blockDim.x);
   step_phase_a<T>(s);
   __threadfence();
   __syncthreads();
-  trace_mark(2);
+  trace_mark(s.trace, 2);
   if (threadIdx.x == 0) atomicAdd(s.ctr + 1, 1u);
   if (selector) step_phase_b<T>(s, c, w2bar);
   if (threadIdx.x == 0) spin_until_geq(s.ctr + 2, (unsigned)nsel_rows);  // selections published
   __syncthreads();
-  trace_mark(3);
+  trace_mark(s.trace, 3);
   if (selector && s.w2_prefetch) fence_proxy_async_smem();  // generic reads of W2 before TMA reuse
   head_segments(a, c);
   __syncthreads();
-  trace_mark(4);
+  trace_mark(s.trace, 4);
   if (warp == a.stages) {
     if (lane == 0) head_produce<T>(a, c);
   } else {
     head_consume<T>(a, c, warp, lane);
   }
   __syncthreads();
-  trace_mark(5);
+  trace_mark(s.trace, 5);
   if (a.pdl) pdl_launch_dependents();
   head_partials(a, c);
-  trace_mark(6);
+  trace_mark(s.trace, 6);
   if (!head_ticket(a, c)) return;
   head_merge(a, c, a.stages * a.stage_bytes);
-  trace_mark(7);
+  trace_mark(s.trace, 7);
   if (threadIdx.x == 0) {
     s.ctr[0] = 0u;
     s.ctr[1] = 0u;
@@ -295,6 +296,7 @@ cudaError_t launch_step(const ds_clusters* c, const ds_router* r, const void* h_
   s.k = k;
   s.w2_prefetch = p.w2_bytes;
   s.ctr = ctr;
+  s.trace = debug_trace();
   const int esz = c->dtype == DS_BF16 ? 2 : 4;
   const size_t smem = head_smem(p.hp.stages, p.hp.stage_bytes, B, c->d, esz, p.hp.lcap, kStepExtra).total;
   return c->dtype == DS_BF16 ? launch_step_t<__nv_bfloat16>(s, smem, p.hp.G, st, pdl)
