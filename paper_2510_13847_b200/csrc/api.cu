@@ -1,6 +1,8 @@
 // api.cu — the C ABI (include/dynaspec.h): synchronous validation, workspace carving, launches.
 #include <cuda_runtime.h>
 
+#include <stdlib.h>
+
 #include <algorithm>
 #include <mutex>
 
@@ -24,6 +26,13 @@ int num_sms() {
     cache[dev] = n > 0 ? n : 148;
   }
   return cache[dev];
+}
+
+// Tree / shared shortlist with >= 4 rows in bf16: the contraction goes to tcgen05 (S5').
+bool use_tc_head(const ds_clusters* c, int B, int k_t, int shared, int64_t max_shortlist) {
+  const char* off = getenv("DS_DISABLE_TC");
+  if (off && off[0] == '1') return false;
+  return shared && c->dtype == DS_BF16 && B >= 4 && tc_head_supported(c, B, k_t, max_shortlist);
 }
 
 static bool dtype_ok(int dt) { return dt == DS_BF16 || dt == DS_F32; }
@@ -179,7 +188,7 @@ size_t dynaspec_head_forward_ws(const ds_clusters* c, int32_t B, int32_t k_t) {
   HeadPlan p;
   if (!c || B < 1 || k_t < 1 || k_t > kMaxKt) return 0;
   if (!head_plan(c, B, k_t, 0, &p)) return 0;
-  return ws_layout(0, p.part_bytes).total;
+  return ws_layout(0, std::max(p.part_bytes, tc_head_part_bytes(c, B, k_t))).total;
 }
 
 ds_status dynaspec_head_forward(const ds_clusters* c, const void* h_new, int32_t B, const int32_t* sel,
@@ -200,10 +209,17 @@ ds_status dynaspec_head_forward(const ds_clusters* c, const void* h_new, int32_t
   const WsLayout L = ws_layout(0, p.part_bytes);
   if (!ws || ws_bytes < L.total) return DS_ERR_WORKSPACE;
   uint8_t* w8 = static_cast<uint8_t*>(ws);
-  cudaError_t err = launch_head(c, p, h_new, B, sel, sel_count, sl_offsets, shared ? 1 : 0, k_t, max_shortlist,
-                                top_ids, top_logits, top_logp, lse, z_out, z_stride,
-                                reinterpret_cast<float*>(w8 + L.head), reinterpret_cast<unsigned*>(w8 + L.counters),
-                                (cudaStream_t)stream, false);
+  cudaError_t err;
+  if (use_tc_head(c, B, k_t, shared, max_shortlist)) {
+    if (ws_bytes < ws_layout(0, tc_head_part_bytes(c, B, k_t)).total) return DS_ERR_WORKSPACE;
+    err = launch_tc_head(c, h_new, B, sel, sel_count, sl_offsets, k_t, max_shortlist, top_ids, top_logits,
+                         top_logp, lse, z_out, z_stride, reinterpret_cast<float*>(w8 + L.head),
+                         reinterpret_cast<unsigned*>(w8 + L.counters), (cudaStream_t)stream, false);
+  } else {
+    err = launch_head(c, p, h_new, B, sel, sel_count, sl_offsets, shared ? 1 : 0, k_t, max_shortlist, top_ids,
+                      top_logits, top_logp, lse, z_out, z_stride, reinterpret_cast<float*>(w8 + L.head),
+                      reinterpret_cast<unsigned*>(w8 + L.counters), (cudaStream_t)stream, false);
+  }
   return err == cudaSuccess ? DS_OK : DS_ERR_CUDA;
 }
 
@@ -213,7 +229,8 @@ size_t dynaspec_draft_step_ws(const ds_clusters* c, const ds_router* r, int32_t 
   if (!head_plan(c, B, k_t, 0, &p)) return 0;
   const size_t meta = meta_plan(r, B).part_bytes;
   const size_t scores = (size_t)B * r->M * sizeof(float);
-  return std::max(ws_layout(align_up(meta, 256) + align_up(scores, 256), p.part_bytes).total,
+  return std::max(ws_layout(align_up(meta, 256) + align_up(scores, 256),
+                            std::max(p.part_bytes, tc_head_part_bytes(c, B, k_t))).total,
                   step_ws_bytes(c, r, B, k_t));
 }
 
@@ -221,6 +238,8 @@ int32_t dynaspec_draft_step_launches(const ds_clusters* c, const ds_router* r, i
                                      int32_t shared, int32_t two_streams) {
   HeadPlan p;
   if (!c || !r || !head_plan(c, B, k_t, 0, &p)) return 0;
+  const int64_t ms = shared ? c->V : 0;
+  if (use_tc_head(c, B, k_t, shared, ms)) return 3;  // meta layer 1, meta layer 2 (+union), tcgen05 head
   if (!two_streams && step_supported(c, r, B, k_t, shared, 0)) return 1;  // fused single-stream step
   return 2 + p.launches;  // meta layer 1, meta layer 2 (+select), head chunks
 }
@@ -246,7 +265,8 @@ ds_status dynaspec_draft_step(const ds_clusters* c, const ds_router* r, const vo
   if (out->z_out && out->z_stride < ms) return DS_ERR_SHAPE;
   const bool two_streams = s_meta != nullptr && s_meta != s_draft;
   if (two_streams && (!ev_fork || !ev_join)) return DS_ERR_SHAPE;
-  const bool fused = !two_streams && step_supported(c, r, B, k_t, shared, ms);
+  const bool tc = use_tc_head(c, B, k_t, shared, ms);
+  const bool fused = !tc && !two_streams && step_supported(c, r, B, k_t, shared, ms);
   if (fused) {  // one persistent launch: router + select + head + epilogue (step.cu)
     const size_t need = step_ws_bytes(c, r, B, k_t);
     if (!ws || need == 0 || ws_bytes < need) return DS_ERR_WORKSPACE;
@@ -271,6 +291,9 @@ ds_status dynaspec_draft_step(const ds_clusters* c, const ds_router* r, const vo
   const size_t score_bytes = (size_t)B * r->M * sizeof(float);
   const WsLayout L = ws_layout(align_up(meta_bytes, 256) + align_up(score_bytes, 256), pmax.part_bytes);
   if (!ws || ws_bytes < L.total) return DS_ERR_WORKSPACE;
+  if (tc && ws_bytes < ws_layout(align_up(meta_bytes, 256) + align_up(score_bytes, 256),
+                                 tc_head_part_bytes(c, B, k_t)).total)
+    return DS_ERR_WORKSPACE;
   uint8_t* w8 = static_cast<uint8_t*>(ws);
   unsigned* counters = reinterpret_cast<unsigned*>(w8 + L.counters);
   float* meta_part = reinterpret_cast<float*>(w8 + L.meta);
@@ -294,9 +317,15 @@ ds_status dynaspec_draft_step(const ds_clusters* c, const ds_router* r, const vo
   cudaStreamIsCapturing(sd, &cap);
   const unsigned evflags = cap == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : cudaEventRecordDefault;
   if (head_begin && cudaEventRecordWithFlags((cudaEvent_t)head_begin, sd, evflags) != cudaSuccess) return DS_ERR_CUDA;
-  err = launch_head(c, p, h_new, B, out->sel, out->sel_count, out->sl_offsets, shared ? 1 : 0, k_t, ms, out->top_ids,
-                    out->top_logits, out->top_logp, out->lse, out->z_out, out->z_stride,
-                    reinterpret_cast<float*>(w8 + L.head), counters, sd, !two_streams && head_begin == nullptr);
+  if (tc) {
+    err = launch_tc_head(c, h_new, B, out->sel, out->sel_count, out->sl_offsets, k_t, ms, out->top_ids,
+                         out->top_logits, out->top_logp, out->lse, out->z_out, out->z_stride,
+                         reinterpret_cast<float*>(w8 + L.head), counters, sd, !two_streams && head_begin == nullptr);
+  } else {
+    err = launch_head(c, p, h_new, B, out->sel, out->sel_count, out->sl_offsets, shared ? 1 : 0, k_t, ms,
+                      out->top_ids, out->top_logits, out->top_logp, out->lse, out->z_out, out->z_stride,
+                      reinterpret_cast<float*>(w8 + L.head), counters, sd, !two_streams && head_begin == nullptr);
+  }
   if (err != cudaSuccess) return DS_ERR_CUDA;
   if (head_end && cudaEventRecordWithFlags((cudaEvent_t)head_end, sd, evflags) != cudaSuccess) return DS_ERR_CUDA;
   return DS_OK;

@@ -134,7 +134,10 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
 }
 // Opt-in phase trace (dynaspec_debug_set_trace): [cta][slot] nanosecond timestamps.
 __device__ __forceinline__ void trace_mark(unsigned long long* t, int slot) {
-  if (t != nullptr && threadIdx.x == 0) t[blockIdx.x * 16 + slot] = globaltimer_ns();
+  if (t != nullptr && threadIdx.x == 0) {
+    t[blockIdx.x * 32 + slot] = globaltimer_ns();
+    t[blockIdx.x * 32 + 16 + slot] = clock64();
+  }
 }
 
 // Spin (one thread) until *ctr >= target, then acquire.

@@ -61,13 +61,13 @@ bool head_plan_ex(const ds_clusters* c, int B, int k_t, int64_t max_shortlist, i
   const int smax = max_smem_optin();
   const int per_row = rowbytes + p->lcap * 8 + 16;
   const int want_rows = std::min(std::min(B, kMaxGroups), max_rows);
-  const int merge_need = p->G * p->rec * 4 + p->G;
+  const int min_stages = std::max(2, (p->G + 31) / 32 - 1);  // merge: G <= 32 * warps
   p->stages = 0;
-  for (int st = kMaxStages; st >= 2; --st) {
-    if (st * p->stage_bytes < merge_need) break;
+  for (int st = kMaxStages; st >= min_stages; --st) {
+    if (st * p->stage_bytes < merge_smem_bytes(p->G, k_t, st + 1)) break;
     const HeadSmem L0 = head_smem(st, p->stage_bytes, 0, c->d, esz, p->lcap, extra);
     const int rows = ((int)smax - (int)L0.total) / per_row;
-    if (rows >= want_rows || (st == 2 && rows >= 1)) {
+    if (rows >= want_rows || (st == min_stages && rows >= 1)) {
       p->stages = st;
       p->rows_per_launch = std::max(1, std::min(want_rows, rows));
       break;

@@ -20,6 +20,10 @@ constexpr int kRingMax = kMaxStages * kStageTarget;
 constexpr int kMaxGroups = 64;               // rows per launch
 // fused step: a1, scores, b1, b2 (fp32, <= 1024 each) + offsets (<= 1025 ints) + flags + scan scratch
 constexpr int kStepExtra = 4096 * 4 + 4112 + 1024 + 256;
+// shared-memory bytes the last-CTA merge needs inside the ring
+__host__ __device__ inline int merge_smem_bytes(int G, int k_t, int nwarps) {
+  return G * (2 + 2 * k_t) * 4 + 2 * nwarps * k_t * 4 + nwarps * 4 + 64;
+}
 
 struct HeadArgs {
   const void* W;             // W_perm [V][d]
@@ -124,10 +128,13 @@ __device__ __forceinline__ void head_init_barriers(const HeadCtx& c, int stages)
   fence_mbar_init();
 }
 
+// sel / sel_count / sl_off may live in global memory (written by an earlier kernel, or by
+// another CTA of this kernel before a fenced counter handshake) or in this CTA's shared memory
+// (fused step): plain generic loads are valid for both.
 __device__ __forceinline__ long long shortlist_len(const HeadArgs& a, int gi) {
-  const int cnt = __ldcg(a.sel_count + gi);
+  const int cnt = a.sel_count[gi];
   if (cnt < 1 || cnt > a.M) return -1;
-  const long long N = __ldcg(a.sl_off + (size_t)gi * (a.M + 1) + cnt);
+  const long long N = a.sl_off[(size_t)gi * (a.M + 1) + cnt];
   return (N >= 1 && N <= a.max_shortlist) ? N : -1;
 }
 
@@ -145,12 +152,12 @@ __device__ __forceinline__ void head_segments(const HeadArgs& a, const HeadCtx& 
     if (N >= 0) {
       s0 = N * g / G;
       n = (int)(N * (g + 1) / G - s0);
-      const int cnt = __ldcg(a.sel_count + gi);
+      const int cnt = a.sel_count[gi];
       const int32_t* so = a.sl_off + (size_t)gi * (a.M + 1);
       // idx = number of i in [1, cnt) with so[i] <= s0  (so[0] = 0 <= s0 always)
       for (int i0 = 1; i0 < cnt; i0 += 32) {
         const int i = i0 + lane;
-        const bool le = i < cnt && __ldcg(so + i) <= s0;
+        const bool le = i < cnt && so[i] <= s0;
         idx += __popc(__ballot_sync(0xffffffffu, le));
       }
     }
@@ -179,8 +186,8 @@ __device__ void head_produce(const HeadArgs& a, const HeadCtx& c) {
     const int32_t* sl = a.sel + (size_t)gi * a.M;
     int i = c.segi[gi];  // cluster holding virtual position s0
     long long pos = s0;
-    long long cl_beg = __ldcg(so + i), cl_end = __ldcg(so + i + 1);
-    long long base = __ldg(a.offsets + __ldcg(sl + i));
+    long long cl_beg = so[i], cl_end = so[i + 1];
+    long long base = __ldg(a.offsets + sl[i]);
     while (pos < s1) {
       const long long lim = cl_end < s1 ? cl_end : s1;
       const int n = (int)min((long long)a.stage_rows, lim - pos);
@@ -196,8 +203,8 @@ __device__ void head_produce(const HeadArgs& a, const HeadCtx& c) {
       if (pos == cl_end && pos < s1) {
         ++i;
         cl_beg = cl_end;
-        cl_end = __ldcg(so + i + 1);
-        base = __ldg(a.offsets + __ldcg(sl + i));
+        cl_end = so[i + 1];
+        base = __ldg(a.offsets + sl[i]);
       }
     }
   }
@@ -348,79 +355,97 @@ __device__ __forceinline__ bool head_ticket(const HeadArgs& a, const HeadCtx& c)
 }
 
 // Last CTA: merge the G partials of every row in CTA order -> lse, top ids (remapped), logp.
+// Rows are merged one after another by the whole CTA: the G records are staged in shared memory
+// (all loads in flight at once), each warp merges a slice of the G sorted lists (k_t rounds of a
+// warp arg-max), and warp 0 merges the per-warp results — two short levels instead of one long.
 __device__ inline void head_merge(const HeadArgs& a, const HeadCtx& c, int ring_bytes) {
   const int G = gridDim.x;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, nw = blockDim.x >> 5;
-  const int rec = 2 + 2 * a.k_t;
+  const int K = a.k_t;
+  const int rec = 2 + 2 * K;
   const int per_row = G * rec;
-  int batch = ring_bytes / (per_row * 4 + G);
-  batch = batch < 1 ? 1 : (batch > nw ? nw : batch);
-  float* mbuf = reinterpret_cast<float*>(c.ring);
-  uint8_t* ptr_base = c.ring + (size_t)batch * per_row * 4;
-  for (int r0 = 0; r0 < a.nrows; r0 += batch) {
-    const int nb = min(batch, a.nrows - r0);
-    for (int rb = 0; rb < nb; ++rb) {
-      const float* src = a.part + (size_t)(r0 + rb) * rec;
-      float* dst = mbuf + (size_t)rb * per_row;
-      for (int idx = tid; idx < per_row; idx += blockDim.x) {
-        const int gg = idx / rec, f = idx - gg * rec;
-        dst[idx] = __ldcg(src + (size_t)gg * a.nrows * rec + f);
+  float* R = reinterpret_cast<float*>(c.ring);          // [G][rec]
+  float* L1v = R + per_row;                             // [nw][K] level-1 values
+  int* L1i = reinterpret_cast<int*>(L1v + nw * K);      // [nw][K] level-1 ids
+  float* red = reinterpret_cast<float*>(L1i + nw * K);  // [nw] partial max / sums
+  (void)ring_bytes;
+  for (int r = 0; r < a.nrows; ++r) {
+    const float* src = a.part + (size_t)r * rec;
+    constexpr int U = 8;
+    for (int base = tid; base < per_row; base += U * blockDim.x) {
+      float v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int idx = base + u * blockDim.x;
+        if (idx < per_row) {
+          const int gg = idx / rec, f = idx - gg * rec;
+          v[u] = __ldcg(src + (size_t)gg * a.nrows * rec + f);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int idx = base + u * blockDim.x;
+        if (idx < per_row) R[idx] = v[u];
       }
     }
     __syncthreads();
-    if (warp < nb) {
-      const int r = r0 + warp;
-      const float* R = mbuf + (size_t)warp * per_row;
-      uint8_t* ptr = ptr_base + (size_t)warp * G;
-      const bool ok = shortlist_len(a, a.shared ? 0 : r) >= 0;
-      float mx = -INFINITY;
-      for (int gg = lane; gg < G; gg += 32) {
-        mx = fmaxf(mx, R[gg * rec]);
-        ptr[gg] = 0;
-      }
-      mx = warp_max(mx);
-      float S = 0.f;
-      for (int gg = lane; gg < G; gg += 32) {
-        const float m = R[gg * rec];
-        if (m > -INFINITY) S += R[gg * rec + 1] * expf(m - mx);
-      }
-      S = warp_sum(S);
-      const float lse = ok ? mx + logf(S) : __int_as_float(0x7fc00000);
-      __syncwarp();
-      float bv;
-      int bid, bl;
-      auto lane_best = [&]() {
-        bv = -INFINITY;
-        bid = INT_MAX;
-        bl = -1;
-        for (int gg = lane; gg < G; gg += 32) {
-          const int p = ptr[gg];
-          if (p >= a.k_t) continue;
-          const float v = R[gg * rec + 2 + 2 * p];
-          const int id = __float_as_int(R[gg * rec + 3 + 2 * p]);
-          if (beats(v, id, bv, bid)) {
-            bv = v;
-            bid = id;
-            bl = gg;
-          }
+    // global max and sum of rescaled partial sums (fixed order: CTA-strided per warp, then warps)
+    float mx = -INFINITY;
+    for (int gg = tid; gg < G; gg += blockDim.x) mx = fmaxf(mx, R[gg * rec]);
+    mx = warp_max(mx);
+    if (lane == 0) red[warp] = mx;
+    __syncthreads();
+    mx = red[0];
+    for (int w = 1; w < nw; ++w) mx = fmaxf(mx, red[w]);
+    __syncthreads();
+    float S = 0.f;
+    for (int gg = tid; gg < G; gg += blockDim.x) {
+      const float m = R[gg * rec];
+      if (m > -INFINITY) S += R[gg * rec + 1] * expf(m - mx);
+    }
+    S = warp_sum(S);
+    if (lane == 0) red[warp] = S;
+    // level 1: warp w merges lists g = w, w + nw, ... (lane j holds list w + j*nw; G <= 32 nw)
+    {
+      const int g0 = warp + lane * nw;
+      int p = 0;
+      for (int qq = 0; qq < K; ++qq) {
+        float v = -INFINITY;
+        int id = INT_MAX, who = lane;
+        if (g0 < G && p < K) {
+          v = R[g0 * rec + 2 + 2 * p];
+          id = __float_as_int(R[g0 * rec + 3 + 2 * p]);
         }
-      };
-      lane_best();
-      for (int qq = 0; qq < a.k_t; ++qq) {
-        float wv = bv;
-        int wid = bid, wl = bl;
-        warp_best(wv, wid, wl);
+        warp_best(v, id, who);
+        if (lane == who) ++p;
         if (lane == 0) {
-          const bool valid = ok && wv > -INFINITY;
-          a.top_ids[(size_t)r * a.k_t + qq] = valid ? wid : -1;
-          a.top_logits[(size_t)r * a.k_t + qq] = valid ? wv : -INFINITY;
-          a.top_logp[(size_t)r * a.k_t + qq] = valid ? wv - lse : -INFINITY;
+          L1v[warp * K + qq] = v;
+          L1i[warp * K + qq] = id;
         }
-        if (wl >= 0 && (wl & 31) == lane) {
-          ptr[wl] = (uint8_t)(ptr[wl] + 1);
-          lane_best();
+      }
+    }
+    __syncthreads();
+    if (warp == 0) {
+      float St = 0.f;
+      for (int w = 0; w < nw; ++w) St += red[w];
+      const bool ok = shortlist_len(a, a.shared ? 0 : r) >= 0;
+      const float lse = ok ? mx + logf(St) : __int_as_float(0x7fc00000);
+      int p = 0;
+      for (int qq = 0; qq < K; ++qq) {
+        float v = -INFINITY;
+        int id = INT_MAX, who = lane;
+        if (lane < nw && p < K) {
+          v = L1v[lane * K + p];
+          id = L1i[lane * K + p];
         }
-        __syncwarp();
+        warp_best(v, id, who);
+        if (lane == who) ++p;
+        if (lane == 0) {
+          const bool valid = ok && v > -INFINITY;
+          a.top_ids[(size_t)r * K + qq] = valid ? id : -1;
+          a.top_logits[(size_t)r * K + qq] = valid ? v : -INFINITY;
+          a.top_logp[(size_t)r * K + qq] = valid ? v - lse : -INFINITY;
+        }
       }
       if (lane == 0) a.lse[r] = lse;
     }

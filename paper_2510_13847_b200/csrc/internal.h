@@ -65,6 +65,15 @@ cudaError_t launch_step(const ds_clusters* c, const ds_router* r, const void* h_
                         float* top_logp, float* lse, float* z_out, int64_t z_stride, void* ws, cudaStream_t st,
                         bool pdl);
 
+// ---- tcgen05 shared-shortlist head (tc_head.cu), bf16, R <= 64 rows sharing one shortlist
+bool tc_head_supported(const ds_clusters* c, int R, int k_t, int64_t max_shortlist);
+size_t tc_head_part_bytes(const ds_clusters* c, int R, int k_t);
+cudaError_t launch_tc_head(const ds_clusters* c, const void* h_new, int R, const int32_t* sel,
+                           const int32_t* sel_count, const int32_t* sl_offsets, int k_t, int64_t max_shortlist,
+                           int32_t* top_ids, float* top_logits, float* top_logp, float* lse, float* z_out,
+                           int64_t z_stride, float* part, unsigned* counter, cudaStream_t st, bool pdl);
+bool use_tc_head(const ds_clusters* c, int B, int k_t, int shared, int64_t max_shortlist);
+
 // ---- offline partition (build.cu)
 size_t build_ws_bytes(int64_t V, int d, int M);
 size_t layout_ws_bytes(int64_t V, int M);

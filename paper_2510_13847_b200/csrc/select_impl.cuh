@@ -92,3 +92,139 @@ __device__ __forceinline__ void router_out(const T* W2, const float* a1, const f
 }
 
 }  // namespace ds
+
+namespace ds {
+
+// ---------------------------------------------------------------- fast variants (fused step)
+
+// Order-preserving map float -> uint32 (larger float => larger key); -0 folded into +0 (R23).
+__device__ __forceinline__ uint32_t ord_key(float x) {
+  const uint32_t u = __float_as_uint(x + 0.0f);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+
+// s[m] = W2[m] . a1 + b2[m] with L = (h_r / E rounded up to a power of two, <= 32) lanes per
+// score, so a warp produces 32 / L scores per pass (W2, a1, b2 in shared memory).
+template <typename T>
+__device__ __forceinline__ void router_scores_fast(const T* W2, const float* a1, const float* b2, int M, int h_r,
+                                                   float* sc) {
+  constexpr int E = Elem<T>::kPer16B;
+  const int chunks = h_r / E;
+  int L = 1;
+  while (L < chunks && L < 32) L <<= 1;
+  const int spw = 32 / L;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int sub = lane % L, slot = lane / L;
+  for (int m0 = warp * spw; m0 < M; m0 += nw * spw) {
+    const int m = m0 + slot;
+    float acc = 0.f;
+    if (m < M) {
+      const T* w = W2 + (size_t)m * h_r;
+      for (int ch = sub; ch < chunks; ch += L) {
+        float wf[E];
+        widen16(*reinterpret_cast<const uint4*>(w + ch * E), wf, w);
+#pragma unroll
+        for (int j = 0; j < E; ++j) acc = fmaf(wf[j], a1[ch * E + j], acc);
+      }
+    }
+    for (int o = L / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (sub == 0 && m < M) sc[m] = acc + b2[m];
+  }
+}
+
+// TopK_k of sc[0..M) under (score desc, id asc) as a bit mask (R7): 4-pass radix select
+// of the k-th largest order key, then every key above it plus the lowest-id ties.
+// Smem: mask [ceil(M/32)] words, hist [256], sh [2].  All threads of the block participate.
+__device__ __forceinline__ void radix_topk_mask(const float* sc, int M, int k, uint32_t* mask, int* hist, int* sh) {
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
+  uint32_t prefix = 0, pmask = 0;
+  int kk = k;
+  for (int shift = 24; shift >= 0; shift -= 8) {
+    for (int i = tid; i < 256; i += nt) hist[i] = 0;
+    __syncthreads();
+    for (int m = tid; m < M; m += nt) {
+      const uint32_t key = ord_key(sc[m]);
+      if ((key & pmask) == prefix) atomicAdd(&hist[(key >> shift) & 255u], 1);
+    }
+    __syncthreads();
+    if (warp == 0) {
+      int cnt[8], tot = 0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        cnt[j] = hist[255 - 8 * lane - j];
+        tot += cnt[j];
+      }
+      int inc = tot;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+      }
+      const int exc = inc - tot;
+      if (exc < kk && kk <= inc) {
+        int run = exc;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          if (run + cnt[j] >= kk) {
+            sh[0] = 255 - 8 * lane - j;
+            sh[1] = kk - run;
+            break;
+          }
+          run += cnt[j];
+        }
+      }
+    }
+    __syncthreads();
+    prefix |= (uint32_t)sh[0] << shift;
+    pmask |= 255u << shift;
+    kk = sh[1];
+    __syncthreads();
+  }
+  if (warp == 0) {
+    int running = 0;
+    for (int c = 0; c * 32 < M; ++c) {
+      const int m = c * 32 + lane;
+      const uint32_t key = m < M ? ord_key(sc[m]) : 0u;
+      const bool gt = m < M && key > prefix;
+      const bool eq = m < M && key == prefix;
+      const uint32_t eb = __ballot_sync(0xffffffffu, eq);
+      const int r = running + __popc(eb & ((1u << lane) - 1u));
+      const uint32_t mb = __ballot_sync(0xffffffffu, gt || (eq && r < kk));
+      if (lane == 0) mask[c] = mb;
+      running += __popc(eb);
+    }
+  }
+  __syncthreads();
+}
+
+// One warp: ascending ids of the set bits + exclusive scan of |C_m| (sl_offsets).
+__device__ __forceinline__ void emit_mask_warp(const uint32_t* mask, int M, const int32_t* offs, int32_t* sel,
+                                               int32_t* cnt_out, int32_t* sl_off) {
+  const int lane = threadIdx.x & 31;
+  int base = 0, run = 0;
+  for (int c = 0; c * 32 < M; ++c) {
+    const int m = c * 32 + lane;
+    const bool f = m < M && ((mask[c] >> lane) & 1u);
+    const uint32_t b = __ballot_sync(0xffffffffu, f);
+    const int pos = base + __popc(b & ((1u << lane) - 1u));
+    const int sz = f ? offs[m + 1] - offs[m] : 0;
+    int inc = sz;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += y;
+    }
+    if (f) {
+      sel[pos] = m;
+      sl_off[pos] = run + inc - sz;
+    }
+    base += __popc(b);
+    run += __shfl_sync(0xffffffffu, inc, 31);
+  }
+  if (lane == 0) {
+    *cnt_out = base;
+    sl_off[base] = run;
+  }
+}
+
+}  // namespace ds

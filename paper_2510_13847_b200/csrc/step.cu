@@ -21,6 +21,33 @@ namespace ds {
 
 constexpr int kStepCH = 2;  // 16-byte chunks per lane per layer-1 task
 
+// Shared-memory carve-up of the fused step's router/selection scratch (inside HeadSmem.extra).
+struct StepExtra {
+  uint32_t a1, sc, b1, b2, offs, mask, hist, sh, sel, sloff, cnt, total;
+};
+__host__ __device__ inline StepExtra step_extra(int M, int rows1) {
+  StepExtra X;
+  uint32_t o = 0;
+  auto take = [&](uint32_t bytes) {
+    const uint32_t at = o;
+    o = (o + bytes + 15u) & ~15u;
+    return at;
+  };
+  X.a1 = take(4u * rows1);
+  X.sc = take(4u * M);
+  X.b1 = take(4u * rows1);
+  X.b2 = take(4u * M);
+  X.offs = take(4u * (M + 1));
+  X.mask = take(4u * 32);
+  X.hist = take(4u * 256);
+  X.sh = take(16);
+  X.sel = take(4u * M);
+  X.sloff = take(4u * (M + 1));
+  X.cnt = take(16);
+  X.total = o;
+  return X;
+}
+
 struct StepArgs {
   HeadArgs h;               // head part; h.sel / sel_count / sl_off point to the step outputs
   const void* W1;
@@ -31,7 +58,8 @@ struct StepArgs {
   const void* e;
   float* scores;            // [B][M]
   float* mpart;             // [KS][B][rows1]
-  int32_t B, h_r, rows1, KC, KS, k, w2_prefetch;
+  uint32_t* maskbuf;        // [B][32] per-row selection masks (tree mode)
+  int32_t B, h_r, rows1, KC, KS, k, w2_prefetch, extra_bytes;
   unsigned* ctr;            // [0] merge ticket, [1] phase-A count, [2] selections published
   unsigned long long* trace;  // opt-in phase timestamps (nullptr)
 };
@@ -75,110 +103,136 @@ __device__ void step_phase_a(const StepArgs& s) {
   }
 }
 
-// Layer 2 + selection for the rows this CTA owns; returns after publishing.
+// Router layer 2 + TopK mask of row b (whole CTA): a1 -> scores -> radix select.
 template <typename T>
-__device__ void step_phase_b(const StepArgs& s, const HeadCtx& c, uint64_t* w2bar) {
+__device__ void step_row_select(const StepArgs& s, uint8_t* ex, const StepExtra& X, const T* W2, int b,
+                                bool write_scores) {
   const int M = s.h.M;
-  float* a1 = reinterpret_cast<float*>(c.extra);
-  float* sc = a1 + 1024;
-  float* b1s = sc + 1024;
-  float* b2s = b1s + 1024;
-  int32_t* offs = reinterpret_cast<int32_t*>(b2s + 1024);
-  uint8_t* flags = reinterpret_cast<uint8_t*>(offs + 1028);
-  int* scratch = reinterpret_cast<int*>(flags + 1024);
-  const T* W2 = s.w2_prefetch ? reinterpret_cast<const T*>(c.ring) : static_cast<const T*>(s.W2);
-  if (threadIdx.x == 0) spin_until_geq(s.ctr + 1, gridDim.x);  // all layer-1 partials visible
-  trace_mark(s.trace, 8);
-  if (s.w2_prefetch) mbar_wait(w2bar, 0);
+  float* a1 = reinterpret_cast<float*>(ex + X.a1);
+  float* sc = reinterpret_cast<float*>(ex + X.sc);
+  router_hidden(s.mpart, s.KS, s.B, b, s.rows1, reinterpret_cast<const float*>(ex + X.b1), s.h_r > 0, a1);
   __syncthreads();
-  trace_mark(s.trace, 9);
-  for (int m = threadIdx.x; m < M; m += blockDim.x) flags[m] = 0;
-  const bool shared = s.h.shared != 0;
-  const int b_lo = shared ? 0 : blockIdx.x;
-  const int b_step = shared ? 1 : gridDim.x;
-  int published = 0;
-  for (int b = b_lo; b < s.B; b += b_step) {
-    __syncthreads();
-    router_hidden(s.mpart, s.KS, s.B, b, s.rows1, b1s, s.h_r > 0, a1);
-    __syncthreads();
-    if (s.h_r > 0) {
-      router_out<T>(W2, a1, b2s, M, s.h_r, sc);
-    } else {
-      for (int m = threadIdx.x; m < M; m += blockDim.x) sc[m] = a1[m];
-    }
-    __syncthreads();
+  trace_mark(s.trace, 11);
+  if (s.h_r > 0) {
+    router_scores_fast<T>(W2, a1, reinterpret_cast<const float*>(ex + X.b2), M, s.h_r, sc);
+  } else {
+    for (int m = threadIdx.x; m < M; m += blockDim.x) sc[m] = a1[m];
+  }
+  __syncthreads();
+  trace_mark(s.trace, 12);
+  if (write_scores)
     for (int m = threadIdx.x; m < M; m += blockDim.x) s.scores[(size_t)b * M + m] = sc[m];
-    rank_select(sc, M, s.k, flags);
-    if (!shared) {
-      __syncthreads();
-      emit_selection(flags, M, offs, const_cast<int32_t*>(s.h.sel) + (size_t)b * M,
-                     const_cast<int32_t*>(s.h.sel_count) + b, const_cast<int32_t*>(s.h.sl_off) + (size_t)b * (M + 1),
-                     scratch);
-      __syncthreads();
-      for (int m = threadIdx.x; m < M; m += blockDim.x) flags[m] = 0;
-      ++published;
-    }
-  }
-  if (shared) {
-    __syncthreads();
-    emit_selection(flags, M, offs, const_cast<int32_t*>(s.h.sel), const_cast<int32_t*>(s.h.sel_count),
-                   const_cast<int32_t*>(s.h.sl_off), scratch);
-    published = 1;
-  }
-  __threadfence();
-  __syncthreads();
-  trace_mark(s.trace, 10);
-  if (threadIdx.x == 0 && published) atomicAdd(s.ctr + 2, (unsigned)published);
+  radix_topk_mask(sc, M, s.k, reinterpret_cast<uint32_t*>(ex + X.mask), reinterpret_cast<int*>(ex + X.hist),
+                  reinterpret_cast<int*>(ex + X.sh));
+  trace_mark(s.trace, 13);
 }
 
 template <typename T>
 __global__ void __launch_bounds__((kMaxStages + 1) * 32, 1) step_kernel(const StepArgs s) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  const HeadArgs& a = s.h;
-  const HeadSmem L = head_smem(a.stages, a.stage_bytes, a.nrows, a.d, (int)sizeof(T), a.lcap, kStepExtra);
+  HeadArgs a = s.h;
+  const HeadSmem L = head_smem(a.stages, a.stage_bytes, a.nrows, a.d, (int)sizeof(T), a.lcap, s.extra_bytes);
   const HeadCtx c = head_ctx(smem, L);
+  const StepExtra X = step_extra(a.M, s.rows1);
+  uint8_t* ex = c.extra;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int M = a.M;
   const bool shared = a.shared != 0;
-  const int nsel_rows = shared ? 1 : s.B;
-  const bool selector = shared ? blockIdx.x == 0 : (int)blockIdx.x < s.B;
+  const bool local = !shared && s.B == 1;  // every CTA selects for itself: no publish round trip
+  const bool row_cta = local || (int)blockIdx.x < s.B;
   uint64_t* w2bar = c.full + 2 * kMaxStages;  // spare barrier slot
+  const bool prefetch = row_cta && s.w2_prefetch > 0;
   if (threadIdx.x == 0) {
     head_init_barriers(c, a.stages);
-    if (selector && s.w2_prefetch) {
+    if (prefetch) {
       mbar_init(w2bar, 1);
       fence_mbar_init();
     }
   }
   __syncthreads();
   // Router constants do not depend on upstream work: stage them before waiting on the previous
-  // kernel (W2 by TMA into the idle ring; b1, b2, offsets by plain loads into `extra`).
-  if (selector) {
-    if (s.w2_prefetch && threadIdx.x == 0) {
+  // kernel (W2 by TMA into the idle ring; b1, b2, offsets by plain loads).
+  if (row_cta) {
+    if (prefetch && threadIdx.x == 0) {
       mbar_arrive_expect_tx(w2bar, (uint32_t)s.w2_prefetch);
       bulk_g2s(c.ring, s.W2, (uint32_t)s.w2_prefetch, w2bar, policy_evict_last());
     }
-    float* b1s = reinterpret_cast<float*>(c.extra) + 2048;
-    float* b2s = b1s + 1024;
-    int32_t* offs = reinterpret_cast<int32_t*>(b2s + 1024);
+    float* b1s = reinterpret_cast<float*>(ex + X.b1);
+    float* b2s = reinterpret_cast<float*>(ex + X.b2);
+    int32_t* offs = reinterpret_cast<int32_t*>(ex + X.offs);
     for (int u = threadIdx.x; u < s.rows1; u += blockDim.x) b1s[u] = __ldg(s.b1 + u);
-    for (int m = threadIdx.x; m < a.M; m += blockDim.x) b2s[m] = s.h_r > 0 ? __ldg(s.b2 + m) : 0.f;
-    for (int m = threadIdx.x; m <= a.M; m += blockDim.x) offs[m] = __ldg(a.offsets + m);
+    for (int m = threadIdx.x; m < M; m += blockDim.x) b2s[m] = s.h_r > 0 ? __ldg(s.b2 + m) : 0.f;
+    for (int m = threadIdx.x; m <= M; m += blockDim.x) offs[m] = __ldg(a.offsets + m);
   }
   trace_mark(s.trace, 0);
   if (a.pdl) pdl_wait();  // h_prev / e / h_new come from upstream kernels
   trace_mark(s.trace, 1);
-  // h_new -> smem (consumer warps), layer-1 partials (all warps)
   head_load_h(a, c, (int)sizeof(T), threadIdx.x, blockDim.x);
-  step_phase_a<T>(s);
+  step_phase_a<T>(s);  // router layer 1, split over every warp of every CTA
   __threadfence();
   __syncthreads();
   trace_mark(s.trace, 2);
   if (threadIdx.x == 0) atomicAdd(s.ctr + 1, 1u);
-  if (selector) step_phase_b<T>(s, c, w2bar);
-  if (threadIdx.x == 0) spin_until_geq(s.ctr + 2, (unsigned)nsel_rows);  // selections published
-  __syncthreads();
+
+  int32_t* sel_s = reinterpret_cast<int32_t*>(ex + X.sel);
+  int32_t* sloff_s = reinterpret_cast<int32_t*>(ex + X.sloff);
+  int32_t* cnt_s = reinterpret_cast<int32_t*>(ex + X.cnt);
+  uint32_t* mask = reinterpret_cast<uint32_t*>(ex + X.mask);
+  const int32_t* offs = reinterpret_cast<const int32_t*>(ex + X.offs);
+  const int mwords = (M + 31) / 32;
+  if (row_cta) {
+    if (threadIdx.x == 0) spin_until_geq(s.ctr + 1, gridDim.x);  // all layer-1 partials visible
+    trace_mark(s.trace, 8);
+    if (prefetch) mbar_wait(w2bar, 0);
+    __syncthreads();
+    const T* W2 = prefetch ? reinterpret_cast<const T*>(c.ring) : static_cast<const T*>(s.W2);
+    const int b = local ? 0 : (int)blockIdx.x;
+    step_row_select<T>(s, ex, X, W2, b, !local || blockIdx.x == 0);
+    if (local) {
+      if (warp == 0) emit_mask_warp(mask, M, offs, sel_s, cnt_s, sloff_s);
+      if (warp == 1 && blockIdx.x == 0)
+        emit_mask_warp(mask, M, offs, const_cast<int32_t*>(a.sel), const_cast<int32_t*>(a.sel_count),
+                       const_cast<int32_t*>(a.sl_off));
+    } else if (shared) {
+      for (int i = threadIdx.x; i < mwords; i += blockDim.x) s.maskbuf[(size_t)b * 32 + i] = mask[i];
+    } else if (warp == 0) {
+      emit_mask_warp(mask, M, offs, const_cast<int32_t*>(a.sel) + (size_t)b * M,
+                     const_cast<int32_t*>(a.sel_count) + b, const_cast<int32_t*>(a.sl_off) + (size_t)b * (M + 1));
+    }
+    __threadfence();
+    __syncthreads();
+    trace_mark(s.trace, 10);
+    if (!local && threadIdx.x == 0) atomicAdd(s.ctr + 2, 1u);
+  }
+  if (!local) {
+    if (threadIdx.x == 0) spin_until_geq(s.ctr + 2, (unsigned)s.B);  // every row's selection published
+    __syncthreads();
+    if (shared) {  // union over the depth's rows (R9), formed by every CTA
+      int32_t* offs_g = reinterpret_cast<int32_t*>(ex + X.offs);
+      if (!row_cta)
+        for (int m = threadIdx.x; m <= M; m += blockDim.x) offs_g[m] = __ldg(a.offsets + m);
+      for (int i = threadIdx.x; i < mwords; i += blockDim.x) {
+        uint32_t u = 0;
+        for (int b = 0; b < s.B; ++b) u |= __ldcg(s.maskbuf + (size_t)b * 32 + i);
+        mask[i] = u;
+      }
+      __syncthreads();
+      if (warp == 0) emit_mask_warp(mask, M, offs, sel_s, cnt_s, sloff_s);
+      if (warp == 1 && blockIdx.x == 0)
+        emit_mask_warp(mask, M, offs, const_cast<int32_t*>(a.sel), const_cast<int32_t*>(a.sel_count),
+                       const_cast<int32_t*>(a.sl_off));
+      __syncthreads();
+    }
+  } else {
+    __syncthreads();
+  }
   trace_mark(s.trace, 3);
-  if (selector && s.w2_prefetch) fence_proxy_async_smem();  // generic reads of W2 before TMA reuse
+  if (local || shared) {  // the head reads this CTA's own copy of the selection
+    a.sel = sel_s;
+    a.sel_count = cnt_s;
+    a.sl_off = sloff_s;
+  }
+  if (prefetch) fence_proxy_async_smem();  // generic reads of W2 in the ring before TMA reuse
   head_segments(a, c);
   __syncthreads();
   trace_mark(s.trace, 4);
@@ -193,6 +247,7 @@ __global__ void __launch_bounds__((kMaxStages + 1) * 32, 1) step_kernel(const St
   head_partials(a, c);
   trace_mark(s.trace, 6);
   if (!head_ticket(a, c)) return;
+  trace_mark(s.trace, 14);
   head_merge(a, c, a.stages * a.stage_bytes);
   trace_mark(s.trace, 7);
   if (threadIdx.x == 0) {
@@ -206,8 +261,8 @@ __global__ void __launch_bounds__((kMaxStages + 1) * 32, 1) step_kernel(const St
 
 struct StepPlan {
   HeadPlan hp;
-  int rows1, KC, KS;
-  size_t mpart_bytes, scores_bytes, head_bytes, total;
+  int rows1, KC, KS, extra;
+  size_t mpart_bytes, scores_bytes, mask_bytes, head_bytes, total;
   int w2_bytes;
 };
 
@@ -215,18 +270,21 @@ static bool step_plan(const ds_clusters* c, const ds_router* r, int B, int k_t, 
                       StepPlan* p) {
   if (B > kMaxGroups) return false;
   if (r->M > 1024 || (r->h_r > 0 ? r->h_r : r->M) > 1024) return false;
-  if (!head_plan_ex(c, B, k_t, max_shortlist, kStepExtra, kMaxGroups, &p->hp)) return false;
+  if (B > num_sms()) return false;
+  p->rows1 = r->h_r > 0 ? r->h_r : r->M;
+  p->extra = (int)step_extra(r->M, p->rows1).total;
+  if (!head_plan_ex(c, B, k_t, max_shortlist, p->extra, kMaxGroups, &p->hp)) return false;
   if (p->hp.rows_per_launch < B) return false;  // one launch must hold every row
   if (!shared && B > p->hp.G) return false;
   const int E = r->dtype == DS_BF16 ? 8 : 4;
   const int esz = r->dtype == DS_BF16 ? 2 : 4;
-  p->rows1 = r->h_r > 0 ? r->h_r : r->M;
   p->KC = kStepCH * 32 * E;
   p->KS = (2 * r->d + p->KC - 1) / p->KC;
   p->mpart_bytes = align_up((size_t)p->KS * B * p->rows1 * sizeof(float), 256);
   p->scores_bytes = align_up((size_t)B * r->M * sizeof(float), 256);
+  p->mask_bytes = align_up((size_t)B * 32 * sizeof(uint32_t), 256);
   p->head_bytes = align_up(p->hp.part_bytes, 256);
-  p->total = 256 + p->mpart_bytes + p->scores_bytes + p->head_bytes;
+  p->total = 256 + p->mpart_bytes + p->scores_bytes + p->mask_bytes + p->head_bytes;
   const size_t w2 = r->h_r > 0 ? (size_t)r->M * r->h_r * esz : 0;
   p->w2_bytes = (w2 > 0 && w2 % 16 == 0 && w2 <= (size_t)p->hp.stages * p->hp.stage_bytes) ? (int)w2 : 0;
   return true;
@@ -276,7 +334,8 @@ cudaError_t launch_step(const ds_clusters* c, const ds_router* r, const void* h_
   unsigned* ctr = reinterpret_cast<unsigned*>(w8);
   float* mpart = reinterpret_cast<float*>(w8 + 256);
   float* sc = scores ? scores : reinterpret_cast<float*>(w8 + 256 + p.mpart_bytes);
-  float* hpart = reinterpret_cast<float*>(w8 + 256 + p.mpart_bytes + p.scores_bytes);
+  uint32_t* maskbuf = reinterpret_cast<uint32_t*>(w8 + 256 + p.mpart_bytes + p.scores_bytes);
+  float* hpart = reinterpret_cast<float*>(w8 + 256 + p.mpart_bytes + p.scores_bytes + p.mask_bytes);
   StepArgs s;
   fill_head_args(s.h, c, p.hp, h_new, 0, B, sel, sel_count, sl_offsets, shared, k_t, max_shortlist, top_ids,
                  top_logits, top_logp, lse, z_out, z_stride, hpart, ctr, pdl);
@@ -295,10 +354,12 @@ cudaError_t launch_step(const ds_clusters* c, const ds_router* r, const void* h_
   s.KS = p.KS;
   s.k = k;
   s.w2_prefetch = p.w2_bytes;
+  s.maskbuf = maskbuf;
+  s.extra_bytes = p.extra;
   s.ctr = ctr;
   s.trace = debug_trace();
   const int esz = c->dtype == DS_BF16 ? 2 : 4;
-  const size_t smem = head_smem(p.hp.stages, p.hp.stage_bytes, B, c->d, esz, p.hp.lcap, kStepExtra).total;
+  const size_t smem = head_smem(p.hp.stages, p.hp.stage_bytes, B, c->d, esz, p.hp.lcap, p.extra).total;
   return c->dtype == DS_BF16 ? launch_step_t<__nv_bfloat16>(s, smem, p.hp.G, st, pdl)
                              : launch_step_t<float>(s, smem, p.hp.G, st, pdl);
 }

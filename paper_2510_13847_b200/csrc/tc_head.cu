@@ -346,7 +346,7 @@ static bool tc_plan(const ds_clusters* c, int R, int k_t, int64_t max_shortlist,
   const int smax = max_smem_optin();
   p->S = 0;
   for (int S = 8; S >= 3; --S) {
-    if ((int64_t)S * kTcABytes < (int64_t)p->hp.G * p->hp.rec * 4 + p->hp.G) break;
+    if (S * kTcABytes < merge_smem_bytes(p->hp.G, k_t, kTcThreads / 32) || p->hp.G > 32 * (kTcThreads / 32)) break;
     if ((int)tc_smem(S, p->N, R, p->hp.lcap).total <= smax) {
       p->S = S;
       break;

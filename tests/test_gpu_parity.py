@@ -116,7 +116,7 @@ def test_exact_regime_pipeline(dtype, shared, fused):
     ro = _oracle_router(rt)
     k_t = 8
     st = Dy.DraftStep(c, r, B, k_t, shared=shared, z_out=True, two_streams=not fused)
-    assert (st.launches == 1) == fused
+    assert (st.launches == 1) == fused  # B = 3 rows: the tcgen05 head needs >= 4
     for t in range(4):
         hp, e, hn = S.step_inputs(B, d, t, dtype, "exact", h_r=h_r)
         st(hp.to(DEV), e.to(DEV), hn.to(DEV), t=t, k_max=8, k_min=2)
@@ -380,3 +380,65 @@ def test_error_codes():
     with pytest.raises(Dy.DynaspecError) as ei:   # k_t > k * min_size
         Dy.DraftStep(c, r, 1, 64)(z, z, z, t=0, k_max=1, k_min=1)
     assert ei.value.name == "DS_ERR_INVALID_BUDGET"
+
+
+# ------------------------------------------------------------------ tcgen05 shared-shortlist head (S5')
+
+@pytest.mark.parametrize("R,d", [(4, 256), (10, 200), (17, 512), (64, 128)])
+def test_tc_head_exact_bit_exact(R, d, monkeypatch):
+    """Tree rows sharing one shortlist on the tensor cores: every logit bit-exact vs the oracle
+    (exact regime keeps partial sums < 2^21 units), and identical to the CUDA-core path."""
+    Dy = _dyn()
+    V, M = 6007, 24
+    q = max(1, min(127, int((2 ** 21 / d) ** 0.5)))
+    W = S.lm_head(V, d, 0, "bf16", "exact", q=q)
+    tau, part = _partition(V, M)
+    c = Dy.Clusters.from_tau(W.to(DEV), torch.as_tensor(tau, dtype=torch.int32, device=DEV), M)
+    hn = S.hidden(R, d, 11, "bf16", "exact", q=q)
+    rng = np.random.default_rng(R)
+    for k in (1, 5, M):
+        sel = np.sort(rng.choice(M, k, replace=False)).astype(np.int32)
+        selt = torch.zeros((1, M), dtype=torch.int32)
+        selt[0, :k] = torch.as_tensor(sel)
+        off = torch.zeros((1, M + 1), dtype=torch.int32)
+        off[0, :k + 1] = torch.as_tensor(O.shortlist_offsets(sel, part["offsets"]), dtype=torch.int32)
+        cnt = torch.tensor([k], dtype=torch.int32)
+        outs = {}
+        for mode in ("tc", "cuda"):
+            monkeypatch.setenv("DS_DISABLE_TC", "0" if mode == "tc" else "1")
+            outs[mode] = Dy.head_forward(c, hn.to(DEV), selt.to(DEV), cnt.to(DEV), off.to(DEV), 8, shared=True,
+                                         z_out=True)
+        V_S = O.shortlist(sel, part["perm"], part["offsets"])
+        zref = O.head(f64(hn), f64(W), V_S)
+        n = len(V_S)
+        for r in range(R):
+            ztc = outs["tc"]["z"][r, :n].cpu().numpy()
+            assert np.array_equal(ztc, zref[r].astype(np.float32)), f"tc logits not exact (R={R}, d={d}, k={k})"
+            assert np.array_equal(ztc, outs["cuda"]["z"][r, :n].cpu().numpy())
+            check_topk(outs["tc"]["top_ids"][r].cpu().numpy(), outs["tc"]["top_logits"][r].cpu().numpy(),
+                       outs["tc"]["top_logp"][r].cpu().numpy(), outs["tc"]["lse"][r].item(), zref[r], V_S, 8,
+                       torch.float32, exact=True)
+            assert outs["tc"]["top_ids"][r].cpu().tolist() == outs["cuda"]["top_ids"][r].cpu().tolist()
+
+
+def test_tc_head_random_regime_qwen_full_size(monkeypatch):
+    """Qwen-2.5 head at full size (V=151936, d=3584, M=256), 10 tree rows, tcgen05 vs oracle."""
+    Dy = _dyn()
+    monkeypatch.setenv("DS_DISABLE_TC", "0")
+    C = S.CONFIGS["qwen25"]
+    W, rt, tau, part, c, r = _setup(C.V, C.d, C.M, C.h_r, "bf16", "random")
+    st = Dy.DraftStep(c, r, C.B, C.k_t, shared=True, z_out=True)
+    assert st.launches == 3
+    hp, e, hn = S.step_inputs(C.B, C.d, 0, "bf16", sibling_eps=0.1)
+    st(hp.to(DEV), e.to(DEV), hn.to(DEV), t=0, k_max=C.k_max, k_min=C.k_min)
+    torch.cuda.synchronize()
+    cnt = st.sel_count[0].item()
+    sel_gpu = st.sel[0, :cnt].cpu().numpy()
+    ref = O.draft_step(part, _oracle_router(rt), Rows(W), f64(hp), f64(e), f64(hn), 0, C.k_max, C.k_min, C.k_t,
+                       shared=True, sel_override=[sel_gpu] * C.B)
+    for b in range(C.B):
+        n = len(ref[b]["V_S"])
+        z = st.z[b, :n].cpu().numpy().astype(np.float64)
+        assert np.max(np.abs(z - ref[b]["z"])) <= 2e-2
+        check_topk(st.top_ids[b].cpu().numpy(), st.top_logits[b].cpu().numpy(), st.top_logp[b].cpu().numpy(),
+                   st.lse[b].item(), ref[b]["z"], ref[b]["V_S"], C.k_t, torch.bfloat16)
