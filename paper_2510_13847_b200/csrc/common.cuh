@@ -205,3 +205,24 @@ __device__ __forceinline__ int block_excl_scan(int v, int* scratch /* >= NT/32 +
 }
 
 }  // namespace ds
+
+namespace ds {
+// Release / acquire at GPU scope (lighter than the sequentially consistent __threadfence()).
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+// One thread: publish this CTA's prior writes (ordered before it by a __syncthreads) and count.
+__device__ __forceinline__ unsigned release_add(unsigned* ctr, unsigned v) {
+  fence_acq_rel_gpu();
+  return atomicAdd(ctr, v);
+}
+// One thread: wait until *ctr >= target with acquire semantics.
+__device__ __forceinline__ void acquire_wait_geq(const unsigned* ctr, unsigned target) {
+  while (ld_acquire_u32(ctr) < target) {
+  }
+  fence_acq_rel_gpu();
+}
+}  // namespace ds

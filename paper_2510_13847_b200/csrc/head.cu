@@ -61,7 +61,7 @@ bool head_plan_ex(const ds_clusters* c, int B, int k_t, int64_t max_shortlist, i
   const int smax = max_smem_optin();
   const int per_row = rowbytes + p->lcap * 8 + 16;
   const int want_rows = std::min(std::min(B, kMaxGroups), max_rows);
-  const int min_stages = std::max(2, (p->G + 31) / 32 - 1);  // merge: G <= 32 * warps
+  const int min_stages = 2;
   p->stages = 0;
   for (int st = kMaxStages; st >= min_stages; --st) {
     if (st * p->stage_bytes < merge_smem_bytes(p->G, k_t, st + 1)) break;

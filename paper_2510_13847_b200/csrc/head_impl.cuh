@@ -22,7 +22,8 @@ constexpr int kMaxGroups = 64;               // rows per launch
 constexpr int kStepExtra = 4096 * 4 + 4112 + 1024 + 256;
 // shared-memory bytes the last-CTA merge needs inside the ring
 __host__ __device__ inline int merge_smem_bytes(int G, int k_t, int nwarps) {
-  return G * (2 + 2 * k_t) * 4 + 2 * nwarps * k_t * 4 + nwarps * 4 + 64;
+  (void)nwarps;
+  return G * (2 + 2 * k_t) * 4 + 2 * G * k_t * 4 + 64;
 }
 
 struct HeadArgs {
@@ -52,7 +53,7 @@ void fill_head_args(HeadArgs& a, const ds_clusters* c, const HeadPlan& p, const 
                     float* z_out, int64_t z_stride, float* part, unsigned* counter, bool pdl);
 
 struct HeadSmem {
-  uint32_t ring, bars, info, misc, sega, segn, segi, h, zl, zid, extra, total;
+  uint32_t ring, bars, info, misc, red, sega, segn, segi, h, zl, zid, extra, total;
 };
 
 __host__ __device__ inline HeadSmem head_smem(int stages, int stage_bytes, int rows, int d, int esz, int lcap,
@@ -67,6 +68,8 @@ __host__ __device__ inline HeadSmem head_smem(int stages, int stage_bytes, int r
   o += kMaxStages * 16;
   L.misc = o;
   o += 16 * 4;
+  L.red = o;
+  o += 64 * 4;
   L.sega = o;
   o += kMaxGroups * 8;
   L.segn = o;
@@ -94,6 +97,7 @@ struct HeadCtx {
   uint64_t* empty;
   int4* info;
   int* misc;
+  float* red;  // block-reduction scratch (64 floats)
   long long* sega;
   int* segn;
   int* segi;   // index (into the group's selection) of the cluster holding the segment start
@@ -110,6 +114,7 @@ __device__ __forceinline__ HeadCtx head_ctx(uint8_t* smem, const HeadSmem& L) {
   c.empty = c.full + kMaxStages;
   c.info = reinterpret_cast<int4*>(smem + L.info);
   c.misc = reinterpret_cast<int*>(smem + L.misc);
+  c.red = reinterpret_cast<float*>(smem + L.red);
   c.sega = reinterpret_cast<long long*>(smem + L.sega);
   c.segn = reinterpret_cast<int*>(smem + L.segn);
   c.segi = reinterpret_cast<int*>(smem + L.segi);
@@ -294,89 +299,100 @@ __device__ __forceinline__ void head_load_h(const HeadArgs& a, const HeadCtx& c,
   for (size_t i = t0; i < nvec; i += nt) dst[i] = src[i];
 }
 
-// Per-CTA partial per row: top-k_t by (logit desc, id asc), max, sum exp(z - max).
+// Block-wide max / sum with a fixed reduction order (warp trees, then warps in index order).
+__device__ __forceinline__ float block_max(float v, float* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  v = warp_max(v);
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  float m = red[0];
+  for (int w = 1; w < nw; ++w) m = fmaxf(m, red[w]);
+  return m;
+}
+__device__ __forceinline__ float block_sum(float v, float* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  v = warp_sum(v);
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  float t = red[0];
+  for (int w = 1; w < nw; ++w) t += red[w];
+  return t;
+}
+
+// Per-CTA partial per row: (max, sum exp(z - max), top-k_t by (logit desc, id asc)).  The top-k_t
+// is found by counting ranks (each logit counts the logits that beat it) — one shallow pass over
+// the CTA's on-chip logits by the whole block instead of k_t dependent arg-max rounds.
 __device__ inline void head_partials(const HeadArgs& a, const HeadCtx& c) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  const int rec = 2 + 2 * a.k_t;
-  for (int r = warp; r < a.nrows; r += nw) {
+  const int K = a.k_t, rec = 2 + 2 * K;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  for (int r = 0; r < a.nrows; ++r) {
     const int gi = a.shared ? 0 : r;
-    const int n = c.segn[gi];
+    const int n = c.segn[gi] > 0 ? c.segn[gi] : 0;
     float* P = a.part + ((size_t)blockIdx.x * a.nrows + r) * rec;
     const float* zr = c.zl + r * a.lcap;
     const int* ir = c.zid + r * a.lcap;
-    float pv = INFINITY, mx = -INFINITY;
-    int pid = -1;
-    for (int qq = 0; qq < a.k_t; ++qq) {
-      float bv = -INFINITY;
-      int bid = INT_MAX, aux = 0;
-      for (int j = lane; j < n; j += 32) {
-        const float v = zr[j];
-        const int id = ir[j];
-        if (beats(pv, pid, v, id) && beats(v, id, bv, bid)) {
-          bv = v;
-          bid = id;
-        }
-      }
-      warp_best(bv, bid, aux);
-      if (qq == 0) mx = bv;
-      if (lane == 0) {
-        P[2 + 2 * qq] = bv;
-        P[3 + 2 * qq] = __int_as_float(bid);
-      }
-      pv = bv;
-      pid = bid;
-      if (bv == -INFINITY) {  // exhausted: pad the rest
-        for (int q2 = qq + 1 + lane; q2 < a.k_t; q2 += 32) {
-          P[2 + 2 * q2] = -INFINITY;
-          P[3 + 2 * q2] = __int_as_float(INT_MAX);
-        }
-        break;
+    float mx = -INFINITY;
+    for (int j = tid; j < n; j += nt) mx = fmaxf(mx, zr[j]);
+    mx = block_max(mx, c.red);
+    for (int j = tid; j < n; j += nt) {
+      const float v = zr[j];
+      const int id = ir[j];
+      int rank = 0;
+      for (int i = 0; i < n; ++i) rank += beats(zr[i], ir[i], v, id);
+      if (rank < K) {
+        P[2 + 2 * rank] = v;
+        P[3 + 2 * rank] = __int_as_float(id);
       }
     }
+    for (int q = n + tid; q < K; q += nt) {
+      P[2 + 2 * q] = -INFINITY;
+      P[3 + 2 * q] = __int_as_float(INT_MAX);
+    }
     float se = 0.f;
-    for (int j = lane; j < n; j += 32) se += expf(zr[j] - mx);
-    se = warp_sum(se);
-    if (lane == 0) {
+    for (int j = tid; j < n; j += nt) se += expf(zr[j] - mx);
+    se = block_sum(se, c.red);
+    if (tid == 0) {
       P[0] = mx;
       P[1] = se;
     }
   }
 }
 
-// Ticket: returns true in the last CTA to finish (all partials visible).
+// Ticket: true in the last CTA to finish (release/acquire: all partials visible to it).
 __device__ __forceinline__ bool head_ticket(const HeadArgs& a, const HeadCtx& c) {
-  __threadfence();
   __syncthreads();
-  if (threadIdx.x == 0) c.misc[0] = (atomicAdd(a.counter, 1u) == (unsigned)(gridDim.x - 1)) ? 1 : 0;
+  if (threadIdx.x == 0) {
+    const bool last = release_add(a.counter, 1u) == (unsigned)(gridDim.x - 1);
+    if (last) fence_acq_rel_gpu();
+    c.misc[0] = last ? 1 : 0;
+  }
   __syncthreads();
-  const bool last = c.misc[0] != 0;
-  if (last) __threadfence();
-  return last;
+  return c.misc[0] != 0;
 }
 
-// Last CTA: merge the G partials of every row in CTA order -> lse, top ids (remapped), logp.
-// Rows are merged one after another by the whole CTA: the G records are staged in shared memory
-// (all loads in flight at once), each warp merges a slice of the G sorted lists (k_t rounds of a
-// warp arg-max), and warp 0 merges the per-warp results — two short levels instead of one long.
+// Last CTA: merge the G partials of every row -> lse, top ids (remapped), logp.
+//  lse  = M + log sum_g S_g exp(m_g - M)            (fixed-order block reduction)
+//  top  : T = the k_t-th best list head; only entries not beaten by T can be in the global
+//         top-k_t (k_t heads are >= T), so rank-count just those survivors.
 __device__ inline void head_merge(const HeadArgs& a, const HeadCtx& c, int ring_bytes) {
   const int G = gridDim.x;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, nw = blockDim.x >> 5;
-  const int K = a.k_t;
-  const int rec = 2 + 2 * K;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int K = a.k_t, rec = 2 + 2 * K;
   const int per_row = G * rec;
-  float* R = reinterpret_cast<float*>(c.ring);          // [G][rec]
-  float* L1v = R + per_row;                             // [nw][K] level-1 values
-  int* L1i = reinterpret_cast<int*>(L1v + nw * K);      // [nw][K] level-1 ids
-  float* red = reinterpret_cast<float*>(L1i + nw * K);  // [nw] partial max / sums
+  float* R = reinterpret_cast<float*>(c.ring);         // [G][rec]
+  float* sv = R + per_row;                             // survivors: values
+  int* si = reinterpret_cast<int*>(sv + G * K);        // survivors: ids
   (void)ring_bytes;
   for (int r = 0; r < a.nrows; ++r) {
     const float* src = a.part + (size_t)r * rec;
     constexpr int U = 8;
-    for (int base = tid; base < per_row; base += U * blockDim.x) {
+    for (int base = tid; base < per_row; base += U * nt) {
       float v[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        const int idx = base + u * blockDim.x;
+        const int idx = base + u * nt;
         if (idx < per_row) {
           const int gg = idx / rec, f = idx - gg * rec;
           v[u] = __ldcg(src + (size_t)gg * a.nrows * rec + f);
@@ -384,71 +400,72 @@ __device__ inline void head_merge(const HeadArgs& a, const HeadCtx& c, int ring_
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        const int idx = base + u * blockDim.x;
+        const int idx = base + u * nt;
         if (idx < per_row) R[idx] = v[u];
       }
     }
+    if (tid == 0) {
+      c.misc[3] = 0;                      // survivor count
+      c.misc[4] = __float_as_int(-INFINITY);
+      c.misc[5] = INT_MAX;                // threshold (value, id): sentinel = keep everything
+    }
     __syncthreads();
-    // global max and sum of rescaled partial sums (fixed order: CTA-strided per warp, then warps)
     float mx = -INFINITY;
-    for (int gg = tid; gg < G; gg += blockDim.x) mx = fmaxf(mx, R[gg * rec]);
-    mx = warp_max(mx);
-    if (lane == 0) red[warp] = mx;
-    __syncthreads();
-    mx = red[0];
-    for (int w = 1; w < nw; ++w) mx = fmaxf(mx, red[w]);
-    __syncthreads();
+    for (int g = tid; g < G; g += nt) mx = fmaxf(mx, R[g * rec]);
+    mx = block_max(mx, c.red);
     float S = 0.f;
-    for (int gg = tid; gg < G; gg += blockDim.x) {
-      const float m = R[gg * rec];
-      if (m > -INFINITY) S += R[gg * rec + 1] * expf(m - mx);
+    for (int g = tid; g < G; g += nt) {
+      const float m = R[g * rec];
+      if (m > -INFINITY) S += R[g * rec + 1] * expf(m - mx);
     }
-    S = warp_sum(S);
-    if (lane == 0) red[warp] = S;
-    // level 1: warp w merges lists g = w, w + nw, ... (lane j holds list w + j*nw; G <= 32 nw)
-    {
-      const int g0 = warp + lane * nw;
-      int p = 0;
-      for (int qq = 0; qq < K; ++qq) {
-        float v = -INFINITY;
-        int id = INT_MAX, who = lane;
-        if (g0 < G && p < K) {
-          v = R[g0 * rec + 2 + 2 * p];
-          id = __float_as_int(R[g0 * rec + 3 + 2 * p]);
-        }
-        warp_best(v, id, who);
-        if (lane == who) ++p;
-        if (lane == 0) {
-          L1v[warp * K + qq] = v;
-          L1i[warp * K + qq] = id;
+    S = block_sum(S, c.red);
+    // threshold: the K-th best head
+    for (int g = tid; g < G; g += nt) {
+      const float hv = R[g * rec + 2];
+      const int hid = __float_as_int(R[g * rec + 3]);
+      if (hv > -INFINITY) {
+        int rank = 0;
+        for (int g2 = 0; g2 < G; ++g2) rank += beats(R[g2 * rec + 2], __float_as_int(R[g2 * rec + 3]), hv, hid);
+        if (rank == K - 1) {
+          c.misc[4] = __float_as_int(hv);
+          c.misc[5] = hid;
         }
       }
     }
     __syncthreads();
-    if (warp == 0) {
-      float St = 0.f;
-      for (int w = 0; w < nw; ++w) St += red[w];
-      const bool ok = shortlist_len(a, a.shared ? 0 : r) >= 0;
-      const float lse = ok ? mx + logf(St) : __int_as_float(0x7fc00000);
-      int p = 0;
-      for (int qq = 0; qq < K; ++qq) {
-        float v = -INFINITY;
-        int id = INT_MAX, who = lane;
-        if (lane < nw && p < K) {
-          v = L1v[lane * K + p];
-          id = L1i[lane * K + p];
-        }
-        warp_best(v, id, who);
-        if (lane == who) ++p;
-        if (lane == 0) {
-          const bool valid = ok && v > -INFINITY;
-          a.top_ids[(size_t)r * K + qq] = valid ? id : -1;
-          a.top_logits[(size_t)r * K + qq] = valid ? v : -INFINITY;
-          a.top_logp[(size_t)r * K + qq] = valid ? v - lse : -INFINITY;
-        }
+    const float tv = __int_as_float(c.misc[4]);
+    const int tidv = c.misc[5];
+    for (int e = tid; e < G * K; e += nt) {
+      const int g = e / K, j = e - g * K;
+      const float v = R[g * rec + 2 + 2 * j];
+      const int id = __float_as_int(R[g * rec + 3 + 2 * j]);
+      if (v > -INFINITY && !beats(tv, tidv, v, id)) {
+        const int slot = atomicAdd(&c.misc[3], 1);
+        sv[slot] = v;
+        si[slot] = id;
       }
-      if (lane == 0) a.lse[r] = lse;
     }
+    __syncthreads();
+    const int ns = c.misc[3];
+    const bool ok = shortlist_len(a, a.shared ? 0 : r) >= 0;
+    const float lse = ok ? mx + logf(S) : __int_as_float(0x7fc00000);
+    for (int s2 = tid; s2 < ns; s2 += nt) {
+      const float v = sv[s2];
+      const int id = si[s2];
+      int rank = 0;
+      for (int i = 0; i < ns; ++i) rank += beats(sv[i], si[i], v, id);
+      if (rank < K) {
+        a.top_ids[(size_t)r * K + rank] = ok ? id : -1;
+        a.top_logits[(size_t)r * K + rank] = ok ? v : -INFINITY;
+        a.top_logp[(size_t)r * K + rank] = ok ? v - lse : -INFINITY;
+      }
+    }
+    for (int q = ns + tid; q < K; q += nt) {
+      a.top_ids[(size_t)r * K + q] = -1;
+      a.top_logits[(size_t)r * K + q] = -INFINITY;
+      a.top_logp[(size_t)r * K + q] = -INFINITY;
+    }
+    if (tid == 0) a.lse[r] = lse;
     __syncthreads();
   }
 }

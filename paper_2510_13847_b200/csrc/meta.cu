@@ -29,21 +29,24 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(const float* __rest
                                                              const int32_t* __restrict__ k_per_row, int shared,
                                                              int32_t* sel, int32_t* sel_count, int32_t* sl_off) {
   __shared__ __align__(16) float s[kMaxM];
-  __shared__ uint8_t flags[kMaxM];
-  __shared__ int scratch[33];
+  __shared__ uint32_t mask[kMaxM / 32], acc[kMaxM / 32];
+  __shared__ int32_t tmp[kMaxM];
   __shared__ int32_t offs[kMaxM + 1];
+  const int words = (M + 31) / 32;
   for (int m = threadIdx.x; m <= M; m += blockDim.x) offs[m] = offsets[m];
-  for (int m = threadIdx.x; m < M; m += blockDim.x) flags[m] = 0;
+  for (int w = threadIdx.x; w < words; w += blockDim.x) acc[w] = 0u;
   const int r_lo = shared ? 0 : blockIdx.x, r_hi = shared ? B : blockIdx.x + 1;
   for (int r = r_lo; r < r_hi; ++r) {
     __syncthreads();
     for (int m = threadIdx.x; m < M; m += blockDim.x) s[m] = scores[(size_t)r * M + m];
     __syncthreads();
-    rank_select(s, M, k_per_row ? k_per_row[r] : k, flags);
+    rank_mask(s, M, k_per_row ? k_per_row[r] : k, mask);
+    __syncthreads();
+    for (int w = threadIdx.x; w < words; w += blockDim.x) acc[w] |= mask[w];
   }
   __syncthreads();
   const int o = shared ? 0 : blockIdx.x;
-  emit_selection(flags, M, offs, sel + (size_t)o * M, sel_count + o, sl_off + (size_t)o * (M + 1), scratch);
+  emit_fast(acc, M, offs, sel + (size_t)o * M, sel_count + o, sl_off + (size_t)o * (M + 1), tmp);
 }
 
 // ------------------------------------------------------------------ layer 1: split-K partials
@@ -113,8 +116,8 @@ __global__ void __launch_bounds__(kMetaThreads) meta_l2_kernel(const float* __re
                                                                unsigned* counter, int pdl) {
   __shared__ __align__(16) float a1[kMaxM];
   __shared__ __align__(16) float s[kMaxM];
-  __shared__ uint8_t flags[kMaxM];
-  __shared__ int scratch[33];
+  __shared__ uint32_t mask[kMaxM / 32], acc[kMaxM / 32];
+  __shared__ int32_t tmp[kMaxM];
   __shared__ int is_last;
   __shared__ float b1s[kMaxM];
   __shared__ float b2s[kMaxM];
@@ -130,39 +133,39 @@ __global__ void __launch_bounds__(kMetaThreads) meta_l2_kernel(const float* __re
   router_hidden(part, KS, B, b, rows1, b1s, h_r > 0, a1);
   __syncthreads();
   if (h_r > 0) {
-    router_out<T>(W2, a1, b2s, M, h_r, s);
+    router_scores_thread<T>(W2, a1, b2s, M, h_r, s);
   } else {
     for (int m = threadIdx.x; m < M; m += blockDim.x) s[m] = a1[m];
   }
   __syncthreads();
-  for (int m = threadIdx.x; m < M; m += blockDim.x) {
-    scores[(size_t)b * M + m] = s[m];
-    flags[m] = 0;
-  }
+  const int words = (M + 31) / 32;
+  for (int m = threadIdx.x; m < M; m += blockDim.x) scores[(size_t)b * M + m] = s[m];
   if (sel == nullptr) return;
-  __syncthreads();
   if (pdl) pdl_launch_dependents();
+  rank_mask(s, M, k_per_row ? k_per_row[b] : k, mask);
+  __syncthreads();
   if (!shared) {
-    rank_select(s, M, k_per_row ? k_per_row[b] : k, flags);
-    __syncthreads();
-    emit_selection(flags, M, offs, sel + (size_t)b * M, sel_count + b, sl_off + (size_t)b * (M + 1), scratch);
+    emit_fast(mask, M, offs, sel + (size_t)b * M, sel_count + b, sl_off + (size_t)b * (M + 1), tmp);
     return;
   }
-  // shared mode: the last row-CTA forms the union of every row's TopK
-  __threadfence();
+  // shared mode: the last row-CTA (scores of every row are published) forms the union of the TopKs
   __syncthreads();
-  if (threadIdx.x == 0) is_last = atomicAdd(counter, 1u) == (unsigned)(gridDim.x - 1);
+  if (threadIdx.x == 0) is_last = release_add(counter, 1u) == (unsigned)(gridDim.x - 1);
   __syncthreads();
   if (!is_last) return;
-  __threadfence();
+  if (threadIdx.x == 0) fence_acq_rel_gpu();
+  __syncthreads();
+  for (int w = threadIdx.x; w < words; w += blockDim.x) acc[w] = 0u;
   for (int r = 0; r < B; ++r) {
     __syncthreads();
     for (int m = threadIdx.x; m < M; m += blockDim.x) s[m] = __ldcg(scores + (size_t)r * M + m);
     __syncthreads();
-    rank_select(s, M, k_per_row ? k_per_row[r] : k, flags);
+    rank_mask(s, M, k_per_row ? k_per_row[r] : k, mask);
+    __syncthreads();
+    for (int w = threadIdx.x; w < words; w += blockDim.x) acc[w] |= mask[w];
   }
   __syncthreads();
-  emit_selection(flags, M, offs, sel, sel_count, sl_off, scratch);
+  emit_fast(acc, M, offs, sel, sel_count, sl_off, tmp);
   if (threadIdx.x == 0) *counter = 0u;
 }
 

@@ -23,7 +23,7 @@ constexpr int kStepCH = 2;  // 16-byte chunks per lane per layer-1 task
 
 // Shared-memory carve-up of the fused step's router/selection scratch (inside HeadSmem.extra).
 struct StepExtra {
-  uint32_t a1, sc, b1, b2, offs, mask, hist, sh, sel, sloff, cnt, total;
+  uint32_t a1, sc, b1, b2, offs, mask, hist, sh, sel, sloff, cnt, tmp, total;
 };
 __host__ __device__ inline StepExtra step_extra(int M, int rows1) {
   StepExtra X;
@@ -44,6 +44,7 @@ __host__ __device__ inline StepExtra step_extra(int M, int rows1) {
   X.sel = take(4u * M);
   X.sloff = take(4u * (M + 1));
   X.cnt = take(16);
+  X.tmp = take(4u * M);
   X.total = o;
   return X;
 }
@@ -114,7 +115,7 @@ __device__ void step_row_select(const StepArgs& s, uint8_t* ex, const StepExtra&
   __syncthreads();
   trace_mark(s.trace, 11);
   if (s.h_r > 0) {
-    router_scores_fast<T>(W2, a1, reinterpret_cast<const float*>(ex + X.b2), M, s.h_r, sc);
+    router_scores_thread<T>(W2, a1, reinterpret_cast<const float*>(ex + X.b2), M, s.h_r, sc);
   } else {
     for (int m = threadIdx.x; m < M; m += blockDim.x) sc[m] = a1[m];
   }
@@ -122,8 +123,8 @@ __device__ void step_row_select(const StepArgs& s, uint8_t* ex, const StepExtra&
   trace_mark(s.trace, 12);
   if (write_scores)
     for (int m = threadIdx.x; m < M; m += blockDim.x) s.scores[(size_t)b * M + m] = sc[m];
-  radix_topk_mask(sc, M, s.k, reinterpret_cast<uint32_t*>(ex + X.mask), reinterpret_cast<int*>(ex + X.hist),
-                  reinterpret_cast<int*>(ex + X.sh));
+  rank_mask(sc, M, s.k, reinterpret_cast<uint32_t*>(ex + X.mask));
+  __syncthreads();
   trace_mark(s.trace, 13);
 }
 
@@ -169,19 +170,19 @@ __global__ void __launch_bounds__((kMaxStages + 1) * 32, 1) step_kernel(const St
   trace_mark(s.trace, 1);
   head_load_h(a, c, (int)sizeof(T), threadIdx.x, blockDim.x);
   step_phase_a<T>(s);  // router layer 1, split over every warp of every CTA
-  __threadfence();
   __syncthreads();
   trace_mark(s.trace, 2);
-  if (threadIdx.x == 0) atomicAdd(s.ctr + 1, 1u);
+  if (threadIdx.x == 0) release_add(s.ctr + 1, 1u);
 
   int32_t* sel_s = reinterpret_cast<int32_t*>(ex + X.sel);
   int32_t* sloff_s = reinterpret_cast<int32_t*>(ex + X.sloff);
   int32_t* cnt_s = reinterpret_cast<int32_t*>(ex + X.cnt);
   uint32_t* mask = reinterpret_cast<uint32_t*>(ex + X.mask);
   const int32_t* offs = reinterpret_cast<const int32_t*>(ex + X.offs);
+  int32_t* tmp = reinterpret_cast<int32_t*>(ex + X.tmp);
   const int mwords = (M + 31) / 32;
   if (row_cta) {
-    if (threadIdx.x == 0) spin_until_geq(s.ctr + 1, gridDim.x);  // all layer-1 partials visible
+    if (threadIdx.x == 0) acquire_wait_geq(s.ctr + 1, gridDim.x);  // all layer-1 partials visible
     trace_mark(s.trace, 8);
     if (prefetch) mbar_wait(w2bar, 0);
     __syncthreads();
@@ -189,23 +190,24 @@ __global__ void __launch_bounds__((kMaxStages + 1) * 32, 1) step_kernel(const St
     const int b = local ? 0 : (int)blockIdx.x;
     step_row_select<T>(s, ex, X, W2, b, !local || blockIdx.x == 0);
     if (local) {
-      if (warp == 0) emit_mask_warp(mask, M, offs, sel_s, cnt_s, sloff_s);
-      if (warp == 1 && blockIdx.x == 0)
-        emit_mask_warp(mask, M, offs, const_cast<int32_t*>(a.sel), const_cast<int32_t*>(a.sel_count),
-                       const_cast<int32_t*>(a.sl_off));
+      emit_fast(mask, M, offs, sel_s, cnt_s, sloff_s, tmp);
+      if (blockIdx.x == 0) {  // CTA 0 also writes the caller's outputs
+        __syncthreads();
+        emit_fast(mask, M, offs, const_cast<int32_t*>(a.sel), const_cast<int32_t*>(a.sel_count),
+                  const_cast<int32_t*>(a.sl_off), tmp);
+      }
     } else if (shared) {
       for (int i = threadIdx.x; i < mwords; i += blockDim.x) s.maskbuf[(size_t)b * 32 + i] = mask[i];
-    } else if (warp == 0) {
-      emit_mask_warp(mask, M, offs, const_cast<int32_t*>(a.sel) + (size_t)b * M,
-                     const_cast<int32_t*>(a.sel_count) + b, const_cast<int32_t*>(a.sl_off) + (size_t)b * (M + 1));
+    } else {
+      emit_fast(mask, M, offs, const_cast<int32_t*>(a.sel) + (size_t)b * M, const_cast<int32_t*>(a.sel_count) + b,
+                const_cast<int32_t*>(a.sl_off) + (size_t)b * (M + 1), tmp);
     }
-    __threadfence();
     __syncthreads();
     trace_mark(s.trace, 10);
-    if (!local && threadIdx.x == 0) atomicAdd(s.ctr + 2, 1u);
+    if (!local && threadIdx.x == 0) release_add(s.ctr + 2, 1u);
   }
   if (!local) {
-    if (threadIdx.x == 0) spin_until_geq(s.ctr + 2, (unsigned)s.B);  // every row's selection published
+    if (threadIdx.x == 0) acquire_wait_geq(s.ctr + 2, (unsigned)s.B);  // every row's selection published
     __syncthreads();
     if (shared) {  // union over the depth's rows (R9), formed by every CTA
       int32_t* offs_g = reinterpret_cast<int32_t*>(ex + X.offs);
@@ -217,10 +219,12 @@ __global__ void __launch_bounds__((kMaxStages + 1) * 32, 1) step_kernel(const St
         mask[i] = u;
       }
       __syncthreads();
-      if (warp == 0) emit_mask_warp(mask, M, offs, sel_s, cnt_s, sloff_s);
-      if (warp == 1 && blockIdx.x == 0)
-        emit_mask_warp(mask, M, offs, const_cast<int32_t*>(a.sel), const_cast<int32_t*>(a.sel_count),
-                       const_cast<int32_t*>(a.sl_off));
+      emit_fast(mask, M, offs, sel_s, cnt_s, sloff_s, tmp);
+      if (blockIdx.x == 0) {
+        __syncthreads();
+        emit_fast(mask, M, offs, const_cast<int32_t*>(a.sel), const_cast<int32_t*>(a.sel_count),
+                  const_cast<int32_t*>(a.sl_off), tmp);
+      }
       __syncthreads();
     }
   } else {

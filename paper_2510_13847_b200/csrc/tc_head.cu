@@ -41,7 +41,7 @@ struct TcArgs {
 };
 
 struct TcSmem {
-  uint32_t a, b, bars, slot, misc, sega, segn, segi, boxes, zl, zid, total;
+  uint32_t a, b, bars, slot, misc, red, sega, segn, segi, boxes, zl, zid, total;
 };
 
 __host__ __device__ inline TcSmem tc_smem(int S, int N, int rows, int lcap) {
@@ -58,6 +58,8 @@ __host__ __device__ inline TcSmem tc_smem(int S, int N, int rows, int lcap) {
   o += 16;
   L.misc = o;
   o += 16 * 4;
+  L.red = o;
+  o += 64 * 4;
   L.sega = o;
   o += kMaxGroups * 8;
   L.segn = o;
@@ -138,6 +140,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_head_kernel(const __grid_con
   c.empty = empty;
   c.info = nullptr;
   c.misc = reinterpret_cast<int*>(smem + L.misc);
+  c.red = reinterpret_cast<float*>(smem + L.red);
   c.sega = reinterpret_cast<long long*>(smem + L.sega);
   c.segn = reinterpret_cast<int*>(smem + L.segn);
   c.segi = reinterpret_cast<int*>(smem + L.segi);

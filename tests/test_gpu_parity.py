@@ -352,7 +352,7 @@ def test_error_codes():
     W = S.lm_head(V, d, 0, "bf16").to(DEV)
     tau = torch.as_tensor(np.arange(V) % M, dtype=torch.int32, device=DEV)
     c = Dy.Clusters.from_tau(W, tau, M)
-    r = Dy.Router(*[x.to(DEV) for x in S.router(d, 4, M, 1, "bf16")])
+    r = Dy.Router(*[x.to(DEV) for x in S.router(d, 8, M, 1, "bf16")])
     s = torch.zeros((1, M), device=DEV)
     with pytest.raises(Dy.DynaspecError) as ei:
         Dy.select(s, c, M + 1)
