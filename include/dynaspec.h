@@ -240,10 +240,11 @@ int32_t dynaspec_draft_step_launches(const ds_clusters* c, const ds_router* r, i
                                      int32_t shared, int32_t two_streams);
 
 /* Debugging: when dev_buf != NULL, the fused step kernel records %globaltimer nanosecond
- * timestamps of its phases into dev_buf[cta * 32 + slot] and the SM clock64() into
- * dev_buf[cta * 32 + 16 + slot] (uint64, >= #SM * 32 entries):
+ * timestamps of its phases into dev_buf[cta * 64 + slot] and the SM clock64() into
+ * dev_buf[cta * 64 + 32 + slot] (uint64, >= #SM * 64 entries):
  * 0 start, 1 after PDL wait, 2 router layer 1 done, 3 selection visible, 4 segments ready,
- * 5 head streamed, 6 partials written, 7 merge done (last CTA), 8/9/10 selector phases.
+ * 5 head streamed, 6 partials written, 7 merge done (last CTA), 8..13 selection phases,
+ * 14 ticket won, 16..20 merge phases.
  * Pass NULL to disable (the default).  Not for concurrent use from several threads. */
 ds_status dynaspec_debug_set_trace(void* dev_buf);
 

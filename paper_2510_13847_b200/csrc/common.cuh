@@ -135,8 +135,8 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
 // Opt-in phase trace (dynaspec_debug_set_trace): [cta][slot] nanosecond timestamps.
 __device__ __forceinline__ void trace_mark(unsigned long long* t, int slot) {
   if (t != nullptr && threadIdx.x == 0) {
-    t[blockIdx.x * 32 + slot] = globaltimer_ns();
-    t[blockIdx.x * 32 + 16 + slot] = clock64();
+    t[blockIdx.x * 64 + slot] = globaltimer_ns();
+    t[blockIdx.x * 64 + 32 + slot] = clock64();
   }
 }
 
@@ -224,5 +224,98 @@ __device__ __forceinline__ void acquire_wait_geq(const unsigned* ctr, unsigned t
   while (ld_acquire_u32(ctr) < target) {
   }
   fence_acq_rel_gpu();
+}
+}  // namespace ds
+
+namespace ds {
+// Block-wide top-K of n items under (value desc, id asc) without a full O(n^2) rank:
+//   T0 = the K-th best of the first S = min(n, max(64, 4K)) items (the K-th best of a subset is
+//        never better than the K-th best of the whole set, so every member of the true top-K is
+//        >= T0);  survivors = items not beaten by T0;  rank-count the survivors only.
+// get(i) -> (v, id) for i < n (items with v == -inf are ignored); emit(rank, v, id) is called
+// once for each rank < min(K, #valid items).  sv / si: smem scratch for up to n survivors.
+// misc: 3 ints of smem.  All threads of the block must call it.
+template <class Get, class Emit>
+__device__ __forceinline__ void block_topk(int n, int K, Get get, Emit emit, float* sv, int* si, int* misc) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int S = min(n, max(64, 4 * K));
+  if (tid == 0) {
+    misc[0] = 0;
+    misc[1] = __float_as_int(-INFINITY);
+    misc[2] = INT_MAX;
+  }
+  __syncthreads();
+  for (int i = tid; i < S; i += nt) {
+    float v;
+    int id;
+    get(i, v, id);
+    if (v == -INFINITY) continue;
+    int rank = 0;
+    for (int j = 0; j < S; ++j) {
+      float v2;
+      int id2;
+      get(j, v2, id2);
+      rank += beats(v2, id2, v, id);
+    }
+    if (rank == K - 1) {
+      misc[1] = __float_as_int(v);
+      misc[2] = id;
+    }
+  }
+  __syncthreads();
+  const float tv = __int_as_float(misc[1]);
+  const int tid0 = misc[2];
+  for (int i = tid; i < n; i += nt) {
+    float v;
+    int id;
+    get(i, v, id);
+    if (v > -INFINITY && !beats(tv, tid0, v, id)) {
+      const int slot = atomicAdd(&misc[0], 1);
+      sv[slot] = v;
+      si[slot] = id;
+    }
+  }
+  __syncthreads();
+  const int ns = misc[0];
+  for (int s2 = tid; s2 < ns; s2 += nt) {
+    const float v = sv[s2];
+    const int id = si[s2];
+    int rank = 0;
+    for (int t = 0; t < ns; ++t) rank += beats(sv[t], si[t], v, id);
+    if (rank < K) emit(rank, v, id);
+  }
+  __syncthreads();
+}
+
+// Online-softmax pair combine: (m1, s1) + (m2, s2) -> (max, s1 e^{m1-M} + s2 e^{m2-M}).
+__device__ __forceinline__ void lse_combine(float& m, float& s, float m2, float s2) {
+  if (m2 == -INFINITY) return;
+  if (m == -INFINITY) {
+    m = m2;
+    s = s2;
+    return;
+  }
+  const float M = fmaxf(m, m2);
+  s = s * expf(m - M) + s2 * expf(m2 - M);
+  m = M;
+}
+// Block-wide (max, sum) combine with a fixed order (warp trees, then warps in index order).
+__device__ __forceinline__ void block_lse(float& m, float& s, float* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float m2 = __shfl_xor_sync(0xffffffffu, m, o);
+    const float s2 = __shfl_xor_sync(0xffffffffu, s, o);
+    lse_combine(m, s, m2, s2);
+  }
+  __syncthreads();
+  if (lane == 0) {
+    red[2 * warp] = m;
+    red[2 * warp + 1] = s;
+  }
+  __syncthreads();
+  m = red[0];
+  s = red[1];
+  for (int w = 1; w < nw; ++w) lse_combine(m, s, red[2 * w], red[2 * w + 1]);
 }
 }  // namespace ds

@@ -321,40 +321,43 @@ __device__ __forceinline__ float block_sum(float v, float* red) {
   return t;
 }
 
-// Per-CTA partial per row: (max, sum exp(z - max), top-k_t by (logit desc, id asc)).  The top-k_t
-// is found by counting ranks (each logit counts the logits that beat it) — one shallow pass over
-// the CTA's on-chip logits by the whole block instead of k_t dependent arg-max rounds.
+// Per-CTA partial per row: (max, sum exp(z - max), top-k_t by (logit desc, id asc)), computed by
+// the whole block with shallow dependency chains (block_topk, block_lse).  Scratch: the ring.
 __device__ inline void head_partials(const HeadArgs& a, const HeadCtx& c) {
   const int K = a.k_t, rec = 2 + 2 * K;
   const int tid = threadIdx.x, nt = blockDim.x;
+  float* sv = reinterpret_cast<float*>(c.ring);
+  int* si = reinterpret_cast<int*>(sv + a.lcap);
   for (int r = 0; r < a.nrows; ++r) {
     const int gi = a.shared ? 0 : r;
     const int n = c.segn[gi] > 0 ? c.segn[gi] : 0;
     float* P = a.part + ((size_t)blockIdx.x * a.nrows + r) * rec;
     const float* zr = c.zl + r * a.lcap;
     const int* ir = c.zid + r * a.lcap;
-    float mx = -INFINITY;
-    for (int j = tid; j < n; j += nt) mx = fmaxf(mx, zr[j]);
-    mx = block_max(mx, c.red);
+    float m = -INFINITY, se = 0.f;
     for (int j = tid; j < n; j += nt) {
-      const float v = zr[j];
-      const int id = ir[j];
-      int rank = 0;
-      for (int i = 0; i < n; ++i) rank += beats(zr[i], ir[i], v, id);
-      if (rank < K) {
-        P[2 + 2 * rank] = v;
-        P[3 + 2 * rank] = __int_as_float(id);
+      const float z = zr[j];
+      if (z > m) {
+        se = se * expf(m - z) + 1.f;
+        m = z;
+      } else {
+        se += expf(z - m);
       }
     }
+    block_lse(m, se, c.red);
+    block_topk(
+        n, K, [&](int i, float& v, int& id) { v = zr[i]; id = ir[i]; },
+        [&](int rank, float v, int id) {
+          P[2 + 2 * rank] = v;
+          P[3 + 2 * rank] = __int_as_float(id);
+        },
+        sv, si, c.misc + 8);
     for (int q = n + tid; q < K; q += nt) {
       P[2 + 2 * q] = -INFINITY;
       P[3 + 2 * q] = __int_as_float(INT_MAX);
     }
-    float se = 0.f;
-    for (int j = tid; j < n; j += nt) se += expf(zr[j] - mx);
-    se = block_sum(se, c.red);
     if (tid == 0) {
-      P[0] = mx;
+      P[0] = m;
       P[1] = se;
     }
   }
@@ -376,14 +379,15 @@ __device__ __forceinline__ bool head_ticket(const HeadArgs& a, const HeadCtx& c)
 //  lse  = M + log sum_g S_g exp(m_g - M)            (fixed-order block reduction)
 //  top  : T = the k_t-th best list head; only entries not beaten by T can be in the global
 //         top-k_t (k_t heads are >= T), so rank-count just those survivors.
-__device__ inline void head_merge(const HeadArgs& a, const HeadCtx& c, int ring_bytes) {
+__device__ inline void head_merge(const HeadArgs& a, const HeadCtx& c, int ring_bytes,
+                                  unsigned long long* trace = nullptr) {
   const int G = gridDim.x;
   const int tid = threadIdx.x, nt = blockDim.x;
   const int K = a.k_t, rec = 2 + 2 * K;
   const int per_row = G * rec;
   float* R = reinterpret_cast<float*>(c.ring);         // [G][rec]
   float* sv = R + per_row;                             // survivors: values
-  int* si = reinterpret_cast<int*>(sv + G * K);        // survivors: ids
+  int* si = reinterpret_cast<int*>(sv + G * K);        // survivors: ids (K best of each CTA at most)
   (void)ring_bytes;
   for (int r = 0; r < a.nrows; ++r) {
     const float* src = a.part + (size_t)r * rec;
@@ -404,69 +408,38 @@ __device__ inline void head_merge(const HeadArgs& a, const HeadCtx& c, int ring_
         if (idx < per_row) R[idx] = v[u];
       }
     }
-    if (tid == 0) {
-      c.misc[3] = 0;                      // survivor count
-      c.misc[4] = __float_as_int(-INFINITY);
-      c.misc[5] = INT_MAX;                // threshold (value, id): sentinel = keep everything
-    }
+    trace_mark(trace, 16);
     __syncthreads();
-    float mx = -INFINITY;
-    for (int g = tid; g < G; g += nt) mx = fmaxf(mx, R[g * rec]);
-    mx = block_max(mx, c.red);
-    float S = 0.f;
-    for (int g = tid; g < G; g += nt) {
-      const float m = R[g * rec];
-      if (m > -INFINITY) S += R[g * rec + 1] * expf(m - mx);
-    }
-    S = block_sum(S, c.red);
-    // threshold: the K-th best head
-    for (int g = tid; g < G; g += nt) {
-      const float hv = R[g * rec + 2];
-      const int hid = __float_as_int(R[g * rec + 3]);
-      if (hv > -INFINITY) {
-        int rank = 0;
-        for (int g2 = 0; g2 < G; ++g2) rank += beats(R[g2 * rec + 2], __float_as_int(R[g2 * rec + 3]), hv, hid);
-        if (rank == K - 1) {
-          c.misc[4] = __float_as_int(hv);
-          c.misc[5] = hid;
-        }
-      }
-    }
-    __syncthreads();
-    const float tv = __int_as_float(c.misc[4]);
-    const int tidv = c.misc[5];
-    for (int e = tid; e < G * K; e += nt) {
-      const int g = e / K, j = e - g * K;
-      const float v = R[g * rec + 2 + 2 * j];
-      const int id = __float_as_int(R[g * rec + 3 + 2 * j]);
-      if (v > -INFINITY && !beats(tv, tidv, v, id)) {
-        const int slot = atomicAdd(&c.misc[3], 1);
-        sv[slot] = v;
-        si[slot] = id;
-      }
-    }
-    __syncthreads();
-    const int ns = c.misc[3];
+    float mx = -INFINITY, S = 0.f;
+    for (int g = tid; g < G; g += nt) lse_combine(mx, S, R[g * rec], R[g * rec + 1]);
+    block_lse(mx, S, c.red);
+    trace_mark(trace, 17);
     const bool ok = shortlist_len(a, a.shared ? 0 : r) >= 0;
     const float lse = ok ? mx + logf(S) : __int_as_float(0x7fc00000);
-    for (int s2 = tid; s2 < ns; s2 += nt) {
-      const float v = sv[s2];
-      const int id = si[s2];
-      int rank = 0;
-      for (int i = 0; i < ns; ++i) rank += beats(sv[i], si[i], v, id);
-      if (rank < K) {
-        a.top_ids[(size_t)r * K + rank] = ok ? id : -1;
-        a.top_logits[(size_t)r * K + rank] = ok ? v : -INFINITY;
-        a.top_logp[(size_t)r * K + rank] = ok ? v - lse : -INFINITY;
-      }
-    }
-    for (int q = ns + tid; q < K; q += nt) {
+    // candidates (g, j) in list order: the first S items are the heads of lists 0.. and beyond
+    block_topk(
+        G * K, K,
+        [&](int e, float& v, int& id) {
+          const int j = e / G, g = e - j * G;  // rank-major order: all heads first
+          v = R[g * rec + 2 + 2 * j];
+          id = __float_as_int(R[g * rec + 3 + 2 * j]);
+        },
+        [&](int rank, float v, int id) {
+          a.top_ids[(size_t)r * K + rank] = ok ? id : -1;
+          a.top_logits[(size_t)r * K + rank] = ok ? v : -INFINITY;
+          a.top_logp[(size_t)r * K + rank] = ok ? v - lse : -INFINITY;
+        },
+        sv, si, c.misc + 8);
+    trace_mark(trace, 19);
+    const int nvalid = c.misc[8];
+    for (int q = nvalid + tid; q < K; q += nt) {
       a.top_ids[(size_t)r * K + q] = -1;
       a.top_logits[(size_t)r * K + q] = -INFINITY;
       a.top_logp[(size_t)r * K + q] = -INFINITY;
     }
     if (tid == 0) a.lse[r] = lse;
     __syncthreads();
+    trace_mark(trace, 20);
   }
 }
 

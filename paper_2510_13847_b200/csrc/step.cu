@@ -23,7 +23,7 @@ constexpr int kStepCH = 2;  // 16-byte chunks per lane per layer-1 task
 
 // Shared-memory carve-up of the fused step's router/selection scratch (inside HeadSmem.extra).
 struct StepExtra {
-  uint32_t a1, sc, b1, b2, offs, mask, hist, sh, sel, sloff, cnt, tmp, total;
+  uint32_t a1, sc, b1, b2, offs, mask, hist, sh, sel, sloff, cnt, tmp, sv, si, total;
 };
 __host__ __device__ inline StepExtra step_extra(int M, int rows1) {
   StepExtra X;
@@ -45,6 +45,8 @@ __host__ __device__ inline StepExtra step_extra(int M, int rows1) {
   X.sloff = take(4u * (M + 1));
   X.cnt = take(16);
   X.tmp = take(4u * M);
+  X.sv = take(4u * M);
+  X.si = take(4u * M);
   X.total = o;
   return X;
 }
@@ -123,8 +125,13 @@ __device__ void step_row_select(const StepArgs& s, uint8_t* ex, const StepExtra&
   trace_mark(s.trace, 12);
   if (write_scores)
     for (int m = threadIdx.x; m < M; m += blockDim.x) s.scores[(size_t)b * M + m] = sc[m];
-  rank_mask(sc, M, s.k, reinterpret_cast<uint32_t*>(ex + X.mask));
-  __syncthreads();
+  uint32_t* mask = reinterpret_cast<uint32_t*>(ex + X.mask);
+  for (int w = threadIdx.x; w < (M + 31) / 32; w += blockDim.x) mask[w] = 0u;
+  // TopK_k under (score desc, id asc) (R7): pruned rank count, bits set per winner
+  block_topk(
+      M, s.k, [&](int i, float& v, int& id) { v = sc[i] + 0.0f; id = i; },
+      [&](int, float, int id) { atomicOr(&mask[id >> 5], 1u << (id & 31)); },
+      reinterpret_cast<float*>(ex + X.sv), reinterpret_cast<int*>(ex + X.si), reinterpret_cast<int*>(ex + X.sh));
   trace_mark(s.trace, 13);
 }
 
@@ -252,7 +259,7 @@ __global__ void __launch_bounds__((kMaxStages + 1) * 32, 1) step_kernel(const St
   trace_mark(s.trace, 6);
   if (!head_ticket(a, c)) return;
   trace_mark(s.trace, 14);
-  head_merge(a, c, a.stages * a.stage_bytes);
+  head_merge(a, c, a.stages * a.stage_bytes, s.trace);
   trace_mark(s.trace, 7);
   if (threadIdx.x == 0) {
     s.ctr[0] = 0u;

@@ -19,10 +19,11 @@ c = D.Clusters.from_tau(W, tau, C.M)
 r = D.Router(*[x.to(dev) for x in S.router(C.d, C.h_r, C.M, 1, "bf16")])
 steps = [D.DraftStep(c, r, 1, C.k_t) for _ in range(C.positions)]
 G = torch.cuda.get_device_properties(0).multi_processor_count
-bufs = [torch.zeros(G * 32, dtype=torch.int64, device=dev) for _ in range(C.positions)]
+bufs = [torch.zeros(G * 64, dtype=torch.int64, device=dev) for _ in range(C.positions)]
 flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
 names = ["start", "pdl", "phaseA", "sel_vis", "segs", "streamed", "partials", "merged", "B:ctrA", "B:w2", "B:pub",
-         "B:hid", "B:out", "B:rank", "ticket"]
+         "B:hid", "B:out", "B:rank", "ticket", "?15", "M:load",
+         "M:lse", "M:thr", "M:surv", "M:done"]
 inp = [[x.to(dev) for x in S.step_inputs(1, C.d, t, "bf16")] for t in range(C.positions)]
 for rep in range(3):
     flush.zero_()
@@ -36,7 +37,7 @@ for rep in range(3):
     torch.cuda.synchronize()
 t_prev_end = None
 for t in range(C.positions):
-    a = bufs[t].view(G, 32).cpu().numpy().astype(np.float64)[:, :16]
+    a = bufs[t].view(G, 64).cpu().numpy().astype(np.float64)[:, :32]
     t0 = a[:, 0][a[:, 0] > 0].min()
     print(f"t={t} k={D.budget(t, C.k_max, C.k_min)}" + (f"  gap since previous merge {1e-3*(t0-t_prev_end):.2f} us"
                                                        if t_prev_end else ""))

@@ -18,9 +18,10 @@ c = D.Clusters.from_tau(W, tau, C.M)
 r = D.Router(*[x.to(dev) for x in S.router(C.d, C.h_r, C.M, 1, "bf16")])
 st = D.DraftStep(c, r, 1, C.k_t)
 G = torch.cuda.get_device_properties(0).multi_processor_count
-buf = torch.zeros(G * 32, dtype=torch.int64, device=dev)
+buf = torch.zeros(G * 64, dtype=torch.int64, device=dev)
 flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
-names = ["start", "pdl", "phaseA", "sel_vis", "segs", "streamed", "partials", "merged", "B:ctrA", "B:w2", "B:pub", "B:hid", "B:out", "B:rank", "ticket"]
+names = ["start", "pdl", "phaseA", "sel_vis", "segs", "streamed", "partials", "merged", "B:ctrA", "B:w2", "B:pub", "B:hid", "B:out", "B:rank", "ticket", "?15", "M:load",
+         "M:lse", "M:thr", "M:surv", "M:done"]
 for t in (0, 2, 2, 2):
     hp, e, hn = [x.to(dev) for x in S.step_inputs(1, C.d, t, "bf16")]
     for rep in range(3):
@@ -31,9 +32,9 @@ for t in (0, 2, 2, 2):
         st(hp, e, hn, t, C.k_max, C.k_min)
         torch.cuda.synchronize()
         D.debug_set_trace(None)
-    a = buf.view(G, 32).cpu().numpy().astype(np.float64)
-    cyc = a[:, 16:]
-    a = a[:, :16]
+    a = buf.view(G, 64).cpu().numpy().astype(np.float64)
+    cyc = a[:, 32:]
+    a = a[:, :32]
     t0 = a[:, 0][a[:, 0] > 0].min()
     ok = (a[:, 6] > 0) & (a[:, 0] > 0)
     mhz = np.median((cyc[ok, 6] - cyc[ok, 0]) / (a[ok, 6] - a[ok, 0]) * 1e3)
