@@ -237,7 +237,7 @@ namespace ds {
 // misc: 3 ints of smem.  All threads of the block must call it.
 template <class Get, class Emit>
 __device__ __forceinline__ void block_topk(int n, int K, Get get, Emit emit, float* sv, int* si, int* misc) {
-  const int tid = threadIdx.x, nt = blockDim.x;
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31;
   const int S = min(n, max(64, 4 * K));
   if (tid == 0) {
     misc[0] = 0;
@@ -245,44 +245,67 @@ __device__ __forceinline__ void block_topk(int n, int K, Get get, Emit emit, flo
     misc[2] = INT_MAX;
   }
   __syncthreads();
-  for (int i = tid; i < S; i += nt) {
-    float v;
-    int id;
-    get(i, v, id);
-    if (v == -INFINITY) continue;
-    int rank = 0;
-    for (int j = 0; j < S; ++j) {
-      float v2;
-      int id2;
-      get(j, v2, id2);
-      rank += beats(v2, id2, v, id);
-    }
-    if (rank == K - 1) {
-      misc[1] = __float_as_int(v);
-      misc[2] = id;
+  // rank of item i among the first S items, split over `sp` lanes (shallower chains)
+  {
+    int sp = 32;
+    while (sp > 1 && S * sp > nt) sp >>= 1;
+    const int groups = nt / sp;
+    for (int base = 0; base < S; base += groups) {
+      const int i = base + tid / sp, part = tid % sp;
+      float v = -INFINITY;
+      int id = INT_MAX;
+      if (i < S && tid < groups * sp) get(i, v, id);
+      int rank = 0;
+      if (v > -INFINITY)
+        for (int j = part; j < S; j += sp) {
+          float v2;
+          int id2;
+          get(j, v2, id2);
+          rank += beats(v2, id2, v, id);
+        }
+      for (int o = sp >> 1; o > 0; o >>= 1) rank += __shfl_xor_sync(0xffffffffu, rank, o);
+      if (part == 0 && v > -INFINITY && rank == K - 1) {
+        misc[1] = __float_as_int(v);
+        misc[2] = id;
+      }
     }
   }
   __syncthreads();
   const float tv = __int_as_float(misc[1]);
   const int tid0 = misc[2];
-  for (int i = tid; i < n; i += nt) {
-    float v;
-    int id;
-    get(i, v, id);
-    if (v > -INFINITY && !beats(tv, tid0, v, id)) {
-      const int slot = atomicAdd(&misc[0], 1);
+  for (int i0 = 0; i0 < n; i0 += nt) {
+    const int i = i0 + tid;
+    float v = -INFINITY;
+    int id = INT_MAX;
+    if (i < n) get(i, v, id);
+    const bool keep = v > -INFINITY && !beats(tv, tid0, v, id);
+    const uint32_t bal = __ballot_sync(0xffffffffu, keep);
+    int slot0 = 0;
+    if (lane == 0 && bal) slot0 = atomicAdd(&misc[0], __popc(bal));
+    slot0 = __shfl_sync(0xffffffffu, slot0, 0);
+    if (keep) {
+      const int slot = slot0 + __popc(bal & ((1u << lane) - 1u));
       sv[slot] = v;
       si[slot] = id;
     }
   }
   __syncthreads();
   const int ns = misc[0];
-  for (int s2 = tid; s2 < ns; s2 += nt) {
-    const float v = sv[s2];
-    const int id = si[s2];
-    int rank = 0;
-    for (int t = 0; t < ns; ++t) rank += beats(sv[t], si[t], v, id);
-    if (rank < K) emit(rank, v, id);
+  {
+    int sp = 32;
+    while (sp > 1 && ns * sp > nt) sp >>= 1;
+    const int groups = nt / sp;
+    for (int base = 0; base < ns; base += groups) {
+      const int s2 = base + tid / sp, part = tid % sp;
+      const bool active = s2 < ns && tid < groups * sp;
+      const float v = active ? sv[s2] : -INFINITY;
+      const int id = active ? si[s2] : INT_MAX;
+      int rank = 0;
+      if (active)
+        for (int t = part; t < ns; t += sp) rank += beats(sv[t], si[t], v, id);
+      for (int o = sp >> 1; o > 0; o >>= 1) rank += __shfl_xor_sync(0xffffffffu, rank, o);
+      if (active && part == 0 && rank < K) emit(rank, v, id);
+    }
   }
   __syncthreads();
 }

@@ -23,7 +23,7 @@ constexpr int kStepExtra = 4096 * 4 + 4112 + 1024 + 256;
 // shared-memory bytes the last-CTA merge needs inside the ring
 __host__ __device__ inline int merge_smem_bytes(int G, int k_t, int nwarps) {
   (void)nwarps;
-  return G * (2 + 2 * k_t) * 4 + 2 * G * k_t * 4 + 64;
+  return G * (2 + 2 * k_t) * 4 + 2 * G * k_t * 4 + 256;
 }
 
 struct HeadArgs {
@@ -385,9 +385,13 @@ __device__ inline void head_merge(const HeadArgs& a, const HeadCtx& c, int ring_
   const int tid = threadIdx.x, nt = blockDim.x;
   const int K = a.k_t, rec = 2 + 2 * K;
   const int per_row = G * rec;
-  float* R = reinterpret_cast<float*>(c.ring);         // [G][rec]
-  float* sv = R + per_row;                             // survivors: values
-  int* si = reinterpret_cast<int*>(sv + G * K);        // survivors: ids (K best of each CTA at most)
+  // staged records: per-CTA (m_g, s_g) and the K candidates of every CTA in rank-major order
+  float* pm = reinterpret_cast<float*>(c.ring);   // [G]
+  float* ps = pm + G;                             // [G]
+  float* cv = ps + G;                             // [K][G] values
+  int* ci = reinterpret_cast<int*>(cv + G * K);   // [K][G] ids
+  float* sv = reinterpret_cast<float*>(ci + G * K);
+  int* si = reinterpret_cast<int*>(sv + G * K);
   (void)ring_bytes;
   for (int r = 0; r < a.nrows; ++r) {
     const float* src = a.part + (size_t)r * rec;
@@ -405,25 +409,26 @@ __device__ inline void head_merge(const HeadArgs& a, const HeadCtx& c, int ring_
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int idx = base + u * nt;
-        if (idx < per_row) R[idx] = v[u];
+        if (idx < per_row) {
+          const int gg = idx / rec, f = idx - gg * rec;
+          if (f == 0) pm[gg] = v[u];
+          else if (f == 1) ps[gg] = v[u];
+          else if ((f & 1) == 0) cv[((f - 2) >> 1) * G + gg] = v[u];
+          else ci[((f - 3) >> 1) * G + gg] = __float_as_int(v[u]);
+        }
       }
     }
-    trace_mark(trace, 16);
     __syncthreads();
+    trace_mark(trace, 16);
     float mx = -INFINITY, S = 0.f;
-    for (int g = tid; g < G; g += nt) lse_combine(mx, S, R[g * rec], R[g * rec + 1]);
+    for (int g = tid; g < G; g += nt) lse_combine(mx, S, pm[g], ps[g]);
     block_lse(mx, S, c.red);
     trace_mark(trace, 17);
     const bool ok = shortlist_len(a, a.shared ? 0 : r) >= 0;
     const float lse = ok ? mx + logf(S) : __int_as_float(0x7fc00000);
-    // candidates (g, j) in list order: the first S items are the heads of lists 0.. and beyond
+    // candidates in rank-major order: the first G items are the heads of the G sorted lists
     block_topk(
-        G * K, K,
-        [&](int e, float& v, int& id) {
-          const int j = e / G, g = e - j * G;  // rank-major order: all heads first
-          v = R[g * rec + 2 + 2 * j];
-          id = __float_as_int(R[g * rec + 3 + 2 * j]);
-        },
+        G * K, K, [&](int e, float& v, int& id) { v = cv[e]; id = ci[e]; },
         [&](int rank, float v, int id) {
           a.top_ids[(size_t)r * K + rank] = ok ? id : -1;
           a.top_logits[(size_t)r * K + rank] = ok ? v : -INFINITY;
