@@ -331,7 +331,7 @@ __device__ inline void head_partials(const HeadArgs& a, const HeadCtx& c) {
   for (int r = 0; r < a.nrows; ++r) {
     const int gi = a.shared ? 0 : r;
     const int n = c.segn[gi] > 0 ? c.segn[gi] : 0;
-    float* P = a.part + ((size_t)blockIdx.x * a.nrows + r) * rec;
+    float* P = a.part + ((size_t)r * gridDim.x + blockIdx.x) * rec;   // [row][cta][rec]
     const float* zr = c.zl + r * a.lcap;
     const int* ir = c.zid + r * a.lcap;
     float m = -INFINITY, se = 0.f;
@@ -394,35 +394,41 @@ __device__ inline void head_merge(const HeadArgs& a, const HeadCtx& c, int ring_
   int* si = reinterpret_cast<int*>(sv + G * K);
   (void)ring_bytes;
   for (int r = 0; r < a.nrows; ++r) {
-    const float* src = a.part + (size_t)r * rec;
-    constexpr int U = 8;
-    for (int base = tid; base < per_row; base += U * nt) {
-      float v[U];
+    const float* src = a.part + (size_t)r * per_row;  // this row's G records, contiguous
+    if ((per_row & 3) == 0 && ((reinterpret_cast<uintptr_t>(src) & 15u) == 0)) {
+      const float4* s4 = reinterpret_cast<const float4*>(src);
+      for (int q = tid; q < per_row / 4; q += nt) {
+        const float4 v4 = __ldcg(s4 + q);
+        const float vv[4] = {v4.x, v4.y, v4.z, v4.w};
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int idx = base + u * nt;
-        if (idx < per_row) {
+        for (int u = 0; u < 4; ++u) {
+          const int idx = 4 * q + u;
           const int gg = idx / rec, f = idx - gg * rec;
-          v[u] = __ldcg(src + (size_t)gg * a.nrows * rec + f);
+          if (f == 0) pm[gg] = vv[u];
+          else if (f == 1) ps[gg] = vv[u];
+          else if ((f & 1) == 0) cv[((f - 2) >> 1) * G + gg] = vv[u];
+          else ci[((f - 3) >> 1) * G + gg] = __float_as_int(vv[u]);
         }
       }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int idx = base + u * nt;
-        if (idx < per_row) {
-          const int gg = idx / rec, f = idx - gg * rec;
-          if (f == 0) pm[gg] = v[u];
-          else if (f == 1) ps[gg] = v[u];
-          else if ((f & 1) == 0) cv[((f - 2) >> 1) * G + gg] = v[u];
-          else ci[((f - 3) >> 1) * G + gg] = __float_as_int(v[u]);
-        }
+    } else {
+      for (int idx = tid; idx < per_row; idx += nt) {
+        const float v = __ldcg(src + idx);
+        const int gg = idx / rec, f = idx - gg * rec;
+        if (f == 0) pm[gg] = v;
+        else if (f == 1) ps[gg] = v;
+        else if ((f & 1) == 0) cv[((f - 2) >> 1) * G + gg] = v;
+        else ci[((f - 3) >> 1) * G + gg] = __float_as_int(v);
       }
     }
     __syncthreads();
     trace_mark(trace, 16);
-    float mx = -INFINITY, S = 0.f;
-    for (int g = tid; g < G; g += nt) lse_combine(mx, S, pm[g], ps[g]);
-    block_lse(mx, S, c.red);
+    float mx = -INFINITY;
+    for (int g = tid; g < G; g += nt) mx = fmaxf(mx, pm[g]);
+    mx = block_max(mx, c.red);
+    float S = 0.f;
+    for (int g = tid; g < G; g += nt)
+      if (pm[g] > -INFINITY) S += ps[g] * expf(pm[g] - mx);
+    S = block_sum(S, c.red);
     trace_mark(trace, 17);
     const bool ok = shortlist_len(a, a.shared ? 0 : r) >= 0;
     const float lse = ok ? mx + logf(S) : __int_as_float(0x7fc00000);

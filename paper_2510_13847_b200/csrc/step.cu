@@ -259,6 +259,7 @@ __global__ void __launch_bounds__((kMaxStages + 1) * 32, 1) step_kernel(const St
   trace_mark(s.trace, 6);
   if (!head_ticket(a, c)) return;
   trace_mark(s.trace, 14);
+  trace_mark(s.trace, 15);  // back-to-back: the cost of one mark
   head_merge(a, c, a.stages * a.stage_bytes, s.trace);
   trace_mark(s.trace, 7);
   if (threadIdx.x == 0) {

@@ -22,7 +22,7 @@ G = torch.cuda.get_device_properties(0).multi_processor_count
 bufs = [torch.zeros(G * 64, dtype=torch.int64, device=dev) for _ in range(C.positions)]
 flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
 names = ["start", "pdl", "phaseA", "sel_vis", "segs", "streamed", "partials", "merged", "B:ctrA", "B:w2", "B:pub",
-         "B:hid", "B:out", "B:rank", "ticket", "?15", "M:load",
+         "B:hid", "B:out", "B:rank", "ticket", "ticket+1", "M:load",
          "M:lse", "M:thr", "M:surv", "M:done"]
 inp = [[x.to(dev) for x in S.step_inputs(1, C.d, t, "bf16")] for t in range(C.positions)]
 for rep in range(3):
@@ -47,4 +47,8 @@ for t in range(C.positions):
         if col.size:
             print(f"  {n:9s} n={col.size:3d} min={1e-3*(col.min()-t0):8.2f} med={1e-3*(np.median(col)-t0):8.2f} "
                   f"max={1e-3*(col.max()-t0):8.2f} us")
+    cy = bufs[t].view(G, 64).cpu().numpy().astype(np.float64)[:, 32:]
+    last = np.argmax(a[:, 7])
+    print("  last-CTA cycles between marks:", {names[i]: int(cy[last, i] - cy[last, 14]) for i in (15, 16, 17, 19, 20, 7)
+                                               if cy[last, i] > 0})
     t_prev_end = a[:, 7][a[:, 7] > 0].max()
