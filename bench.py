@@ -280,7 +280,12 @@ def run_ours(args, ws, rank, local):
         for a, b in lst:
             a.record(); b.record()
 
-    def cycle(i, timed_heads=True):
+    # Fused mode: every launch of the cycle IS the dominant kernel, so its average duration is the
+    # event-timed cycle / launches (events between launches would break the PDL chaining).
+    # Two-kernel modes: events bracket each head launch on its stream.
+    timed_heads = not fused
+
+    def cycle(i):
         for t in range(C.positions):
             hp, e, hn = inputs[i][t]
             steppers[t](hp, e, hn, t, C.k_max, C.k_min, head_events=head_ev[i][t] if timed_heads else None)
@@ -328,10 +333,13 @@ def run_ours(args, ws, rank, local):
     barrier(ws)
     clocks = clk.stop()
     step_ms = [a.elapsed_time(b) for a, b in ev]
-    # head-kernel durations (events around each head launch, recorded on S_d inside the graph)
+    # dominant-kernel durations
     for i in range(args.steps):
         j = (args.warmup + i) % pool
         for t in range(C.positions):
+            if not timed_heads:
+                head_ms.append(step_ms[i] / C.positions)
+                continue
             try:
                 head_ms.append(head_ev[j][t][0].elapsed_time(head_ev[j][t][1]))
             except RuntimeError:
@@ -416,6 +424,9 @@ def run_ours(args, ws, rank, local):
                          "frac": achieved / peak if achieved else None,
                          "traffic": committed_traffic(C.name, B), "kernel": ("ds::step_kernel (router + select + gathered head + epilogue, one launch)" if fused
                                     else "ds::head_kernel (S5+S6)"),
+                         "duration_source": ("CUDA events around each timed cycle / launches per cycle (every launch "
+                                             "is the dominant kernel; PDL-chained)" if fused else
+                                             "CUDA events around each head launch"),
                          "peak_source": peak_src, "frac_of_8TBps": achieved / 8000.0 if achieved else None},
             "cpu_baseline": cpu,
             "e2e": e2e,

@@ -239,6 +239,30 @@ ds_status dynaspec_draft_step(const ds_clusters* c, const ds_router* r, const vo
 int32_t dynaspec_draft_step_launches(const ds_clusters* c, const ds_router* r, int32_t B, int32_t k_t,
                                      int32_t shared, int32_t two_streams);
 
+/* ---------------------------------------------------------------- cluster sharding (multi-GPU) */
+
+/* Keep, for each of `rows` selection rows, only the selected clusters in [m_lo, m_hi) (the
+ * cluster range a rank owns), preserving ascending order, and rebuild sl_offsets over them.
+ * Same layouts as dynaspec_select.  Errors: DS_ERR_INVALID_CLUSTER_ID for a bad range. */
+ds_status dynaspec_restrict_selection(const int32_t* sel, const int32_t* sel_count, const int32_t* sl_offsets,
+                                      int32_t rows, const ds_clusters* c, int32_t m_lo, int32_t m_hi, int32_t* out_sel,
+                                      int32_t* out_count, int32_t* out_sl_offsets, ds_stream_t stream);
+
+/* As dynaspec_head_forward (same workspace size), but instead of the final outputs emit one
+ * record per row: records[r] = {max z, sum exp(z - max), (z, id) of the top-k_t by (z desc,
+ * id asc), padded with (-inf, INT_MAX)} as 2 + 2 k_t floats (ids bit-cast).  A rank holding
+ * only rows [offsets[m_lo], offsets[m_hi]) of W_perm passes a ds_clusters whose W_perm points
+ * offsets[m_lo] rows before its slice and a selection restricted to [m_lo, m_hi). */
+ds_status dynaspec_head_partial(const ds_clusters* c, const void* h_new, int32_t B, const int32_t* sel,
+                                const int32_t* sel_count, const int32_t* sl_offsets, int32_t shared, int32_t k_t,
+                                int64_t max_shortlist, float* records, void* ws, size_t ws_bytes, ds_stream_t stream);
+
+/* Merge G per-rank records (device [G][B][2 + 2 k_t], rank-major as an all-gather produces them)
+ * in rank order into lse / top_ids / top_logits / top_logp exactly as dynaspec_head_forward
+ * defines them (softmax over the union of the ranks' shortlists).  G <= 64. */
+ds_status dynaspec_merge_records(const float* records, int32_t G, int32_t B, int32_t k_t, int32_t* top_ids,
+                                 float* top_logits, float* top_logp, float* lse, ds_stream_t stream);
+
 /* Debugging: when dev_buf != NULL, the fused step kernel records %globaltimer nanosecond
  * timestamps of its phases into dev_buf[cta * 64 + slot] and the SM clock64() into
  * dev_buf[cta * 64 + 32 + slot] (uint64, >= #SM * 64 entries):

@@ -223,6 +223,50 @@ ds_status dynaspec_head_forward(const ds_clusters* c, const void* h_new, int32_t
   return err == cudaSuccess ? DS_OK : DS_ERR_CUDA;
 }
 
+ds_status dynaspec_restrict_selection(const int32_t* sel, const int32_t* sel_count, const int32_t* sl_offsets,
+                                      int32_t rows, const ds_clusters* c, int32_t m_lo, int32_t m_hi, int32_t* out_sel,
+                                      int32_t* out_count, int32_t* out_sl_offsets, ds_stream_t stream) {
+  if (!c || !c->offsets || !sel || !sel_count || !sl_offsets || !out_sel || !out_count || !out_sl_offsets || rows < 1)
+    return DS_ERR_SHAPE;
+  if (c->M < 1 || c->M > kMaxMHost) return DS_ERR_INVALID_CLUSTER_COUNT;
+  if (m_lo < 0 || m_hi > c->M || m_lo > m_hi) return DS_ERR_INVALID_CLUSTER_ID;
+  return launch_restrict(sel, sel_count, rows, c->M, c->offsets, m_lo, m_hi, out_sel, out_count, out_sl_offsets,
+                         (cudaStream_t)stream) == cudaSuccess
+             ? DS_OK
+             : DS_ERR_CUDA;
+}
+
+ds_status dynaspec_head_partial(const ds_clusters* c, const void* h_new, int32_t B, const int32_t* sel,
+                                const int32_t* sel_count, const int32_t* sl_offsets, int32_t shared, int32_t k_t,
+                                int64_t max_shortlist, float* records, void* ws, size_t ws_bytes, ds_stream_t stream) {
+  ds_status s = check_clusters(c);
+  if (s != DS_OK) return s;
+  if (!h_new || !sel || !sel_count || !sl_offsets || !records || B < 1) return DS_ERR_SHAPE;
+  if (k_t < 1 || k_t > kMaxKt) return DS_ERR_INVALID_BUDGET;
+  if (max_shortlist < 0) return DS_ERR_SHAPE;
+  HeadPlan p;
+  if (!head_plan(c, B, k_t, max_shortlist, &p)) return DS_ERR_UNSUPPORTED;
+  const WsLayout L = ws_layout(0, p.part_bytes);
+  if (!ws || ws_bytes < L.total) return DS_ERR_WORKSPACE;
+  uint8_t* w8 = static_cast<uint8_t*>(ws);
+  // the final-output pointers are unused in record mode; pass the record buffer as a harmless target
+  cudaError_t err = launch_head(c, p, h_new, B, sel, sel_count, sl_offsets, shared ? 1 : 0, k_t, max_shortlist,
+                                reinterpret_cast<int32_t*>(records), records, records, records, nullptr, 0,
+                                reinterpret_cast<float*>(w8 + L.head), reinterpret_cast<unsigned*>(w8 + L.counters),
+                                (cudaStream_t)stream, false, records);
+  return err == cudaSuccess ? DS_OK : DS_ERR_CUDA;
+}
+
+ds_status dynaspec_merge_records(const float* records, int32_t G, int32_t B, int32_t k_t, int32_t* top_ids,
+                                 float* top_logits, float* top_logp, float* lse, ds_stream_t stream) {
+  if (!records || !top_ids || !top_logits || !top_logp || !lse || G < 1 || G > 64 || B < 1) return DS_ERR_SHAPE;
+  if (k_t < 1 || k_t > kMaxKt) return DS_ERR_INVALID_BUDGET;
+  return launch_merge_records(records, G, B, k_t, top_ids, top_logits, top_logp, lse, (cudaStream_t)stream) ==
+                 cudaSuccess
+             ? DS_OK
+             : DS_ERR_CUDA;
+}
+
 size_t dynaspec_draft_step_ws(const ds_clusters* c, const ds_router* r, int32_t B, int32_t k_t) {
   HeadPlan p;
   if (!c || !r || B < 1 || k_t < 1 || k_t > kMaxKt) return 0;

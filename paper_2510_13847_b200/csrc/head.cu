@@ -122,6 +122,7 @@ void fill_head_args(HeadArgs& a, const ds_clusters* c, const HeadPlan& p, const 
   a.z_stride = z_stride;
   a.part = part;
   a.counter = counter;
+  a.record_out = nullptr;
 }
 
 template <typename T>
@@ -150,13 +151,14 @@ cudaError_t launch_head(const ds_clusters* c, const HeadPlan& p, const void* h_n
                         const int32_t* sel_count, const int32_t* sl_offsets, int shared, int k_t,
                         int64_t max_shortlist, int32_t* top_ids, float* top_logits, float* top_logp, float* lse,
                         float* z_out, int64_t z_stride, float* part, unsigned* counter, cudaStream_t st,
-                        bool pdl) {
+                        bool pdl, float* records) {
   const int esz = c->dtype == DS_BF16 ? 2 : 4;
   for (int r0 = 0; r0 < B; r0 += p.rows_per_launch) {
     const int nr = std::min(p.rows_per_launch, B - r0);
     HeadArgs a;
     fill_head_args(a, c, p, h_new, r0, nr, sel, sel_count, sl_offsets, shared, k_t, max_shortlist, top_ids,
                    top_logits, top_logp, lse, z_out, z_stride, part, counter, pdl && r0 == 0);
+    a.record_out = records ? records + (size_t)r0 * (2 + 2 * k_t) : nullptr;
     const size_t smem = head_smem(p.stages, p.stage_bytes, nr, c->d, esz, p.lcap, 0).total;
     cudaError_t e = c->dtype == DS_BF16 ? launch_head_t<__nv_bfloat16>(a, smem, p.G, st, pdl && r0 == 0)
                                         : launch_head_t<float>(a, smem, p.G, st, pdl && r0 == 0);

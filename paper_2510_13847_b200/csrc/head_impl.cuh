@@ -43,8 +43,9 @@ struct HeadArgs {
   float* lse;
   float* z_out;
   int64_t z_stride;
-  float* part;               // [G][nrows][2 + 2 k_t]
+  float* part;               // [nrows][G][2 + 2 k_t]
   unsigned* counter;         // [0] = merge ticket (the fused step also uses [1], [2])
+  float* record_out;         // nullable [nrows][2 + 2 k_t]: emit the merged (max, sum, top-k) record
 };
 
 void fill_head_args(HeadArgs& a, const ds_clusters* c, const HeadPlan& p, const void* h_new, int r0, int nr,
@@ -375,13 +376,63 @@ __device__ __forceinline__ bool head_ticket(const HeadArgs& a, const HeadCtx& c)
   return c.misc[0] != 0;
 }
 
+// Merge step shared by the last-CTA merge and the cross-rank merge: staged per-partial (m_g, s_g)
+// and K candidates per partial in rank-major order -> lse and top-k (or the merged record).
+__device__ inline void merge_finish(const HeadArgs& a, const HeadCtx& c, int G, int r, const float* pm,
+                                    const float* ps, const float* cv, const int* ci, float* sv, int* si,
+                                    bool valid_row, unsigned long long* trace) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int K = a.k_t, rec = 2 + 2 * K;
+    float mx = -INFINITY;
+    for (int g = tid; g < G; g += nt) mx = fmaxf(mx, pm[g]);
+    mx = block_max(mx, c.red);
+    float S = 0.f;
+    for (int g = tid; g < G; g += nt)
+      if (pm[g] > -INFINITY) S += ps[g] * expf(pm[g] - mx);
+    S = block_sum(S, c.red);
+    trace_mark(trace, 17);
+    const bool ok = valid_row && mx > -INFINITY;
+    const float lse = ok ? mx + logf(S) : __int_as_float(0x7fc00000);
+    // candidates in rank-major order: the first G items are the heads of the G sorted lists
+    block_topk(
+        G * K, K, [&](int e, float& v, int& id) { v = cv[e]; id = ci[e]; },
+        [&](int rank, float v, int id) {
+          if (a.record_out) {
+            a.record_out[(size_t)r * rec + 2 + 2 * rank] = v;
+            a.record_out[(size_t)r * rec + 3 + 2 * rank] = __int_as_float(id);
+          } else {
+            a.top_ids[(size_t)r * K + rank] = ok ? id : -1;
+            a.top_logits[(size_t)r * K + rank] = ok ? v : -INFINITY;
+            a.top_logp[(size_t)r * K + rank] = ok ? v - lse : -INFINITY;
+          }
+        },
+        sv, si, c.misc + 8);
+    trace_mark(trace, 19);
+    const int nvalid = c.misc[8];
+    for (int q = nvalid + tid; q < K; q += nt) {
+      if (a.record_out) {
+        a.record_out[(size_t)r * rec + 2 + 2 * q] = -INFINITY;
+        a.record_out[(size_t)r * rec + 3 + 2 * q] = __int_as_float(INT_MAX);
+      } else {
+        a.top_ids[(size_t)r * K + q] = -1;
+        a.top_logits[(size_t)r * K + q] = -INFINITY;
+        a.top_logp[(size_t)r * K + q] = -INFINITY;
+      }
+    }
+    if (a.record_out && tid == 0) {
+      a.record_out[(size_t)r * rec] = mx;
+      a.record_out[(size_t)r * rec + 1] = S;
+    }
+  if (tid == 0 && !a.record_out) a.lse[r] = lse;
+}
+
 // Last CTA: merge the G partials of every row -> lse, top ids (remapped), logp.
 //  lse  = M + log sum_g S_g exp(m_g - M)            (fixed-order block reduction)
 //  top  : T = the k_t-th best list head; only entries not beaten by T can be in the global
 //         top-k_t (k_t heads are >= T), so rank-count just those survivors.
 __device__ inline void head_merge(const HeadArgs& a, const HeadCtx& c, int ring_bytes,
-                                  unsigned long long* trace = nullptr) {
-  const int G = gridDim.x;
+                                  unsigned long long* trace = nullptr, int G_override = 0) {
+  const int G = G_override > 0 ? G_override : (int)gridDim.x;
   const int tid = threadIdx.x, nt = blockDim.x;
   const int K = a.k_t, rec = 2 + 2 * K;
   const int per_row = G * rec;
@@ -422,33 +473,7 @@ __device__ inline void head_merge(const HeadArgs& a, const HeadCtx& c, int ring_
     }
     __syncthreads();
     trace_mark(trace, 16);
-    float mx = -INFINITY;
-    for (int g = tid; g < G; g += nt) mx = fmaxf(mx, pm[g]);
-    mx = block_max(mx, c.red);
-    float S = 0.f;
-    for (int g = tid; g < G; g += nt)
-      if (pm[g] > -INFINITY) S += ps[g] * expf(pm[g] - mx);
-    S = block_sum(S, c.red);
-    trace_mark(trace, 17);
-    const bool ok = shortlist_len(a, a.shared ? 0 : r) >= 0;
-    const float lse = ok ? mx + logf(S) : __int_as_float(0x7fc00000);
-    // candidates in rank-major order: the first G items are the heads of the G sorted lists
-    block_topk(
-        G * K, K, [&](int e, float& v, int& id) { v = cv[e]; id = ci[e]; },
-        [&](int rank, float v, int id) {
-          a.top_ids[(size_t)r * K + rank] = ok ? id : -1;
-          a.top_logits[(size_t)r * K + rank] = ok ? v : -INFINITY;
-          a.top_logp[(size_t)r * K + rank] = ok ? v - lse : -INFINITY;
-        },
-        sv, si, c.misc + 8);
-    trace_mark(trace, 19);
-    const int nvalid = c.misc[8];
-    for (int q = nvalid + tid; q < K; q += nt) {
-      a.top_ids[(size_t)r * K + q] = -1;
-      a.top_logits[(size_t)r * K + q] = -INFINITY;
-      a.top_logp[(size_t)r * K + q] = -INFINITY;
-    }
-    if (tid == 0) a.lse[r] = lse;
+    merge_finish(a, c, G, r, pm, ps, cv, ci, sv, si, shortlist_len(a, a.shared ? 0 : r) >= 0, trace);
     __syncthreads();
     trace_mark(trace, 20);
   }

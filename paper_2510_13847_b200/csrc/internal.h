@@ -54,7 +54,7 @@ cudaError_t launch_head(const ds_clusters* c, const HeadPlan& p, const void* h_n
                         const int32_t* sel_count, const int32_t* sl_offsets, int shared, int k_t,
                         int64_t max_shortlist, int32_t* top_ids, float* top_logits, float* top_logp,
                         float* lse, float* z_out, int64_t z_stride, float* part, unsigned* counter,
-                        cudaStream_t st, bool pdl);
+                        cudaStream_t st, bool pdl, float* records = nullptr);
 
 // ---- fused one-launch draft step (step.cu): router + select + head + epilogue
 bool step_supported(const ds_clusters* c, const ds_router* r, int B, int k_t, int shared, int64_t max_shortlist);
@@ -73,6 +73,12 @@ cudaError_t launch_tc_head(const ds_clusters* c, const void* h_new, int R, const
                            int32_t* top_ids, float* top_logits, float* top_logp, float* lse, float* z_out,
                            int64_t z_stride, float* part, unsigned* counter, cudaStream_t st, bool pdl);
 bool use_tc_head(const ds_clusters* c, int B, int k_t, int shared, int64_t max_shortlist);
+
+// ---- cluster sharding (shard.cu)
+cudaError_t launch_restrict(const int32_t* sel, const int32_t* cnt, int rows, int M, const int32_t* offsets, int m_lo,
+                            int m_hi, int32_t* osel, int32_t* ocnt, int32_t* ooff, cudaStream_t st);
+cudaError_t launch_merge_records(const float* records, int G, int B, int K, int32_t* top_ids, float* top_logits,
+                                 float* top_logp, float* lse, cudaStream_t st);
 
 // ---- offline partition (build.cu)
 size_t build_ws_bytes(int64_t V, int d, int M);

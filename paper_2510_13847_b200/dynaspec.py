@@ -77,6 +77,10 @@ def _load():
                                           c_int32, c_int32, c_int32, c_int32, POINTER(DsStepOutputs), P, c_size_t,
                                           P, P, P, P, P, P]),
         "dynaspec_debug_set_trace": (c_int32, [P]),
+        "dynaspec_restrict_selection": (c_int32, [P, P, P, c_int32, POINTER(DsClusters), c_int32, c_int32, P, P, P, P]),
+        "dynaspec_head_partial": (c_int32, [POINTER(DsClusters), P, c_int32, P, P, P, c_int32, c_int32, c_int64, P, P,
+                                            c_size_t, P]),
+        "dynaspec_merge_records": (c_int32, [P, c_int32, c_int32, c_int32, P, P, P, P, P]),
         "dynaspec_draft_step_launches": (c_int32, [POINTER(DsClusters), POINTER(DsRouter), c_int32, c_int32,
                                                    c_int32, c_int32]),
     }
@@ -94,7 +98,7 @@ EXPORTED = [
     "dynaspec_build_clusters_ws", "dynaspec_build_clusters", "dynaspec_layout_ws", "dynaspec_layout",
     "dynaspec_meta_score_ws", "dynaspec_meta_score", "dynaspec_select", "dynaspec_head_forward_ws",
     "dynaspec_head_forward", "dynaspec_draft_step_ws", "dynaspec_draft_step", "dynaspec_draft_step_launches",
-    "dynaspec_debug_set_trace",
+    "dynaspec_debug_set_trace", "dynaspec_restrict_selection", "dynaspec_head_partial", "dynaspec_merge_records",
 ]
 
 
@@ -173,6 +177,22 @@ class Clusters:
 
     def max_shortlist(self, k):
         return _lib.dynaspec_max_shortlist(self.struct(), k)
+
+    def shard(self, m_lo, m_hi, copy=True):
+        """View of this partition holding only W_perm rows of clusters [m_lo, m_hi) (cluster
+        sharding): W_perm is a (copied) slice, addressed through a base pointer
+        offsets[m_lo] rows before it, so global row indices keep working for owned clusters."""
+        off = self.offsets.cpu()
+        r0, r1 = int(off[m_lo]), int(off[m_hi])
+        sl = self.W_perm[r0:r1].clone() if copy else self.W_perm[r0:r1]
+        v = Clusters.__new__(Clusters)
+        v.tau, v.perm, v.offsets, v.W_perm = self.tau, self.perm, self.offsets, sl
+        v.min_size, v.max_size, v.V, v.d, v.M, v.dtype = self.min_size, self.max_size, self.V, self.d, self.M, self.dtype
+        v.m_lo, v.m_hi, v.row0 = m_lo, m_hi, r0
+        base = sl.data_ptr() - r0 * self.d * sl.element_size()
+        v._s = DsClusters(self.V, self.d, self.M, _DTYPE[self.dtype], self.min_size, self.max_size, _ptr(self.tau),
+                          _ptr(self.perm), _ptr(self.offsets), c_void_p(base))
+        return v
 
     @classmethod
     def from_tau(cls, W, tau, M):
@@ -280,6 +300,47 @@ def head_forward(clusters, h_new, sel, sel_count, sl_offsets, k_t, shared=False,
                                       _ptr(out["top_logits"]), _ptr(out["top_logp"]), _ptr(out["lse"]), _ptr(z), zs,
                                       ws.ptr(), ws.nbytes, _stream()), "dynaspec_head_forward")
     out["z"] = z
+    return out
+
+
+# ---------------------------------------------------------------------------- cluster sharding
+
+def restrict_selection(sel, sel_count, sl_offsets, clusters, m_lo, m_hi):
+    rows, M = sel.shape
+    o_sel = torch.zeros_like(sel)
+    o_cnt = torch.zeros_like(sel_count)
+    o_off = torch.zeros_like(sl_offsets)
+    _check(_lib.dynaspec_restrict_selection(_ptr(sel), _ptr(sel_count), _ptr(sl_offsets), rows, clusters.struct(),
+                                            m_lo, m_hi, _ptr(o_sel), _ptr(o_cnt), _ptr(o_off), _stream()),
+           "dynaspec_restrict_selection")
+    return o_sel, o_cnt, o_off
+
+
+def head_partial(clusters, h_new, sel, sel_count, sl_offsets, k_t, shared=False, max_shortlist=0, ws=None,
+                 records=None):
+    """Per-row records {max, sum exp, top-k_t (z, id)} of this shard (dynaspec_head_partial)."""
+    B = h_new.shape[0]
+    rec = 2 + 2 * k_t
+    if records is None:
+        records = torch.empty((B, rec), dtype=torch.float32, device=h_new.device)
+    ws = (ws or Workspace(256, h_new.device)).ensure(_lib.dynaspec_head_forward_ws(clusters.struct(), B, k_t))
+    _check(_lib.dynaspec_head_partial(clusters.struct(), _ptr(h_new), B, _ptr(sel), _ptr(sel_count),
+                                      _ptr(sl_offsets), int(shared), k_t, max_shortlist, _ptr(records), ws.ptr(),
+                                      ws.nbytes, _stream()), "dynaspec_head_partial")
+    return records
+
+
+def merge_records(records, k_t):
+    """records: [G][B][2 + 2 k_t] (rank-major) -> dict(top_ids, top_logits, top_logp, lse)."""
+    G, B, _ = records.shape
+    dev = records.device
+    out = {"top_ids": torch.empty((B, k_t), dtype=torch.int32, device=dev),
+           "top_logits": torch.empty((B, k_t), dtype=torch.float32, device=dev),
+           "top_logp": torch.empty((B, k_t), dtype=torch.float32, device=dev),
+           "lse": torch.empty(B, dtype=torch.float32, device=dev)}
+    _check(_lib.dynaspec_merge_records(_ptr(records.contiguous()), G, B, k_t, _ptr(out["top_ids"]),
+                                       _ptr(out["top_logits"]), _ptr(out["top_logp"]), _ptr(out["lse"]), _stream()),
+           "dynaspec_merge_records")
     return out
 
 

@@ -1,0 +1,124 @@
+"""Multi-rank host logic on CPU with the gloo backend (world_size 2): request-row sharding,
+token-balanced cluster ranges, and the cluster-sharded record protocol (per-rank records over the
+owned clusters -> all-gather -> rank-order merge) against the unsharded oracle."""
+import math
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2510_13847_b200 import parallel as P
+
+
+def test_row_range_partitions():
+    for B in (1, 7, 64, 512):
+        for G in (1, 2, 3, 8):
+            rs = [P.row_range(B, g, G) for g in range(G)]
+            assert rs[0][0] == 0 and rs[-1][1] == B
+            assert all(rs[g][1] == rs[g + 1][0] for g in range(G - 1))
+            assert max(r1 - r0 for r0, r1 in rs) - min(r1 - r0 for r0, r1 in rs) <= 1
+
+
+def test_cluster_ranges_balanced_and_covering():
+    rng = np.random.default_rng(0)
+    for M, G in [(256, 2), (512, 8), (64, 4), (5, 5)]:
+        sizes = rng.integers(1, 1000, size=M)
+        off = np.concatenate([[0], np.cumsum(sizes)])
+        rs = P.cluster_ranges(off.tolist(), G)
+        assert rs[0][0] == 0 and rs[-1][1] == M and all(lo < hi for lo, hi in rs)
+        assert all(rs[g][1] == rs[g + 1][0] for g in range(G - 1))
+        toks = [off[hi] - off[lo] for lo, hi in rs]
+        if M >= 8 * G:
+            assert max(toks) <= off[-1] / G + sizes.max() + 1
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _record(z, ids, k):
+    """A shard's record: (max, sum exp(z - max), top-k (z, id) by (z desc, id asc), padded)."""
+    rec = np.full(2 + 2 * k, -np.inf)
+    rec[3::2] = np.iinfo(np.int32).max
+    if len(z):
+        m = z.max()
+        rec[0], rec[1] = m, np.exp(z - m).sum()
+        order = np.lexsort((ids, -z))[:k]
+        for q, j in enumerate(order):
+            rec[2 + 2 * q], rec[3 + 2 * q] = z[j], ids[j]
+    else:
+        rec[1] = 0.0
+    return rec
+
+
+def _merge(records, k):
+    """Rank-order merge of records (the protocol dynaspec_merge_records implements)."""
+    ms = records[:, 0]
+    M = ms[np.isfinite(ms)].max()
+    S = sum(r[1] * math.exp(r[0] - M) for r in records if np.isfinite(r[0]))
+    cand = [(r[2 + 2 * q], int(r[3 + 2 * q])) for r in records for q in range(k) if np.isfinite(r[2 + 2 * q])]
+    cand.sort(key=lambda x: (-x[0], x[1]))
+    return M + math.log(S), [c[1] for c in cand[:k]]
+
+
+def _worker(rank, world, port, result_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from oracle import dynaspec_oracle as O
+    from synth import inputs as S
+    V, d, M, k, kt, B = 3000, 32, 20, 6, 8, 3
+    W = S.lm_head(V, d, 0, "f32").double().numpy()
+    tau = S.random_partition(V, M, 2)
+    perm, off = O.layout(tau, M)
+    rt = [None if x is None else x.double().numpy() for x in S.router(d, 8, M, 1, "f32")]
+    hp, e, hn = [x.double().numpy() for x in S.step_inputs(B, d, 0, "f32")]
+    lo, hi = P.cluster_ranges(off.tolist(), world)[rank]
+    scores = O.meta_score(*rt, hp, e)                      # replicated
+    recs = []
+    for b in range(B):
+        sel = O.select(scores[b], k)
+        own = sel[(sel >= lo) & (sel < hi)]                # restricted selection
+        VS = O.shortlist(own, perm, off) if len(own) else np.zeros(0, dtype=np.int64)
+        z = O.head(hn[b], W, VS)[0] if len(VS) else np.zeros(0)
+        recs.append(_record(z, VS, kt))
+    mine = torch.tensor(np.stack(recs), dtype=torch.float64)
+    out = [torch.zeros_like(mine) for _ in range(world)]
+    dist.all_gather(out, mine)                            # the one exchange step
+    gathered = torch.stack(out).numpy()                    # [G][B][rec]
+    res = []
+    for b in range(B):
+        lse, ids = _merge(gathered[:, b, :], kt)
+        ref = O.epilogue(O.head(hn[b], W, O.shortlist(O.select(scores[b], k), perm, off))[0],
+                         O.shortlist(O.select(scores[b], k), perm, off), kt)
+        res.append((abs(lse - ref["lse"]), ids == ref["top_ids"].tolist()))
+    # request sharding: max over ranks of a per-rank time
+    t = torch.tensor([float(rank + 1)], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    result_q.put((rank, res, float(t.item())))
+    dist.destroy_process_group()
+
+
+def test_cluster_sharded_protocol_gloo_world2():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    results = [q.get(timeout=300) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, res, tmax in results:
+        assert tmax == 2.0
+        for dlse, same in res:
+            assert dlse < 1e-12 and same
