@@ -440,9 +440,10 @@ def dense_baseline(D, clusters, inputs, B, C, dev, flush, reps=20):
     """Dense full-vocabulary head with the same epilogue: (a) our kernel with k = M (all clusters),
     (b) torch/cuBLAS matmul + logsumexp + topk.  Cold L2 before each rep."""
     M = clusters.M
-    sel = torch.arange(M, dtype=torch.int32, device=dev).repeat(B, 1).contiguous()
-    cnt = torch.full((B,), M, dtype=torch.int32, device=dev)
-    off = clusters.offsets.repeat(B, 1).contiguous()
+    rows = 1 if C.shared else B        # tree mode: one (full) shortlist shared by the depth's rows
+    sel = torch.arange(M, dtype=torch.int32, device=dev).repeat(rows, 1).contiguous()
+    cnt = torch.full((rows,), M, dtype=torch.int32, device=dev)
+    off = clusters.offsets.repeat(rows, 1).contiguous()
     ws = D.Workspace(D.lib().dynaspec_head_forward_ws(clusters.struct(), B, C.k_t), dev)
     hn = inputs[0][2][2]
     res = {}
@@ -451,7 +452,7 @@ def dense_baseline(D, clusters, inputs, B, C, dev, flush, reps=20):
         flush.zero_()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
-        D.head_forward(clusters, hn, sel, cnt, off, C.k_t, ws=ws)
+        D.head_forward(clusters, hn, sel, cnt, off, C.k_t, shared=C.shared, ws=ws)
         b.record()
         torch.cuda.synchronize()
         if i >= 3:

@@ -342,3 +342,87 @@ __device__ __forceinline__ void block_lse(float& m, float& s, float* red) {
   for (int w = 1; w < nw; ++w) lse_combine(m, s, red[2 * w], red[2 * w + 1]);
 }
 }  // namespace ds
+
+namespace ds {
+// Warp-level counterpart of block_topk (one warp, no block barriers): pruned rank count.
+// sv / si: this warp's smem scratch (>= n entries).  Returns the number of survivors.
+template <class Get, class Emit>
+__device__ __forceinline__ int warp_topk(int n, int K, Get get, Emit emit, float* sv, int* si) {
+  const int lane = threadIdx.x & 31;
+  const int S = min(n, max(32, 2 * K));
+  float tv = -INFINITY;
+  int tid0 = INT_MAX;
+  bool found = false;
+  for (int i = lane; i < S; i += 32) {
+    float v;
+    int id;
+    get(i, v, id);
+    if (v == -INFINITY) continue;
+    int rank = 0;
+    for (int j = 0; j < S; ++j) {
+      float v2;
+      int id2;
+      get(j, v2, id2);
+      rank += beats(v2, id2, v, id);
+    }
+    if (rank == K - 1) {
+      tv = v;
+      tid0 = id;
+      found = true;
+    }
+  }
+  const uint32_t who = __ballot_sync(0xffffffffu, found);
+  if (who) {
+    const int src = __ffs(who) - 1;
+    tv = __shfl_sync(0xffffffffu, tv, src);
+    tid0 = __shfl_sync(0xffffffffu, tid0, src);
+  }
+  int base = 0;
+  for (int i0 = 0; i0 < n; i0 += 32) {
+    const int i = i0 + lane;
+    float v = -INFINITY;
+    int id = INT_MAX;
+    if (i < n) get(i, v, id);
+    const bool keep = v > -INFINITY && !beats(tv, tid0, v, id);
+    const uint32_t b = __ballot_sync(0xffffffffu, keep);
+    if (keep) {
+      const int pos = base + __popc(b & ((1u << lane) - 1u));
+      sv[pos] = v;
+      si[pos] = id;
+    }
+    base += __popc(b);
+  }
+  __syncwarp();
+  for (int s2 = lane; s2 < base; s2 += 32) {
+    const float v = sv[s2];
+    const int id = si[s2];
+    int rank = 0;
+    for (int t = 0; t < base; ++t) rank += beats(sv[t], si[t], v, id);
+    if (rank < K) emit(rank, v, id);
+  }
+  __syncwarp();
+  return base;
+}
+
+// Warp-level (max, sum exp(z - max)) of z[0..n).
+__device__ __forceinline__ void warp_lse_items(const float* z, int n, float& m, float& s) {
+  const int lane = threadIdx.x & 31;
+  m = -INFINITY;
+  s = 0.f;
+  for (int j = lane; j < n; j += 32) {
+    const float x = z[j];
+    if (x > m) {
+      s = s * expf(m - x) + 1.f;
+      m = x;
+    } else {
+      s += expf(x - m);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float m2 = __shfl_xor_sync(0xffffffffu, m, o);
+    const float s2 = __shfl_xor_sync(0xffffffffu, s, o);
+    lse_combine(m, s, m2, s2);
+  }
+}
+}  // namespace ds

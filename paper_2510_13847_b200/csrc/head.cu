@@ -26,10 +26,11 @@ __global__ void __launch_bounds__((kMaxStages + 1) * 32, 1) head_kernel(const He
   }
   __syncthreads();
   if (a.pdl) pdl_launch_dependents();
-  head_partials(a, c);
-  if (!head_ticket(a, c)) return;
-  head_merge(a, c, a.stages * a.stage_bytes);
-  if (threadIdx.x == 0) *a.counter = 0u;  // leave the ticket at zero for the next launch
+  head_partials(a, c, a.stages * a.stage_bytes);
+  const int j = head_ticket(a, c);
+  if (j < 0) return;
+  head_merge(a, c, a.stages * a.stage_bytes, nullptr, 0, j, min(a.nrows, (int)gridDim.x));
+  head_merge_done(a, 0);  // leave the counters at zero for the next launch
 }
 
 // ------------------------------------------------------------------ host side

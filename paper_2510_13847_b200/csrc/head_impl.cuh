@@ -324,9 +324,40 @@ __device__ __forceinline__ float block_sum(float v, float* red) {
 
 // Per-CTA partial per row: (max, sum exp(z - max), top-k_t by (logit desc, id asc)), computed by
 // the whole block with shallow dependency chains (block_topk, block_lse).  Scratch: the ring.
-__device__ inline void head_partials(const HeadArgs& a, const HeadCtx& c) {
+__device__ inline void head_partials(const HeadArgs& a, const HeadCtx& c, int ring_bytes) {
   const int K = a.k_t, rec = 2 + 2 * K;
   const int tid = threadIdx.x, nt = blockDim.x;
+  if (a.nrows > 1 && (nt >> 5) * 8 * a.lcap <= ring_bytes) {
+    // several rows: one warp per row, warp-level lse and pruned top-k (no block barriers)
+    const int warp = tid >> 5, lane = tid & 31, nw = nt >> 5;
+    float* sv = reinterpret_cast<float*>(c.ring) + (size_t)warp * 2 * a.lcap;
+    int* si = reinterpret_cast<int*>(sv + a.lcap);
+    for (int r = warp; r < a.nrows; r += nw) {
+      const int gi = a.shared ? 0 : r;
+      const int n = c.segn[gi] > 0 ? c.segn[gi] : 0;
+      float* P = a.part + ((size_t)r * gridDim.x + blockIdx.x) * rec;
+      const float* zr = c.zl + r * a.lcap;
+      const int* ir = c.zid + r * a.lcap;
+      float m, se;
+      warp_lse_items(zr, n, m, se);
+      warp_topk(
+          n, K, [&](int i, float& v, int& id) { v = zr[i]; id = ir[i]; },
+          [&](int rank, float v, int id) {
+            P[2 + 2 * rank] = v;
+            P[3 + 2 * rank] = __int_as_float(id);
+          },
+          sv, si);
+      for (int q = n + lane; q < K; q += 32) {
+        P[2 + 2 * q] = -INFINITY;
+        P[3 + 2 * q] = __int_as_float(INT_MAX);
+      }
+      if (lane == 0) {
+        P[0] = m;
+        P[1] = se;
+      }
+    }
+    return;
+  }
   float* sv = reinterpret_cast<float*>(c.ring);
   int* si = reinterpret_cast<int*>(sv + a.lcap);
   for (int r = 0; r < a.nrows; ++r) {
@@ -364,16 +395,38 @@ __device__ inline void head_partials(const HeadArgs& a, const HeadCtx& c) {
   }
 }
 
-// Ticket: true in the last CTA to finish (release/acquire: all partials visible to it).
-__device__ __forceinline__ bool head_ticket(const HeadArgs& a, const HeadCtx& c) {
+// Ticket: every CTA takes an arrival index (release: its partials are visible before).  The last
+// nm = min(nrows, G) arrivals become mergers: each waits (acquire) until all G partials are in
+// and merges rows j, j + nm, ... (j = its rank among the mergers), so R rows merge in parallel.
+// Returns the merger rank j, or -1 for CTAs that only contributed partials.
+__device__ __forceinline__ int head_ticket(const HeadArgs& a, const HeadCtx& c) {
   __syncthreads();
+  const int G = gridDim.x;
+  const int nm = min(a.nrows, G);
   if (threadIdx.x == 0) {
-    const bool last = release_add(a.counter, 1u) == (unsigned)(gridDim.x - 1);
-    if (last) fence_acq_rel_gpu();
-    c.misc[0] = last ? 1 : 0;
+    const int t = (int)release_add(a.counter, 1u);
+    int j = t - (G - nm);
+    if (j >= 0) acquire_wait_geq(a.counter, (unsigned)G);
+    c.misc[0] = j >= 0 ? j : -1;
   }
   __syncthreads();
-  return c.misc[0] != 0;
+  return c.misc[0];
+}
+
+// After merging: the last merger to finish resets the ticket (and `extra_ctrs` more counters that
+// follow it: the fused step's phase counters) for the next launch.
+__device__ __forceinline__ void head_merge_done(const HeadArgs& a, int extra_ctrs) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int nm = min(a.nrows, (int)gridDim.x);
+    unsigned* done = a.counter + 3;
+    if ((int)release_add(done, 1u) == nm - 1) {
+      fence_acq_rel_gpu();
+      a.counter[0] = 0u;
+      for (int i = 1; i <= extra_ctrs; ++i) a.counter[i] = 0u;
+      *done = 0u;
+    }
+  }
 }
 
 // Merge step shared by the last-CTA merge and the cross-rank merge: staged per-partial (m_g, s_g)
@@ -431,7 +484,8 @@ __device__ inline void merge_finish(const HeadArgs& a, const HeadCtx& c, int G, 
 //  top  : T = the k_t-th best list head; only entries not beaten by T can be in the global
 //         top-k_t (k_t heads are >= T), so rank-count just those survivors.
 __device__ inline void head_merge(const HeadArgs& a, const HeadCtx& c, int ring_bytes,
-                                  unsigned long long* trace = nullptr, int G_override = 0) {
+                                  unsigned long long* trace = nullptr, int G_override = 0, int r_begin = 0,
+                                  int r_step = 1) {
   const int G = G_override > 0 ? G_override : (int)gridDim.x;
   const int tid = threadIdx.x, nt = blockDim.x;
   const int K = a.k_t, rec = 2 + 2 * K;
@@ -444,7 +498,7 @@ __device__ inline void head_merge(const HeadArgs& a, const HeadCtx& c, int ring_
   float* sv = reinterpret_cast<float*>(ci + G * K);
   int* si = reinterpret_cast<int*>(sv + G * K);
   (void)ring_bytes;
-  for (int r = 0; r < a.nrows; ++r) {
+  for (int r = r_begin; r < a.nrows; r += r_step) {
     const float* src = a.part + (size_t)r * per_row;  // this row's G records, contiguous
     if ((per_row & 3) == 0 && ((reinterpret_cast<uintptr_t>(src) & 15u) == 0)) {
       const float4* s4 = reinterpret_cast<const float4*>(src);

@@ -255,18 +255,15 @@ __global__ void __launch_bounds__((kMaxStages + 1) * 32, 1) step_kernel(const St
   __syncthreads();
   trace_mark(s.trace, 5);
   if (a.pdl) pdl_launch_dependents();
-  head_partials(a, c);
+  head_partials(a, c, a.stages * a.stage_bytes);
   trace_mark(s.trace, 6);
-  if (!head_ticket(a, c)) return;
+  const int j = head_ticket(a, c);
+  if (j < 0) return;
   trace_mark(s.trace, 14);
   trace_mark(s.trace, 15);  // back-to-back: the cost of one mark
-  head_merge(a, c, a.stages * a.stage_bytes, s.trace);
+  head_merge(a, c, a.stages * a.stage_bytes, s.trace, 0, j, min(a.nrows, (int)gridDim.x));
   trace_mark(s.trace, 7);
-  if (threadIdx.x == 0) {
-    s.ctr[0] = 0u;
-    s.ctr[1] = 0u;
-    s.ctr[2] = 0u;
-  }
+  head_merge_done(a, 2);  // also resets the phase counters ctr[1], ctr[2]
 }
 
 // ------------------------------------------------------------------ host side

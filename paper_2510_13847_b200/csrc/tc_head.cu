@@ -291,10 +291,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_head_kernel(const __grid_con
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(t.tmem_cols) : "memory");
   }
   if (a.pdl) pdl_launch_dependents();
-  head_partials(a, c);
-  if (!head_ticket(a, c)) return;
-  head_merge(a, c, t.S * kTcABytes);
-  if (threadIdx.x == 0) *a.counter = 0u;
+  head_partials(a, c, t.S * kTcABytes);
+  const int j = head_ticket(a, c);
+  if (j < 0) return;
+  head_merge(a, c, t.S * kTcABytes, nullptr, 0, j, min(a.nrows, (int)gridDim.x));
+  head_merge_done(a, 0);
 }
 
 // ------------------------------------------------------------------ host side
