@@ -158,8 +158,12 @@ __global__ void __launch_bounds__((kMaxStages + 1) * 32, 1) step_kernel(const St
     }
   }
   __syncthreads();
-  // Router constants do not depend on upstream work: stage them before waiting on the previous
-  // kernel (W2 by TMA into the idle ring; b1, b2, offsets by plain loads).
+  trace_mark(s.trace, 0);
+  if (a.pdl) pdl_wait();  // h_prev / e / h_new come from upstream kernels
+  trace_mark(s.trace, 1);
+  // Router constants (W2 by TMA into the idle ring; b1, b2, offsets by plain loads).  Issued after
+  // the PDL wait so that the early-launched CTAs do not compete with the previous step's merge
+  // for L2; they land while phase A runs.
   if (row_cta) {
     if (prefetch && threadIdx.x == 0) {
       mbar_arrive_expect_tx(w2bar, (uint32_t)s.w2_prefetch);
@@ -167,14 +171,11 @@ __global__ void __launch_bounds__((kMaxStages + 1) * 32, 1) step_kernel(const St
     }
     float* b1s = reinterpret_cast<float*>(ex + X.b1);
     float* b2s = reinterpret_cast<float*>(ex + X.b2);
-    int32_t* offs = reinterpret_cast<int32_t*>(ex + X.offs);
+    int32_t* offs_w = reinterpret_cast<int32_t*>(ex + X.offs);
     for (int u = threadIdx.x; u < s.rows1; u += blockDim.x) b1s[u] = __ldg(s.b1 + u);
     for (int m = threadIdx.x; m < M; m += blockDim.x) b2s[m] = s.h_r > 0 ? __ldg(s.b2 + m) : 0.f;
-    for (int m = threadIdx.x; m <= M; m += blockDim.x) offs[m] = __ldg(a.offsets + m);
+    for (int m = threadIdx.x; m <= M; m += blockDim.x) offs_w[m] = __ldg(a.offsets + m);
   }
-  trace_mark(s.trace, 0);
-  if (a.pdl) pdl_wait();  // h_prev / e / h_new come from upstream kernels
-  trace_mark(s.trace, 1);
   head_load_h(a, c, (int)sizeof(T), threadIdx.x, blockDim.x);
   step_phase_a<T>(s);  // router layer 1, split over every warp of every CTA
   __syncthreads();
