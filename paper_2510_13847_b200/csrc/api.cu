@@ -35,6 +35,12 @@ bool use_tc_head(const ds_clusters* c, int B, int k_t, int shared, int64_t max_s
   return shared && c->dtype == DS_BF16 && B >= 4 && tc_head_supported(c, B, k_t, max_shortlist);
 }
 
+bool use_tc_batched(const ds_clusters* c, int B, int k_t, int shared, bool z_out) {
+  const char* off = getenv("DS_DISABLE_TC");
+  if (off && off[0] == '1') return false;
+  return !shared && !z_out && c->dtype == DS_BF16 && B >= 8 && tc_batched_supported(c, B, k_t);
+}
+
 static bool dtype_ok(int dt) { return dt == DS_BF16 || dt == DS_F32; }
 
 static ds_status check_clusters(const ds_clusters* c) {
@@ -188,7 +194,8 @@ size_t dynaspec_head_forward_ws(const ds_clusters* c, int32_t B, int32_t k_t) {
   HeadPlan p;
   if (!c || B < 1 || k_t < 1 || k_t > kMaxKt) return 0;
   if (!head_plan(c, B, k_t, 0, &p)) return 0;
-  return ws_layout(0, std::max(p.part_bytes, tc_head_part_bytes(c, B, k_t))).total;
+  return ws_layout(0, std::max(std::max(p.part_bytes, tc_head_part_bytes(c, B, k_t)),
+                               tc_batched_ws_bytes(c, B, k_t))).total;
 }
 
 ds_status dynaspec_head_forward(const ds_clusters* c, const void* h_new, int32_t B, const int32_t* sel,
@@ -210,7 +217,11 @@ ds_status dynaspec_head_forward(const ds_clusters* c, const void* h_new, int32_t
   if (!ws || ws_bytes < L.total) return DS_ERR_WORKSPACE;
   uint8_t* w8 = static_cast<uint8_t*>(ws);
   cudaError_t err;
-  if (use_tc_head(c, B, k_t, shared, max_shortlist)) {
+  if (use_tc_batched(c, B, k_t, shared, z_out != nullptr)) {
+    if (ws_bytes < ws_layout(0, tc_batched_ws_bytes(c, B, k_t)).total) return DS_ERR_WORKSPACE;
+    err = launch_tc_batched(c, h_new, B, sel, sel_count, k_t, top_ids, top_logits, top_logp, lse, w8 + L.head,
+                            reinterpret_cast<unsigned*>(w8 + L.counters), (cudaStream_t)stream);
+  } else if (use_tc_head(c, B, k_t, shared, max_shortlist)) {
     if (ws_bytes < ws_layout(0, tc_head_part_bytes(c, B, k_t)).total) return DS_ERR_WORKSPACE;
     err = launch_tc_head(c, h_new, B, sel, sel_count, sl_offsets, k_t, max_shortlist, top_ids, top_logits,
                          top_logp, lse, z_out, z_stride, reinterpret_cast<float*>(w8 + L.head),
@@ -274,7 +285,8 @@ size_t dynaspec_draft_step_ws(const ds_clusters* c, const ds_router* r, int32_t 
   const size_t meta = meta_plan(r, B).part_bytes;
   const size_t scores = (size_t)B * r->M * sizeof(float);
   return std::max(ws_layout(align_up(meta, 256) + align_up(scores, 256),
-                            std::max(p.part_bytes, tc_head_part_bytes(c, B, k_t))).total,
+                            std::max(std::max(p.part_bytes, tc_head_part_bytes(c, B, k_t)),
+                                     tc_batched_ws_bytes(c, B, k_t))).total,
                   step_ws_bytes(c, r, B, k_t));
 }
 
@@ -284,6 +296,8 @@ int32_t dynaspec_draft_step_launches(const ds_clusters* c, const ds_router* r, i
   if (!c || !r || !head_plan(c, B, k_t, 0, &p)) return 0;
   const int64_t ms = shared ? c->V : 0;
   if (use_tc_head(c, B, k_t, shared, ms)) return 3;  // meta layer 1, meta layer 2 (+union), tcgen05 head
+  if (use_tc_batched(c, B, k_t, shared, false))
+    return 2 + 2 * ((B + 127) / 128);  // meta x2, then (union + tcgen05 head) per 128 rows
   if (!two_streams && step_supported(c, r, B, k_t, shared, 0)) return 1;  // fused single-stream step
   return 2 + p.launches;  // meta layer 1, meta layer 2 (+select), head chunks
 }
@@ -310,7 +324,8 @@ ds_status dynaspec_draft_step(const ds_clusters* c, const ds_router* r, const vo
   const bool two_streams = s_meta != nullptr && s_meta != s_draft;
   if (two_streams && (!ev_fork || !ev_join)) return DS_ERR_SHAPE;
   const bool tc = use_tc_head(c, B, k_t, shared, ms);
-  const bool fused = !tc && !two_streams && step_supported(c, r, B, k_t, shared, ms);
+  const bool tcb = !tc && use_tc_batched(c, B, k_t, shared, out->z_out != nullptr);
+  const bool fused = !tc && !tcb && !two_streams && step_supported(c, r, B, k_t, shared, ms);
   if (fused) {  // one persistent launch: router + select + head + epilogue (step.cu)
     const size_t need = step_ws_bytes(c, r, B, k_t);
     if (!ws || need == 0 || ws_bytes < need) return DS_ERR_WORKSPACE;
@@ -361,7 +376,13 @@ ds_status dynaspec_draft_step(const ds_clusters* c, const ds_router* r, const vo
   cudaStreamIsCapturing(sd, &cap);
   const unsigned evflags = cap == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : cudaEventRecordDefault;
   if (head_begin && cudaEventRecordWithFlags((cudaEvent_t)head_begin, sd, evflags) != cudaSuccess) return DS_ERR_CUDA;
-  if (tc) {
+  if (tcb) {
+    if (ws_bytes < ws_layout(align_up(meta_bytes, 256) + align_up(score_bytes, 256),
+                             tc_batched_ws_bytes(c, B, k_t)).total)
+      return DS_ERR_WORKSPACE;
+    err = launch_tc_batched(c, h_new, B, out->sel, out->sel_count, k_t, out->top_ids, out->top_logits,
+                            out->top_logp, out->lse, w8 + L.head, counters, sd);
+  } else if (tc) {
     err = launch_tc_head(c, h_new, B, out->sel, out->sel_count, out->sl_offsets, k_t, ms, out->top_ids,
                          out->top_logits, out->top_logp, out->lse, out->z_out, out->z_stride,
                          reinterpret_cast<float*>(w8 + L.head), counters, sd, !two_streams && head_begin == nullptr);

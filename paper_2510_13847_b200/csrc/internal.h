@@ -73,6 +73,13 @@ cudaError_t launch_tc_head(const ds_clusters* c, const void* h_new, int R, const
                            int32_t* top_ids, float* top_logits, float* top_logp, float* lse, float* z_out,
                            int64_t z_stride, float* part, unsigned* counter, cudaStream_t st, bool pdl);
 bool use_tc_head(const ds_clusters* c, int B, int k_t, int shared, int64_t max_shortlist);
+// batched per-row rows (each with its own selection), streamed once as their union on tcgen05
+bool tc_batched_supported(const ds_clusters* c, int B, int k_t);
+size_t tc_batched_ws_bytes(const ds_clusters* c, int B, int k_t);
+cudaError_t launch_tc_batched(const ds_clusters* c, const void* h_new, int B, const int32_t* sel,
+                              const int32_t* sel_count, int k_t, int32_t* top_ids, float* top_logits,
+                              float* top_logp, float* lse, void* ws, unsigned* counter, cudaStream_t st);
+bool use_tc_batched(const ds_clusters* c, int B, int k_t, int shared, bool z_out);
 
 // ---- cluster sharding (shard.cu)
 cudaError_t launch_restrict(const int32_t* sel, const int32_t* cnt, int rows, int M, const int32_t* offsets, int m_lo,

@@ -22,6 +22,7 @@
 
 #include "head_impl.cuh"
 #include "internal.h"
+#include "select_impl.cuh"
 
 namespace ds {
 
@@ -38,13 +39,18 @@ struct TcArgs {
   int32_t S;        // ring stages
   int32_t kchunks;  // ceil(d / 64)
   int32_t tmem_cols;
+  int32_t online;   // 1: per-row running (max, sum, top-k) per tile instead of on-chip logit buffers
+  const uint32_t* rowmask;  // nullable [nrows][32]: clusters each row selected (per-row batched mode)
 };
 
 struct TcSmem {
-  uint32_t a, b, bars, slot, misc, red, sega, segn, segi, boxes, zl, zid, total;
+  uint32_t a, b, bars, slot, misc, red, sega, segn, segi, boxes, zl, zid, stage, tokid, cid, runm, runs, lst, scr,
+      total;
 };
 
-__host__ __device__ inline TcSmem tc_smem(int S, int N, int rows, int lcap) {
+constexpr int kTcScr = 128 + kMaxKt;  // per-warp warp_topk scratch entries (online mode)
+
+__host__ __device__ inline TcSmem tc_smem(int S, int N, int rows, int lcap, int online = 0, int K = 0) {
   TcSmem L;
   uint32_t o = 0;
   L.a = o;
@@ -70,9 +76,24 @@ __host__ __device__ inline TcSmem tc_smem(int S, int N, int rows, int lcap) {
   L.boxes = o;
   o += kTcMaxBoxes * 16;
   L.zl = o;
-  o += (uint32_t)rows * lcap * 4;
+  o += online ? 0u : (uint32_t)rows * lcap * 4;
   L.zid = o;
-  o += (uint32_t)rows * lcap * 4;
+  o += online ? 0u : (uint32_t)rows * lcap * 4;
+  L.stage = o;
+  o += online ? (uint32_t)rows * 128 * 4 : 0u;
+  L.tokid = o;
+  o += online ? 128u * 4 : 0u;
+  L.cid = o;
+  o += online ? 128u * 4 : 0u;
+  L.runm = o;
+  o += online ? (uint32_t)rows * 4 : 0u;
+  L.runs = o;
+  o += online ? (uint32_t)rows * 4 : 0u;
+  o = (o + 15u) & ~15u;
+  L.lst = o;
+  o += online ? 2u * rows * K * 8 : 0u;
+  L.scr = o;
+  o += online ? 4u * kTcScr * 8 : 0u;
   L.total = o;
   return L;
 }
@@ -125,7 +146,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_head_kernel(const __grid_con
                                                                 const TcArgs t) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const HeadArgs& a = t.h;
-  const TcSmem L = tc_smem(t.S, t.N, a.nrows, a.lcap);
+  const TcSmem L = tc_smem(t.S, t.N, a.nrows, a.lcap, t.online, a.k_t);
   uint8_t* sa = smem + L.a;
   uint8_t* sb = smem + L.b;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.bars);
@@ -190,7 +211,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_head_kernel(const __grid_con
       while (pos < s1 && nb < kTcMaxBoxes) {
         const long long lim = cl_end < s1 ? cl_end : s1;
         const int m = (int)min((long long)kTcBoxRows, lim - pos);
-        boxes[nb++] = make_int4((int)(base + (pos - cl_beg)), (int)(pos - s0), m, 0);
+        boxes[nb++] = make_int4((int)(base + (pos - cl_beg)), (int)(pos - s0), m, __ldcg(a.sel + i));
         pos += m;
         if (pos == cl_end && pos < s1) {
           ++i;
@@ -252,7 +273,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_head_kernel(const __grid_con
       }
     }
     __syncwarp();
-  } else {
+  } else if (!t.online) {
     // epilogue warps 2..5: TMEM lane quarter q = warp % 4 holds tokens 32q .. 32q + 31 of a tile
     const int q = warp & 3;
     const int row = 32 * q + lane;
@@ -261,26 +282,133 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_head_kernel(const __grid_con
       const int buf = tile & 1;
       mbar_wait(&tfull[buf], ((uint32_t)tile >> 1) & 1u);
       tc_fence_after();
-      float v[64];
       const uint32_t taddr = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(buf * t.N);
-      for (int c0 = 0; c0 < t.N; c0 += 16) tmem_ld16(taddr + c0, v + c0);
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[buf]);
       const int bi = tile * kTcBoxes + row / kTcBoxRows, r = row % kTcBoxRows;
+      int local = -1, tok = 0;
       if (bi < nboxes) {
         const int4 bx = boxes[bi];
         if (r < bx.z) {
-          const int local = bx.y + r;
-          const int tok = __ldg(a.perm + bx.x + r);
-          const long long vpos = c.sega[0] + local;
-          for (int rr = 0; rr < nr; ++rr) {
-            const float z = v[rr] + 0.0f;
-            c.zl[rr * a.lcap + local] = z;
-            c.zid[rr * a.lcap + local] = tok;
-            if (a.z_out) a.z_out[(size_t)rr * a.z_stride + vpos] = z;
+          local = bx.y + r;
+          tok = __ldg(a.perm + bx.x + r);
+        }
+      }
+      const long long vpos = c.sega[0] + local;
+      for (int c0 = 0; c0 < t.N; c0 += 16) {
+        float v[16];
+        tmem_ld16(taddr + c0, v);
+        if (local >= 0) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const int rr = c0 + j;
+            if (rr < nr) {
+              const float z = v[j] + 0.0f;
+              c.zl[rr * a.lcap + local] = z;
+              c.zid[rr * a.lcap + local] = tok;
+              if (a.z_out) a.z_out[(size_t)rr * a.z_stride + vpos] = z;
+            }
           }
         }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[buf]);
+    }
+  } else {
+    // online epilogue: stage the tile's logits (masked to each row's own clusters), then warp
+    // ew = warp - 2 folds rows ew, ew + 4, ... into their running (max, sum exp) and top-k_t.
+    const int q = warp & 3, ew = warp - 2;
+    const int row = 32 * q + lane;
+    const int nr = a.nrows, K = a.k_t;
+    float* stage = reinterpret_cast<float*>(smem + L.stage);
+    int* tokid = reinterpret_cast<int*>(smem + L.tokid);
+    float* runm = reinterpret_cast<float*>(smem + L.runm);
+    float* runs = reinterpret_cast<float*>(smem + L.runs);
+    float2* lst = reinterpret_cast<float2*>(smem + L.lst);  // [2][nr][K] (value, id bits)
+    float* sv = reinterpret_cast<float*>(smem + L.scr) + (size_t)ew * 2 * kTcScr;
+    int* si = reinterpret_cast<int*>(sv + kTcScr);
+    for (int i = threadIdx.x - 64; i < nr * K; i += 128) lst[i] = make_float2(-INFINITY, __int_as_float(INT_MAX));
+    for (int i = threadIdx.x - 64; i < nr; i += 128) {
+      runm[i] = -INFINITY;
+      runs[i] = 0.f;
+    }
+    named_bar_sync(2, 128);
+    for (int tile = 0; tile < ntiles; ++tile) {
+      const int buf = tile & 1;
+      mbar_wait(&tfull[buf], ((uint32_t)tile >> 1) & 1u);
+      tc_fence_after();
+      const int bi = tile * kTcBoxes + row / kTcBoxRows, r = row % kTcBoxRows;
+      bool valid = false;
+      int tok = INT_MAX, cl = 0;
+      if (bi < nboxes) {
+        const int4 bx = boxes[bi];
+        if (r < bx.z) {
+          valid = true;
+          tok = __ldg(a.perm + bx.x + r);
+          cl = bx.w;
+        }
+      }
+      tokid[row] = tok;
+      const uint32_t taddr = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(buf * t.N);
+      for (int c0 = 0; c0 < t.N; c0 += 16) {
+        float v[16];
+        tmem_ld16(taddr + c0, v);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const int rr = c0 + j;
+          if (rr < nr) {
+            bool ok = valid;
+            if (ok && t.rowmask) ok = (__ldg(t.rowmask + (size_t)rr * 32 + (cl >> 5)) >> (cl & 31)) & 1u;
+            stage[rr * 128 + row] = ok ? v[j] + 0.0f : -INFINITY;
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[buf]);
+      named_bar_sync(2, 128);
+      const int cur = tile & 1, nxt = cur ^ 1;
+      for (int rr = ew; rr < nr; rr += 4) {
+        const float* zr = stage + rr * 128;
+        float m, se;
+        warp_lse_items(zr, 128, m, se);
+        if (lane == 0) {
+          float M0 = runm[rr], S0 = runs[rr];
+          lse_combine(M0, S0, m, se);
+          runm[rr] = M0;
+          runs[rr] = S0;
+        }
+        const float2* lc = lst + ((size_t)cur * nr + rr) * K;
+        float2* ln = lst + ((size_t)nxt * nr + rr) * K;
+        const int nsv = warp_topk(
+            128 + K, K,
+            [&](int i, float& v, int& id) {
+              if (i < 128) {
+                v = zr[i];
+                id = tokid[i];
+              } else {
+                v = lc[i - 128].x;
+                id = __float_as_int(lc[i - 128].y);
+              }
+            },
+            [&](int rank, float v, int id) { ln[rank] = make_float2(v, __int_as_float(id)); }, sv, si);
+        for (int qq = nsv + lane; qq < K; qq += 32) ln[qq] = make_float2(-INFINITY, __int_as_float(INT_MAX));
+        __syncwarp();
+      }
+      named_bar_sync(2, 128);
+    }
+    // per-CTA partial records [row][cta][rec]
+    const int fin = ntiles & 1;  // buffer holding the latest lists
+    const int rec = 2 + 2 * K;
+    for (int rr = ew; rr < nr; rr += 4) {
+      float* P = a.part + ((size_t)rr * gridDim.x + blockIdx.x) * rec;
+      const float2* lf = lst + ((size_t)fin * nr + rr) * K;
+      for (int qq = lane; qq < K; qq += 32) {
+        P[2 + 2 * qq] = lf[qq].x;
+        P[3 + 2 * qq] = lf[qq].y;
+      }
+      if (lane == 0) {
+        P[0] = runm[rr];
+        P[1] = runs[rr];
       }
     }
   }
@@ -291,11 +419,38 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_head_kernel(const __grid_con
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(t.tmem_cols) : "memory");
   }
   if (a.pdl) pdl_launch_dependents();
-  head_partials(a, c, t.S * kTcABytes);
+  if (!t.online) head_partials(a, c, t.S * kTcABytes);
   const int j = head_ticket(a, c);
   if (j < 0) return;
   head_merge(a, c, t.S * kTcABytes, nullptr, 0, j, min(a.nrows, (int)gridDim.x));
   head_merge_done(a, 0);
+}
+
+// Union of B rows' selections (one CTA): per-row cluster bit masks + the ascending union with
+// its sl_offsets — the shortlist the batched head streams once for all rows.
+__global__ void __launch_bounds__(256) union_kernel(const int32_t* __restrict__ sel, const int32_t* __restrict__ cnt,
+                                                    int B, int M, const int32_t* __restrict__ offsets,
+                                                    uint32_t* __restrict__ rowmask, int32_t* usel, int32_t* ucnt,
+                                                    int32_t* usloff) {
+  extern __shared__ __align__(16) uint32_t us[];
+  uint32_t* acc = us;                                   // [32]
+  uint32_t* rm = us + 32;                               // [B][32]
+  int32_t* offs = reinterpret_cast<int32_t*>(rm + B * 32);  // [M+1]
+  int32_t* tmp = offs + M + 1;                          // [M]
+  for (int i = threadIdx.x; i < 32 + B * 32; i += blockDim.x) us[i] = 0u;
+  for (int m = threadIdx.x; m <= M; m += blockDim.x) offs[m] = offsets[m];
+  __syncthreads();
+  for (int r = 0; r < B; ++r) {
+    const int n = cnt[r];
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      const int m = sel[(size_t)r * M + i];
+      atomicOr(&acc[m >> 5], 1u << (m & 31));
+      atomicOr(&rm[r * 32 + (m >> 5)], 1u << (m & 31));
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < B * 32; i += blockDim.x) rowmask[i] = rm[i];
+  emit_fast(acc, M, offs, usel, ucnt, usloff, tmp);
 }
 
 // ------------------------------------------------------------------ host side
@@ -330,12 +485,13 @@ static bool make_map(CUtensorMap* m, const void* base, uint64_t rows, uint64_t d
 
 struct TcPlan {
   HeadPlan hp;  // G, lcap, rec, part_bytes
-  int N, S, tmem_cols;
+  int N, S, tmem_cols, online;
   size_t smem;
 };
 
-static bool tc_plan(const ds_clusters* c, int R, int k_t, int64_t max_shortlist, TcPlan* p) {
-  if (c->dtype != DS_BF16 || R < 1 || R > 64 || (c->d % 8) != 0) return false;
+static bool tc_plan(const ds_clusters* c, int R, int k_t, int64_t max_shortlist, TcPlan* p, int online = 0) {
+  if (c->dtype != DS_BF16 || R < 1 || R > (online ? 128 : 64) || (c->d % 8) != 0) return false;
+  p->online = online;
   p->N = ((R + 15) / 16) * 16;
   p->tmem_cols = 32;
   while (p->tmem_cols < 2 * p->N) p->tmem_cols *= 2;
@@ -343,6 +499,7 @@ static bool tc_plan(const ds_clusters* c, int R, int k_t, int64_t max_shortlist,
   const int64_t ms = (max_shortlist > 0 && max_shortlist < c->V) ? max_shortlist : c->V;
   p->hp.lcap = (int)((ms + p->hp.G - 1) / p->hp.G);
   if ((p->hp.lcap + kTcBoxRows - 1) / kTcBoxRows + c->M > kTcMaxBoxes) return false;
+  if (online && k_t > kMaxKt) return false;
   p->hp.rec = 2 + 2 * k_t;
   p->hp.rows_per_launch = R;
   p->hp.launches = 1;
@@ -351,14 +508,92 @@ static bool tc_plan(const ds_clusters* c, int R, int k_t, int64_t max_shortlist,
   p->S = 0;
   for (int S = 8; S >= 3; --S) {
     if (S * kTcABytes < merge_smem_bytes(p->hp.G, k_t, kTcThreads / 32) || p->hp.G > 32 * (kTcThreads / 32)) break;
-    if ((int)tc_smem(S, p->N, R, p->hp.lcap).total <= smax) {
+    if ((int)tc_smem(S, p->N, R, p->hp.lcap, online, k_t).total <= smax) {
       p->S = S;
       break;
     }
   }
   if (p->S == 0) return false;
-  p->smem = tc_smem(p->S, p->N, R, p->hp.lcap).total;
+  p->smem = tc_smem(p->S, p->N, R, p->hp.lcap, online, k_t).total;
   return encode_fn() != nullptr;
+}
+
+// Batched per-row mode: rows with their own selections, streamed once as their union.
+constexpr int kTcBatchRows = 128;
+
+bool tc_batched_supported(const ds_clusters* c, int B, int k_t) {
+  TcPlan p;
+  return c->M <= 1024 && tc_plan(c, std::min(B, kTcBatchRows), k_t, 0, &p, 1);
+}
+
+size_t tc_batched_ws_bytes(const ds_clusters* c, int B, int k_t) {
+  TcPlan p;
+  if (!tc_plan(c, std::min(B, kTcBatchRows), k_t, 0, &p, 1)) return 0;
+  const int rows = std::min(B, kTcBatchRows);
+  return align_up(p.hp.part_bytes, 256) + align_up((size_t)rows * 32 * 4, 256) +
+         align_up((size_t)(2 * c->M + 8) * 4, 256);
+}
+
+static cudaError_t launch_tc_kernel(const TcPlan& p, const CUtensorMap& mw, const CUtensorMap& mh, const TcArgs& t,
+                                    cudaStream_t st, bool pdl) {
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(tc_head_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem_optin());
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(p.hp.G);
+  cfg.blockDim = dim3(kTcThreads);
+  cfg.dynamicSmemBytes = p.smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, tc_head_kernel, mw, mh, t);
+}
+
+cudaError_t launch_tc_batched(const ds_clusters* c, const void* h_new, int B, const int32_t* sel,
+                              const int32_t* sel_count, int k_t, int32_t* top_ids, float* top_logits,
+                              float* top_logp, float* lse, void* ws, unsigned* counter, cudaStream_t st) {
+  const int esz = 2;
+  for (int r0 = 0; r0 < B; r0 += kTcBatchRows) {
+    const int nr = std::min(kTcBatchRows, B - r0);
+    TcPlan p;
+    if (!tc_plan(c, nr, k_t, 0, &p, 1)) return cudaErrorInvalidValue;
+    uint8_t* w8 = static_cast<uint8_t*>(ws);
+    float* part = reinterpret_cast<float*>(w8);
+    uint32_t* rowmask = reinterpret_cast<uint32_t*>(w8 + align_up(p.hp.part_bytes, 256));
+    int32_t* usel = reinterpret_cast<int32_t*>(w8 + align_up(p.hp.part_bytes, 256) +
+                                               align_up((size_t)std::min(B, kTcBatchRows) * 32 * 4, 256));
+    int32_t* ucnt = usel + c->M;
+    int32_t* usloff = ucnt + 4;
+    const size_t usm = (size_t)(32 + nr * 32) * 4 + (size_t)(2 * c->M + 1) * 4;
+    union_kernel<<<1, 256, usm, st>>>(sel + (size_t)r0 * c->M, sel_count + r0, nr, c->M, c->offsets, rowmask, usel,
+                                      ucnt, usloff);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    CUtensorMap mw, mh;
+    if (!make_map(&mw, c->W_perm, (uint64_t)c->V, (uint64_t)c->d, kTcBoxRows)) return cudaErrorInvalidValue;
+    const void* h0 = static_cast<const uint8_t*>(h_new) + (size_t)r0 * c->d * esz;
+    if (!make_map(&mh, h0, (uint64_t)nr, (uint64_t)c->d, (uint32_t)p.N)) return cudaErrorInvalidValue;
+    TcArgs t;
+    fill_head_args(t.h, c, p.hp, h0, 0, nr, usel, ucnt, usloff, 1, k_t, 0, top_ids + (size_t)r0 * k_t,
+                   top_logits + (size_t)r0 * k_t, top_logp + (size_t)r0 * k_t, lse + r0, nullptr, 0, part, counter,
+                   false);
+    t.h.h = h0;
+    t.N = p.N;
+    t.S = p.S;
+    t.kchunks = (c->d + kTcK - 1) / kTcK;
+    t.tmem_cols = p.tmem_cols;
+    t.online = 1;
+    t.rowmask = rowmask;
+    e = launch_tc_kernel(p, mw, mh, t, st, false);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
 
 bool tc_head_supported(const ds_clusters* c, int R, int k_t, int64_t max_shortlist) {
@@ -387,23 +622,9 @@ cudaError_t launch_tc_head(const ds_clusters* c, const void* h_new, int R, const
   t.S = p.S;
   t.kchunks = (c->d + kTcK - 1) / kTcK;
   t.tmem_cols = p.tmem_cols;
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(tc_head_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem_optin());
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(p.hp.G);
-  cfg.blockDim = dim3(kTcThreads);
-  cfg.dynamicSmemBytes = p.smem;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = pdl ? 1 : 0;
-  return cudaLaunchKernelEx(&cfg, tc_head_kernel, mw, mh, t);
+  t.online = 0;
+  t.rowmask = nullptr;
+  return launch_tc_kernel(p, mw, mh, t, st, pdl);
 }
 
 }  // namespace ds

@@ -442,3 +442,64 @@ def test_tc_head_random_regime_qwen_full_size(monkeypatch):
         assert np.max(np.abs(z - ref[b]["z"])) <= 2e-2
         check_topk(st.top_ids[b].cpu().numpy(), st.top_logits[b].cpu().numpy(), st.top_logp[b].cpu().numpy(),
                    st.lse[b].item(), ref[b]["z"], ref[b]["V_S"], C.k_t, torch.bfloat16)
+
+
+# ------------------------------------------------------------------ batched per-row rows on tcgen05 (K5/S5')
+
+@pytest.mark.parametrize("B", [8, 13, 64, 130])
+def test_tc_batched_per_row_exact(B, monkeypatch):
+    """Independent rows with their own selections, streamed once as their union on the tensor cores
+    with per-row cluster masks and online (max, sum, top-k): top ids / logits / lse equal the oracle
+    (exact regime) and the CUDA-core per-row path."""
+    Dy = _dyn()
+    V, d, M, k, kt = 9001, 256, 32, 6, 10
+    q = max(1, min(127, int((2 ** 21 / d) ** 0.5)))
+    W = S.lm_head(V, d, 0, "bf16", "exact", q=q)
+    tau, part = _partition(V, M)
+    c = Dy.Clusters.from_tau(W.to(DEV), torch.as_tensor(tau, dtype=torch.int32, device=DEV), M)
+    hn = S.hidden(B, d, 17, "bf16", "exact", q=q)
+    rng = np.random.default_rng(B)
+    sel = torch.zeros((B, M), dtype=torch.int32)
+    off = torch.zeros((B, M + 1), dtype=torch.int32)
+    cnt = torch.full((B,), k, dtype=torch.int32)
+    sels = []
+    for b in range(B):
+        sb = np.sort(rng.choice(M, k, replace=False))
+        sels.append(sb)
+        sel[b, :k] = torch.as_tensor(sb)
+        off[b, :k + 1] = torch.as_tensor(O.shortlist_offsets(sb, part["offsets"]))
+    outs = {}
+    for mode in ("tc", "cuda"):
+        monkeypatch.setenv("DS_DISABLE_TC", "0" if mode == "tc" else "1")
+        outs[mode] = Dy.head_forward(c, hn.to(DEV), sel.to(DEV), cnt.to(DEV), off.to(DEV), kt)
+    torch.cuda.synchronize()
+    for b in range(B):
+        V_S = O.shortlist(sels[b], part["perm"], part["offsets"])
+        z = O.head(f64(hn)[b], f64(W), V_S)[0]
+        check_topk(outs["tc"]["top_ids"][b].cpu().numpy(), outs["tc"]["top_logits"][b].cpu().numpy(),
+                   outs["tc"]["top_logp"][b].cpu().numpy(), outs["tc"]["lse"][b].item(), z, V_S, kt, torch.float32,
+                   exact=True)
+    assert torch.equal(outs["tc"]["top_ids"], outs["cuda"]["top_ids"])
+    assert torch.equal(outs["tc"]["top_logits"], outs["cuda"]["top_logits"])
+
+
+def test_tc_batched_draft_step_llama3_b16(monkeypatch):
+    """Draft step at Llama-3 size with 16 independent rows (batched tcgen05 path) vs the oracle."""
+    Dy = _dyn()
+    monkeypatch.setenv("DS_DISABLE_TC", "0")
+    C = S.CONFIGS["llama3"]
+    B = 16
+    W, rt, tau, part, c, r = _setup(C.V, C.d, C.M, C.h_r, "bf16", "random")
+    st = Dy.DraftStep(c, r, B, C.k_t)
+    assert st.launches == 4
+    hp, e, hn = S.step_inputs(B, C.d, 2, "bf16")
+    st(hp.to(DEV), e.to(DEV), hn.to(DEV), t=2, k_max=C.k_max, k_min=C.k_min)
+    torch.cuda.synchronize()
+    Wo, ro = Rows(W), _oracle_router(rt)
+    for b in range(B):
+        cnt = st.sel_count[b].item()
+        sel_gpu = st.sel[b, :cnt].cpu().numpy()
+        ref = O.draft_step(part, ro, Wo, f64(hp[b:b + 1]), f64(e[b:b + 1]), f64(hn[b:b + 1]), 2, C.k_max, C.k_min,
+                           C.k_t, sel_override=[sel_gpu])[0]
+        check_topk(st.top_ids[b].cpu().numpy(), st.top_logits[b].cpu().numpy(), st.top_logp[b].cpu().numpy(),
+                   st.lse[b].item(), ref["z"], ref["V_S"], C.k_t, torch.bfloat16)
