@@ -346,8 +346,9 @@ def run_ours(args, ws, rank, local):
                 head_ms.append(float("nan"))
     # algorithmic bytes per head launch: shortlist rows x d x b_w + h_new + perm ids + outputs
     bw = 2 if args.dtype == "bf16" else 4
-    vs_sizes = []
+    vs_sizes, union_list = [], []
     # replay each pool entry once more (untimed) to read back its shortlist sizes
+    clusters_sizes = np.diff(clusters.offsets.cpu().numpy().astype(np.int64))
     sizes_by_pool = {}
     for j in sorted({(args.warmup + i) % pool for i in range(args.steps)}):
         run(j)
@@ -357,14 +358,20 @@ def run_ours(args, ws, rank, local):
             st = steppers[t]
             cnt = st.sel_count.cpu()
             offs = st.sl_offsets.cpu()
-            per_t.append([int(offs[r, cnt[r]]) for r in range(cnt.numel())])
+            sel = st.sel.cpu()
+            rows_each = [int(offs[r, cnt[r]]) for r in range(cnt.numel())]
+            union = sorted({int(m) for r in range(cnt.numel()) for m in sel[r, :cnt[r]].tolist()})
+            csz = clusters_sizes[union].sum() if union else 0
+            per_t.append((rows_each, int(csz)))
         sizes_by_pool[j] = per_t
     for i in range(args.steps):
         j = (args.warmup + i) % pool
         for t in range(C.positions):
-            n_rows = sizes_by_pool[j][t]
-            vs = sum(n_rows)
-            vs_sizes.append(vs / len(n_rows))
+            n_rows, union_rows = sizes_by_pool[j][t]
+            vs_sizes.append(sum(n_rows) / len(n_rows))
+            union_list.append(union_rows)
+            # algorithmic bytes: the UNION of the rows' shortlists is streamed once
+            vs = union_rows
             hb_ = vs * C.d * bw + 4 * vs + B * C.d * bw + B * (C.k_t * 12 + 4)
             if fused:  # the fused kernel also streams the router: W1, W2, x = [h_prev || e]
                 hb_ += (max(C.h_r, 0) or C.M) * 2 * C.d * bw + C.M * C.h_r * bw + B * 2 * C.d * bw + B * C.M * 4
@@ -413,6 +420,8 @@ def run_ours(args, ws, rank, local):
                        "parallelism": f"request-sharded x{ws} (no data-path collective)",
                        "us_per_draft_step": dyn_us_per_pos,
                        "mean_shortlist_rows": float(np.mean(vs_sizes)),
+                       "mean_union_rows": float(np.mean(union_list)),
+                       "union_fraction_of_V": float(np.mean(union_list)) / C.V,
                        "l2": "flushed (512 MB write) before every step, outside the timed event pair",
                        "cuda_graph": use_graph, **part_info,
                        "dense_us_per_draft_step": dense["best_us"], "dense_detail": dense,

@@ -411,6 +411,7 @@ __device__ __forceinline__ void warp_lse_items(const float* z, int n, float& m, 
   s = 0.f;
   for (int j = lane; j < n; j += 32) {
     const float x = z[j];
+    if (x == -INFINITY) continue;  // masked (not in this row's shortlist)
     if (x > m) {
       s = s * expf(m - x) + 1.f;
       m = x;

@@ -369,6 +369,7 @@ __device__ inline void head_partials(const HeadArgs& a, const HeadCtx& c, int ri
     float m = -INFINITY, se = 0.f;
     for (int j = tid; j < n; j += nt) {
       const float z = zr[j];
+      if (z == -INFINITY) continue;
       if (z > m) {
         se = se * expf(m - z) + 1.f;
         m = z;
