@@ -360,6 +360,33 @@ __device__ inline void head_partials(const HeadArgs& a, const HeadCtx& c, int ri
   }
   float* sv = reinterpret_cast<float*>(c.ring);
   int* si = reinterpret_cast<int*>(sv + a.lcap);
+  if (a.nrows == 1 && c.segn[0] <= 1024) {
+    // one row, few logits: one warp, no block barriers (barriers dominate at this size)
+    if (tid < 32) {
+      const int n = c.segn[0] > 0 ? c.segn[0] : 0;
+      float* P = a.part + (size_t)blockIdx.x * rec;
+      const float* zr = c.zl;
+      const int* ir = c.zid;
+      float m, se;
+      warp_lse_items(zr, n, m, se);
+      warp_topk(
+          n, K, [&](int i, float& v, int& id) { v = zr[i]; id = ir[i]; },
+          [&](int rank, float v, int id) {
+            P[2 + 2 * rank] = v;
+            P[3 + 2 * rank] = __int_as_float(id);
+          },
+          sv, si);
+      for (int q = n + tid; q < K; q += 32) {
+        P[2 + 2 * q] = -INFINITY;
+        P[3 + 2 * q] = __int_as_float(INT_MAX);
+      }
+      if (tid == 0) {
+        P[0] = m;
+        P[1] = se;
+      }
+    }
+    return;
+  }
   for (int r = 0; r < a.nrows; ++r) {
     const int gi = a.shared ? 0 : r;
     const int n = c.segn[gi] > 0 ? c.segn[gi] : 0;
@@ -435,20 +462,23 @@ __device__ __forceinline__ void head_merge_done(const HeadArgs& a, int extra_ctr
 __device__ inline void merge_finish(const HeadArgs& a, const HeadCtx& c, int G, int r, const float* pm,
                                     const float* ps, const float* cv, const int* ci, float* sv, int* si,
                                     bool valid_row, unsigned long long* trace) {
-  const int tid = threadIdx.x, nt = blockDim.x;
+  const int tid = threadIdx.x;
   const int K = a.k_t, rec = 2 + 2 * K;
-    float mx = -INFINITY;
-    for (int g = tid; g < G; g += nt) mx = fmaxf(mx, pm[g]);
-    mx = block_max(mx, c.red);
-    float S = 0.f;
-    for (int g = tid; g < G; g += nt)
-      if (pm[g] > -INFINITY) S += ps[g] * expf(pm[g] - mx);
-    S = block_sum(S, c.red);
+  // one warp: the G records are already staged in shared memory, so barriers would dominate
+  if (tid < 32) {
+    float mx = -INFINITY, S = 0.f;
+    for (int g = tid; g < G; g += 32) lse_combine(mx, S, pm[g], ps[g]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float m2 = __shfl_xor_sync(0xffffffffu, mx, o);
+      const float s2 = __shfl_xor_sync(0xffffffffu, S, o);
+      lse_combine(mx, S, m2, s2);
+    }
     trace_mark(trace, 17);
     const bool ok = valid_row && mx > -INFINITY;
     const float lse = ok ? mx + logf(S) : __int_as_float(0x7fc00000);
     // candidates in rank-major order: the first G items are the heads of the G sorted lists
-    block_topk(
+    const int nsv = warp_topk(
         G * K, K, [&](int e, float& v, int& id) { v = cv[e]; id = ci[e]; },
         [&](int rank, float v, int id) {
           if (a.record_out) {
@@ -460,10 +490,9 @@ __device__ inline void merge_finish(const HeadArgs& a, const HeadCtx& c, int G, 
             a.top_logp[(size_t)r * K + rank] = ok ? v - lse : -INFINITY;
           }
         },
-        sv, si, c.misc + 8);
+        sv, si);
     trace_mark(trace, 19);
-    const int nvalid = c.misc[8];
-    for (int q = nvalid + tid; q < K; q += nt) {
+    for (int q = nsv + tid; q < K; q += 32) {
       if (a.record_out) {
         a.record_out[(size_t)r * rec + 2 + 2 * q] = -INFINITY;
         a.record_out[(size_t)r * rec + 3 + 2 * q] = __int_as_float(INT_MAX);
@@ -473,11 +502,15 @@ __device__ inline void merge_finish(const HeadArgs& a, const HeadCtx& c, int G, 
         a.top_logp[(size_t)r * K + q] = -INFINITY;
       }
     }
-    if (a.record_out && tid == 0) {
-      a.record_out[(size_t)r * rec] = mx;
-      a.record_out[(size_t)r * rec + 1] = S;
+    if (tid == 0) {
+      if (a.record_out) {
+        a.record_out[(size_t)r * rec] = mx;
+        a.record_out[(size_t)r * rec + 1] = S;
+      } else {
+        a.lse[r] = lse;
+      }
     }
-  if (tid == 0 && !a.record_out) a.lse[r] = lse;
+  }
 }
 
 // Last CTA: merge the G partials of every row -> lse, top ids (remapped), logp.

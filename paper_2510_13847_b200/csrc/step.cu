@@ -76,6 +76,7 @@ __device__ void step_phase_a(const StepArgs& s) {
   const T* W1 = static_cast<const T*>(s.W1);
   const T* hp = static_cast<const T*>(s.h_prev);
   const T* ev = static_cast<const T*>(s.e);
+  const uint64_t keep = policy_evict_last();
   for (int t = blockIdx.x * nw + warp; t < tasks; t += gridDim.x * nw) {
     const int u = t % s.rows1, ks = t / s.rows1;
     const int k0 = ks * s.KC;
@@ -83,7 +84,7 @@ __device__ void step_phase_a(const StepArgs& s) {
 #pragma unroll
     for (int j = 0; j < kStepCH; ++j) {
       const int k = k0 + lane * E + j * 32 * E;
-      wv[j] = (k < dr && k < k0 + s.KC) ? __ldg(reinterpret_cast<const uint4*>(W1 + (size_t)u * dr + k))
+      wv[j] = (k < dr && k < k0 + s.KC) ? ld_evict_last_v4(W1 + (size_t)u * dr + k, keep)
                                         : make_uint4(0, 0, 0, 0);
     }
     for (int b = 0; b < s.B; ++b) {
