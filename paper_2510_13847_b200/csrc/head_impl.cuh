@@ -462,53 +462,51 @@ __device__ __forceinline__ void head_merge_done(const HeadArgs& a, int extra_ctr
 __device__ inline void merge_finish(const HeadArgs& a, const HeadCtx& c, int G, int r, const float* pm,
                                     const float* ps, const float* cv, const int* ci, float* sv, int* si,
                                     bool valid_row, unsigned long long* trace) {
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, nt = blockDim.x;
   const int K = a.k_t, rec = 2 + 2 * K;
-  // one warp: the G records are already staged in shared memory, so barriers would dominate
-  if (tid < 32) {
-    float mx = -INFINITY, S = 0.f;
-    for (int g = tid; g < G; g += 32) lse_combine(mx, S, pm[g], ps[g]);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const float m2 = __shfl_xor_sync(0xffffffffu, mx, o);
-      const float s2 = __shfl_xor_sync(0xffffffffu, S, o);
-      lse_combine(mx, S, m2, s2);
+  // block-parallel (measured faster than a single warp here: the G x K candidate set is wide)
+  float mx = -INFINITY;
+  for (int g = tid; g < G; g += nt) mx = fmaxf(mx, pm[g]);
+  mx = block_max(mx, c.red);
+  float S = 0.f;
+  for (int g = tid; g < G; g += nt)
+    if (pm[g] > -INFINITY) S += ps[g] * expf(pm[g] - mx);
+  S = block_sum(S, c.red);
+  trace_mark(trace, 17);
+  const bool ok = valid_row && mx > -INFINITY;
+  const float lse = ok ? mx + logf(S) : __int_as_float(0x7fc00000);
+  // candidates in rank-major order: the first G items are the heads of the G sorted lists
+  block_topk(
+      G * K, K, [&](int e, float& v, int& id) { v = cv[e]; id = ci[e]; },
+      [&](int rank, float v, int id) {
+        if (a.record_out) {
+          a.record_out[(size_t)r * rec + 2 + 2 * rank] = v;
+          a.record_out[(size_t)r * rec + 3 + 2 * rank] = __int_as_float(id);
+        } else {
+          a.top_ids[(size_t)r * K + rank] = ok ? id : -1;
+          a.top_logits[(size_t)r * K + rank] = ok ? v : -INFINITY;
+          a.top_logp[(size_t)r * K + rank] = ok ? v - lse : -INFINITY;
+        }
+      },
+      sv, si, c.misc + 8);
+  trace_mark(trace, 19);
+  const int nvalid = c.misc[8];
+  for (int q = nvalid + tid; q < K; q += nt) {
+    if (a.record_out) {
+      a.record_out[(size_t)r * rec + 2 + 2 * q] = -INFINITY;
+      a.record_out[(size_t)r * rec + 3 + 2 * q] = __int_as_float(INT_MAX);
+    } else {
+      a.top_ids[(size_t)r * K + q] = -1;
+      a.top_logits[(size_t)r * K + q] = -INFINITY;
+      a.top_logp[(size_t)r * K + q] = -INFINITY;
     }
-    trace_mark(trace, 17);
-    const bool ok = valid_row && mx > -INFINITY;
-    const float lse = ok ? mx + logf(S) : __int_as_float(0x7fc00000);
-    // candidates in rank-major order: the first G items are the heads of the G sorted lists
-    const int nsv = warp_topk(
-        G * K, K, [&](int e, float& v, int& id) { v = cv[e]; id = ci[e]; },
-        [&](int rank, float v, int id) {
-          if (a.record_out) {
-            a.record_out[(size_t)r * rec + 2 + 2 * rank] = v;
-            a.record_out[(size_t)r * rec + 3 + 2 * rank] = __int_as_float(id);
-          } else {
-            a.top_ids[(size_t)r * K + rank] = ok ? id : -1;
-            a.top_logits[(size_t)r * K + rank] = ok ? v : -INFINITY;
-            a.top_logp[(size_t)r * K + rank] = ok ? v - lse : -INFINITY;
-          }
-        },
-        sv, si);
-    trace_mark(trace, 19);
-    for (int q = nsv + tid; q < K; q += 32) {
-      if (a.record_out) {
-        a.record_out[(size_t)r * rec + 2 + 2 * q] = -INFINITY;
-        a.record_out[(size_t)r * rec + 3 + 2 * q] = __int_as_float(INT_MAX);
-      } else {
-        a.top_ids[(size_t)r * K + q] = -1;
-        a.top_logits[(size_t)r * K + q] = -INFINITY;
-        a.top_logp[(size_t)r * K + q] = -INFINITY;
-      }
-    }
-    if (tid == 0) {
-      if (a.record_out) {
-        a.record_out[(size_t)r * rec] = mx;
-        a.record_out[(size_t)r * rec + 1] = S;
-      } else {
-        a.lse[r] = lse;
-      }
+  }
+  if (tid == 0) {
+    if (a.record_out) {
+      a.record_out[(size_t)r * rec] = mx;
+      a.record_out[(size_t)r * rec + 1] = S;
+    } else {
+      a.lse[r] = lse;
     }
   }
 }
