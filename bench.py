@@ -390,6 +390,8 @@ def run_ours(args, ws, rank, local):
 
     # ---- dense comparator (untimed above): full-V head + log-softmax + top-k_t
     dyn_us_per_pos = 1e3 * ms_per_step / C.positions
+    stream_bw = gathered_stream_bandwidth(D, steppers, inputs, C, B, dev, flush, bw) if (fused and not args.profile) \
+        else None
     if args.profile:
         dense, e2e = {"best_us": float("nan")}, None
         args.no_cpu_baseline = True
@@ -428,7 +430,8 @@ def run_ours(args, ws, rank, local):
                        "speedup_vs_dense": dense["best_us"] / dyn_us_per_pos if dyn_us_per_pos else None,
                        "head_share_of_step": head_share,
                        "step_mode": "fused one-launch step" if fused else "two kernels per step",
-                       "two_stream_mode": None if args.profile else two},
+                       "two_stream_mode": None if args.profile else two,
+                       "gathered_block_streaming": stream_bw},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak if achieved else None,
                          "traffic": committed_traffic(C.name, B), "kernel": ("ds::step_kernel (router + select + gathered head + epilogue, one launch)" if fused
@@ -443,6 +446,41 @@ def run_ours(args, ws, rank, local):
             "clocks": clocks,
         }
         print(json.dumps(line))
+
+
+def gathered_stream_bandwidth(D, steppers, inputs, C, B, dev, flush, bw, reps=3):
+    """Untimed instrumented cycles (dynaspec_debug_set_trace): HBM bandwidth of the streaming phase
+    of the fused step on the gathered cluster blocks = shortlist bytes / (last CTA done streaming
+    - first CTA started streaming), per draft position, over a cold-L2 cycle."""
+    G = torch.cuda.get_device_properties(dev).multi_processor_count
+    bufs = [torch.zeros(G * 64, dtype=torch.int64, device=dev) for _ in range(C.positions)]
+    per_t = [[] for _ in range(C.positions)]
+    for rep in range(reps):
+        flush.zero_()
+        for b in bufs:
+            b.zero_()
+        torch.cuda.synchronize()
+        for t in range(C.positions):
+            D.debug_set_trace(bufs[t])
+            steppers[t](*inputs[rep][t], t, C.k_max, C.k_min)
+        D.debug_set_trace(None)
+        torch.cuda.synchronize()
+        for t in range(C.positions):
+            a = bufs[t].view(G, 64)[:, :32].cpu().numpy().astype(np.float64)
+            st = steppers[t]
+            cnt = st.sel_count.cpu()
+            offs = st.sl_offsets.cpu()
+            rows = sum(int(offs[r, cnt[r]]) for r in range(cnt.numel()))
+            t0, t1 = a[:, 4][a[:, 4] > 0].min(), a[:, 5][a[:, 5] > 0].max()
+            per_t[t].append(rows * C.d * bw / ((t1 - t0) * 1e-9) / 1e9)
+    out = {"gbs_by_position": [float(np.median(v)) for v in per_t]}
+    out["gbs_mean"] = float(np.mean(out["gbs_by_position"]))
+    peak, _ = measured_peaks()
+    out["frac_of_measured_peak"] = out["gbs_mean"] / peak
+    out["frac_of_8TBps"] = out["gbs_mean"] / 8000.0
+    out["how"] = ("in-kernel %globaltimer trace: shortlist bytes / (max over CTAs of end-of-streaming - min over "
+                  "CTAs of start-of-streaming), cold L2 at the first position, median of 3 cycles")
+    return out
 
 
 def dense_baseline(D, clusters, inputs, B, C, dev, flush, reps=20):

@@ -122,3 +122,33 @@ def test_cluster_sharded_protocol_gloo_world2():
         assert tmax == 2.0
         for dlse, same in res:
             assert dlse < 1e-12 and same
+
+
+def _bench_worker(rank, world, port, q):
+    os.environ.update({"MASTER_ADDR": "127.0.0.1", "MASTER_PORT": str(port), "RANK": str(rank),
+                       "WORLD_SIZE": str(world), "LOCAL_RANK": str(rank)})
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("bench", os.path.join(os.path.dirname(os.path.dirname(
+        os.path.abspath(__file__))), "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    ws, r, local = bench.dist_setup(None)
+    bench.barrier(ws)
+    m = bench.max_over_ranks(float(10 * (rank + 1)), ws)
+    q.put((r, ws, m))
+    dist.destroy_process_group()
+
+
+def test_bench_distributed_helpers_gloo_world2():
+    """bench.py's launch plumbing (env rendezvous, barrier, max-over-ranks timing) at world size 2."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_bench_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert res == [(0, 2, 20.0), (1, 2, 20.0)]
