@@ -239,6 +239,27 @@ ds_status dynaspec_draft_step(const ds_clusters* c, const ds_router* r, const vo
 int32_t dynaspec_draft_step_launches(const ds_clusters* c, const ds_router* r, int32_t B, int32_t k_t,
                                      int32_t shared, int32_t two_streams);
 
+/* ---------------------------------------------------------------- draft tree (Alg. 1 lines 12-18) */
+
+/* One step of the draft-tree bookkeeping for R current beams (R = 1 at j = 0):
+ *   cu[b][q] = top_logp[b][q] + last_scores[b]                       (line 12; last_scores NULL => 0)
+ *   node arrays at [node_base, node_base + R k_t): token, cu, parent node (last_nodes[b], or -1
+ *   when NULL), step                                                  (line 13: d, d_scores)
+ *   next_* [k_t]: the k_t best expansions by (cu desc, flat index b k_t + q asc) (R24): token
+ *   (x_j, line 15), score (last_step_scores, line 14), node index, parent beam b (h_j, line 16).
+ * top_ids / top_logp are the head outputs [R][k_t] (-1 / -inf padding is skipped; next_* are padded
+ * with -1 / -inf).  R <= 64, k_t <= 64.  One CTA; all device pointers. */
+ds_status dynaspec_tree_step(const int32_t* top_ids, const float* top_logp, int32_t R, int32_t k_t,
+                             const float* last_scores, const int32_t* last_nodes, int32_t step, int32_t node_base,
+                             int32_t* node_tok, float* node_score, int32_t* node_parent, int32_t* node_step,
+                             int32_t* next_tok, float* next_score, int32_t* next_node, int32_t* next_beam,
+                             ds_stream_t stream);
+
+/* Re-rank the draft list d by d_scores (line 18): out_nodes[0..n_out) = the node indices of
+ * the n_out best valid nodes by (score desc, node index asc) (R24), -1 padded.  n_nodes <= 16384. */
+ds_status dynaspec_tree_rerank(const float* node_score, const int32_t* node_tok, int32_t n_nodes, int32_t n_out,
+                               int32_t* out_nodes, ds_stream_t stream);
+
 /* ---------------------------------------------------------------- cluster sharding (multi-GPU) */
 
 /* Keep, for each of `rows` selection rows, only the selected clusters in [m_lo, m_hi) (the

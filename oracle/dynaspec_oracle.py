@@ -19,6 +19,7 @@ Steps:
   O5 head              z = <h_new, W[v]> for v in V_S           P:262 (Alg. 1 line 10)
   O6 epilogue          log_softmax, TopK_{k_t}, remap2realid    P:263-264 (Alg. 1 line 11), R14/R7
   O7 dense             full-vocabulary head p = softmax(H W_LM)  P:182 (§4.1)
+  NEXT-1 tree_step / tree_rerank   beam bookkeeping + re-rank    P:265-271 (Alg. 1 lines 12-18), R24
 
 Pins: tests/test_oracle_*.py (golden values from SPEC/the worked example E2E-1,
 closed forms, brute force on tiny inputs, invariants).  Every function below is
@@ -359,3 +360,49 @@ def draft_step(part, router, W, h_prev, e, h_new, t, k_max, k_min, k_t, shared=F
                    V_S=V_S, z=z)
         out.append(res)
     return out
+
+
+# ---------------------------------------------------------------------------
+# NEXT-1  tree / beam bookkeeping   (Alg. 1 lines 12-18; reading R24 in DESIGN.md)
+# ---------------------------------------------------------------------------
+
+
+def tree_step(top_ids, top_logp, last_scores, last_nodes, step, node_base, k_t):
+    """One step of Alg. 1 lines 12-16 for R current beams (R = 1 at j = 0):
+      line 12: cu_scores[b, q] = TopP_j[b, q] + last_step_scores[b]
+      line 13: d <- d + T~_j (all R x k_t expansions, with their cu_scores, step and parent node)
+      line 14: TopC_j, last_step_scores <- TopK_{k_t}(cu_scores) over the flattened (b, q) expansions,
+               ties -> lower flat index b * k_t + q (R24)
+      line 15: x_j = T~_j[TopC_j];  line 16: h_j <- h~[beam of TopC_j]
+    top_ids / top_logp: [R][k_t] from the head (id -1 / -inf padding is skipped).
+    Returns (nodes, next) with nodes = list of (token, score, parent_node, step) appended at
+    node_base + b * k_t + q, and next = dict(tok, score, node, beam) for the k_t kept expansions."""
+    top_ids = np.atleast_2d(np.asarray(top_ids))
+    top_logp = np.atleast_2d(np.asarray(top_logp, dtype=np.float64))
+    R, K = top_ids.shape
+    last_scores = np.zeros(R) if last_scores is None else np.asarray(last_scores, dtype=np.float64)
+    last_nodes = np.full(R, -1) if last_nodes is None else np.asarray(last_nodes)
+    cu = top_logp + last_scores[:, None]
+    nodes = []
+    for b in range(R):
+        for q in range(K):
+            nodes.append((int(top_ids[b, q]), float(cu[b, q]), int(last_nodes[b]), step))
+    flat = cu.reshape(-1)
+    valid = top_ids.reshape(-1) >= 0
+    keys = [(-flat[i], i) for i in range(R * K) if valid[i]]
+    keys.sort()
+    keep = [i for _, i in keys[:k_t]]
+    nxt = {"tok": np.array([int(top_ids.reshape(-1)[i]) for i in keep]),
+           "score": np.array([flat[i] for i in keep]),
+           "node": np.array([node_base + i for i in keep]),
+           "beam": np.array([i // K for i in keep])}
+    return nodes, nxt
+
+
+def tree_rerank(nodes, n_out):
+    """Alg. 1 line 18: re-rank the draft list d by d_scores (descending); ties -> lower node index
+    (nodes are numbered step-major, so earlier steps win, then beam order; R24).  Returns the
+    indices of the best n_out valid nodes."""
+    keyed = [(-sc, i) for i, (tok, sc, par, st) in enumerate(nodes) if tok >= 0]
+    keyed.sort()
+    return np.array([k[1] for k in keyed[:n_out]], dtype=np.int64)

@@ -278,6 +278,32 @@ ds_status dynaspec_merge_records(const float* records, int32_t G, int32_t B, int
              : DS_ERR_CUDA;
 }
 
+ds_status dynaspec_tree_step(const int32_t* top_ids, const float* top_logp, int32_t R, int32_t k_t,
+                             const float* last_scores, const int32_t* last_nodes, int32_t step, int32_t node_base,
+                             int32_t* node_tok, float* node_score, int32_t* node_parent, int32_t* node_step,
+                             int32_t* next_tok, float* next_score, int32_t* next_node, int32_t* next_beam,
+                             ds_stream_t stream) {
+  if (!top_ids || !top_logp || !node_tok || !node_score || !node_parent || !node_step || !next_tok || !next_score ||
+      !next_node || !next_beam || R < 1 || R > 64)
+    return DS_ERR_SHAPE;
+  if (k_t < 1 || k_t > kMaxKt) return DS_ERR_INVALID_BUDGET;
+  if (step < 0 || node_base < 0) return DS_ERR_SHAPE;
+  return launch_tree_step(top_ids, top_logp, R, k_t, last_scores, last_nodes, step, node_base, node_tok, node_score,
+                          node_parent, node_step, next_tok, next_score, next_node, next_beam,
+                          (cudaStream_t)stream) == cudaSuccess
+             ? DS_OK
+             : DS_ERR_CUDA;
+}
+
+ds_status dynaspec_tree_rerank(const float* node_score, const int32_t* node_tok, int32_t n_nodes, int32_t n_out,
+                               int32_t* out_nodes, ds_stream_t stream) {
+  if (!node_score || !node_tok || !out_nodes || n_nodes < 1 || n_out < 1) return DS_ERR_SHAPE;
+  if (n_nodes > 16384) return DS_ERR_UNSUPPORTED;
+  return launch_tree_rerank(node_score, node_tok, n_nodes, n_out, out_nodes, (cudaStream_t)stream) == cudaSuccess
+             ? DS_OK
+             : DS_ERR_CUDA;
+}
+
 size_t dynaspec_draft_step_ws(const ds_clusters* c, const ds_router* r, int32_t B, int32_t k_t) {
   HeadPlan p;
   if (!c || !r || B < 1 || k_t < 1 || k_t > kMaxKt) return 0;

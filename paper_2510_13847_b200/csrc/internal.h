@@ -87,6 +87,14 @@ cudaError_t launch_restrict(const int32_t* sel, const int32_t* cnt, int rows, in
 cudaError_t launch_merge_records(const float* records, int G, int B, int K, int32_t* top_ids, float* top_logits,
                                  float* top_logp, float* lse, cudaStream_t st);
 
+// ---- draft-tree bookkeeping (tree.cu)
+cudaError_t launch_tree_step(const int32_t* top_ids, const float* top_logp, int R, int K, const float* last_scores,
+                             const int32_t* last_nodes, int step, int node_base, int32_t* node_tok, float* node_score,
+                             int32_t* node_parent, int32_t* node_step, int32_t* next_tok, float* next_score,
+                             int32_t* next_node, int32_t* next_beam, cudaStream_t st);
+cudaError_t launch_tree_rerank(const float* node_score, const int32_t* node_tok, int n, int n_out, int32_t* out_nodes,
+                               cudaStream_t st);
+
 // ---- offline partition (build.cu)
 size_t build_ws_bytes(int64_t V, int d, int M);
 size_t layout_ws_bytes(int64_t V, int M);

@@ -77,6 +77,8 @@ def _load():
                                           c_int32, c_int32, c_int32, c_int32, POINTER(DsStepOutputs), P, c_size_t,
                                           P, P, P, P, P, P]),
         "dynaspec_debug_set_trace": (c_int32, [P]),
+        "dynaspec_tree_step": (c_int32, [P, P, c_int32, c_int32, P, P, c_int32, c_int32, P, P, P, P, P, P, P, P, P]),
+        "dynaspec_tree_rerank": (c_int32, [P, P, c_int32, c_int32, P, P]),
         "dynaspec_restrict_selection": (c_int32, [P, P, P, c_int32, POINTER(DsClusters), c_int32, c_int32, P, P, P, P]),
         "dynaspec_head_partial": (c_int32, [POINTER(DsClusters), P, c_int32, P, P, P, c_int32, c_int32, c_int64, P, P,
                                             c_size_t, P]),
@@ -99,6 +101,7 @@ EXPORTED = [
     "dynaspec_meta_score_ws", "dynaspec_meta_score", "dynaspec_select", "dynaspec_head_forward_ws",
     "dynaspec_head_forward", "dynaspec_draft_step_ws", "dynaspec_draft_step", "dynaspec_draft_step_launches",
     "dynaspec_debug_set_trace", "dynaspec_restrict_selection", "dynaspec_head_partial", "dynaspec_merge_records",
+    "dynaspec_tree_step", "dynaspec_tree_rerank",
 ]
 
 
@@ -301,6 +304,41 @@ def head_forward(clusters, h_new, sel, sel_count, sl_offsets, k_t, shared=False,
                                       ws.ptr(), ws.nbytes, _stream()), "dynaspec_head_forward")
     out["z"] = z
     return out
+
+
+# ---------------------------------------------------------------------------- draft tree (NEXT-1)
+
+class DraftTree:
+    """Device-resident draft list d (Alg. 1 lines 12-18) for up to `capacity` nodes."""
+
+    def __init__(self, k_t, capacity, device="cuda"):
+        self.k_t, self.capacity = k_t, capacity
+        z = lambda dt: torch.zeros(capacity, dtype=dt, device=device)
+        self.tok, self.score, self.parent, self.step = z(torch.int32), z(torch.float32), z(torch.int32), z(torch.int32)
+        self.next_tok = torch.zeros(k_t, dtype=torch.int32, device=device)
+        self.next_score = torch.zeros(k_t, dtype=torch.float32, device=device)
+        self.next_node = torch.zeros(k_t, dtype=torch.int32, device=device)
+        self.next_beam = torch.zeros(k_t, dtype=torch.int32, device=device)
+        self.n = 0
+
+    def step(self, top_ids, top_logp, j):
+        """Fold the head outputs [R][k_t] of draft step j into the tree (R = 1 at j = 0)."""
+        R = top_ids.shape[0]
+        first = j == 0
+        last_s = None if first else self.next_score.clone()
+        last_n = None if first else self.next_node.clone()
+        _check(_lib.dynaspec_tree_step(_ptr(top_ids), _ptr(top_logp), R, self.k_t, _ptr(last_s), _ptr(last_n), j,
+                                       self.n, _ptr(self.tok), _ptr(self.score), _ptr(self.parent), _ptr(self.step),
+                                       _ptr(self.next_tok), _ptr(self.next_score), _ptr(self.next_node),
+                                       _ptr(self.next_beam), _stream()), "dynaspec_tree_step")
+        self.n += R * self.k_t
+        return self
+
+    def rerank(self, n_out):
+        out = torch.empty(n_out, dtype=torch.int32, device=self.tok.device)
+        _check(_lib.dynaspec_tree_rerank(_ptr(self.score), _ptr(self.tok), self.n, n_out, _ptr(out), _stream()),
+               "dynaspec_tree_rerank")
+        return out
 
 
 # ---------------------------------------------------------------------------- cluster sharding

@@ -328,3 +328,79 @@ def test_shared_mode_union():
     u = O.select_shared(s, 3)
     ref = sorted(set().union(*[set(O.select(s[r], 3).tolist()) for r in range(4)]))
     assert u.tolist() == ref
+
+
+# ----------------------------------------------------------------- NEXT-1 tree bookkeeping
+
+def test_tree_greedy_chain_closed_form():
+    # k_t = 1: one chain; scores are the running sums of the chosen log-probs.
+    logps = [-0.1, -0.7, -0.2]
+    toks = [5, 9, 2]
+    last, lastn, base, chain = None, None, 0, []
+    for j, (tk, lp) in enumerate(zip(toks, logps)):
+        nodes, nxt = O.tree_step([[tk]], [[lp]], last, lastn, j, base, 1)
+        base += 1
+        last, lastn = nxt["score"], nxt["node"]
+        chain.append((int(nxt["tok"][0]), float(nxt["score"][0])))
+    assert [c[0] for c in chain] == toks
+    assert np.allclose([c[1] for c in chain], np.cumsum(logps))
+
+
+def test_tree_step_hand_example():
+    # two beams, k_t = 2: cu = TopP + last; keep the 2 best of 4 expansions (ties -> lower index)
+    nodes, nxt = O.tree_step([[3, 1], [7, 2]], [[-0.5, -1.0], [-0.1, -0.5]], [-1.0, -1.2], [10, 11], 1, 20, 2)
+    assert [n[1] for n in nodes] == [-1.5, -2.0, -1.3, -1.7]
+    assert [n[2] for n in nodes] == [10, 10, 11, 11]
+    assert nxt["tok"].tolist() == [7, 3] and nxt["node"].tolist() == [22, 20] and nxt["beam"].tolist() == [1, 0]
+    _, nx2 = O.tree_step([[3, 1]], [[-0.5, -0.5]], [0.0], [-1], 0, 0, 1)
+    assert nx2["tok"].tolist() == [3]                                  # tie -> lower flat index
+
+
+def _enumerate_paths(logp_of, V, depth):
+    """All token paths of length `depth` with their summed log-probs (brute force)."""
+    paths = [((), 0.0)]
+    for _ in range(depth):
+        paths = [(p + (v,), s + logp_of(p, v)) for p, s in paths for v in range(V)]
+    return paths
+
+
+def test_tree_beam_equals_exhaustive_when_nothing_is_pruned():
+    # SPEC S:408/S:422: with k_t >= (number of expansions), beam search keeps every path, so the
+    # draft list d equals the exhaustive enumeration of all paths with the same scores.
+    V, depth, K = 3, 3, 27
+    rng = np.random.default_rng(4)
+    table = {}
+
+    def logp_of(prefix, v):
+        if prefix not in table:
+            z = rng.standard_normal(V)
+            table[prefix] = z - np.log(np.exp(z).sum())
+        return table[prefix][v]
+
+    exhaustive = {}
+    for dpt in range(1, depth + 1):
+        for p, sc in _enumerate_paths(logp_of, V, dpt):
+            exhaustive[p] = sc
+    beams = [()]
+    last, lastn, base = None, None, 0
+    allnodes, paths_of_node = [], {}
+    for j in range(depth):
+        ids = [[v for v in range(V)] + [-1] * (K - V) for _ in beams]
+        lps = [[logp_of(b, v) for v in range(V)] + [-np.inf] * (K - V) for b in beams]
+        nodes, nxt = O.tree_step(ids, lps, last, lastn, j, base, K)
+        for i, nd in enumerate(nodes):
+            if nd[0] >= 0:
+                paths_of_node[base + i] = beams[i // K] + (nd[0],)
+        allnodes += nodes
+        beams = [beams[b] + (int(t),) for b, t in zip(nxt["beam"], nxt["tok"])]
+        base += len(nodes)
+        last, lastn = nxt["score"], nxt["node"]
+    got = {paths_of_node[i]: allnodes[i][1] for i in paths_of_node}
+    assert set(got) == set(exhaustive)
+    assert all(abs(got[p] - exhaustive[p]) < 1e-12 for p in got)
+    # re-rank: the best n nodes are closed under parents (scores never increase along a path)
+    top = O.tree_rerank(allnodes, 10)
+    chosen = set(top.tolist())
+    for i in chosen:
+        par = allnodes[i][2]
+        assert par == -1 or par in chosen
