@@ -314,7 +314,7 @@ class DraftTree:
     def __init__(self, k_t, capacity, device="cuda"):
         self.k_t, self.capacity = k_t, capacity
         z = lambda dt: torch.zeros(capacity, dtype=dt, device=device)
-        self.tok, self.score, self.parent, self.step = z(torch.int32), z(torch.float32), z(torch.int32), z(torch.int32)
+        self.tok, self.score, self.parent, self.depth = z(torch.int32), z(torch.float32), z(torch.int32), z(torch.int32)
         self.next_tok = torch.zeros(k_t, dtype=torch.int32, device=device)
         self.next_score = torch.zeros(k_t, dtype=torch.float32, device=device)
         self.next_node = torch.zeros(k_t, dtype=torch.int32, device=device)
@@ -328,7 +328,7 @@ class DraftTree:
         last_s = None if first else self.next_score.clone()
         last_n = None if first else self.next_node.clone()
         _check(_lib.dynaspec_tree_step(_ptr(top_ids), _ptr(top_logp), R, self.k_t, _ptr(last_s), _ptr(last_n), j,
-                                       self.n, _ptr(self.tok), _ptr(self.score), _ptr(self.parent), _ptr(self.step),
+                                       self.n, _ptr(self.tok), _ptr(self.score), _ptr(self.parent), _ptr(self.depth),
                                        _ptr(self.next_tok), _ptr(self.next_score), _ptr(self.next_node),
                                        _ptr(self.next_beam), _stream()), "dynaspec_tree_step")
         self.n += R * self.k_t
