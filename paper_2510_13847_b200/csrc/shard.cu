@@ -101,7 +101,7 @@ size_t merge_records_smem(int G, int K) { return (size_t)(2 * G + 4 * G * K) * 4
 cudaError_t launch_merge_records(const float* records, int G, int B, int K, int32_t* top_ids, float* top_logits,
                                  float* top_logp, float* lse, cudaStream_t st) {
   const size_t smem = merge_records_smem(G, K);
-  if (smem > 48 * 1024) {
+  if (smem > 40 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(merge_records_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }

@@ -73,7 +73,7 @@ cudaError_t launch_tree_step(const int32_t* top_ids, const float* top_logp, int 
                              int32_t* node_parent, int32_t* node_step, int32_t* next_tok, float* next_score,
                              int32_t* next_node, int32_t* next_beam, cudaStream_t st) {
   const size_t smem = (size_t)R * K * 12;
-  if (smem > 48 * 1024) {
+  if (smem > 40 * 1024) {  // opt in above the default (static smem counts too)
     cudaError_t e = cudaFuncSetAttribute(tree_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
@@ -86,7 +86,7 @@ cudaError_t launch_tree_step(const int32_t* top_ids, const float* top_logp, int 
 cudaError_t launch_tree_rerank(const float* node_score, const int32_t* node_tok, int n, int n_out, int32_t* out_nodes,
                                cudaStream_t st) {
   const size_t smem = (size_t)n * 8;
-  if (smem > 48 * 1024) {
+  if (smem > 40 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(tree_rerank_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }

@@ -18,7 +18,7 @@ def test_tree_step_bit_exact(R, K):
     tree = D.DraftTree(K, 4 * R * K + 16)
     ref_nodes, last_s, last_n, base = [], None, None, 0
     for j in range(3):
-        RR = 1 if j == 0 else min(R, K)
+        RR = 1 if j == 0 else len(last_s)          # beams = valid expansions kept at j - 1
         # dyadic log-probs (exact in fp32 sums), with deliberate duplicates to exercise ties
         lp = -rng.integers(0, 6, size=(RR, K)).astype(np.float64) / 4.0
         lp = np.sort(lp, axis=1)[:, ::-1].copy()
@@ -28,6 +28,8 @@ def test_tree_step_bit_exact(R, K):
             lp[0, -1] = -np.inf
         tree.step(torch.as_tensor(ids, dtype=torch.int32, device=DEV),
                   torch.as_tensor(lp, dtype=torch.float32, device=DEV), j)
+        if R == 1 and j == 0:
+            pass
         nodes, nxt = O.tree_step(ids, lp, last_s, last_n, j, base, K)
         ref_nodes += nodes
         base += RR * K
