@@ -324,6 +324,8 @@ class DraftTree:
     def step(self, top_ids, top_logp, j):
         """Fold the head outputs [R][k_t] of draft step j into the tree (R = 1 at j = 0)."""
         R = top_ids.shape[0]
+        if self.n + R * self.k_t > self.capacity:
+            raise ValueError(f"DraftTree capacity {self.capacity} exceeded")
         first = j == 0
         last_s = None if first else self.next_score.clone()
         last_n = None if first else self.next_node.clone()

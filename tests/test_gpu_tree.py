@@ -15,7 +15,7 @@ DEV = "cuda"
 def test_tree_step_bit_exact(R, K):
     from paper_2510_13847_b200 import dynaspec as D
     rng = np.random.default_rng(R * 100 + K)
-    tree = D.DraftTree(K, 4 * R * K + 16)
+    tree = D.DraftTree(K, 3 * K * K + 16)
     ref_nodes, last_s, last_n, base = [], None, None, 0
     for j in range(3):
         RR = 1 if j == 0 else len(last_s)          # beams = valid expansions kept at j - 1
