@@ -399,6 +399,7 @@ def run_ours(args, ws, rank, local):
         dense = dense_baseline(D, clusters, inputs, B, C, dev, flush)
         e2e = e2e_run(D, steppers, clusters, router, C, B, args, dev, flush, ws)
         two = two_stream_run(D, clusters, router, inputs, C, B, args, dev, flush)
+        overlap = core_overlap_run(D, clusters, router, inputs, C, B, args, dev, flush)
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
@@ -431,7 +432,8 @@ def run_ours(args, ws, rank, local):
                        "head_share_of_step": head_share,
                        "step_mode": "fused one-launch step" if fused else "two kernels per step",
                        "two_stream_mode": None if args.profile else two,
-                       "gathered_block_streaming": stream_bw},
+                       "gathered_block_streaming": stream_bw,
+                       "drafter_core_overlap": None if args.profile else overlap},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak if achieved else None,
                          "traffic": committed_traffic(C.name, B), "kernel": ("ds::step_kernel (router + select + gathered head + epilogue, one launch)" if fused
@@ -553,6 +555,83 @@ def two_stream_run(D, clusters, router, inputs, C, B, args, dev, flush):
         if i >= 3:
             times.append(a.elapsed_time(b))
     return {"us_per_draft_step": 1e3 * statistics.mean(times) / C.positions, "launches_per_step": st[0].launches}
+
+
+def core_overlap_run(D, clusters, router, inputs, C, B, args, dev, flush, reps=10):
+    """NEXT-2 / the paper's T_D model: T_D ~ T_embed + max{T_core, T_meta} + T_index+gemm.
+    A same-bytes stand-in for the EAGLE drafter block (fc 2d -> 3.5d, ReLU, 3.5d -> d; bf16
+    cuBLAS on S_d; it is the caller's work, not part of this library) runs each step; the
+    router + TopK either wait for it (serialized, one stream) or run on S_m concurrently
+    (dynaspec_step_route on S_m || core on S_d, join, dynaspec_step_head)."""
+    import torch.nn.functional as F
+    g = torch.Generator(device=dev)
+    g.manual_seed(77)
+    f = int(3.5 * C.d)
+    Wc1 = (torch.randn((f, 2 * C.d), generator=g, device=dev) * 0.01).to(torch.bfloat16)
+    Wc2 = (torch.randn((C.d, f), generator=g, device=dev) * 0.01).to(torch.bfloat16)
+    core_bytes = (Wc1.numel() + Wc2.numel()) * 2
+    st_ser = [D.DraftStep(clusters, router, B, C.k_t, shared=C.shared, device=dev) for _ in range(C.positions)]
+    st_ovl = [D.DraftStep(clusters, router, B, C.k_t, shared=C.shared, device=dev) for _ in range(C.positions)]
+    hbuf = [torch.empty((B, C.d), dtype=torch.bfloat16, device=dev) for _ in range(C.positions)]
+    s_meta = torch.cuda.Stream(device=dev)
+    ev_f = [torch.cuda.Event() for _ in range(C.positions)]
+    ev_j = [torch.cuda.Event() for _ in range(C.positions)]
+
+    def core(t):
+        hp, e, _ = inputs[0][t]
+        hbuf[t].copy_(F.linear(F.relu(F.linear(torch.cat([hp, e], 1), Wc1)), Wc2))
+
+    def serialized():
+        for t in range(C.positions):
+            hp, e, _ = inputs[0][t]
+            core(t)
+            st_ser[t](hp, e, hbuf[t], t, C.k_max, C.k_min)
+
+    def overlapped():
+        cur = torch.cuda.current_stream()
+        for t in range(C.positions):
+            hp, e, _ = inputs[0][t]
+            ev_f[t].record(cur)
+            s_meta.wait_event(ev_f[t])
+            st_ovl[t].route(hp, e, t, C.k_max, C.k_min, s_meta)   # S_m
+            core(t)                                               # S_d
+            ev_j[t].record(s_meta)
+            cur.wait_event(ev_j[t])                               # "sync S_m, S_d"
+            st_ovl[t].head(hbuf[t], t, C.k_max, C.k_min, cur)
+
+    def core_only():
+        for t in range(C.positions):
+            core(t)
+
+    res = {}
+    for name, fn in (("core_only", core_only), ("serialized", serialized), ("overlapped", overlapped)):
+        s = torch.cuda.Stream(device=dev)
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            fn()
+        torch.cuda.current_stream().wait_stream(s)
+        torch.cuda.synchronize()
+        gph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gph):
+            fn()
+        ts = []
+        for i in range(reps + 2):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            gph.replay()
+            b.record()
+            torch.cuda.synchronize()
+            if i >= 2:
+                ts.append(a.elapsed_time(b))
+        res[name + "_us_per_step"] = 1e3 * statistics.median(ts) / C.positions
+    res["core_stand_in_bytes"] = int(core_bytes)
+    res["router_hidden_us"] = res["serialized_us_per_step"] - res["overlapped_us_per_step"]
+    res["head_after_core_us"] = res["overlapped_us_per_step"] - res["core_only_us_per_step"]
+    res["how"] = ("one cycle per CUDA graph, cold L2 per cycle; core = bf16 fc 2d->3.5d, ReLU, 3.5d->d "
+                  "(cuBLAS stand-in for the EAGLE block); serialized = core then the fused one-launch step; "
+                  "overlapped = router on S_m || core on S_d, then the head")
+    return res
 
 
 def e2e_run(D, steppers, clusters, router, C, B, args, dev, flush, ws, reps=None):

@@ -234,6 +234,23 @@ ds_status dynaspec_draft_step(const ds_clusters* c, const ds_router* r, const vo
                               ds_event_t ev_fork, ds_event_t ev_join, ds_event_t head_begin,
                               ds_event_t head_end);
 
+/* The two halves of a draft step, for callers that overlap the router with their drafter core
+ * (Alg. 1 lines 8-10: "the router runs on a separate parallel CUDA stream and completes
+ * while the drafter's attention/MLP is executing"):
+ *   caller: record an event on S_d; make s_meta wait on it; dynaspec_step_route(.., s_meta);
+ *           enqueue the drafter core on S_d (producing h_new); record an event on s_meta and make
+ *           S_d wait on it ("sync S_m, S_d"); dynaspec_step_head(.., S_d).
+ * route: router + TopK + sl_offsets into out->scores / sel / sel_count / sl_offsets (2 launches).
+ * head:  the gathered head + epilogue over that selection into out->top_* / lse / z_out.
+ * Workspaces: route needs dynaspec_draft_step_ws bytes of its own; head needs its own workspace
+ * of dynaspec_head_forward_ws bytes (the two may run concurrently, so they must not share). */
+ds_status dynaspec_step_route(const ds_clusters* c, const ds_router* r, const void* h_prev, const void* e, int32_t B,
+                              int32_t t, int32_t k_max, int32_t k_min, int32_t shared, const ds_step_outputs* out,
+                              void* ws, size_t ws_bytes, ds_stream_t s_meta);
+ds_status dynaspec_step_head(const ds_clusters* c, const void* h_new, int32_t B, int32_t t, int32_t k_max,
+                             int32_t k_min, int32_t k_t, int32_t shared, const ds_step_outputs* out, void* ws,
+                             size_t ws_bytes, ds_stream_t s_draft);
+
 /* Number of kernel launches one dynaspec_draft_step enqueues (for launch accounting):
  * 1 for the fused single-stream step, 2 + head chunks for the two-stream path. */
 int32_t dynaspec_draft_step_launches(const ds_clusters* c, const ds_router* r, int32_t B, int32_t k_t,

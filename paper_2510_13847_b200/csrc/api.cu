@@ -304,6 +304,45 @@ ds_status dynaspec_tree_rerank(const float* node_score, const int32_t* node_tok,
              : DS_ERR_CUDA;
 }
 
+ds_status dynaspec_step_route(const ds_clusters* c, const ds_router* r, const void* h_prev, const void* e, int32_t B,
+                              int32_t t, int32_t k_max, int32_t k_min, int32_t shared, const ds_step_outputs* out,
+                              void* ws, size_t ws_bytes, ds_stream_t s_meta) {
+  ds_status s = check_clusters(c);
+  if (s != DS_OK) return s;
+  if ((s = check_router(r)) != DS_OK) return s;
+  if (r->M != c->M || r->d != c->d) return DS_ERR_SHAPE;
+  if (!h_prev || !e || !out || !out->sel || !out->sel_count || !out->sl_offsets || B < 1) return DS_ERR_SHAPE;
+  const int32_t k = dynaspec_budget(t, k_max, k_min);
+  if (k < 1 || k_max > c->M) return DS_ERR_INVALID_BUDGET;
+  const size_t meta_bytes = meta_plan(r, B).part_bytes;
+  const size_t score_bytes = (size_t)B * r->M * sizeof(float);
+  const WsLayout L = ws_layout(align_up(meta_bytes, 256) + align_up(score_bytes, 256), 0);
+  if (!ws || ws_bytes < L.total) return DS_ERR_WORKSPACE;
+  uint8_t* w8 = static_cast<uint8_t*>(ws);
+  float* scores = out->scores ? out->scores : reinterpret_cast<float*>(w8 + L.meta + align_up(meta_bytes, 256));
+  return launch_meta(r, h_prev, e, B, scores, reinterpret_cast<float*>(w8 + L.meta),
+                     reinterpret_cast<unsigned*>(w8 + L.counters) + 1, c->offsets, k, nullptr, shared ? 1 : 0,
+                     out->sel, out->sel_count, out->sl_offsets, (cudaStream_t)s_meta, false) == cudaSuccess
+             ? DS_OK
+             : DS_ERR_CUDA;
+}
+
+ds_status dynaspec_step_head(const ds_clusters* c, const void* h_new, int32_t B, int32_t t, int32_t k_max,
+                             int32_t k_min, int32_t k_t, int32_t shared, const ds_step_outputs* out, void* ws,
+                             size_t ws_bytes, ds_stream_t s_draft) {
+  ds_status s = check_clusters(c);
+  if (s != DS_OK) return s;
+  if (!h_new || !out || B < 1) return DS_ERR_SHAPE;
+  const int32_t k = dynaspec_budget(t, k_max, k_min);
+  if (k < 1 || k_max > c->M) return DS_ERR_INVALID_BUDGET;
+  if (k_t < 1 || k_t > kMaxKt || (int64_t)k_t > (int64_t)k * c->min_size) return DS_ERR_INVALID_BUDGET;
+  const int64_t ms = shared ? c->V : dynaspec_max_shortlist(c, k);
+  if (out->z_out && out->z_stride < ms) return DS_ERR_SHAPE;
+  return dynaspec_head_forward(c, h_new, B, out->sel, out->sel_count, out->sl_offsets, shared, k_t, ms, out->top_ids,
+                               out->top_logits, out->top_logp, out->lse, out->z_out, out->z_stride, ws, ws_bytes,
+                               s_draft);
+}
+
 size_t dynaspec_draft_step_ws(const ds_clusters* c, const ds_router* r, int32_t B, int32_t k_t) {
   HeadPlan p;
   if (!c || !r || B < 1 || k_t < 1 || k_t > kMaxKt) return 0;

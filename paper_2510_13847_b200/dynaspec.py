@@ -77,6 +77,10 @@ def _load():
                                           c_int32, c_int32, c_int32, c_int32, POINTER(DsStepOutputs), P, c_size_t,
                                           P, P, P, P, P, P]),
         "dynaspec_debug_set_trace": (c_int32, [P]),
+        "dynaspec_step_route": (c_int32, [POINTER(DsClusters), POINTER(DsRouter), P, P, c_int32, c_int32, c_int32,
+                                          c_int32, c_int32, POINTER(DsStepOutputs), P, c_size_t, P]),
+        "dynaspec_step_head": (c_int32, [POINTER(DsClusters), P, c_int32, c_int32, c_int32, c_int32, c_int32, c_int32,
+                                         POINTER(DsStepOutputs), P, c_size_t, P]),
         "dynaspec_tree_step": (c_int32, [P, P, c_int32, c_int32, P, P, c_int32, c_int32, P, P, P, P, P, P, P, P, P]),
         "dynaspec_tree_rerank": (c_int32, [P, P, c_int32, c_int32, P, P]),
         "dynaspec_restrict_selection": (c_int32, [P, P, P, c_int32, POINTER(DsClusters), c_int32, c_int32, P, P, P, P]),
@@ -101,7 +105,7 @@ EXPORTED = [
     "dynaspec_meta_score_ws", "dynaspec_meta_score", "dynaspec_select", "dynaspec_head_forward_ws",
     "dynaspec_head_forward", "dynaspec_draft_step_ws", "dynaspec_draft_step", "dynaspec_draft_step_launches",
     "dynaspec_debug_set_trace", "dynaspec_restrict_selection", "dynaspec_head_partial", "dynaspec_merge_records",
-    "dynaspec_tree_step", "dynaspec_tree_rerank",
+    "dynaspec_tree_step", "dynaspec_tree_rerank", "dynaspec_step_route", "dynaspec_step_head",
 ]
 
 
@@ -434,6 +438,24 @@ class DraftStep:
                                         c_void_p(self.s_meta.cuda_stream) if self.s_meta is not None else None,
                                         self.ev_fork, self.ev_join, hb, he), "dynaspec_draft_step")
         return self
+
+    def route(self, h_prev, e, t, k_max, k_min, stream):
+        """Router + TopK half of the step (Alg. 1 line 8) on `stream` (S_m)."""
+        if not hasattr(self, "ws_head"):
+            self.ws_head = Workspace(_lib.dynaspec_head_forward_ws(self.c.struct(), self.B, self.k_t),
+                                     self.ws.buf.device)
+        _check(_lib.dynaspec_step_route(self.c.struct(), self.r.struct(), _ptr(h_prev), _ptr(e), self.B, t, k_max,
+                                        k_min, int(self.shared), ctypes.byref(self._o), self.ws.ptr(), self.ws.nbytes,
+                                        _stream(stream)), "dynaspec_step_route")
+
+    def head(self, h_new, t, k_max, k_min, stream):
+        """Head + epilogue half of the step (Alg. 1 lines 10-11) on `stream` (S_d)."""
+        if not hasattr(self, "ws_head"):
+            self.ws_head = Workspace(_lib.dynaspec_head_forward_ws(self.c.struct(), self.B, self.k_t),
+                                     self.ws.buf.device)
+        _check(_lib.dynaspec_step_head(self.c.struct(), _ptr(h_new), self.B, t, k_max, k_min, self.k_t,
+                                       int(self.shared), ctypes.byref(self._o), self.ws_head.ptr(),
+                                       self.ws_head.nbytes, _stream(stream)), "dynaspec_step_head")
 
     def outputs(self):
         return {k: getattr(self, k) for k in ("scores", "sel", "sel_count", "sl_offsets", "top_ids", "top_logits",
