@@ -20,6 +20,7 @@ Steps:
   O6 epilogue          log_softmax, TopK_{k_t}, remap2realid    P:263-264 (Alg. 1 line 11), R14/R7
   O7 dense             full-vocabulary head p = softmax(H W_LM)  P:182 (§4.1)
   NEXT-1 tree_step / tree_rerank   beam bookkeeping + re-rank    P:265-271 (Alg. 1 lines 12-18), R24
+  NEXT-3 frequency_ranking, fr_head  FR-Spec / PA-FR prefix heads P:184-192, App. A.1
 
 Pins: tests/test_oracle_*.py (golden values from SPEC/the worked example E2E-1,
 closed forms, brute force on tiny inputs, invariants).  Every function below is
@@ -406,3 +407,25 @@ def tree_rerank(nodes, n_out):
     keyed = [(-sc, i) for i, (tok, sc, par, st) in enumerate(nodes) if tok >= 0]
     keyed.sort()
     return np.array([k[1] for k in keyed[:n_out]], dtype=np.int64)
+
+
+# ---------------------------------------------------------------------------
+# NEXT-3  static frequency-ranked heads: FR-Spec and PA-FR (App. A.1)
+# ---------------------------------------------------------------------------
+
+
+def frequency_ranking(counts):
+    """pi_f: token ids by descending corpus count, ties -> lower token id."""
+    counts = np.asarray(counts)
+    return np.lexsort((np.arange(counts.size), -counts)).astype(np.int64)
+
+
+def fr_head(h_new, W, pi_f, K, k_t):
+    """p_stat = softmax(H~ W~), W~[:, j] = W_LM[:, V_high[j]], V_high = pi_f[:K] (P:186-191);
+    the shortlist is the K most frequent tokens in frequency order."""
+    V_S = np.asarray(pi_f[:K], dtype=np.int64)
+    out = []
+    for h in np.atleast_2d(np.asarray(h_new, np.float64)):
+        z = head(h, W, V_S)[0]
+        out.append(dict(epilogue(z, V_S, min(k_t, K)), z=z, V_S=V_S))
+    return out

@@ -460,3 +460,48 @@ class DraftStep:
     def outputs(self):
         return {k: getattr(self, k) for k in ("scores", "sel", "sel_count", "sl_offsets", "top_ids", "top_logits",
                                                "top_logp", "lse", "z")}
+
+
+# ---------------------------------------------------------------------------- static heads (NEXT-3)
+
+class FrequencyHead:
+    """FR-Spec / PA-FR static shortlist heads (App. A.1) on the same kernels:
+    W is stored in frequency order (a drafter-side copy, like W_perm) and the shortlist of step t
+    is the prefix [0, K) — one contiguous run, expressed as a one-cluster partition."""
+
+    def __init__(self, W, pi_f):
+        _need_cuda(W)
+        self.V, self.d = W.shape
+        self.perm = torch.as_tensor(pi_f, dtype=torch.int32, device=W.device).contiguous()
+        self.W_freq = W.index_select(0, self.perm.long()).contiguous()
+        self._views = {}
+
+    def _view(self, K):
+        if K not in self._views:
+            dev = self.W_freq.device
+            off = torch.tensor([0, K], dtype=torch.int32, device=dev)
+            sel = torch.zeros((1, 1), dtype=torch.int32, device=dev)
+            cnt = torch.ones(1, dtype=torch.int32, device=dev)
+            sl = torch.tensor([[0, K]], dtype=torch.int32, device=dev)
+            c = Clusters.__new__(Clusters)
+            c.tau, c.perm, c.offsets, c.W_perm = None, self.perm, off, self.W_freq
+            c.min_size = c.max_size = K
+            c.V, c.d, c.M, c.dtype = self.V, self.d, 1, self.W_freq.dtype
+            c._s = DsClusters(self.V, self.d, 1, _DTYPE[c.dtype], K, K, None, _ptr(self.perm), _ptr(off),
+                              _ptr(self.W_freq))
+            self._views[K] = (c, sel, cnt, sl, off)
+        return self._views[K]
+
+    def forward(self, h_new, K, k_t, z_out=False, ws=None):
+        """Top-k_t / lse / logp over the K most frequent tokens (ids are vocabulary ids)."""
+        c, sel, cnt, sl, _ = self._view(int(K))
+        return head_forward(c, h_new, sel, cnt, sl, k_t, shared=True, max_shortlist=int(K), z_out=z_out, ws=ws)
+
+    def forward_pa_fr(self, h_new, t, K_max, k_t, z_out=False, ws=None):
+        """PA-FR: the prefix length shrinks with the draft position, K_fr(t) (App. A.1)."""
+        return self.forward(h_new, pa_fr_budget(t, K_max), k_t, z_out=z_out, ws=ws)
+
+
+def pa_fr_budget(t, K_max):
+    """K_fr(t) = K_max for t < 2, else max(1, floor(K_max / (t + 1))) (App. A.1, P:404-410)."""
+    return K_max if t < 2 else max(1, K_max // (t + 1))

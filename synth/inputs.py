@@ -241,3 +241,15 @@ def to_f64(x):
     if x is None:
         return None
     return x.detach().to("cpu", torch.float64).numpy()
+
+
+def zipf_token_counts(V, seed=3, a=1.1, n_tokens=10_000_000):
+    """Synthetic corpus token counts (Zipf(a) over a random permutation of the vocabulary) — the
+    stand-in for the FR-Spec frequency statistics (the paper's corpora are out of scope)."""
+    rng = np.random.default_rng(seed)
+    ranks = rng.permutation(V)
+    p = 1.0 / (np.arange(1, V + 1) ** a)
+    p /= p.sum()
+    counts = np.zeros(V, dtype=np.int64)
+    counts[ranks] = rng.multinomial(n_tokens, p)
+    return counts

@@ -503,3 +503,32 @@ def test_tc_batched_draft_step_llama3_b16(monkeypatch):
                            C.k_t, sel_override=[sel_gpu])[0]
         check_topk(st.top_ids[b].cpu().numpy(), st.top_logits[b].cpu().numpy(), st.top_logp[b].cpu().numpy(),
                    st.lse[b].item(), ref["z"], ref["V_S"], C.k_t, torch.bfloat16)
+
+
+# ------------------------------------------------------------------ static frequency heads (NEXT-3)
+
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+def test_frequency_heads_fr_and_pa_fr(dtype):
+    """FR-Spec (fixed K) and PA-FR (K_fr(t)) prefix heads vs the oracle at the Llama-3 shape."""
+    Dy = _dyn()
+    C = S.CONFIGS["llama3"]
+    W = S.lm_head(C.V, C.d, 0, dtype)
+    pi = O.frequency_ranking(S.zipf_token_counts(C.V))
+    fh = Dy.FrequencyHead(W.to(DEV), pi)
+    hn = S.hidden(2, C.d, 9, dtype)
+    Wo = Rows(W)
+    for t in (0, 2, 5):
+        for K in (32768, O.budget_pa_fr(t, 32768)):
+            out = fh.forward(hn.to(DEV), K, 8, z_out=True)
+            ref = O.fr_head(f64(hn), Wo, pi, K, 8)
+            tdt = S.TORCH_DTYPES[dtype]
+            for b in range(2):
+                z = out["z"][b, :K].cpu().numpy().astype(np.float64)
+                if dtype == "bf16":
+                    assert np.max(np.abs(z - ref[b]["z"])) <= 2e-2
+                else:
+                    rms = np.sqrt(np.mean(ref[b]["z"] ** 2))
+                    assert np.all(np.abs(z - ref[b]["z"]) <= 1e-5 * np.maximum(np.abs(ref[b]["z"]), rms))
+                check_topk(out["top_ids"][b].cpu().numpy(), out["top_logits"][b].cpu().numpy(),
+                           out["top_logp"][b].cpu().numpy(), out["lse"][b].item(), ref[b]["z"], ref[b]["V_S"], 8,
+                           tdt)

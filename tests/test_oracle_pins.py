@@ -404,3 +404,21 @@ def test_tree_beam_equals_exhaustive_when_nothing_is_pruned():
     for i in chosen:
         par = allnodes[i][2]
         assert par == -1 or par in chosen
+
+
+# ----------------------------------------------------------------- NEXT-3 static frequency heads
+
+def test_frequency_ranking_and_fr_head():
+    assert O.frequency_ranking([0, 5, 5, 1]).tolist() == [1, 2, 3, 0]          # ties -> lower id
+    assert O.frequency_ranking([3, 3, 3]).tolist() == [0, 1, 2]                # uniform -> identity
+    rng = np.random.default_rng(2)
+    W = rng.standard_normal((50, 8))
+    h = rng.standard_normal(8)
+    pi = O.frequency_ranking(rng.integers(0, 100, 50))
+    full = O.fr_head(h, W, pi, 50, 5)[0]
+    dense = O.dense_head(h, W, 5)[0]
+    assert full["top_ids"].tolist() == dense["top_ids"].tolist()               # K = |V| -> dense
+    assert abs(full["lse"] - dense["lse"]) < 1e-12
+    small = O.fr_head(h, W, pi, 10, 3)[0]
+    assert set(small["V_S"].tolist()) <= set(O.fr_head(h, W, pi, 20, 3)[0]["V_S"].tolist())   # nesting S:359
+    assert [O.budget_pa_fr(t, 32768) for t in range(4)] == [32768, 32768, 10922, 8192]     # App. A.1
