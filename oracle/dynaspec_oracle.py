@@ -21,6 +21,7 @@ Steps:
   O7 dense             full-vocabulary head p = softmax(H W_LM)  P:182 (§4.1)
   NEXT-1 tree_step / tree_rerank   beam bookkeeping + re-rank    P:265-271 (Alg. 1 lines 12-18), R24
   NEXT-3 frequency_ranking, fr_head  FR-Spec / PA-FR prefix heads P:184-192, App. A.1
+  NEXT-4 verify_chain      lossless acceptance + residual sampling  Eq. 3, R25
 
 Pins: tests/test_oracle_*.py (golden values from SPEC/the worked example E2E-1,
 closed forms, brute force on tiny inputs, invariants).  Every function below is
@@ -429,3 +430,56 @@ def fr_head(h_new, W, pi_f, K, k_t):
         z = head(h, W, V_S)[0]
         out.append(dict(epilogue(z, V_S, min(k_t, K)), z=z, V_S=V_S))
     return out
+
+
+# ---------------------------------------------------------------------------
+# NEXT-4  lossless verification of a drafted chain   (Eq. 3 P:82-89 and its footnote to
+#         Leviathan et al. §3; reading R25 in DESIGN.md)
+# ---------------------------------------------------------------------------
+
+
+def softmax_full(logits):
+    """p = softmax(l) over the full vocabulary, fp64."""
+    l = np.asarray(logits, dtype=np.float64)
+    m = l.max()
+    e = np.exp(l - m)
+    return e / e.sum()
+
+
+def embed_q(V, q_ids, q_logits, q_lse):
+    """q over the full vocabulary: exp(z - lse) on the shortlist tokens, 0 off V_S."""
+    q = np.zeros(V, dtype=np.float64)
+    q[np.asarray(q_ids, dtype=np.int64)] = np.exp(np.asarray(q_logits, np.float64) - float(q_lse))
+    return q
+
+
+def sample_inverse_cdf(w, u):
+    """R25: the first token x (id order) whose cumulative weight exceeds u * sum(w)."""
+    c = np.cumsum(np.asarray(w, dtype=np.float64))
+    return int(np.searchsorted(c, u * c[-1], side="right"))
+
+
+def verify_chain(p_logits, q_ids, q_logits, q_lse, x, u_acc, u_res):
+    """Speculative-sampling verification of one chain of gamma drafted tokens x.
+
+    p_logits: (gamma+1, V) target logits at the gamma+1 positions; q_i (i < gamma) is the drafter's
+    shortlist distribution embedded in V.  Position i is accepted iff u_acc[i] < min(1, p_i(x_i)/q_i(x_i))
+    (Eq. 3); at the first rejection the corrective token is drawn from the normalised residual
+    (p_i - q_i)_+ with u_res; if all gamma are accepted, a bonus token is drawn from p_gamma with u_res.
+    Returns (accepted_count, committed tokens (accepted_count + 1 of them))."""
+    p_logits = np.asarray(p_logits, dtype=np.float64)
+    gamma = len(x)
+    V = p_logits.shape[1]
+    for i in range(gamma):
+        p = softmax_full(p_logits[i])
+        q = embed_q(V, q_ids[i], q_logits[i], q_lse[i])
+        xi = int(x[i])
+        if q[xi] <= 0.0:
+            raise OracleError("InvalidProposal")
+        if u_acc[i] < min(1.0, p[xi] / q[xi]):
+            continue
+        r = np.maximum(p - q, 0.0)
+        if r.sum() <= 0.0:  # R25: p == q numerically -> sample from p
+            r = p
+        return i, [int(t) for t in x[:i]] + [sample_inverse_cdf(r, u_res)]
+    return gamma, [int(t) for t in x] + [sample_inverse_cdf(softmax_full(p_logits[gamma]), u_res)]

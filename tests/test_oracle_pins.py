@@ -422,3 +422,62 @@ def test_frequency_ranking_and_fr_head():
     small = O.fr_head(h, W, pi, 10, 3)[0]
     assert set(small["V_S"].tolist()) <= set(O.fr_head(h, W, pi, 20, 3)[0]["V_S"].tolist())   # nesting S:359
     assert [O.budget_pa_fr(t, 32768) for t in range(4)] == [32768, 32768, 10922, 8192]     # App. A.1
+
+
+# ----------------------------------------------------------------- NEXT-4 lossless verification
+
+def test_sample_inverse_cdf_brute():
+    w = [0.0, 1.0, 0.0, 3.0]
+    assert O.sample_inverse_cdf(w, 0.0) == 1                 # zero-weight tokens are never drawn
+    assert O.sample_inverse_cdf(w, 0.2499) == 1
+    assert O.sample_inverse_cdf(w, 0.25) == 3                # first cumulative strictly above u*Z (R25)
+    assert O.sample_inverse_cdf(w, 0.999999) == 3
+
+
+def test_verify_two_token_example():
+    """|V|=2, p=[.6,.4], q=[.5,.5]: beta = 0.9; rejecting token 1 leaves all residual on 0."""
+    pl = np.log([[0.6, 0.4], [0.3, 0.7]])
+    qi, ql, qs = [[0, 1]], [[0.0, 0.0]], [math.log(2.0)]
+    assert O.verify_chain(pl, qi, ql, qs, [1], [0.85], 0.99) == (0, [0])      # 0.85 >= 0.4/0.5 -> reject
+    assert O.verify_chain(pl, qi, ql, qs, [1], [0.79], 0.2) == (1, [1, 0])    # accept; bonus from p_1
+    assert O.verify_chain(pl, qi, ql, qs, [1], [0.79], 0.5) == (1, [1, 1])
+    grid = (np.arange(1000) + 0.5) / 1000
+    acc = [np.mean([O.verify_chain(pl, qi, ql, qs, [x], [u], 0.5)[0] for u in grid]) for x in (0, 1)]
+    assert abs(0.5 * acc[0] + 0.5 * acc[1] - 0.9) < 1e-12                     # Eq. 3: sum min(p, q)
+
+
+def test_verify_q_equals_p_accepts_everything():
+    rng = np.random.default_rng(4)
+    pl = rng.standard_normal((4, 16)) * 2
+    lse = [float(np.log(np.exp(r).sum())) for r in pl]
+    ids = [np.arange(16)] * 3
+    for u in (0.0, 0.5, 0.999999):
+        n, com = O.verify_chain(pl, ids, pl[:3], lse[:3], [3, 7, 1], [u] * 3, 0.3)
+        assert n == 3 and com[:3] == [3, 7, 1] and len(com) == 4
+
+
+def test_verify_invalid_proposal():
+    with pytest.raises(O.OracleError):
+        O.verify_chain(np.zeros((2, 4)), [[0, 1]], [[0.0, 0.0]], [math.log(2)], [3], [0.1], 0.1)
+
+
+def test_verify_monte_carlo_exactness():
+    """the committed tokens follow the target law (TV < 0.02-0.03) even though q is zero off its
+    shortlist; position 1 given acceptance at 0 follows p_1."""
+    rng = np.random.default_rng(5)
+    V, n = 8, 30000
+    pl = rng.standard_normal((3, V)) * 1.5
+    p = [O.softmax_full(r) for r in pl]
+    S = [np.array([0, 2, 3, 5, 6]), np.array([1, 2, 4, 7])]
+    ql = [rng.standard_normal(len(s)) for s in S]
+    qs = [float(np.log(np.exp(z).sum())) for z in ql]
+    q = [O.embed_q(V, S[i], ql[i], qs[i]) for i in range(2)]
+    first, second = np.zeros(V), np.zeros(V)
+    for _ in range(n):
+        x = [int(rng.choice(V, p=q[i])) for i in range(2)]
+        k, com = O.verify_chain(pl, S, ql, qs, x, rng.random(2), rng.random())
+        first[com[0]] += 1
+        if k >= 1:
+            second[com[1]] += 1
+    assert 0.5 * np.abs(first / n - p[0]).sum() < 0.02
+    assert 0.5 * np.abs(second / second.sum() - p[1]).sum() < 0.03
