@@ -301,6 +301,39 @@ ds_status dynaspec_head_partial(const ds_clusters* c, const void* h_new, int32_t
 ds_status dynaspec_merge_records(const float* records, int32_t G, int32_t B, int32_t k_t, int32_t* top_ids,
                                  float* top_logits, float* top_logp, float* lse, ds_stream_t stream);
 
+/* ---------------------------------------------------------------- lossless verification (NEXT-4) */
+
+/* Materialise the shortlist V_S as vocabulary ids in shortlist order (S4): for each of `rows`
+ * selection rows (B per-row, or 1 for a shared selection), ids[r][sl_offsets[r][i] + u] =
+ * perm[offsets[sel[r][i]] + u] for u < |C_{sel[r][i]}|.  `stride` (int32 elements between rows) must
+ * be >= the row's shortlist length.  This is the id list that pairs with z_out of the head. */
+ds_status dynaspec_shortlist_ids(const ds_clusters* c, int32_t rows, const int32_t* sel, const int32_t* sel_count,
+                                 const int32_t* sl_offsets, int64_t stride, int32_t* ids, ds_stream_t stream);
+
+/* Workspace bytes of dynaspec_verify_chain.  The workspace must be zeroed once (dynaspec_ws_init)
+ * before its first use; every call leaves it zeroed again (it holds a dense [B][V] q buffer). */
+size_t dynaspec_verify_ws(int64_t V, int32_t B, int32_t gamma);
+
+/* Speculative-sampling verification of B drafted chains (Eq. 3, via the rule its footnote
+ * cites; reading R25 in DESIGN.md).  All pointers are device memory.
+ *   p_logits [B][gamma+1][V] (dtype DS_BF16 / DS_F32): the target's logits at the gamma+1 positions.
+ *   q_ids / q_logits [B][gamma][q_stride]: drafter shortlist ids and logits z (the head's z_out and
+ *     dynaspec_shortlist_ids), q_count [B][gamma] valid entries, q_lse [B][gamma] the head's lse:
+ *     q_i(v) = exp(z - lse) on the shortlist, 0 off it.
+ *   x / x_slot [B][gamma]: drafted tokens and their slot in the shortlist (q_ids[..][slot] == x).
+ *   u_acc [B][gamma], u_res [B]: uniforms in [0, 1) (the caller's random numbers).
+ * Position i is accepted iff u_acc < p_i(x_i) / q_i(x_i); at the first rejection j the corrective token
+ * is the first v (id order) whose cumulative (p_j - q_j)_+ exceeds u_res * sum; with no rejection the
+ * bonus token is drawn the same way from p_gamma (R25).  Outputs: accepted[b] = j and committed[b][0..j]
+ * (accepted tokens, then the corrective / bonus token); accepted[b] = -1 and committed[b][0] = -1 when
+ * the first non-accepted position has x_slot / x inconsistent with q_ids (InvalidProposal).
+ * Limits: gamma in [0, 32], V a multiple of 8 (16-byte rows).  Two launches on `stream`. */
+ds_status dynaspec_verify_chain(const void* p_logits, int32_t dtype, int64_t V, int32_t B, int32_t gamma,
+                                const int32_t* q_ids, const float* q_logits, int64_t q_stride, const int32_t* q_count,
+                                const float* q_lse, const int32_t* x, const int32_t* x_slot, const float* u_acc,
+                                const float* u_res, int32_t* accepted, int32_t* committed, void* ws, size_t ws_bytes,
+                                ds_stream_t stream);
+
 /* Debugging: when dev_buf != NULL, the fused step kernel records %globaltimer nanosecond
  * timestamps of its phases into dev_buf[cta * 64 + slot] and the SM clock64() into
  * dev_buf[cta * 64 + 32 + slot] (uint64, >= #SM * 64 entries):

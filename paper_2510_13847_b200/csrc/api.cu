@@ -304,6 +304,39 @@ ds_status dynaspec_tree_rerank(const float* node_score, const int32_t* node_tok,
              : DS_ERR_CUDA;
 }
 
+ds_status dynaspec_shortlist_ids(const ds_clusters* c, int32_t rows, const int32_t* sel, const int32_t* sel_count,
+                                 const int32_t* sl_offsets, int64_t stride, int32_t* ids, ds_stream_t stream) {
+  ds_status s = check_clusters(c);
+  if (s != DS_OK) return s;
+  if (!sel || !sel_count || !sl_offsets || !ids || rows < 1 || stride < 1) return DS_ERR_SHAPE;
+  return launch_shortlist_ids(c, rows, sel, sel_count, sl_offsets, stride, ids, (cudaStream_t)stream) == cudaSuccess
+             ? DS_OK
+             : DS_ERR_CUDA;
+}
+
+size_t dynaspec_verify_ws(int64_t V, int32_t B, int32_t gamma) {
+  if (V < 1 || B < 1 || gamma < 0 || gamma > 32) return 0;
+  return verify_ws_bytes(V, B, gamma);
+}
+
+ds_status dynaspec_verify_chain(const void* p_logits, int32_t dtype, int64_t V, int32_t B, int32_t gamma,
+                                const int32_t* q_ids, const float* q_logits, int64_t q_stride, const int32_t* q_count,
+                                const float* q_lse, const int32_t* x, const int32_t* x_slot, const float* u_acc,
+                                const float* u_res, int32_t* accepted, int32_t* committed, void* ws, size_t ws_bytes,
+                                ds_stream_t stream) {
+  if (!dtype_ok(dtype)) return DS_ERR_DTYPE;
+  if (!p_logits || !u_res || !accepted || !committed || B < 1 || V < 1 || V > INT32_MAX || gamma < 0)
+    return DS_ERR_SHAPE;
+  if (gamma > 32 || V % 8 != 0) return DS_ERR_UNSUPPORTED;
+  if (gamma > 0 && (!q_ids || !q_logits || !q_count || !q_lse || !x || !x_slot || !u_acc || q_stride < 1))
+    return DS_ERR_SHAPE;
+  if (!ws || ws_bytes < verify_ws_bytes(V, B, gamma)) return DS_ERR_WORKSPACE;
+  return launch_verify(p_logits, dtype, V, B, gamma, q_ids, q_logits, q_stride, q_count, q_lse, x, x_slot, u_acc,
+                       u_res, accepted, committed, ws, (cudaStream_t)stream) == cudaSuccess
+             ? DS_OK
+             : DS_ERR_CUDA;
+}
+
 ds_status dynaspec_step_route(const ds_clusters* c, const ds_router* r, const void* h_prev, const void* e, int32_t B,
                               int32_t t, int32_t k_max, int32_t k_min, int32_t shared, const ds_step_outputs* out,
                               void* ws, size_t ws_bytes, ds_stream_t s_meta) {

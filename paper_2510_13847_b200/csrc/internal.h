@@ -95,6 +95,15 @@ cudaError_t launch_tree_step(const int32_t* top_ids, const float* top_logp, int 
 cudaError_t launch_tree_rerank(const float* node_score, const int32_t* node_tok, int n, int n_out, int32_t* out_nodes,
                                cudaStream_t st);
 
+// ---- lossless verification + shortlist ids (verify.cu)
+size_t verify_ws_bytes(int64_t V, int B, int gamma);
+cudaError_t launch_verify(const void* p_logits, int dtype, int64_t V, int B, int gamma, const int32_t* q_ids,
+                          const float* q_logits, int64_t q_stride, const int32_t* q_count, const float* q_lse,
+                          const int32_t* x, const int32_t* x_slot, const float* u_acc, const float* u_res,
+                          int32_t* accepted, int32_t* committed, void* ws, cudaStream_t st);
+cudaError_t launch_shortlist_ids(const ds_clusters* c, int rows, const int32_t* sel, const int32_t* cnt,
+                                 const int32_t* sl_off, int64_t stride, int32_t* ids, cudaStream_t st);
+
 // ---- offline partition (build.cu)
 size_t build_ws_bytes(int64_t V, int d, int M);
 size_t layout_ws_bytes(int64_t V, int M);

@@ -87,6 +87,10 @@ def _load():
         "dynaspec_head_partial": (c_int32, [POINTER(DsClusters), P, c_int32, P, P, P, c_int32, c_int32, c_int64, P, P,
                                             c_size_t, P]),
         "dynaspec_merge_records": (c_int32, [P, c_int32, c_int32, c_int32, P, P, P, P, P]),
+        "dynaspec_shortlist_ids": (c_int32, [POINTER(DsClusters), c_int32, P, P, P, c_int64, P, P]),
+        "dynaspec_verify_ws": (c_size_t, [c_int64, c_int32, c_int32]),
+        "dynaspec_verify_chain": (c_int32, [P, c_int32, c_int64, c_int32, c_int32, P, P, c_int64, P, P, P, P, P, P,
+                                            P, P, P, c_size_t, P]),
         "dynaspec_draft_step_launches": (c_int32, [POINTER(DsClusters), POINTER(DsRouter), c_int32, c_int32,
                                                    c_int32, c_int32]),
     }
@@ -106,6 +110,7 @@ EXPORTED = [
     "dynaspec_head_forward", "dynaspec_draft_step_ws", "dynaspec_draft_step", "dynaspec_draft_step_launches",
     "dynaspec_debug_set_trace", "dynaspec_restrict_selection", "dynaspec_head_partial", "dynaspec_merge_records",
     "dynaspec_tree_step", "dynaspec_tree_rerank", "dynaspec_step_route", "dynaspec_step_head",
+    "dynaspec_shortlist_ids", "dynaspec_verify_ws", "dynaspec_verify_chain",
 ]
 
 
@@ -505,3 +510,41 @@ class FrequencyHead:
 def pa_fr_budget(t, K_max):
     """K_fr(t) = K_max for t < 2, else max(1, floor(K_max / (t + 1))) (App. A.1, P:404-410)."""
     return K_max if t < 2 else max(1, K_max // (t + 1))
+
+
+# ---------------------------------------------------------------------------- verification (NEXT-4)
+
+def shortlist_ids(clusters, sel, sel_count, sl_offsets, stride, rows=None):
+    """dynaspec_shortlist_ids: V_S as vocabulary ids in shortlist order, [rows][stride] (-1 padded)."""
+    _need_cuda(sel, sel_count, sl_offsets)
+    rows = sel_count.shape[0] if rows is None else rows
+    ids = torch.full((rows, stride), -1, dtype=torch.int32, device=sel.device)
+    _check(_lib.dynaspec_shortlist_ids(clusters.struct(), rows, _ptr(sel), _ptr(sel_count), _ptr(sl_offsets), stride,
+                                       _ptr(ids), _stream()), "dynaspec_shortlist_ids")
+    return ids
+
+
+class Verifier:
+    """dynaspec_verify_chain with a persistent (self-zeroing) workspace (Eq. 3; R25)."""
+
+    def __init__(self, V, B, gamma, device="cuda"):
+        self.V, self.B, self.gamma = V, B, gamma
+        self.ws = Workspace(_lib.dynaspec_verify_ws(V, B, gamma), device)
+        self.accepted = torch.zeros(B, dtype=torch.int32, device=device)
+        self.committed = torch.full((B, gamma + 1), -1, dtype=torch.int32, device=device)
+
+    def __call__(self, p_logits, q_ids, q_logits, q_count, q_lse, x, x_slot, u_acc, u_res):
+        _need_cuda(p_logits, u_res)
+        B, g1, V = p_logits.shape
+        if (B, g1 - 1, V) != (self.B, self.gamma, self.V):
+            raise ValueError("shape does not match the Verifier")
+        g = self.gamma
+        stride = q_ids.shape[-1] if g > 0 else 1
+        _check(_lib.dynaspec_verify_chain(_ptr(p_logits), _DTYPE[p_logits.dtype], V, B, g,
+                                          _ptr(q_ids) if g else None, _ptr(q_logits) if g else None, stride,
+                                          _ptr(q_count) if g else None, _ptr(q_lse) if g else None,
+                                          _ptr(x) if g else None, _ptr(x_slot) if g else None,
+                                          _ptr(u_acc) if g else None, _ptr(u_res), _ptr(self.accepted),
+                                          _ptr(self.committed), self.ws.ptr(), self.ws.nbytes, _stream()),
+               "dynaspec_verify_chain")
+        return self.accepted, self.committed

@@ -253,3 +253,30 @@ def zipf_token_counts(V, seed=3, a=1.1, n_tokens=10_000_000):
     counts = np.zeros(V, dtype=np.int64)
     counts[ranks] = rng.multinomial(n_tokens, p)
     return counts
+
+
+def verify_inputs(B, gamma, V, n_short, seed=11, dtype="bf16", logit_std=3.0, q_noise=0.5):
+    """Synthetic verification workload (NEXT-4): target logits [B][gamma+1][V] ~ N(0, logit_std^2)
+    (peaked next-token distributions); for each drafted position a shortlist of the n_short tokens
+    with the largest noisy target logit (random order) whose drafter logits are the target's logits
+    there + N(0, q_noise^2) (a drafter that approximates the target); q_lse is left to the caller.  Uniforms u_acc [B][gamma], u_res [B] and
+    u_draw [B][gamma] (for picking the drafted tokens) in [0, 1)."""
+    g = _gen(seed)
+    p = torch.randn((B, gamma + 1, V), generator=g) * logit_std
+    p = p.to(TORCH_DTYPES[dtype])
+    pf = p.float()
+    # the shortlist holds the n_short tokens with the largest noisy target logit (a drafter shortlist
+    # that captures most, not all, of the target mass), in random order
+    ids = torch.empty((B, gamma, n_short), dtype=torch.int32)
+    for b in range(B):
+        for i in range(gamma):
+            noisy = pf[b, i] + torch.randn(V, generator=g) * logit_std
+            top = torch.topk(noisy, n_short).indices
+            ids[b, i] = top[torch.randperm(n_short, generator=g)].to(torch.int32)
+    ql = torch.empty((B, gamma, n_short), dtype=torch.float32)
+    for b in range(B):
+        for i in range(gamma):
+            ql[b, i] = pf[b, i, ids[b, i].long()] + torch.randn(n_short, generator=g) * q_noise
+    u = torch.rand((B, 2 * gamma + 1), generator=g, dtype=torch.float64)
+    return dict(p_logits=p, q_ids=ids, q_logits=ql, u_acc=u[:, :gamma].float(), u_draw=u[:, gamma:2 * gamma],
+                u_res=u[:, 2 * gamma].float())
