@@ -400,6 +400,8 @@ def run_ours(args, ws, rank, local):
         e2e = e2e_run(D, steppers, clusters, router, C, B, args, dev, flush, ws)
         two = two_stream_run(D, clusters, router, inputs, C, B, args, dev, flush)
         overlap = core_overlap_run(D, clusters, router, inputs, C, B, args, dev, flush)
+        static = static_heads_run(D, clusters, inputs, C, B, dev, flush)
+        verify = verify_run(D, C, dev, flush, int(round(float(np.mean(vs_sizes)))))
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
@@ -433,7 +435,9 @@ def run_ours(args, ws, rank, local):
                        "step_mode": "fused one-launch step" if fused else "two kernels per step",
                        "two_stream_mode": None if args.profile else two,
                        "gathered_block_streaming": stream_bw,
-                       "drafter_core_overlap": None if args.profile else overlap},
+                       "drafter_core_overlap": None if args.profile else overlap,
+                       "static_frequency_heads": None if args.profile else static,
+                       "verification": None if args.profile else verify},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak if achieved else None,
                          "traffic": committed_traffic(C.name, B), "kernel": ("ds::step_kernel (router + select + gathered head + epilogue, one launch)" if fused
@@ -632,6 +636,106 @@ def core_overlap_run(D, clusters, router, inputs, C, B, args, dev, flush, reps=1
                   "(cuBLAS stand-in for the EAGLE block); serialized = core then the fused one-launch step; "
                   "overlapped = router on S_m || core on S_d, then the head")
     return res
+
+
+def static_heads_run(D, clusters, inputs, C, B, dev, flush, reps=10):
+    """NEXT-3: FR-Spec (fixed K = 32768, the paper's FR-Spec 32k) and PA-FR (K_fr(t), App. A.1)
+    prefix heads on the same kernels, one cycle per CUDA graph, cold L2; synthetic Zipf counts for pi_f."""
+    from synth import inputs as S_
+    counts = S_.zipf_token_counts(C.V)
+    pi = torch.as_tensor(np.lexsort((np.arange(C.V), -counts)), dtype=torch.int64)  # descending count, id asc
+    Wv = torch.empty_like(clusters.W_perm)
+    Wv[clusters.perm.long()] = clusters.W_perm
+    fh = D.FrequencyHead(Wv, pi.to(dev))
+    del Wv
+    torch.cuda.empty_cache()
+    K = min(32768, C.V)
+    wss = [D.Workspace(1 << 20, dev) for _ in range(C.positions)]
+    res = {}
+    for name, kfn in (("fr_spec_32k", lambda t: K), ("pa_fr", lambda t: D.pa_fr_budget(t, K))):
+        def cyc():
+            for t in range(C.positions):
+                fh.forward(inputs[0][t][2], kfn(t), C.k_t, ws=wss[t])
+        s = torch.cuda.Stream(device=dev)
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            cyc()
+        torch.cuda.current_stream().wait_stream(s)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            cyc()
+        ts = []
+        for i in range(reps + 2):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            g.replay()
+            b.record()
+            torch.cuda.synchronize()
+            if i >= 2:
+                ts.append(a.elapsed_time(b))
+        res[name + "_us_per_step"] = 1e3 * statistics.median(ts) / C.positions
+        res[name + "_mean_K"] = float(np.mean([kfn(t) for t in range(C.positions)]))
+    del fh
+    torch.cuda.empty_cache()
+    res["how"] = "frequency-permuted W copy, shortlist = prefix [0, K) as one contiguous run; same head kernels"
+    return res
+
+
+def verify_run(D, C, dev, flush, n_short, B=64, reps=10):
+    """NEXT-4: lossless verification of B drafted chains of gamma = positions tokens against synthetic
+    target logits [B][gamma+1][V] (bf16), drafter shortlists of n_short ids (the measured mean |V_S|)."""
+    g_ = torch.Generator(device=dev)
+    g_.manual_seed(5)
+    gam, V = C.positions, C.V
+    p = (torch.randn((B, gam + 1, V), generator=g_, device=dev) * 3).to(torch.bfloat16)
+    noisy = p[:, :gam].float() + torch.randn((B, gam, V), generator=g_, device=dev) * 3
+    ids = torch.topk(noisy, n_short, dim=-1).indices.to(torch.int32).contiguous()
+    del noisy
+    ql = (torch.gather(p[:, :gam].float(), 2, ids.long()) +
+          torch.randn((B, gam, n_short), generator=g_, device=dev) * 0.5).contiguous()
+    q_lse = torch.logsumexp(ql, dim=-1).contiguous()
+    slot = torch.multinomial(torch.softmax(ql.reshape(-1, n_short), -1), 1, generator=g_).reshape(B, gam)
+    x = torch.gather(ids, 2, slot.unsqueeze(-1)).squeeze(-1).contiguous()
+    slot = slot.to(torch.int32).contiguous()
+    cnt = torch.full((B, gam), n_short, dtype=torch.int32, device=dev)
+    u_acc = torch.rand((B, gam), generator=g_, device=dev)
+    u_res = torch.rand(B, generator=g_, device=dev)
+    ver = D.Verifier(V, B, gam, dev)
+    call = lambda: ver(p, ids, ql, cnt, q_lse, x, slot, u_acc, u_res)
+    s = torch.cuda.Stream(device=dev)
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        call()
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        call()
+    ts = []
+    for i in range(reps + 2):
+        flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        g.replay()
+        b.record()
+        torch.cuda.synchronize()
+        if i >= 2:
+            ts.append(a.elapsed_time(b))
+    us = 1e3 * statistics.median(ts)
+    target_bytes = B * (gam + 1) * V * 2
+    resid_bytes = B * V * (2 + 4) + 2 * B * n_short * 8
+    peak, _ = measured_peaks()
+    acc = ver.accepted.float().mean().item()
+    out = {"chains": B, "gamma": gam, "V": V, "n_short": n_short, "us_per_call": us,
+           "chains_per_s": B / (us / 1e6), "mean_accepted": acc,
+           "target_logit_bytes": target_bytes, "residual_pass_bytes": resid_bytes,
+           "achieved_GBps": (target_bytes + resid_bytes) / (us / 1e6) / 1e9}
+    out["frac"] = out["achieved_GBps"] / peak
+    del p, ids, ql, ver
+    torch.cuda.empty_cache()
+    return out
 
 
 def e2e_run(D, steppers, clusters, router, C, B, args, dev, flush, ws, reps=None):
