@@ -24,18 +24,35 @@ def needs_build():
     return any(os.path.getmtime(p) > t for p in deps)
 
 
+def _compile(src, obj):
+    cmd = [NVCC, *[f for f in FLAGS if f != "-shared"], "-c", "-o", obj, src]
+    return subprocess.run(cmd, capture_output=True, text=True)
+
+
 def build(force=False, verbose=False):
+    """One nvcc per translation unit in parallel, then one shared-library link."""
     if not force and not needs_build():
         return OUT
-    os.makedirs(os.path.dirname(OUT), exist_ok=True)
-    cmd = [NVCC, *FLAGS, "-o", OUT, *sources()]
-    r = subprocess.run(cmd, capture_output=True, text=True)
+    from concurrent.futures import ThreadPoolExecutor
+    odir = os.path.join(HERE, "lib", "obj")
+    os.makedirs(odir, exist_ok=True)
+    srcs = sources()
+    objs = [os.path.join(odir, os.path.basename(s)[:-3] + ".o") for s in srcs]
+    with ThreadPoolExecutor(max_workers=min(len(srcs), os.cpu_count() or 4)) as ex:
+        results = list(ex.map(_compile, srcs, objs))
+    log = ""
+    for s, r in zip(srcs, results):
+        log += r.stderr
+        if r.returncode != 0:
+            raise RuntimeError(f"nvcc failed on {os.path.basename(s)}:\n" + r.stdout + r.stderr)
+    r = subprocess.run([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", OUT, *objs],
+                       capture_output=True, text=True)
     if r.returncode != 0:
-        raise RuntimeError("nvcc failed:\n" + r.stdout + r.stderr)
+        raise RuntimeError("nvcc link failed:\n" + r.stdout + r.stderr)
     if verbose:
-        print(r.stderr)
+        print(log)
     with open(os.path.join(HERE, "lib", "ptxas.log"), "w") as f:
-        f.write(r.stderr)
+        f.write(log)
     return OUT
 
 

@@ -148,6 +148,14 @@ __device__ __forceinline__ void trace_mark(unsigned long long* t, int slot) {
   }
 }
 
+// Same, from lane 0 of the calling warp (for code that only one warp of the CTA still runs).
+__device__ __forceinline__ void trace_mark_w(unsigned long long* t, int slot) {
+  if (t != nullptr && (threadIdx.x & 31) == 0) {
+    t[blockIdx.x * 64 + slot] = globaltimer_ns();
+    t[blockIdx.x * 64 + 32 + slot] = clock64();
+  }
+}
+
 // Spin (one thread) until *ctr >= target, then acquire.
 __device__ __forceinline__ void spin_until_geq(const unsigned* ctr, unsigned target) {
   while (ld_volatile_u32(ctr) < target) {
@@ -433,5 +441,51 @@ __device__ __forceinline__ void warp_lse_items(const float* z, int n, float& m, 
     const float s2 = __shfl_xor_sync(0xffffffffu, s, o);
     lse_combine(m, s, m2, s2);
   }
+}
+}  // namespace ds
+
+namespace ds {
+// ------------------------------------------------------------------ thread-block clusters (DSMEM)
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t cluster_nctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t cluster_id_x() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t cluster_count_x() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%nclusterid.x;" : "=r"(r));
+  return r;
+}
+// Address of the same shared-memory variable in CTA `rank` of this cluster.
+__device__ __forceinline__ uint32_t mapa_u32(uint32_t local_smem_addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local_smem_addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void st_cluster_f32(uint32_t addr, float v) {
+  asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
+}
+__device__ __forceinline__ void st_cluster_u32(uint32_t addr, uint32_t v) {
+  asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+// Cluster barrier (every thread of every CTA of the cluster; warp-converged).
+__device__ __forceinline__ void cluster_arrive_relaxed() {
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_arrive_release() {
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait_acquire() {
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 }  // namespace ds

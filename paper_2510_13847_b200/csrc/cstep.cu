@@ -1,0 +1,727 @@
+// cstep.cu — one DynaSpec draft step for a single row (B = 1) with the router computed per
+// thread-block CLUSTER, so the step needs no grid-wide barrier before the head streams.
+//
+// Why: at B = 1 the step is latency-bound (P:283 T_D model; SURVEY §8(d) latency budget).  The
+// grid-wide variant (step.cu) spends ~2 us on a global counter handshake between router layer 1
+// and layer 2 and ~5 us on single-CTA layer 2 + TopK.  Here every cluster of Q CTAs (Q = 16 when
+// the GPU fits it, one CTA per SM) evaluates the whole router r_theta([h_prev ‖ e]) (P:198-199,
+// Alg. 1 line 8) by itself:
+//   * CTA q streams rows [q h_r/Q, (q+1) h_r/Q) of W1 by TMA into its ring — issued before the
+//     PDL wait, since router weights do not depend on the upstream kernel — and dots them with
+//     [h_prev ‖ e] (each W1 row = two d-element halves, so a half is exactly one head row);
+//   * hidden activations a = ReLU(W1 x + b1) are broadcast into every CTA of the cluster through
+//     distributed shared memory (st.shared::cluster) + one hardware cluster barrier;
+//   * CTA q computes the scores s_m = W2_m . a + b2_m of its slice of M and broadcasts them;
+//   * CTA q ranks its own slice against all M scores (rank < k <=> in TopK_k under (score desc,
+//     id asc), R7) and broadcasts the selected ids; every CTA then forms the ascending
+//     selection and shortlist offsets (R8) locally.  The scores are bit-identical in every
+//     cluster (same code, same order), so all clusters agree on the shortlist.
+// The gathered head streams the CTA's segment through the TMA ring of head_impl.cuh; each
+// consumer warp folds its logits into an online (max, sum exp) and a lane-distributed sorted
+// top-k_t list while the next slots are in flight.  Lists are merged in two levels
+// without float atomics (R19): the CTA's warps, then the last CTA to take the global ticket merges
+// the G per-CTA records (CTA order).
+#include <algorithm>
+#include <stdlib.h>
+
+#include "head_impl.cuh"
+#include "internal.h"
+#include "select_impl.cuh"
+
+namespace ds {
+
+constexpr int kCStepMaxKt = 32;  // one list entry per lane
+
+struct CStepArgs {
+  HeadArgs h;              // head part; sel / sel_count / sl_off are redirected to shared memory
+  const void* W1;          // [rows1][2d]
+  const float* b1;         // [rows1]
+  const void* W2;          // [M][h_r] (h_r > 0)
+  const float* b2;         // [M]
+  const void* h_prev;      // [d]
+  const void* e;           // [d]
+  float* scores;           // [M] (nullable)
+  int32_t* sel_out;        // [M]
+  int32_t* cnt_out;        // [1]
+  int32_t* sloff_out;      // [M+1]
+  int32_t h_r, rows1, k, extra_bytes;
+  unsigned long long* crec;  // [G][2 + k_t] per-CTA records: max, sum (float bits), then k_t keys
+  unsigned* ctr;             // [0] ticket over CTAs
+  unsigned long long* trace;
+};
+
+// Shared-memory carve-up (inside HeadSmem.extra).
+struct CExtra {
+  uint32_t xs, p1, a1, sc, w2s, b1s, b2s, offs, selb, mask, sel, sloff, cnt, tmp, wm, ws, wl, surv, out, misc, total;
+};
+__host__ __device__ inline CExtra cstep_extra(int d, int esz, int M, int h_r, int rows1, int Q, int K, int S, int C) {
+  CExtra X;
+  uint32_t o = 0;
+  auto take = [&](uint32_t bytes) {
+    const uint32_t at = o;
+    o = (o + bytes + 15u) & ~15u;
+    return at;
+  };
+  const int U = (rows1 + Q - 1) / Q;
+  const int Ms = h_r > 0 ? (M + Q - 1) / Q : 0;
+  X.xs = take(2u * d * esz);
+  X.p1 = take(4u * 2 * U);
+  X.a1 = take(4u * (h_r > 0 ? h_r : 1));
+  X.sc = take(4u * ((M + 3) & ~3));
+  X.w2s = take((uint32_t)Ms * (h_r > 0 ? h_r : 0) * esz);
+  X.b1s = take(4u * U);
+  X.b2s = take(4u * (Ms > 0 ? Ms : 1));
+  X.offs = take(4u * (M + 1));
+  X.selb = take((uint32_t)(M + 3) & ~3u);
+  X.mask = take(4u * 32);
+  X.sel = take(4u * M);
+  X.sloff = take(4u * (M + 1));
+  X.cnt = take(16);
+  X.tmp = take(4u * M);
+  X.wm = take(4u * S);
+  X.ws = take(4u * S);
+  X.wl = take(8u * S * K);
+  X.surv = take(8u * S * K);
+  X.out = take(8u * K);
+  X.misc = take(64);
+  X.total = o;
+  return X;
+}
+
+// ---------------------------------------------------------------- total order as one 64-bit key
+// key = ord_key(z) << 32 | ~id: a larger key is a larger logit, or an equal logit with a lower
+// token id (R7, R23: -0 folded into +0).  0 is below every valid key (padding).
+__device__ __forceinline__ unsigned long long tok_key(float z, int id) {
+  return ((unsigned long long)ord_key(z) << 32) | (unsigned long long)(~(uint32_t)id);
+}
+__device__ __forceinline__ float key_value(unsigned long long k) {
+  const uint32_t u = (uint32_t)(k >> 32);
+  return __uint_as_float((u & 0x80000000u) ? (u & 0x7fffffffu) : ~u);
+}
+__device__ __forceinline__ int key_id(unsigned long long k) { return (int)(~(uint32_t)k); }
+
+// Warp-distributed sorted list (lane r < K holds the r-th best key; 0 = empty).  `kth` mirrors
+// lane K-1's entry, so a candidate that cannot enter costs one compare.
+__device__ __forceinline__ void list_insert(unsigned long long& mine, unsigned long long& kth, unsigned long long x,
+                                            int K, int lane) {
+  if (x <= kth) return;  // warp-uniform
+  const uint32_t lanes = K >= 32 ? 0xffffffffu : ((1u << K) - 1u);
+  const int pos = __popc(__ballot_sync(0xffffffffu, mine > x) & lanes);
+  const unsigned long long up = __shfl_up_sync(0xffffffffu, mine, 1);
+  if (lane > pos) mine = up;
+  else if (lane == pos) mine = x;
+  kth = __shfl_sync(0xffffffffu, mine, K - 1);
+}
+
+// Online softmax accumulation of one logit (warp-uniform state).
+__device__ __forceinline__ void lse_push(float& m, float& s, float z) {
+  if (z > m) {
+    s = s * expf(m - z) + 1.f;
+    m = z;
+  } else {
+    s += expf(z - m);
+  }
+}
+
+// Two staged rows against two (possibly different) vectors: lane-parallel fp32 partials + warp
+// trees (R18), as dot2 in head_impl.cuh.
+template <typename T>
+__device__ __forceinline__ void dot2x(const T* __restrict__ w0, const T* __restrict__ w1, const T* __restrict__ x0,
+                                      const T* __restrict__ x1, int d, int lane, float& z0, float& z1) {
+  constexpr int E = Elem<T>::kPer16B;
+  float a0 = 0.f, a1 = 0.f, b0 = 0.f, b1 = 0.f;
+#pragma unroll 2
+  for (int c = lane * E; c < d; c += 32 * E) {
+    float xf[E], yf[E], uf[E], vf[E];
+    widen16(*reinterpret_cast<const uint4*>(w0 + c), xf, w0);
+    widen16(*reinterpret_cast<const uint4*>(w1 + c), yf, w0);
+    widen16(*reinterpret_cast<const uint4*>(x0 + c), uf, w0);
+    widen16(*reinterpret_cast<const uint4*>(x1 + c), vf, w0);
+#pragma unroll
+    for (int j = 0; j < E; j += 2) {
+      a0 = fmaf(xf[j], uf[j], a0);
+      b0 = fmaf(yf[j], vf[j], b0);
+      a1 = fmaf(xf[j + 1], uf[j + 1], a1);
+      b1 = fmaf(yf[j + 1], vf[j + 1], b1);
+    }
+  }
+  z0 = warp_sum(a0 + a1);
+  z1 = warp_sum(b0 + b1);
+}
+
+// Consumer warp `w` (ring slot w): gathered-head logits of the CTA's segment folded on the fly into
+// (m, s) and the warp's sorted top-K list.
+template <typename T>
+__device__ __forceinline__ void cstep_consume(const HeadArgs& a, const HeadCtx& c, int w, int lane, uint32_t k0,
+                                              float& m, float& s, unsigned long long& mine) {
+  const T* hs = static_cast<const T*>(c.hs);
+  const int K = a.k_t;
+  unsigned long long kth = 0ull;
+  m = -INFINITY;
+  s = 0.f;
+  mine = 0ull;
+  for (uint32_t k = k0;; ++k) {
+    mbar_wait(&c.full[w], k & 1u);
+    const int4 inf = c.info[w];
+    if (inf.z < 0) break;
+    const T* st = reinterpret_cast<const T*>(c.ring + (size_t)w * a.stage_bytes);
+    const long long zbase = c.sega[0] + inf.y;
+    for (int rr = 0; rr < inf.z; rr += 2) {
+      const bool two = rr + 1 < inf.z;
+      const int tok0 = __ldg(a.perm + inf.w + rr);
+      const int tok1 = two ? __ldg(a.perm + inf.w + rr + 1) : 0;
+      const T* w0 = st + (size_t)rr * a.d;
+      float z0, z1;
+      dot2<T>(w0, two ? w0 + a.d : w0, hs, a.d, lane, z0, z1);
+      lse_push(m, s, z0);
+      list_insert(mine, kth, tok_key(z0, tok0), K, lane);
+      if (two) {
+        lse_push(m, s, z1);
+        list_insert(mine, kth, tok_key(z1, tok1), K, lane);
+      }
+      if (a.z_out && lane == 0) {
+        a.z_out[zbase + rr] = z0;
+        if (two) a.z_out[zbase + rr + 1] = z1;
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&c.empty[w]);
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__((kMaxStages + 1) * 32, 1) cstep_kernel(const CStepArgs s) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  HeadArgs a = s.h;
+  const HeadSmem L = head_smem(a.stages, a.stage_bytes, 1, a.d, (int)sizeof(T), a.lcap, s.extra_bytes);
+  const HeadCtx c = head_ctx(smem, L);
+  constexpr int E = Elem<T>::kPer16B;
+  const int Q = (int)cluster_nctarank(), q = (int)cluster_ctarank();
+  const int cid = (int)cluster_id_x(), C = (int)cluster_count_x();
+  const int M = a.M, d = a.d, K = a.k_t, S = a.stages;
+  const CExtra X = cstep_extra(d, (int)sizeof(T), M, s.h_r, s.rows1, Q, K, S, C);
+  uint8_t* ex = c.extra;
+  T* xs = reinterpret_cast<T*>(ex + X.xs);
+  float* p1 = reinterpret_cast<float*>(ex + X.p1);
+  float* a1 = reinterpret_cast<float*>(ex + X.a1);
+  float* sc = reinterpret_cast<float*>(ex + X.sc);
+  T* w2s = reinterpret_cast<T*>(ex + X.w2s);
+  float* b1s = reinterpret_cast<float*>(ex + X.b1s);
+  float* b2s = reinterpret_cast<float*>(ex + X.b2s);
+  int32_t* offs = reinterpret_cast<int32_t*>(ex + X.offs);
+  uint8_t* selb = ex + X.selb;
+  uint32_t* mask = reinterpret_cast<uint32_t*>(ex + X.mask);
+  int32_t* sel_s = reinterpret_cast<int32_t*>(ex + X.sel);
+  int32_t* sloff_s = reinterpret_cast<int32_t*>(ex + X.sloff);
+  int32_t* cnt_s = reinterpret_cast<int32_t*>(ex + X.cnt);
+  int32_t* tmp = reinterpret_cast<int32_t*>(ex + X.tmp);
+  float* wm = reinterpret_cast<float*>(ex + X.wm);
+  float* wsum = reinterpret_cast<float*>(ex + X.ws);
+  unsigned long long* wl = reinterpret_cast<unsigned long long*>(ex + X.wl);
+  unsigned long long* surv = reinterpret_cast<unsigned long long*>(ex + X.surv);
+  unsigned long long* out = reinterpret_cast<unsigned long long*>(ex + X.out);
+  int* misc = reinterpret_cast<int*>(ex + X.misc);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+  uint64_t* xbar = c.full + 2 * kMaxStages;  // spare barrier slots: x + h_new, W2 slice
+  uint64_t* wbar = xbar + 1;
+
+  // this CTA's router rows (layer-1 units) and score slice
+  const int u0 = s.rows1 * q / Q, u1 = s.rows1 * (q + 1) / Q, U = u1 - u0;
+  const int nh = 2 * U;                                   // half rows of W1 (d elements each)
+  const int n1 = (nh + a.stage_rows - 1) / a.stage_rows;  // ring loads of router rows
+  const int ms0 = s.h_r > 0 ? M * q / Q : u0, ms1 = s.h_r > 0 ? M * (q + 1) / Q : u1;  // score slice
+  const uint32_t hb = (uint32_t)d * (uint32_t)sizeof(T);
+  const uint32_t w2_bytes = (uint32_t)(ms1 - ms0) * (uint32_t)(s.h_r > 0 ? s.h_r : 0) * (uint32_t)sizeof(T);
+
+  if (threadIdx.x == 0) {
+    head_init_barriers(c, S);
+    mbar_init(xbar, 1);
+    mbar_init(wbar, 1);
+    fence_mbar_init();
+  }
+  for (int m = threadIdx.x; m < M; m += blockDim.x) selb[m] = 0;
+  if (threadIdx.x < 8) misc[threadIdx.x] = 0;
+  __syncthreads();
+  cluster_arrive_relaxed();  // paired with the wait before the first DSMEM store
+  trace_mark(s.trace, 0);
+  if (warp == S) {
+    if (lane == 0) {
+      // router weights are constants: stream them before the PDL wait (W2 slice, then W1 rows)
+      const uint64_t keep = policy_evict_last();
+      if (w2_bytes > 0) {
+        mbar_arrive_expect_tx(wbar, w2_bytes);
+        bulk_g2s(w2s, static_cast<const T*>(s.W2) + (size_t)ms0 * s.h_r, w2_bytes, wbar, keep);
+      }
+      const uint8_t* src = static_cast<const uint8_t*>(s.W1) + (size_t)u0 * 2 * hb;
+      auto issue = [&](int it) {
+        const int sl = it % S;
+        mbar_wait(&c.empty[sl], ((uint32_t)(it / S) & 1u) ^ 1u);
+        const int j0 = it * a.stage_rows, n = min(a.stage_rows, nh - j0);
+        c.info[sl] = make_int4(j0, 0, n, 0);
+        mbar_arrive_expect_tx(&c.full[sl], (uint32_t)n * hb);
+        bulk_g2s(c.ring + (size_t)sl * a.stage_bytes, src + (size_t)j0 * hb, (uint32_t)n * hb, &c.full[sl], keep);
+      };
+      const int first = min(n1, S);
+      for (int it = 0; it < first; ++it) issue(it);
+      // activations come from upstream kernels: x = [h_prev ‖ e] and h_new, one barrier
+      if (a.pdl) pdl_wait();
+      mbar_arrive_expect_tx(xbar, 3u * hb);
+      const uint64_t stream = policy_evict_first();
+      bulk_g2s(xs, s.h_prev, hb, xbar, stream);
+      bulk_g2s(reinterpret_cast<uint8_t*>(xs) + hb, s.e, hb, xbar, stream);
+      bulk_g2s(c.hs, a.h, hb, xbar, stream);
+      for (int it = first; it < n1; ++it) issue(it);
+    }
+    __syncwarp();
+  } else {
+    const int tid = threadIdx.x, nt = S * 32;
+    if (s.h_r > 0)
+      for (int i = tid; i < ms1 - ms0; i += nt) b2s[i] = __ldg(s.b2 + ms0 + i);
+    for (int i = tid; i < U; i += nt) b1s[i] = __ldg(s.b1 + u0 + i);
+    for (int m = tid; m <= M; m += nt) offs[m] = __ldg(a.offsets + m);
+    mbar_wait(xbar, 0);
+    trace_mark(s.trace, 1);
+    // router layer 1 on this CTA's rows: half row j dots h_prev (j even) or e (j odd) (R4)
+    for (uint32_t kk = 0;; ++kk) {
+      const int it = (int)kk * S + warp;
+      if (it >= n1) break;
+      mbar_wait(&c.full[warp], kk & 1u);
+      const int4 inf = c.info[warp];
+      const T* st = reinterpret_cast<const T*>(c.ring + (size_t)warp * a.stage_bytes);
+      for (int rr = 0; rr < inf.z; rr += 2) {
+        const int j = inf.x + rr;
+        const bool two = rr + 1 < inf.z;
+        const T* w0 = st + (size_t)rr * d;
+        float z0, z1;
+        dot2x<T>(w0, two ? w0 + d : w0, xs + (size_t)(j & 1) * d, xs + (size_t)((j + 1) & 1) * d, d, lane, z0, z1);
+        if (lane == 0) {
+          p1[j] = z0;
+          if (two) p1[j + 1] = z1;
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&c.empty[warp]);
+    }
+  }
+  __syncthreads();  // p1 complete (the producer lane has issued every router row by now)
+  trace_mark(s.trace, 2);
+  cluster_wait_acquire();  // every CTA of the cluster is running: DSMEM stores are safe
+  // a = ReLU(W1 x + b1) for this CTA's units -> a1[] of every CTA in the cluster (linear router:
+  // the units are the scores themselves)
+  {
+    float* dstv = s.h_r > 0 ? a1 : sc;
+    for (int t = threadIdx.x; t < U * Q; t += blockDim.x) {
+      const int u = t / Q, dst = t - u * Q;
+      const float z = (p1[2 * u] + p1[2 * u + 1]) + b1s[u];
+      st_cluster_f32(mapa_u32(smem_u32(dstv + u0 + u), (uint32_t)dst), s.h_r > 0 ? fmaxf(z, 0.f) : z);
+    }
+  }
+  cluster_arrive_release();
+  cluster_wait_acquire();
+  trace_mark(s.trace, 8);
+  if (s.h_r > 0) {  // layer 2 on this CTA's score slice -> every CTA's sc[]
+    if (w2_bytes > 0) mbar_wait(wbar, 0);
+    // lanes per score: h_r / E chunks of 16 bytes, at most 32, a power of two
+    int sub = 32;
+    while (sub > 1 && sub * E > s.h_r) sub >>= 1;
+    const int per_warp = 32 / sub, part = lane % sub, slot = lane / sub;
+    for (int m = ms0 + warp * per_warp + slot; m - slot < ms1; m += nwarps * per_warp) {
+      float acc = 0.f;
+      if (m < ms1) {
+        const T* w = w2s + (size_t)(m - ms0) * s.h_r;
+        for (int j = part * E; j < s.h_r; j += sub * E) {
+          float wf[E];
+          widen16(*reinterpret_cast<const uint4*>(w + j), wf, w);
+#pragma unroll
+          for (int u = 0; u < E; ++u) acc = fmaf(wf[u], a1[j + u], acc);
+        }
+      }
+      for (int o = sub >> 1; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      if (m < ms1) {
+        acc += b2s[m - ms0];
+        for (int dst = part; dst < Q; dst += sub) st_cluster_f32(mapa_u32(smem_u32(sc + m), (uint32_t)dst), acc);
+      }
+    }
+    cluster_arrive_release();
+    cluster_wait_acquire();
+  }
+  trace_mark(s.trace, 12);
+  // TopK_k under (score desc, id asc) (R7): rank this CTA's slice against all M scores
+  // (sub lanes per score), broadcast the winners' flags
+  {
+    const int nsl = ms1 - ms0;
+    int sub = 32;
+    while (sub > 1 && sub * nsl > (int)blockDim.x) sub >>= 1;
+    const int groups = blockDim.x / sub;
+    for (int i0 = 0; i0 < nsl; i0 += groups) {
+      const int i = i0 + threadIdx.x / sub, part = threadIdx.x % sub;
+      const bool act = i < nsl && (int)threadIdx.x < groups * sub;
+      const int m = ms0 + i;
+      const float key = act ? sc[m] + 0.0f : 0.f;
+      int rank = 0;
+      if (act)
+        for (int j = part; j < M; j += sub) {
+          const float o = sc[j] + 0.0f;
+          rank += (o > key) | ((o == key) & (j < m));
+        }
+      for (int o = sub >> 1; o > 0; o >>= 1) rank += __shfl_xor_sync(0xffffffffu, rank, o);
+      if (act && rank < s.k)
+        for (int dst = part; dst < Q; dst += sub)
+          asm volatile("st.shared::cluster.u8 [%0], %1;" ::"r"(mapa_u32(smem_u32(selb + m), (uint32_t)dst)),
+                       "r"(1u)
+                       : "memory");
+    }
+  }
+  cluster_arrive_release();
+  cluster_wait_acquire();
+  trace_mark(s.trace, 13);
+  {
+    const int Mr = (M + 31) & ~31;
+    for (int m = threadIdx.x; m < Mr; m += blockDim.x) {
+      const uint32_t b = __ballot_sync(0xffffffffu, m < M && selb[m] != 0);
+      if (lane == 0) mask[m >> 5] = b;
+    }
+  }
+  __syncthreads();
+  emit_fast(mask, M, offs, sel_s, cnt_s, sloff_s, tmp);
+  __syncthreads();
+  if (cid == 0 && q == 0) {  // the caller's copies of scores / selection / offsets
+    const int cnt = *cnt_s;
+    for (int i = threadIdx.x; i < M; i += blockDim.x) {
+      if (s.scores) s.scores[i] = sc[i];
+      if (i < cnt) s.sel_out[i] = sel_s[i];
+    }
+    for (int i = threadIdx.x; i <= cnt; i += blockDim.x) s.sloff_out[i] = sloff_s[i];
+    if (threadIdx.x == 0) *s.cnt_out = cnt;
+  }
+  trace_mark(s.trace, 3);
+  a.sel = sel_s;
+  a.sel_count = cnt_s;
+  a.sl_off = sloff_s;
+  fence_proxy_async_smem();  // the ring was read by generic loads (W1 rows) before TMA reuses it
+  head_segments(a, c);
+  __syncthreads();
+  trace_mark(s.trace, 4);
+  if (warp == S) {
+    if (lane == 0) head_produce<T>(a, c, (uint32_t)n1);
+  } else {  // logits folded into per-warp (m, s) + a sorted top-K list while the ring streams
+    float m, se;
+    unsigned long long mine;
+    cstep_consume<T>(a, c, warp, lane, n1 > warp ? (uint32_t)((n1 - 1 - warp) / S + 1) : 0u, m, se, mine);
+    if (lane < K) wl[warp * K + lane] = mine;
+    if (lane == 0) {
+      wm[warp] = m;
+      wsum[warp] = se;
+    }
+  }
+  for (int r = threadIdx.x; r < K; r += blockDim.x) out[r] = 0ull;
+  __syncthreads();
+  trace_mark(s.trace, 5);
+  if (a.pdl) pdl_launch_dependents();
+  const int G = (int)gridDim.x, g = (int)blockIdx.x, rec = 2 + K;
+  // CTA record.  Top-K: every warp list entry e = L_w[r] counts the entries of the other lists
+  // that beat it; its rank in the CTA is r + that count (keys are distinct), so all entries are
+  // placed in parallel.  (max, sum): one thread folds the S warp pairs in warp order.
+  if (warp < S && lane < K) {
+    const unsigned long long e = wl[warp * K + lane];
+    if (e != 0ull) {
+      int rank = lane;
+      for (int w2 = 0; w2 < S; ++w2) {  // independent loads: issue-bound, not latency-chained
+        if (w2 == warp) continue;
+        const unsigned long long* L2 = wl + w2 * K;
+#pragma unroll 8
+        for (int j = 0; j < K; ++j) rank += L2[j] > e;
+      }
+      if (rank < K) out[rank] = e;
+    }
+  } else if (warp == S && lane == 0) {
+    float M = -INFINITY;
+    for (int w2 = 0; w2 < S; ++w2) M = fmaxf(M, wm[w2]);
+    float sum = 0.f;
+    if (M > -INFINITY)
+      for (int w2 = 0; w2 < S; ++w2)
+        if (wm[w2] > -INFINITY) sum += wsum[w2] * expf(wm[w2] - M);
+    unsigned long long* my = s.crec + (size_t)g * rec;
+    my[0] = (unsigned long long)__float_as_uint(M);
+    my[1] = (unsigned long long)__float_as_uint(sum);
+  }
+  __syncthreads();
+  for (int r = threadIdx.x; r < K; r += blockDim.x) s.crec[(size_t)g * rec + 2 + r] = out[r];
+  __syncthreads();
+  trace_mark(s.trace, 9);
+  if (threadIdx.x == 0) misc[1] = release_add(s.ctr, 1u) == (unsigned)(G - 1);
+  __syncthreads();
+  trace_mark(s.trace, 6);
+  if (!misc[1]) return;
+  fence_acq_rel_gpu();  // every thread reads the other CTAs' records
+  trace_mark(s.trace, 14);
+
+  // Globally last CTA: merge the G records (CTA order) -> lse, top-k_t.  Scratch: ring.
+  const int GK2 = (G * K + 1) & ~1;
+  unsigned long long* fk = reinterpret_cast<unsigned long long*>(c.ring);  // [G][K]
+  unsigned long long* fsurv = fk + GK2;                                    // [G*K], 16-byte aligned
+  float* fm = reinterpret_cast<float*>(fsurv + GK2);                       // [G]
+  float* fs = fm + G;                                                      // [G]
+  float* wpart = fs + G;                                                   // [32] per-warp partial sums
+  unsigned long long* Tsh = reinterpret_cast<unsigned long long*>(wpart + 32);
+  unsigned* Msh = reinterpret_cast<unsigned*>(Tsh + 1);
+  int* nsh = reinterpret_cast<int*>(Msh + 1);
+  if (threadIdx.x == 0) {
+    *Tsh = 0ull;
+    *Msh = 0u;
+    *nsh = 0;
+  }
+  {  // one batch of independent loads per thread (all records in flight at once)
+    constexpr int kB = 12;
+    const int n = G * rec, nt = blockDim.x;
+    for (int i0 = threadIdx.x; i0 < n; i0 += kB * nt) {
+      unsigned long long v[kB];
+#pragma unroll
+      for (int u = 0; u < kB; ++u) v[u] = i0 + u * nt < n ? __ldcg(s.crec + i0 + u * nt) : 0ull;
+#pragma unroll
+      for (int u = 0; u < kB; ++u) {
+        const int i = i0 + u * nt;
+        if (i < n) {
+          const int gg = i / rec, f = i - gg * rec;
+          if (f == 0) fm[gg] = __uint_as_float((uint32_t)v[u]);
+          else if (f == 1) fs[gg] = __uint_as_float((uint32_t)v[u]);
+          else fk[gg * K + f - 2] = v[u];
+        }
+      }
+    }
+  }
+  __syncthreads();
+  trace_mark(s.trace, 15);
+  // lower bounds on the K-th best key: T1 = best K-th entry of a list, T2 = K-th best list head;
+  // the max score (order-preserving integer key: exact and order-free)
+  for (int t = threadIdx.x; t < G; t += blockDim.x) {
+    unsigned long long lb = fk[t * K + K - 1];
+    if (G >= K) {
+      const unsigned long long h = fk[t * K];
+      int rank = 0;
+#pragma unroll 8
+      for (int j = 0; j < G; ++j) rank += fk[j * K] > h;
+      if (h != 0ull && rank == K - 1) lb = max(lb, h);
+    }
+    if (lb != 0ull) atomicMax(Tsh, lb);
+    if (fm[t] > -INFINITY) atomicMax(Msh, ord_key(fm[t]));
+  }
+  __syncthreads();
+  const unsigned long long Tb = *Tsh;
+  const uint32_t Mk = *Msh;
+  const float Mx = Mk ? __uint_as_float((Mk & 0x80000000u) ? (Mk & 0x7fffffffu) : ~Mk) : -INFINITY;
+  {
+    float part = 0.f;
+    for (int t = threadIdx.x; t < G; t += blockDim.x) {
+      int cnt = 0;  // survivors: the list's prefix >= Tb
+      while (cnt < K && fk[t * K + cnt] != 0ull && fk[t * K + cnt] >= Tb) ++cnt;
+      if (cnt > 0) {
+        const int at = atomicAdd(nsh, cnt);
+        for (int r = 0; r < cnt; ++r) fsurv[at + r] = fk[t * K + r];
+      }
+      if (fm[t] > -INFINITY) part += fs[t] * expf(fm[t] - Mx);
+    }
+    part = warp_sum(part);  // sum_g s_g e^{m_g - M}: xor tree per warp, then warps in order
+    if (lane == 0) wpart[warp] = part;
+  }
+  __syncthreads();
+  const int ns = *nsh;
+  for (int t = threadIdx.x; t < ns; t += blockDim.x) {
+    const unsigned long long x = fsurv[t];
+    int rank = 0;
+#pragma unroll 8
+    for (int j = 0; j < ns; ++j) rank += fsurv[j] > x;
+    if (rank < K) out[rank] = x;
+  }
+  if (threadIdx.x == 0) {
+    float sum = 0.f;
+    for (int w2 = 0; w2 < nwarps; ++w2) sum += wpart[w2];
+    wpart[31] = sum;
+  }
+  __syncthreads();
+  const bool ok = Mx > -INFINITY;
+  const float lse = ok ? Mx + logf(wpart[31]) : __int_as_float(0x7fc00000);
+  for (int r = threadIdx.x; r < K; r += blockDim.x) {
+    const unsigned long long x = out[r];
+    const bool v = ok && x != 0ull;
+    const float z = v ? key_value(x) : -INFINITY;
+    a.top_ids[r] = v ? key_id(x) : -1;
+    a.top_logits[r] = z;
+    a.top_logp[r] = v ? z - lse : -INFINITY;
+  }
+  if (threadIdx.x == 0) {
+    a.lse[0] = lse;
+    *s.ctr = 0u;  // ticket reset for the next launch (ordered after this grid by stream / PDL wait)
+  }
+  trace_mark(s.trace, 7);
+}
+
+// ------------------------------------------------------------------ host side
+
+// Cluster size: DS_CLUSTER_Q (0 disables the cluster step), default 16 (non-portable; one cluster
+// per GPC).  Clusters per launch: the hardware's co-residency limit at one CTA per SM.
+static int cluster_q() {
+  const char* v = getenv("DS_CLUSTER_Q");
+  if (v && v[0]) return atoi(v);
+  return 16;
+}
+
+template <typename T>
+static cudaError_t cstep_configure() {
+  static int done[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (done[dev]) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(cstep_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem_optin());
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(cstep_kernel<T>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  if (e != cudaSuccess) return e;
+  done[dev] = 1;
+  return cudaSuccess;
+}
+
+static int max_clusters(int Q) {
+  static int cache[64][33];
+  static bool init = false;
+  if (!init) {
+    for (auto& row : cache)
+      for (int& x : row) x = -1;
+    init = true;
+  }
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64 || Q < 1 || Q > 32) return 0;
+  if (cache[dev][Q] >= 0) return cache[dev][Q];
+  int n = 0;
+  if (cstep_configure<__nv_bfloat16>() == cudaSuccess) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(Q);
+    cfg.blockDim = dim3((kMaxStages + 1) * 32);
+    cfg.dynamicSmemBytes = max_smem_optin();
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = Q;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (cudaOccupancyMaxActiveClusters(&n, cstep_kernel<__nv_bfloat16>, &cfg) != cudaSuccess) n = 0;
+  }
+  cudaGetLastError();  // a refused query leaves no sticky error
+  cache[dev][Q] = n;
+  return n;
+}
+
+struct CStepPlan {
+  HeadPlan hp;
+  int Q, C, extra, rows1;
+  size_t smem, total;
+};
+
+static bool cstep_plan(const ds_clusters* c, const ds_router* r, int B, int k_t, int64_t max_shortlist, int shared,
+                       CStepPlan* p) {
+  if (B != 1 || shared || k_t > kCStepMaxKt) return false;
+  const int Q = cluster_q();
+  if (Q < 2 || Q > 16) return false;
+  const int C = max_clusters(Q);
+  if (C < 1 || C * Q < 64) return false;  // too few SMs would stream the head slowly
+  p->Q = Q;
+  p->C = C;
+  p->rows1 = r->h_r > 0 ? r->h_r : r->M;
+  const int esz = c->dtype == DS_BF16 ? 2 : 4;
+  const int x0 = (int)cstep_extra(c->d, esz, c->M, r->h_r, p->rows1, Q, k_t, kMaxStages, C).total;
+  if (!head_plan_ex(c, 1, k_t, max_shortlist, x0, 1, &p->hp, C * Q)) return false;
+  // logits never touch shared memory here (online per-warp state): no per-CTA logit buffer, and
+  // the freed bytes go back to the ring
+  p->hp.lcap = 0;
+  const int smax = max_smem_optin();
+  for (int st = kMaxStages; st >= 2; --st) {
+    const int xb = (int)cstep_extra(c->d, esz, c->M, r->h_r, p->rows1, Q, k_t, st, C).total;
+    const size_t sm = head_smem(st, p->hp.stage_bytes, 1, c->d, esz, 0, xb).total;
+    if (sm <= (size_t)smax) {
+      p->hp.stages = st;
+      p->extra = xb;
+      p->smem = sm;
+      break;
+    }
+    if (st == 2) return false;
+  }
+  // the last CTA merges the G records inside its ring
+  const size_t G = (size_t)C * Q;
+  if (G * (16 * k_t + 8) + 256 > (size_t)p->hp.stages * p->hp.stage_bytes) return false;
+  p->total = 256 + align_up(G * (2 + k_t) * sizeof(unsigned long long), 256);
+  return true;
+}
+
+bool cstep_supported(const ds_clusters* c, const ds_router* r, int B, int k_t, int shared, int64_t max_shortlist) {
+  CStepPlan p;
+  return cstep_plan(c, r, B, k_t, max_shortlist, shared, &p);
+}
+
+size_t cstep_ws_bytes(const ds_clusters* c, const ds_router* r, int B, int k_t) {
+  CStepPlan p;
+  return cstep_plan(c, r, B, k_t, 0, 0, &p) ? p.total : 0;
+}
+
+template <typename T>
+static cudaError_t launch_cstep_t(const CStepArgs& s, size_t smem, int Q, int C, cudaStream_t st, bool pdl) {
+  cudaError_t e = cstep_configure<T>();
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(C * Q);
+  cfg.blockDim = dim3((s.h.stages + 1) * 32);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = Q;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 2 : 1;
+  return cudaLaunchKernelEx(&cfg, cstep_kernel<T>, s);
+}
+
+static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+cudaError_t launch_cstep(const ds_clusters* c, const ds_router* r, const void* h_prev, const void* e,
+                         const void* h_new, int k, int k_t, int64_t max_shortlist, float* scores, int32_t* sel,
+                         int32_t* sel_count, int32_t* sl_offsets, int32_t* top_ids, float* top_logits,
+                         float* top_logp, float* lse, float* z_out, int64_t z_stride, void* ws, cudaStream_t st,
+                         bool pdl) {
+  CStepPlan p;
+  if (!cstep_plan(c, r, 1, k_t, max_shortlist, 0, &p)) return cudaErrorInvalidValue;
+  uint8_t* w8 = static_cast<uint8_t*>(ws);
+  CStepArgs s;
+  fill_head_args(s.h, c, p.hp, h_new, 0, 1, sel, sel_count, sl_offsets, 0, k_t, max_shortlist, top_ids, top_logits,
+                 top_logp, lse, z_out, z_stride, nullptr, reinterpret_cast<unsigned*>(w8), pdl);
+  s.W1 = r->W1;
+  s.b1 = r->b1;
+  s.W2 = r->W2;
+  s.b2 = r->b2;
+  s.h_prev = h_prev;
+  s.e = e;
+  s.scores = scores;
+  s.sel_out = sel;
+  s.cnt_out = sel_count;
+  s.sloff_out = sl_offsets;
+  s.h_r = r->h_r;
+  s.rows1 = p.rows1;
+  s.k = k;
+  s.extra_bytes = p.extra;
+  s.crec = reinterpret_cast<unsigned long long*>(w8 + 256);
+  s.ctr = reinterpret_cast<unsigned*>(w8);
+  s.trace = debug_trace();
+  return c->dtype == DS_BF16 ? launch_cstep_t<__nv_bfloat16>(s, p.smem, p.Q, p.C, st, pdl)
+                             : launch_cstep_t<float>(s, p.smem, p.Q, p.C, st, pdl);
+}
+
+bool cstep_pointers_ok(const ds_router* r, const void* h_prev, const void* e, const void* h_new) {
+  return aligned16(h_prev) && aligned16(e) && aligned16(h_new) && aligned16(r->W1) &&
+         (r->h_r == 0 || aligned16(r->W2));
+}
+
+}  // namespace ds

@@ -49,13 +49,13 @@ int max_smem_optin() {
 }
 
 bool head_plan_ex(const ds_clusters* c, int B, int k_t, int64_t max_shortlist, int extra, int max_rows,
-                  HeadPlan* p) {
+                  HeadPlan* p, int G) {
   const int esz = c->dtype == DS_BF16 ? 2 : 4;
   const int rowbytes = c->d * esz;
   if (rowbytes > 2 * kStageTarget || (rowbytes % 16) != 0) return false;
   p->stage_rows = std::max(1, kStageTarget / rowbytes);
   p->stage_bytes = p->stage_rows * rowbytes;
-  p->G = num_sms();
+  p->G = G > 0 ? G : num_sms();
   const int64_t ms = (max_shortlist > 0 && max_shortlist < c->V) ? max_shortlist : c->V;
   p->lcap = (int)((ms + p->G - 1) / p->G);
   p->rec = 2 + 2 * k_t;

@@ -177,13 +177,13 @@ __device__ __forceinline__ void head_segments(const HeadArgs& a, const HeadCtx& 
 
 // Producer (one lane): stream every segment as runs of whole rows, slot it % stages.
 template <typename T>
-__device__ void head_produce(const HeadArgs& a, const HeadCtx& c) {
+__device__ void head_produce(const HeadArgs& a, const HeadCtx& c, uint32_t it0 = 0) {
   const uint64_t pol = policy_evict_first();
   const uint32_t rowbytes = (uint32_t)a.d * (uint32_t)sizeof(T);
   const uint8_t* W = static_cast<const uint8_t*>(a.W);
   const int ngroups = a.shared ? 1 : a.nrows;
   const uint32_t S = (uint32_t)a.stages;
-  uint32_t it = 0;
+  uint32_t it = it0;  // ring iterations already used by this launch (the cluster step's router rows)
   for (int gi = 0; gi < ngroups; ++gi) {
     const int nseg = c.segn[gi];
     if (nseg <= 0) continue;
@@ -252,9 +252,9 @@ __device__ __forceinline__ void dot2(const T* __restrict__ w0, const T* __restri
 
 // Consumer warp `w` owns ring slot `w`.
 template <typename T>
-__device__ void head_consume(const HeadArgs& a, const HeadCtx& c, int w, int lane) {
+__device__ void head_consume(const HeadArgs& a, const HeadCtx& c, int w, int lane, uint32_t k0 = 0) {
   const T* hs = static_cast<const T*>(c.hs);
-  for (uint32_t k = 0;; ++k) {
+  for (uint32_t k = k0;; ++k) {
     mbar_wait(&c.full[w], k & 1u);
     const int4 inf = c.info[w];
     if (inf.z < 0) break;

@@ -48,7 +48,7 @@ struct HeadPlan {
 };
 bool head_plan(const ds_clusters* c, int B, int k_t, int64_t max_shortlist, HeadPlan* p);
 bool head_plan_ex(const ds_clusters* c, int B, int k_t, int64_t max_shortlist, int extra_smem, int max_rows,
-                  HeadPlan* p);
+                  HeadPlan* p, int G = 0 /* CTAs per launch; 0 = one per SM */);
 int max_smem_optin();
 cudaError_t launch_head(const ds_clusters* c, const HeadPlan& p, const void* h_new, int B, const int32_t* sel,
                         const int32_t* sel_count, const int32_t* sl_offsets, int shared, int k_t,
@@ -64,6 +64,16 @@ cudaError_t launch_step(const ds_clusters* c, const ds_router* r, const void* h_
                         int32_t* sel, int32_t* sel_count, int32_t* sl_offsets, int32_t* top_ids, float* top_logits,
                         float* top_logp, float* lse, float* z_out, int64_t z_stride, void* ws, cudaStream_t st,
                         bool pdl);
+
+// ---- cluster draft step (cstep.cu): B = 1, router per thread-block cluster (DSMEM), no grid barrier
+bool cstep_supported(const ds_clusters* c, const ds_router* r, int B, int k_t, int shared, int64_t max_shortlist);
+size_t cstep_ws_bytes(const ds_clusters* c, const ds_router* r, int B, int k_t);
+bool cstep_pointers_ok(const ds_router* r, const void* h_prev, const void* e, const void* h_new);  // 16 B TMA
+cudaError_t launch_cstep(const ds_clusters* c, const ds_router* r, const void* h_prev, const void* e,
+                         const void* h_new, int k, int k_t, int64_t max_shortlist, float* scores, int32_t* sel,
+                         int32_t* sel_count, int32_t* sl_offsets, int32_t* top_ids, float* top_logits,
+                         float* top_logp, float* lse, float* z_out, int64_t z_stride, void* ws, cudaStream_t st,
+                         bool pdl);
 
 // ---- tcgen05 shared-shortlist head (tc_head.cu), bf16, R <= 64 rows sharing one shortlist
 bool tc_head_supported(const ds_clusters* c, int R, int k_t, int64_t max_shortlist);

@@ -309,7 +309,7 @@ bool step_supported(const ds_clusters* c, const ds_router* r, int B, int k_t, in
 size_t step_ws_bytes(const ds_clusters* c, const ds_router* r, int B, int k_t) {
   StepPlan p;
   if (!step_plan(c, r, B, k_t, 0, 0, &p) && !step_plan(c, r, B, k_t, 0, 1, &p)) return 0;
-  return p.total;
+  return std::max(p.total, cstep_ws_bytes(c, r, B, k_t));
 }
 
 template <typename T>
@@ -339,6 +339,10 @@ cudaError_t launch_step(const ds_clusters* c, const ds_router* r, const void* h_
                         int32_t* sel, int32_t* sel_count, int32_t* sl_offsets, int32_t* top_ids, float* top_logits,
                         float* top_logp, float* lse, float* z_out, int64_t z_stride, void* ws, cudaStream_t st,
                         bool pdl) {
+  // B = 1: the cluster step (cstep.cu) needs no grid-wide barrier before the head streams
+  if (cstep_supported(c, r, B, k_t, shared, max_shortlist) && cstep_pointers_ok(r, h_prev, e, h_new))
+    return launch_cstep(c, r, h_prev, e, h_new, k, k_t, max_shortlist, scores, sel, sel_count, sl_offsets, top_ids,
+                        top_logits, top_logp, lse, z_out, z_stride, ws, st, pdl);
   StepPlan p;
   if (!step_plan(c, r, B, k_t, max_shortlist, shared, &p)) return cudaErrorInvalidValue;
   uint8_t* w8 = static_cast<uint8_t*>(ws);

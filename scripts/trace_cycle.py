@@ -24,6 +24,10 @@ flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
 names = ["start", "pdl", "phaseA", "sel_vis", "segs", "streamed", "partials", "merged", "B:ctrA", "B:w2", "B:pub",
          "B:hid", "B:out", "B:rank", "ticket", "ticket+1", "M:load",
          "M:lse", "M:thr", "M:surv", "M:done"]
+CSTEP = os.environ.get("DS_CLUSTER_Q", "16") != "0"
+if CSTEP:  # cluster step (cstep.cu) mark slots
+    names = ["start", "pdl", "L1done", "sel", "segs", "streamed", "counted", "merged", "a1_bar", "cta_rec",
+             "-", "-", "sc_bar", "rank", "last", "recs_read", "fin_merge", "-", "-", "-", "-"]
 inp = [[x.to(dev) for x in S.step_inputs(1, C.d, t, "bf16")] for t in range(C.positions)]
 for rep in range(3):
     flush.zero_()
@@ -44,11 +48,16 @@ for t in range(C.positions):
     for i, n in enumerate(names):
         col = a[:, i]
         col = col[col > 0]
-        if col.size:
+        if col.size and n != "-":
             print(f"  {n:9s} n={col.size:3d} min={1e-3*(col.min()-t0):8.2f} med={1e-3*(np.median(col)-t0):8.2f} "
                   f"max={1e-3*(col.max()-t0):8.2f} us")
     cy = bufs[t].view(G, 64).cpu().numpy().astype(np.float64)[:, 32:]
     last = np.argmax(a[:, 7])
-    print("  last-CTA cycles between marks:", {names[i]: int(cy[last, i] - cy[last, 14]) for i in (15, 16, 17, 19, 20, 7)
-                                               if cy[last, i] > 0})
+    if CSTEP:  # cluster step: per-CTA SM-cycle deltas from 'start' (median over CTAs)
+        ok = cy[:, 0] > 0
+        print("  median SM cycles since start:", {n: int(np.median(cy[ok & (cy[:, i] > 0), i] - cy[ok & (cy[:, i] > 0), 0]))
+                                                  for i, n in enumerate(names) if n != "-" and (cy[ok, i] > 0).any()})
+    if not CSTEP:
+        print("  last-CTA cycles between marks:", {names[i]: int(cy[last, i] - cy[last, 14])
+                                                   for i in (15, 16, 17, 19, 20, 7) if cy[last, i] > 0})
     t_prev_end = a[:, 7][a[:, 7] > 0].max()
