@@ -16,8 +16,9 @@
 //     id asc), R7) and broadcasts the selected ids; every CTA then forms the ascending
 //     selection and shortlist offsets (R8) locally.  The scores are bit-identical in every
 //     cluster (same code, same order), so all clusters agree on the shortlist.
-// The gathered head streams the CTA's segment through the TMA ring of head_impl.cuh; each
-// consumer warp folds its logits into an online (max, sum exp) and a lane-distributed sorted
+// The gathered head: CTA g streams segment g of the shortlist through the TMA ring of
+// head_impl.cuh, its producer lane deriving the segment from the TopK mask (no block-wide prefix
+// sum on the critical path); each consumer warp folds its logits into an online (max, sum exp) and a lane-distributed sorted
 // top-k_t list while the next slots are in flight.  Lists are merged in two levels
 // without float atomics (R19): the CTA's warps, then the last CTA to take the global ticket merges
 // the G per-CTA records (CTA order).
@@ -47,6 +48,8 @@ struct CStepArgs {
   int32_t h_r, rows1, k, extra_bytes;
   unsigned long long* crec;  // [G][2 + k_t] per-CTA records: max, sum (float bits), then k_t keys
   unsigned* ctr;             // [0] ticket over CTAs
+  unsigned long long* gT;    // running grid-wide lower bound on the K-th best key (atomicMax)
+  unsigned* gM;              // running max of the CTAs' max logits (order-preserving key, atomicMax)
   unsigned long long* trace;
 };
 
@@ -80,7 +83,7 @@ __host__ __device__ inline CExtra cstep_extra(int d, int esz, int M, int h_r, in
   X.tmp = take(4u * M);
   X.wm = take(4u * S);
   X.ws = take(4u * S);
-  X.wl = take(8u * S * K);
+  X.wl = take(16u * S * K);
   X.surv = take(8u * S * K);
   X.out = take(8u * K);
   X.misc = take(64);
@@ -149,6 +152,68 @@ __device__ __forceinline__ void dot2x(const T* __restrict__ w0, const T* __restr
   z1 = warp_sum(b0 + b1);
 }
 
+// Producer warp: the CTA's segment [N g / G, N (g+1) / G) of the virtual shortlist (the selected
+// clusters in ascending id, R8; N = |V_S| = sum of their sizes), streamed by lane 0 as runs
+// of whole W_perm rows.  The 32 lanes derive N and the segment start from the TopK mask (lane j:
+// mask word j, one warp scan), so no block-wide prefix sum sits between the selection and the first
+// TMA copy.  info = (-, virtual shortlist position, rows, first W_perm row).
+template <typename T>
+__device__ void cstep_produce(const HeadArgs& a, const HeadCtx& c, const uint32_t* mask, const int32_t* offs, int g,
+                              int G, uint32_t it0) {
+  const int lane = threadIdx.x & 31;
+  const int words = (a.M + 31) >> 5;  // <= 32 (M <= 1024)
+  const uint32_t mybits = lane < words ? mask[lane] : 0u;
+  long long wsum = 0;
+  for (uint32_t b = mybits; b; b &= b - 1u) {
+    const int m = (lane << 5) + __ffs(b) - 1;
+    wsum += offs[m + 1] - offs[m];
+  }
+  long long inc = wsum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const long long y = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += y;
+  }
+  const long long N = __shfl_sync(0xffffffffu, inc, 31);
+  const long long s0 = N * g / G, s1 = N * (g + 1) / G;
+  const uint32_t past = __ballot_sync(0xffffffffu, inc > s0);  // words ending after s0
+  const int w0 = past ? __ffs(past) - 1 : 32;
+  const long long vstart = __shfl_sync(0xffffffffu, inc - wsum, w0 & 31);
+  if (lane != 0) return;
+  const uint64_t pol = policy_evict_first();
+  const uint32_t rowbytes = (uint32_t)a.d * (uint32_t)sizeof(T);
+  const uint8_t* W = static_cast<const uint8_t*>(a.W);
+  const uint32_t S = (uint32_t)a.stages;
+  uint32_t it = it0;
+  long long vpos = vstart;  // virtual position of the current cluster's first row
+  for (int w = w0; w < words && vpos < s1 && s0 < s1; ++w) {
+    for (uint32_t bits = mask[w]; bits && vpos < s1; bits &= bits - 1u) {
+      const int m = (w << 5) + __ffs(bits) - 1;
+      const int beg = offs[m], sz = offs[m + 1] - beg;
+      const long long lo = max(s0, vpos), hi = min(s1, vpos + sz);
+      for (long long p = lo; p < hi;) {
+        const int n = (int)min((long long)a.stage_rows, hi - p);
+        const int row = beg + (int)(p - vpos);
+        const uint32_t sl = it % S;
+        mbar_wait(&c.empty[sl], ((it / S) & 1u) ^ 1u);
+        c.info[sl] = make_int4(0, (int)p, n, row);
+        mbar_arrive_expect_tx(&c.full[sl], (uint32_t)n * rowbytes);
+        bulk_g2s(c.ring + (size_t)sl * a.stage_bytes, W + (size_t)row * rowbytes, (uint32_t)n * rowbytes,
+                 &c.full[sl], pol);
+        ++it;
+        p += n;
+      }
+      vpos += sz;
+    }
+  }
+  for (uint32_t j = 0; j < S; ++j, ++it) {  // one end-of-stream marker per slot
+    const uint32_t sl = it % S;
+    mbar_wait(&c.empty[sl], ((it / S) & 1u) ^ 1u);
+    c.info[sl] = make_int4(-1, 0, -1, 0);
+    mbar_arrive(&c.full[sl]);
+  }
+}
+
 // Consumer warp `w` (ring slot w): gathered-head logits of the CTA's segment folded on the fly into
 // (m, s) and the warp's sorted top-K list.
 template <typename T>
@@ -165,7 +230,7 @@ __device__ __forceinline__ void cstep_consume(const HeadArgs& a, const HeadCtx& 
     const int4 inf = c.info[w];
     if (inf.z < 0) break;
     const T* st = reinterpret_cast<const T*>(c.ring + (size_t)w * a.stage_bytes);
-    const long long zbase = c.sega[0] + inf.y;
+    const long long zbase = inf.y;  // virtual shortlist position of the slot's first row
     for (int rr = 0; rr < inf.z; rr += 2) {
       const bool two = rr + 1 < inf.z;
       const int tok0 = __ldg(a.perm + inf.w + rr);
@@ -383,27 +448,10 @@ __global__ void __launch_bounds__((kMaxStages + 1) * 32, 1) cstep_kernel(const C
     }
   }
   __syncthreads();
-  emit_fast(mask, M, offs, sel_s, cnt_s, sloff_s, tmp);
-  __syncthreads();
-  if (cid == 0 && q == 0) {  // the caller's copies of scores / selection / offsets
-    const int cnt = *cnt_s;
-    for (int i = threadIdx.x; i < M; i += blockDim.x) {
-      if (s.scores) s.scores[i] = sc[i];
-      if (i < cnt) s.sel_out[i] = sel_s[i];
-    }
-    for (int i = threadIdx.x; i <= cnt; i += blockDim.x) s.sloff_out[i] = sloff_s[i];
-    if (threadIdx.x == 0) *s.cnt_out = cnt;
-  }
-  trace_mark(s.trace, 3);
-  a.sel = sel_s;
-  a.sel_count = cnt_s;
-  a.sl_off = sloff_s;
   fence_proxy_async_smem();  // the ring was read by generic loads (W1 rows) before TMA reuses it
-  head_segments(a, c);
-  __syncthreads();
   trace_mark(s.trace, 4);
   if (warp == S) {
-    if (lane == 0) head_produce<T>(a, c, (uint32_t)n1);
+    cstep_produce<T>(a, c, mask, offs, (int)blockIdx.x, (int)gridDim.x, (uint32_t)n1);
   } else {  // logits folded into per-warp (m, s) + a sorted top-K list while the ring streams
     float m, se;
     unsigned long long mine;
@@ -417,36 +465,79 @@ __global__ void __launch_bounds__((kMaxStages + 1) * 32, 1) cstep_kernel(const C
   for (int r = threadIdx.x; r < K; r += blockDim.x) out[r] = 0ull;
   __syncthreads();
   trace_mark(s.trace, 5);
+  if (cid == 0 && q == 0) {  // the caller's copies of scores / selection / offsets (S3 outputs)
+    emit_fast(mask, M, offs, sel_s, cnt_s, sloff_s, tmp);
+    __syncthreads();
+    const int cnt = *cnt_s;
+    for (int i = threadIdx.x; i < M; i += blockDim.x) {
+      if (s.scores) s.scores[i] = sc[i];
+      if (i < cnt) s.sel_out[i] = sel_s[i];
+    }
+    for (int i = threadIdx.x; i <= cnt; i += blockDim.x) s.sloff_out[i] = sloff_s[i];
+    if (threadIdx.x == 0) *s.cnt_out = cnt;
+  }
   if (a.pdl) pdl_launch_dependents();
   const int G = (int)gridDim.x, g = (int)blockIdx.x, rec = 2 + K;
-  // CTA record.  Top-K: every warp list entry e = L_w[r] counts the entries of the other lists
-  // that beat it; its rank in the CTA is r + that count (keys are distinct), so all entries are
-  // placed in parallel.  (max, sum): one thread folds the S warp pairs in warp order.
-  if (warp < S && lane < K) {
-    const unsigned long long e = wl[warp * K + lane];
-    if (e != 0ull) {
-      int rank = lane;
-      for (int w2 = 0; w2 < S; ++w2) {  // independent loads: issue-bound, not latency-chained
-        if (w2 == warp) continue;
-        const unsigned long long* L2 = wl + w2 * K;
-#pragma unroll 8
-        for (int j = 0; j < K; ++j) rank += L2[j] > e;
-      }
-      if (rank < K) out[rank] = e;
-    }
-  } else if (warp == S && lane == 0) {
+  // CTA record = (max, sum) of its logits + its CANDIDATES for the global top-K: the warp-list
+  // entries >= Tb, where Tb is the best lower bound on the global K-th best known here (a warp
+  // list's K-th entry; the running grid-wide bound gT, raised by every CTA that published before).
+  // No ranking unless more than K entries pass (then the CTA keeps its best K), so the last CTAs —
+  // the critical path — publish almost nothing.
+  unsigned long long* Tb_s = reinterpret_cast<unsigned long long*>(misc + 8);  // misc[8..9]
+  if (threadIdx.x == 0) {
+    unsigned long long own = 0ull;
+    for (int w2 = 0; w2 < S; ++w2) own = max(own, wl[w2 * K + K - 1]);
+    Tb_s[1] = own;
+    Tb_s[0] = max(own, ld_relaxed_u64(s.gT));
+  } else if (threadIdx.x == 32) {  // (max, sum exp) of the warps, folded in warp order
     float M = -INFINITY;
     for (int w2 = 0; w2 < S; ++w2) M = fmaxf(M, wm[w2]);
     float sum = 0.f;
     if (M > -INFINITY)
       for (int w2 = 0; w2 < S; ++w2)
         if (wm[w2] > -INFINITY) sum += wsum[w2] * expf(wm[w2] - M);
-    unsigned long long* my = s.crec + (size_t)g * rec;
-    my[0] = (unsigned long long)__float_as_uint(M);
-    my[1] = (unsigned long long)__float_as_uint(sum);
+    reinterpret_cast<float*>(misc)[4] = M;
+    reinterpret_cast<float*>(misc)[5] = sum;
   }
   __syncthreads();
-  for (int r = threadIdx.x; r < K; r += blockDim.x) s.crec[(size_t)g * rec + 2 + r] = out[r];
+  {
+    const unsigned long long Tb = Tb_s[0];
+    unsigned long long* cand = wl + S * K;  // scratch after the lists (X.wl holds 2 S K keys)
+    const int n = S * K;
+    for (int i0 = 0; i0 < n; i0 += blockDim.x) {
+      const int i = i0 + threadIdx.x;
+      const unsigned long long x = i < n ? wl[i] : 0ull;
+      const bool keep = x != 0ull && x >= Tb;
+      const uint32_t bal = __ballot_sync(0xffffffffu, keep);
+      int base = 0;
+      if (lane == 0 && bal) base = atomicAdd(&misc[3], __popc(bal));
+      base = __shfl_sync(0xffffffffu, base, 0);
+      if (keep) cand[base + __popc(bal & ((1u << lane) - 1u))] = x;
+    }
+    __syncthreads();
+    const int nc = misc[3];
+    unsigned long long* my = s.crec + (size_t)g * rec;
+    if (nc <= K) {
+      for (int r = threadIdx.x; r < K; r += blockDim.x) my[2 + r] = r < nc ? cand[r] : 0ull;
+    } else {  // keep the CTA's best K candidates (rank count; keys are distinct)
+      for (int t = threadIdx.x; t < nc; t += blockDim.x) {
+        const unsigned long long x = cand[t];
+        int rank = 0;
+#pragma unroll 8
+        for (int j = 0; j < nc; ++j) rank += cand[j] > x;
+        if (rank < K) my[2 + rank] = x;
+        if (rank == K - 1) Tb_s[1] = max(Tb_s[1], x);  // the CTA's own K-th best: a global lower bound
+      }
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+      const float M = reinterpret_cast<float*>(misc)[4], sum = reinterpret_cast<float*>(misc)[5];
+      my[0] = (unsigned long long)__float_as_uint(M) | ((unsigned long long)__float_as_uint(sum) << 32);
+      my[1] = (unsigned long long)min(nc, K);
+      if (Tb_s[1] != 0ull) atomicMax(s.gT, Tb_s[1]);
+      if (M > -INFINITY) atomicMax(s.gM, ord_key(M));
+    }
+  }
   __syncthreads();
   trace_mark(s.trace, 9);
   if (threadIdx.x == 0) misc[1] = release_add(s.ctr, 1u) == (unsigned)(G - 1);
@@ -456,72 +547,85 @@ __global__ void __launch_bounds__((kMaxStages + 1) * 32, 1) cstep_kernel(const C
   fence_acq_rel_gpu();  // every thread reads the other CTAs' records
   trace_mark(s.trace, 14);
 
-  // Globally last CTA: merge the G records (CTA order) -> lse, top-k_t.  Scratch: ring.
+  // Globally last CTA: every global top-K member is among the records' candidates (it passed its
+  // CTA's bound, itself <= the K-th best); keep those >= the final bound, rank them; lse over the
+  // G (max, sum) pairs in CTA order.  Scratch: the ring.
   const int GK2 = (G * K + 1) & ~1;
   unsigned long long* fk = reinterpret_cast<unsigned long long*>(c.ring);  // [G][K]
-  unsigned long long* fsurv = fk + GK2;                                    // [G*K], 16-byte aligned
+  unsigned long long* fsurv = fk + GK2;                                    // [G*K]
   float* fm = reinterpret_cast<float*>(fsurv + GK2);                       // [G]
   float* fs = fm + G;                                                      // [G]
-  float* wpart = fs + G;                                                   // [32] per-warp partial sums
-  unsigned long long* Tsh = reinterpret_cast<unsigned long long*>(wpart + 32);
-  unsigned* Msh = reinterpret_cast<unsigned*>(Tsh + 1);
-  int* nsh = reinterpret_cast<int*>(Msh + 1);
-  if (threadIdx.x == 0) {
-    *Tsh = 0ull;
-    *Msh = 0u;
-    *nsh = 0;
-  }
+  float* wpart = fs + G;                                                   // [32]
+  int* nsh = reinterpret_cast<int*>(wpart + 32);                          // [0] count, [2..3] T2
+  if (threadIdx.x == 0) *nsh = 0;
+  unsigned long long Tfin = 0ull;
+  uint32_t Mk = 0u;
   {  // one batch of independent loads per thread (all records in flight at once)
     constexpr int kB = 12;
-    const int n = G * rec, nt = blockDim.x;
-    for (int i0 = threadIdx.x; i0 < n; i0 += kB * nt) {
+    const int nrec = G * rec, nt = blockDim.x;
+    Tfin = ld_relaxed_u64(s.gT);
+    Mk = *reinterpret_cast<volatile unsigned*>(s.gM);
+    for (int i0 = threadIdx.x; i0 < nrec; i0 += kB * nt) {
       unsigned long long v[kB];
 #pragma unroll
-      for (int u = 0; u < kB; ++u) v[u] = i0 + u * nt < n ? __ldcg(s.crec + i0 + u * nt) : 0ull;
+      for (int u = 0; u < kB; ++u) v[u] = i0 + u * nt < nrec ? __ldcg(s.crec + i0 + u * nt) : 0ull;
 #pragma unroll
       for (int u = 0; u < kB; ++u) {
         const int i = i0 + u * nt;
-        if (i < n) {
+        if (i < nrec) {
           const int gg = i / rec, f = i - gg * rec;
-          if (f == 0) fm[gg] = __uint_as_float((uint32_t)v[u]);
-          else if (f == 1) fs[gg] = __uint_as_float((uint32_t)v[u]);
-          else fk[gg * K + f - 2] = v[u];
+          if (f == 0) {
+            fm[gg] = __uint_as_float((uint32_t)v[u]);
+            fs[gg] = __uint_as_float((uint32_t)(v[u] >> 32));
+          } else if (f >= 2) {
+            fk[gg * K + f - 2] = v[u];
+          }
         }
       }
     }
   }
   __syncthreads();
   trace_mark(s.trace, 15);
-  // lower bounds on the K-th best key: T1 = best K-th entry of a list, T2 = K-th best list head;
-  // the max score (order-preserving integer key: exact and order-free)
+  // T2 = the K-th best of the records' best candidates (K distinct keys >= it): with T1 this leaves
+  // about K survivors instead of every candidate above the weaker T1
+  unsigned long long* heads = fsurv;  // scratch until the compaction below
+  unsigned long long* T2s = reinterpret_cast<unsigned long long*>(nsh + 2);
+  if (threadIdx.x == 0) *T2s = 0ull;
   for (int t = threadIdx.x; t < G; t += blockDim.x) {
-    unsigned long long lb = fk[t * K + K - 1];
-    if (G >= K) {
-      const unsigned long long h = fk[t * K];
-      int rank = 0;
-#pragma unroll 8
-      for (int j = 0; j < G; ++j) rank += fk[j * K] > h;
-      if (h != 0ull && rank == K - 1) lb = max(lb, h);
-    }
-    if (lb != 0ull) atomicMax(Tsh, lb);
-    if (fm[t] > -INFINITY) atomicMax(Msh, ord_key(fm[t]));
+    unsigned long long h = 0ull;
+#pragma unroll 4
+    for (int r = 0; r < K; ++r) h = max(h, fk[t * K + r]);
+    heads[t] = h;
   }
   __syncthreads();
-  const unsigned long long Tb = *Tsh;
-  const uint32_t Mk = *Msh;
+  if (G >= K)
+    for (int t = threadIdx.x; t < G; t += blockDim.x) {
+      const unsigned long long h = heads[t];
+      int rank = 0;
+#pragma unroll 8
+      for (int j = 0; j < G; ++j) rank += heads[j] > h;
+      if (h != 0ull && rank == K - 1) *T2s = h;
+    }
+  __syncthreads();
+  Tfin = max(Tfin, *T2s);
+  __syncthreads();  // heads (in fsurv) consumed before the compaction overwrites them
   const float Mx = Mk ? __uint_as_float((Mk & 0x80000000u) ? (Mk & 0x7fffffffu) : ~Mk) : -INFINITY;
   {
-    float part = 0.f;
-    for (int t = threadIdx.x; t < G; t += blockDim.x) {
-      int cnt = 0;  // survivors: the list's prefix >= Tb
-      while (cnt < K && fk[t * K + cnt] != 0ull && fk[t * K + cnt] >= Tb) ++cnt;
-      if (cnt > 0) {
-        const int at = atomicAdd(nsh, cnt);
-        for (int r = 0; r < cnt; ++r) fsurv[at + r] = fk[t * K + r];
-      }
-      if (fm[t] > -INFINITY) part += fs[t] * expf(fm[t] - Mx);
+    const int n = G * K;
+    for (int i0 = 0; i0 < n; i0 += blockDim.x) {
+      const int i = i0 + threadIdx.x;
+      const unsigned long long x = i < n ? fk[i] : 0ull;
+      const bool keep = x != 0ull && x >= Tfin;
+      const uint32_t bal = __ballot_sync(0xffffffffu, keep);
+      int base = 0;
+      if (lane == 0 && bal) base = atomicAdd(nsh, __popc(bal));
+      base = __shfl_sync(0xffffffffu, base, 0);
+      if (keep) fsurv[base + __popc(bal & ((1u << lane) - 1u))] = x;
     }
-    part = warp_sum(part);  // sum_g s_g e^{m_g - M}: xor tree per warp, then warps in order
+    float part = 0.f;  // sum_g s_g e^{m_g - M}: xor tree per warp, then the warps in order
+    for (int t = threadIdx.x; t < G; t += blockDim.x)
+      if (fm[t] > -INFINITY) part += fs[t] * expf(fm[t] - Mx);
+    part = warp_sum(part);
     if (lane == 0) wpart[warp] = part;
   }
   __syncthreads();
@@ -551,7 +655,9 @@ __global__ void __launch_bounds__((kMaxStages + 1) * 32, 1) cstep_kernel(const C
   }
   if (threadIdx.x == 0) {
     a.lse[0] = lse;
-    *s.ctr = 0u;  // ticket reset for the next launch (ordered after this grid by stream / PDL wait)
+    *s.ctr = 0u;  // reset for the next launch (ordered after this grid by stream / PDL wait)
+    *s.gT = 0ull;
+    *s.gM = 0u;
   }
   trace_mark(s.trace, 7);
 }
@@ -714,6 +820,8 @@ cudaError_t launch_cstep(const ds_clusters* c, const ds_router* r, const void* h
   s.extra_bytes = p.extra;
   s.crec = reinterpret_cast<unsigned long long*>(w8 + 256);
   s.ctr = reinterpret_cast<unsigned*>(w8);
+  s.gT = reinterpret_cast<unsigned long long*>(w8 + 64);
+  s.gM = reinterpret_cast<unsigned*>(w8 + 72);
   s.trace = debug_trace();
   return c->dtype == DS_BF16 ? launch_cstep_t<__nv_bfloat16>(s, p.smem, p.Q, p.C, st, pdl)
                              : launch_cstep_t<float>(s, p.smem, p.Q, p.C, st, pdl);

@@ -13,7 +13,7 @@ from ctypes import c_int32, c_int64, c_size_t, c_uint64, c_void_p, POINTER
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libdynaspec.so")
+LIB_PATH = os.environ.get("DS_LIB_PATH") or os.path.join(_HERE, "lib", "libdynaspec.so")  # override: A/B builds
 
 DS_BF16, DS_F32 = 0, 1
 _DTYPE = {torch.bfloat16: DS_BF16, torch.float32: DS_F32}
