@@ -46,10 +46,9 @@ struct CStepArgs {
   int32_t* cnt_out;        // [1]
   int32_t* sloff_out;      // [M+1]
   int32_t h_r, rows1, k, extra_bytes;
-  unsigned long long* crec;  // [G][2 + k_t] per-CTA records: max, sum (float bits), then k_t keys
-  unsigned* ctr;             // [0] ticket over CTAs
-  unsigned long long* gT;    // running grid-wide lower bound on the K-th best key (atomicMax)
-  unsigned* gM;              // running max of the CTAs' max logits (order-preserving key, atomicMax)
+  unsigned long long* crec;  // [G][2 + k_t] per-CTA records (max | sum, count + 1, k_t keys); 0 = not yet
+                             // written (the merger zeroes them after reading)
+  unsigned* ctr;             // unused (the merger polls the records)
   unsigned long long* trace;
 };
 
@@ -305,7 +304,7 @@ __global__ void __launch_bounds__((kMaxStages + 1) * 32, 1) cstep_kernel(const C
     fence_mbar_init();
   }
   for (int m = threadIdx.x; m < M; m += blockDim.x) selb[m] = 0;
-  if (threadIdx.x < 8) misc[threadIdx.x] = 0;
+  if (threadIdx.x < 16) misc[threadIdx.x] = 0;
   __syncthreads();
   cluster_arrive_relaxed();  // paired with the wait before the first DSMEM store
   trace_mark(s.trace, 0);
@@ -478,18 +477,20 @@ __global__ void __launch_bounds__((kMaxStages + 1) * 32, 1) cstep_kernel(const C
   }
   if (a.pdl) pdl_launch_dependents();
   const int G = (int)gridDim.x, g = (int)blockIdx.x, rec = 2 + K;
-  // CTA record = (max, sum) of its logits + its CANDIDATES for the global top-K: the warp-list
-  // entries >= Tb, where Tb is the best lower bound on the global K-th best known here (a warp
-  // list's K-th entry; the running grid-wide bound gT, raised by every CTA that published before).
-  // No ranking unless more than K entries pass (then the CTA keeps its best K), so the last CTAs —
-  // the critical path — publish almost nothing.
+  // CTA record = (max, sum) of its logits + its best min(nc, K) candidates for the global top-K.
+  // Candidates: the warp-list entries >= Tb, Tb = max(best K-th entry of a warp list, K-th best warp
+  // head) — both have K keys above them, so Tb <= the CTA's (and the grid's) K-th best.  Record words
+  // are never 0 (padding = 1, below every key: a key's low word ~id has bit 31 set), so the merger
+  // polls the data itself: no fence, no ticket.
   unsigned long long* Tb_s = reinterpret_cast<unsigned long long*>(misc + 8);  // misc[8..9]
-  if (threadIdx.x == 0) {
-    unsigned long long own = 0ull;
-    for (int w2 = 0; w2 < S; ++w2) own = max(own, wl[w2 * K + K - 1]);
-    Tb_s[1] = own;
-    Tb_s[0] = max(own, ld_relaxed_u64(s.gT));
-  } else if (threadIdx.x == 32) {  // (max, sum exp) of the warps, folded in warp order
+  if (threadIdx.x < (unsigned)S) {  // K-th best warp head (heads: entry 0 of each sorted list)
+    const unsigned long long h = wl[threadIdx.x * K];
+    int rank = 0;
+    for (int w2 = 0; w2 < S; ++w2) rank += wl[w2 * K] > h;
+    unsigned long long t = wl[threadIdx.x * K + K - 1];
+    if (h != 0ull && rank == K - 1) t = max(t, h);
+    if (t != 0ull) atomicMax(Tb_s, t);
+  } else if (threadIdx.x == 32 * ((S + 31) / 32)) {  // (max, sum exp) of the warps, in warp order
     float M = -INFINITY;
     for (int w2 = 0; w2 < S; ++w2) M = fmaxf(M, wm[w2]);
     float sum = 0.f;
@@ -517,61 +518,49 @@ __global__ void __launch_bounds__((kMaxStages + 1) * 32, 1) cstep_kernel(const C
     __syncthreads();
     const int nc = misc[3];
     unsigned long long* my = s.crec + (size_t)g * rec;
-    if (nc <= K) {
-      for (int r = threadIdx.x; r < K; r += blockDim.x) my[2 + r] = r < nc ? cand[r] : 0ull;
-    } else {  // keep the CTA's best K candidates (rank count; keys are distinct)
-      for (int t = threadIdx.x; t < nc; t += blockDim.x) {
-        const unsigned long long x = cand[t];
-        int rank = 0;
-#pragma unroll 8
-        for (int j = 0; j < nc; ++j) rank += cand[j] > x;
-        if (rank < K) my[2 + rank] = x;
-        if (rank == K - 1) Tb_s[1] = max(Tb_s[1], x);  // the CTA's own K-th best: a global lower bound
-      }
-      __syncthreads();
+    for (int r = nc + threadIdx.x; r < K; r += blockDim.x) my[2 + r] = 1ull;  // padding
+    for (int t = threadIdx.x; t < nc; t += blockDim.x) {  // rank (keys are distinct), sorted record
+      const unsigned long long x = cand[t];
+      int rank = 0;
+#pragma unroll 4
+      for (int j = 0; j < nc; ++j) rank += cand[j] > x;
+      if (rank < K) my[2 + rank] = x;
     }
     if (threadIdx.x == 0) {
       const float M = reinterpret_cast<float*>(misc)[4], sum = reinterpret_cast<float*>(misc)[5];
       my[0] = (unsigned long long)__float_as_uint(M) | ((unsigned long long)__float_as_uint(sum) << 32);
-      my[1] = (unsigned long long)min(nc, K);
-      if (Tb_s[1] != 0ull) atomicMax(s.gT, Tb_s[1]);
-      if (M > -INFINITY) atomicMax(s.gM, ord_key(M));
+      my[1] = (unsigned long long)min(nc, K) + 1ull;
     }
   }
-  __syncthreads();
   trace_mark(s.trace, 9);
-  if (threadIdx.x == 0) misc[1] = release_add(s.ctr, 1u) == (unsigned)(G - 1);
-  __syncthreads();
-  trace_mark(s.trace, 6);
-  if (!misc[1]) return;
-  fence_acq_rel_gpu();  // every thread reads the other CTAs' records
-  trace_mark(s.trace, 14);
+  if (g != 0) return;
 
-  // Globally last CTA: every global top-K member is among the records' candidates (it passed its
-  // CTA's bound, itself <= the K-th best); keep those >= the final bound, rank them; lse over the
-  // G (max, sum) pairs in CTA order.  Scratch: the ring.
+  // Merger (CTA 0): wait for every record word to land, then every global top-K member is among the
+  // records' candidates (it passed its CTA's bound); keep those >= T2 = the K-th best record head,
+  // rank them; lse over the G (max, sum) pairs in CTA order.  Scratch: the ring.
   const int GK2 = (G * K + 1) & ~1;
   unsigned long long* fk = reinterpret_cast<unsigned long long*>(c.ring);  // [G][K]
   unsigned long long* fsurv = fk + GK2;                                    // [G*K]
   float* fm = reinterpret_cast<float*>(fsurv + GK2);                       // [G]
   float* fs = fm + G;                                                      // [G]
-  float* wpart = fs + G;                                                   // [32]
-  int* nsh = reinterpret_cast<int*>(wpart + 32);                          // [0] count, [2..3] T2
-  if (threadIdx.x == 0) *nsh = 0;
-  unsigned long long Tfin = 0ull;
-  uint32_t Mk = 0u;
-  {  // one batch of independent loads per thread (all records in flight at once)
-    constexpr int kB = 12;
+  float* wpart = fs + G;                                                   // [32] warp maxima, sums
+  int* nsh = reinterpret_cast<int*>(wpart + 64);                           // [0] count, [2..3] T2
+  unsigned long long* T2s = reinterpret_cast<unsigned long long*>(nsh + 2);
+  if (threadIdx.x == 0) {
+    *nsh = 0;
+    *T2s = 0ull;
+  }
+  {
+    constexpr int kB = 8;
     const int nrec = G * rec, nt = blockDim.x;
-    Tfin = ld_relaxed_u64(s.gT);
-    Mk = *reinterpret_cast<volatile unsigned*>(s.gM);
     for (int i0 = threadIdx.x; i0 < nrec; i0 += kB * nt) {
       unsigned long long v[kB];
 #pragma unroll
-      for (int u = 0; u < kB; ++u) v[u] = i0 + u * nt < nrec ? __ldcg(s.crec + i0 + u * nt) : 0ull;
+      for (int u = 0; u < kB; ++u) v[u] = i0 + u * nt < nrec ? __ldcg(s.crec + i0 + u * nt) : 1ull;
 #pragma unroll
       for (int u = 0; u < kB; ++u) {
         const int i = i0 + u * nt;
+        while (v[u] == 0ull) v[u] = ld_relaxed_u64(s.crec + i);  // not written yet: poll L2 (asm volatile)
         if (i < nrec) {
           const int gg = i / rec, f = i - gg * rec;
           if (f == 0) {
@@ -585,37 +574,34 @@ __global__ void __launch_bounds__((kMaxStages + 1) * 32, 1) cstep_kernel(const C
     }
   }
   __syncthreads();
-  trace_mark(s.trace, 15);
-  // T2 = the K-th best of the records' best candidates (K distinct keys >= it): with T1 this leaves
-  // about K survivors instead of every candidate above the weaker T1
-  unsigned long long* heads = fsurv;  // scratch until the compaction below
-  unsigned long long* T2s = reinterpret_cast<unsigned long long*>(nsh + 2);
-  if (threadIdx.x == 0) *T2s = 0ull;
-  for (int t = threadIdx.x; t < G; t += blockDim.x) {
-    unsigned long long h = 0ull;
-#pragma unroll 4
-    for (int r = 0; r < K; ++r) h = max(h, fk[t * K + r]);
-    heads[t] = h;
-  }
-  __syncthreads();
+  trace_mark(s.trace, 14);
+  for (int i = threadIdx.x; i < G * rec; i += blockDim.x) s.crec[i] = 0ull;  // ready for the next launch
+  // T2 = the K-th best record head (records are sorted; K distinct keys >= it); the max score
   if (G >= K)
     for (int t = threadIdx.x; t < G; t += blockDim.x) {
-      const unsigned long long h = heads[t];
+      const unsigned long long h = fk[t * K];
       int rank = 0;
 #pragma unroll 8
-      for (int j = 0; j < G; ++j) rank += heads[j] > h;
-      if (h != 0ull && rank == K - 1) *T2s = h;
+      for (int j = 0; j < G; ++j) rank += fk[j * K] > h;
+      if (h > 1ull && rank == K - 1) *T2s = h;
     }
-  __syncthreads();
-  Tfin = max(Tfin, *T2s);
-  __syncthreads();  // heads (in fsurv) consumed before the compaction overwrites them
-  const float Mx = Mk ? __uint_as_float((Mk & 0x80000000u) ? (Mk & 0x7fffffffu) : ~Mk) : -INFINITY;
   {
+    float mx = -INFINITY;
+    for (int t = threadIdx.x; t < G; t += blockDim.x) mx = fmaxf(mx, fm[t]);
+    mx = warp_max(mx);
+    if (lane == 0) wpart[warp] = mx;
+  }
+  __syncthreads();
+  trace_mark(s.trace, 15);
+  float Mx = -INFINITY;
+  for (int w2 = 0; w2 < nwarps; ++w2) Mx = fmaxf(Mx, wpart[w2]);
+  {
+    const unsigned long long Tfin = *T2s;
     const int n = G * K;
     for (int i0 = 0; i0 < n; i0 += blockDim.x) {
       const int i = i0 + threadIdx.x;
       const unsigned long long x = i < n ? fk[i] : 0ull;
-      const bool keep = x != 0ull && x >= Tfin;
+      const bool keep = x > 1ull && x >= Tfin;
       const uint32_t bal = __ballot_sync(0xffffffffu, keep);
       int base = 0;
       if (lane == 0 && bal) base = atomicAdd(nsh, __popc(bal));
@@ -626,7 +612,7 @@ __global__ void __launch_bounds__((kMaxStages + 1) * 32, 1) cstep_kernel(const C
     for (int t = threadIdx.x; t < G; t += blockDim.x)
       if (fm[t] > -INFINITY) part += fs[t] * expf(fm[t] - Mx);
     part = warp_sum(part);
-    if (lane == 0) wpart[warp] = part;
+    if (lane == 0) wpart[32 + warp] = part;
   }
   __syncthreads();
   const int ns = *nsh;
@@ -637,28 +623,20 @@ __global__ void __launch_bounds__((kMaxStages + 1) * 32, 1) cstep_kernel(const C
     for (int j = 0; j < ns; ++j) rank += fsurv[j] > x;
     if (rank < K) out[rank] = x;
   }
-  if (threadIdx.x == 0) {
-    float sum = 0.f;
-    for (int w2 = 0; w2 < nwarps; ++w2) sum += wpart[w2];
-    wpart[31] = sum;
-  }
   __syncthreads();
+  float sum = 0.f;
+  for (int w2 = 0; w2 < nwarps; ++w2) sum += wpart[32 + w2];
   const bool ok = Mx > -INFINITY;
-  const float lse = ok ? Mx + logf(wpart[31]) : __int_as_float(0x7fc00000);
+  const float lse = ok ? Mx + logf(sum) : __int_as_float(0x7fc00000);
   for (int r = threadIdx.x; r < K; r += blockDim.x) {
     const unsigned long long x = out[r];
-    const bool v = ok && x != 0ull;
+    const bool v = ok && x > 1ull;
     const float z = v ? key_value(x) : -INFINITY;
     a.top_ids[r] = v ? key_id(x) : -1;
     a.top_logits[r] = z;
     a.top_logp[r] = v ? z - lse : -INFINITY;
   }
-  if (threadIdx.x == 0) {
-    a.lse[0] = lse;
-    *s.ctr = 0u;  // reset for the next launch (ordered after this grid by stream / PDL wait)
-    *s.gT = 0ull;
-    *s.gM = 0u;
-  }
+  if (threadIdx.x == 0) a.lse[0] = lse;
   trace_mark(s.trace, 7);
 }
 
@@ -755,7 +733,7 @@ static bool cstep_plan(const ds_clusters* c, const ds_router* r, int B, int k_t,
   }
   // the last CTA merges the G records inside its ring
   const size_t G = (size_t)C * Q;
-  if (G * (16 * k_t + 8) + 256 > (size_t)p->hp.stages * p->hp.stage_bytes) return false;
+  if (G * (16 * k_t + 8) + 512 > (size_t)p->hp.stages * p->hp.stage_bytes) return false;
   p->total = 256 + align_up(G * (2 + k_t) * sizeof(unsigned long long), 256);
   return true;
 }
@@ -820,8 +798,6 @@ cudaError_t launch_cstep(const ds_clusters* c, const ds_router* r, const void* h
   s.extra_bytes = p.extra;
   s.crec = reinterpret_cast<unsigned long long*>(w8 + 256);
   s.ctr = reinterpret_cast<unsigned*>(w8);
-  s.gT = reinterpret_cast<unsigned long long*>(w8 + 64);
-  s.gM = reinterpret_cast<unsigned*>(w8 + 72);
   s.trace = debug_trace();
   return c->dtype == DS_BF16 ? launch_cstep_t<__nv_bfloat16>(s, p.smem, p.Q, p.C, st, pdl)
                              : launch_cstep_t<float>(s, p.smem, p.Q, p.C, st, pdl);

@@ -306,10 +306,18 @@ bool step_supported(const ds_clusters* c, const ds_router* r, int B, int k_t, in
   return step_plan(c, r, B, k_t, max_shortlist, shared, &p);
 }
 
-size_t step_ws_bytes(const ds_clusters* c, const ds_router* r, int B, int k_t) {
+// The cluster step's records live after the grid-wide step's scratch, so the two kernels never
+// alias (the cluster step's merger relies on its record words reading 0 between launches).
+static size_t grid_step_ws(const ds_clusters* c, const ds_router* r, int B, int k_t) {
   StepPlan p;
   if (!step_plan(c, r, B, k_t, 0, 0, &p) && !step_plan(c, r, B, k_t, 0, 1, &p)) return 0;
-  return std::max(p.total, cstep_ws_bytes(c, r, B, k_t));
+  return align_up(p.total, 256);
+}
+
+size_t step_ws_bytes(const ds_clusters* c, const ds_router* r, int B, int k_t) {
+  const size_t g = grid_step_ws(c, r, B, k_t);
+  if (g == 0) return 0;
+  return g + cstep_ws_bytes(c, r, B, k_t);
 }
 
 template <typename T>
@@ -342,7 +350,8 @@ cudaError_t launch_step(const ds_clusters* c, const ds_router* r, const void* h_
   // B = 1: the cluster step (cstep.cu) needs no grid-wide barrier before the head streams
   if (cstep_supported(c, r, B, k_t, shared, max_shortlist) && cstep_pointers_ok(r, h_prev, e, h_new))
     return launch_cstep(c, r, h_prev, e, h_new, k, k_t, max_shortlist, scores, sel, sel_count, sl_offsets, top_ids,
-                        top_logits, top_logp, lse, z_out, z_stride, ws, st, pdl);
+                        top_logits, top_logp, lse, z_out, z_stride,
+                        static_cast<uint8_t*>(ws) + grid_step_ws(c, r, B, k_t), st, pdl);
   StepPlan p;
   if (!step_plan(c, r, B, k_t, max_shortlist, shared, &p)) return cudaErrorInvalidValue;
   uint8_t* w8 = static_cast<uint8_t*>(ws);
