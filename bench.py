@@ -272,6 +272,8 @@ def run_ours(args, ws, rank, local):
     steppers = [D.DraftStep(clusters, router, B, C.k_t, shared=C.shared, two_streams=False, device=dev)
                 for _ in range(C.positions)]
     fused = steppers[0].launches == 1
+    # B = 1 per-row steps run as the cluster step (cstep.cu) unless DS_CLUSTER_Q=0
+    cluster_step = fused and B == 1 and not C.shared and os.environ.get("DS_CLUSTER_Q", "16") != "0"
     kb = [budget_of(t, C) for t in range(C.positions)]
     flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
     head_ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
@@ -440,7 +442,9 @@ def run_ours(args, ws, rank, local):
                        "verification": None if args.profile else verify},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak if achieved else None,
-                         "traffic": committed_traffic(C.name, B), "kernel": ("ds::step_kernel (router + select + gathered head + epilogue, one launch)" if fused
+                         "traffic": committed_traffic(C.name, B), "kernel": (("ds::cstep_kernel (cluster step: router per 16-CTA cluster over DSMEM + select + gathered "
+                                     "head + epilogue, one launch)" if cluster_step else
+                                     "ds::step_kernel (router + select + gathered head + epilogue, one launch)") if fused
                                     else "ds::head_kernel (S5+S6)"),
                          "duration_source": ("CUDA events around each timed cycle / launches per cycle (every launch "
                                              "is the dominant kernel; PDL-chained)" if fused else

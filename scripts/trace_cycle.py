@@ -26,8 +26,8 @@ names = ["start", "pdl", "phaseA", "sel_vis", "segs", "streamed", "partials", "m
          "M:lse", "M:thr", "M:surv", "M:done"]
 CSTEP = os.environ.get("DS_CLUSTER_Q", "16") != "0"
 if CSTEP:  # cluster step (cstep.cu) mark slots
-    names = ["start", "pdl", "L1done", "sel", "segs", "streamed", "counted", "merged", "a1_bar", "cta_rec",
-             "-", "-", "sc_bar", "rank", "last", "recs_read", "fin_merge", "-", "-", "-", "-"]
+    names = ["start", "pdl", "L1done", "-", "stream0", "streamed", "-", "merged", "a1_bar", "cta_rec",
+             "-", "-", "sc_bar", "mask", "recs_seen", "T2", "-", "-", "-", "-", "-"]
 inp = [[x.to(dev) for x in S.step_inputs(1, C.d, t, "bf16")] for t in range(C.positions)]
 for rep in range(3):
     flush.zero_()
