@@ -547,7 +547,8 @@ __global__ void __launch_bounds__((kMaxStages + 1) * 32, 1) cstep_kernel(const C
   int* nsh = reinterpret_cast<int*>(wpart + 64);                           // [0] count, [2..3] T2
   unsigned long long* T2s = reinterpret_cast<unsigned long long*>(nsh + 2);
   if (threadIdx.x == 0) {
-    *nsh = 0;
+    nsh[0] = 0;
+    nsh[1] = 0;
     *T2s = 0ull;
   }
   {
@@ -575,26 +576,25 @@ __global__ void __launch_bounds__((kMaxStages + 1) * 32, 1) cstep_kernel(const C
   }
   __syncthreads();
   trace_mark(s.trace, 14);
-  for (int i = threadIdx.x; i < G * rec; i += blockDim.x) s.crec[i] = 0ull;  // ready for the next launch
-  // T2 = the K-th best record head (records are sorted; K distinct keys >= it); the max score
-  if (G >= K)
-    for (int t = threadIdx.x; t < G; t += blockDim.x) {
-      const unsigned long long h = fk[t * K];
-      int rank = 0;
-#pragma unroll 8
-      for (int j = 0; j < G; ++j) rank += fk[j * K] > h;
-      if (h > 1ull && rank == K - 1) *T2s = h;
-    }
+  // T2 = the best of the per-warp K-th best record heads (records are sorted; each warp's K-th best
+  // of its 32 heads has K distinct keys above it); max score as an order-preserving integer
   {
-    float mx = -INFINITY;
-    for (int t = threadIdx.x; t < G; t += blockDim.x) mx = fmaxf(mx, fm[t]);
-    mx = warp_max(mx);
-    if (lane == 0) wpart[warp] = mx;
+    const int t = threadIdx.x;
+    const unsigned long long h = t < G ? fk[t * K] : 0ull;
+    if (t - lane < G) {  // warps holding heads: rank among the warp's 32 lanes by shuffles
+      int rank = 0;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) rank += __shfl_sync(0xffffffffu, h, j) > h;
+      if (h > 1ull && rank == K - 1) atomicMax(T2s, h);
+      const uint32_t mk = (t < G && fm[t] > -INFINITY) ? ord_key(fm[t]) : 0u;
+      const uint32_t wmk = __reduce_max_sync(0xffffffffu, mk);
+      if (lane == 0 && wmk) atomicMax(reinterpret_cast<unsigned*>(nsh + 1), wmk);
+    }
   }
   __syncthreads();
   trace_mark(s.trace, 15);
-  float Mx = -INFINITY;
-  for (int w2 = 0; w2 < nwarps; ++w2) Mx = fmaxf(Mx, wpart[w2]);
+  const uint32_t Mk = reinterpret_cast<const unsigned*>(nsh)[1];
+  const float Mx = Mk ? __uint_as_float((Mk & 0x80000000u) ? (Mk & 0x7fffffffu) : ~Mk) : -INFINITY;
   {
     const unsigned long long Tfin = *T2s;
     const int n = G * K;
@@ -638,6 +638,7 @@ __global__ void __launch_bounds__((kMaxStages + 1) * 32, 1) cstep_kernel(const C
   }
   if (threadIdx.x == 0) a.lse[0] = lse;
   trace_mark(s.trace, 7);
+  for (int i = threadIdx.x; i < G * rec; i += blockDim.x) s.crec[i] = 0ull;  // ready for the next launch
 }
 
 // ------------------------------------------------------------------ host side
