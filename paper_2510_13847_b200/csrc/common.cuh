@@ -145,6 +145,11 @@ __device__ __forceinline__ void trace_mark(unsigned long long* t, int slot) {
   if (t != nullptr && threadIdx.x == 0) {
     t[blockIdx.x * 64 + slot] = globaltimer_ns();
     t[blockIdx.x * 64 + 32 + slot] = clock64();
+    if (slot == 0) {
+      uint32_t sm;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+      t[blockIdx.x * 64 + 31] = sm + 1u;  // trace slot 31: SM id + 1
+    }
   }
 }
 

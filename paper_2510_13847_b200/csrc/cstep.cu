@@ -151,57 +151,44 @@ __device__ __forceinline__ void dot2x(const T* __restrict__ w0, const T* __restr
   z1 = warp_sum(b0 + b1);
 }
 
-// Producer warp: the CTA's segment [N g / G, N (g+1) / G) of the virtual shortlist (the selected
-// clusters in ascending id, R8; N = |V_S| = sum of their sizes), streamed by lane 0 as runs
-// of whole W_perm rows.  The 32 lanes derive N and the segment start from the TopK mask (lane j:
-// mask word j, one warp scan), so no block-wide prefix sum sits between the selection and the first
-// TMA copy.  info = (-, virtual shortlist position, rows, first W_perm row).
+// Producer lane: the CTA's share of the virtual shortlist (the selected clusters in ascending id,
+// R8; |V_S| = sum of their sizes), streamed as chunks of at most `stage_rows` whole W_perm
+// rows that never cross a cluster boundary.  Chunk c (in shortlist order) goes to CTA c mod G, so
+// at any moment the grid reads one contiguous window of the shortlist: per-CTA stream times no
+// longer depend on which address range a CTA was given (a contiguous per-CTA segment made the
+// slowest CTA ~1.2x the mean, the slowness following the address range, not the SM).
+// info = (-, virtual shortlist position, rows, first W_perm row).
 template <typename T>
 __device__ void cstep_produce(const HeadArgs& a, const HeadCtx& c, const uint32_t* mask, const int32_t* offs, int g,
                               int G, uint32_t it0) {
-  const int lane = threadIdx.x & 31;
-  const int words = (a.M + 31) >> 5;  // <= 32 (M <= 1024)
-  const uint32_t mybits = lane < words ? mask[lane] : 0u;
-  long long wsum = 0;
-  for (uint32_t b = mybits; b; b &= b - 1u) {
-    const int m = (lane << 5) + __ffs(b) - 1;
-    wsum += offs[m + 1] - offs[m];
-  }
-  long long inc = wsum;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const long long y = __shfl_up_sync(0xffffffffu, inc, o);
-    if (lane >= o) inc += y;
-  }
-  const long long N = __shfl_sync(0xffffffffu, inc, 31);
-  const long long s0 = N * g / G, s1 = N * (g + 1) / G;
-  const uint32_t past = __ballot_sync(0xffffffffu, inc > s0);  // words ending after s0
-  const int w0 = past ? __ffs(past) - 1 : 32;
-  const long long vstart = __shfl_sync(0xffffffffu, inc - wsum, w0 & 31);
-  if (lane != 0) return;
+  if ((threadIdx.x & 31) != 0) return;
+  const int words = (a.M + 31) >> 5;
   const uint64_t pol = policy_evict_first();
   const uint32_t rowbytes = (uint32_t)a.d * (uint32_t)sizeof(T);
   const uint8_t* W = static_cast<const uint8_t*>(a.W);
   const uint32_t S = (uint32_t)a.stages;
+  const int R = a.stage_rows;
   uint32_t it = it0;
-  long long vpos = vstart;  // virtual position of the current cluster's first row
-  for (int w = w0; w < words && vpos < s1 && s0 < s1; ++w) {
-    for (uint32_t bits = mask[w]; bits && vpos < s1; bits &= bits - 1u) {
+  long long vpos = 0;  // virtual position of the current cluster's first row
+  long long cb = 0;    // global index of the current cluster's first chunk
+  long long cn = g;    // next chunk this CTA streams
+  for (int w = 0; w < words; ++w) {
+    for (uint32_t bits = mask[w]; bits; bits &= bits - 1u) {
       const int m = (w << 5) + __ffs(bits) - 1;
       const int beg = offs[m], sz = offs[m + 1] - beg;
-      const long long lo = max(s0, vpos), hi = min(s1, vpos + sz);
-      for (long long p = lo; p < hi;) {
-        const int n = (int)min((long long)a.stage_rows, hi - p);
-        const int row = beg + (int)(p - vpos);
+      const long long nch = (sz + R - 1) / R;
+      for (; cn < cb + nch; cn += G) {
+        const int j0 = (int)(cn - cb) * R;
+        const int n = min(R, sz - j0);
         const uint32_t sl = it % S;
         mbar_wait(&c.empty[sl], ((it / S) & 1u) ^ 1u);
-        c.info[sl] = make_int4(0, (int)p, n, row);
+        c.info[sl] = make_int4(0, (int)(vpos + j0), n, beg + j0);
         mbar_arrive_expect_tx(&c.full[sl], (uint32_t)n * rowbytes);
-        bulk_g2s(c.ring + (size_t)sl * a.stage_bytes, W + (size_t)row * rowbytes, (uint32_t)n * rowbytes,
+        bulk_g2s(c.ring + (size_t)sl * a.stage_bytes, W + (size_t)(beg + j0) * rowbytes, (uint32_t)n * rowbytes,
                  &c.full[sl], pol);
         ++it;
-        p += n;
       }
+      cb += nch;
       vpos += sz;
     }
   }
