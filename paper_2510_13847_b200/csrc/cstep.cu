@@ -54,7 +54,7 @@ struct CStepArgs {
 
 // Shared-memory carve-up (inside HeadSmem.extra).
 struct CExtra {
-  uint32_t xs, p1, a1, sc, w2s, b1s, b2s, offs, selb, mask, sel, sloff, cnt, tmp, wm, ws, wl, surv, out, misc, total;
+  uint32_t xs, p1, a1, sc, w2s, b1s, b2s, offs, selb, xb, mask, sel, sloff, cnt, tmp, wm, ws, wl, surv, out, misc, total;
 };
 __host__ __device__ inline CExtra cstep_extra(int d, int esz, int M, int h_r, int rows1, int Q, int K, int S, int C) {
   CExtra X;
@@ -74,7 +74,8 @@ __host__ __device__ inline CExtra cstep_extra(int d, int esz, int M, int h_r, in
   X.b1s = take(4u * U);
   X.b2s = take(4u * (Ms > 0 ? Ms : 1));
   X.offs = take(4u * (M + 1));
-  X.selb = take((uint32_t)(M + 3) & ~3u);
+  X.selb = take(4u * M);  // u32 TopK flags (st.async writes 4-byte words)
+  X.xb = take(3 * 8);     // mbarriers of the three cluster exchanges
   X.mask = take(4u * 32);
   X.sel = take(4u * M);
   X.sloff = take(4u * (M + 1));
@@ -260,7 +261,8 @@ __global__ void __launch_bounds__((kMaxStages + 1) * 32, 1) cstep_kernel(const C
   float* b1s = reinterpret_cast<float*>(ex + X.b1s);
   float* b2s = reinterpret_cast<float*>(ex + X.b2s);
   int32_t* offs = reinterpret_cast<int32_t*>(ex + X.offs);
-  uint8_t* selb = ex + X.selb;
+  uint32_t* selb = reinterpret_cast<uint32_t*>(ex + X.selb);
+  uint64_t* xb = reinterpret_cast<uint64_t*>(ex + X.xb);  // [0] a, [1] scores, [2] TopK flags
   uint32_t* mask = reinterpret_cast<uint32_t*>(ex + X.mask);
   int32_t* sel_s = reinterpret_cast<int32_t*>(ex + X.sel);
   int32_t* sloff_s = reinterpret_cast<int32_t*>(ex + X.sloff);
@@ -288,12 +290,17 @@ __global__ void __launch_bounds__((kMaxStages + 1) * 32, 1) cstep_kernel(const C
     head_init_barriers(c, S);
     mbar_init(xbar, 1);
     mbar_init(wbar, 1);
+    // the three exchanges: each CTA expects every value of the cluster-wide vector (own included)
+    for (int i = 0; i < 3; ++i) mbar_init(&xb[i], 1);
+    mbar_arrive_expect_tx(&xb[0], 4u * (uint32_t)s.rows1);
+    if (s.h_r > 0) mbar_arrive_expect_tx(&xb[1], 4u * (uint32_t)M);
+    mbar_arrive_expect_tx(&xb[2], 4u * (uint32_t)s.k);  // exactly k ranks are < k (distinct keys)
     fence_mbar_init();
   }
   for (int m = threadIdx.x; m < M; m += blockDim.x) selb[m] = 0;
   if (threadIdx.x < 16) misc[threadIdx.x] = 0;
   __syncthreads();
-  cluster_arrive_relaxed();  // paired with the wait before the first DSMEM store
+  cluster_arrive_relaxed();  // paired with the wait before the first DSMEM store (barrier inits are fenced)
   trace_mark(s.trace, 0);
   if (warp == S) {
     if (lane == 0) {
@@ -364,11 +371,11 @@ __global__ void __launch_bounds__((kMaxStages + 1) * 32, 1) cstep_kernel(const C
     for (int t = threadIdx.x; t < U * Q; t += blockDim.x) {
       const int u = t / Q, dst = t - u * Q;
       const float z = (p1[2 * u] + p1[2 * u + 1]) + b1s[u];
-      st_cluster_f32(mapa_u32(smem_u32(dstv + u0 + u), (uint32_t)dst), s.h_r > 0 ? fmaxf(z, 0.f) : z);
+      st_async_u32(mapa_u32(smem_u32(dstv + u0 + u), (uint32_t)dst), __float_as_uint(s.h_r > 0 ? fmaxf(z, 0.f) : z),
+                   mapa_u32(smem_u32(&xb[0]), (uint32_t)dst));
     }
   }
-  cluster_arrive_release();
-  cluster_wait_acquire();
+  mbar_wait_cluster(&xb[0], 0);
   trace_mark(s.trace, 8);
   if (s.h_r > 0) {  // layer 2 on this CTA's score slice -> every CTA's sc[]
     if (w2_bytes > 0) mbar_wait(wbar, 0);
@@ -390,11 +397,12 @@ __global__ void __launch_bounds__((kMaxStages + 1) * 32, 1) cstep_kernel(const C
       for (int o = sub >> 1; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
       if (m < ms1) {
         acc += b2s[m - ms0];
-        for (int dst = part; dst < Q; dst += sub) st_cluster_f32(mapa_u32(smem_u32(sc + m), (uint32_t)dst), acc);
+        for (int dst = part; dst < Q; dst += sub)
+          st_async_u32(mapa_u32(smem_u32(sc + m), (uint32_t)dst), __float_as_uint(acc),
+                       mapa_u32(smem_u32(&xb[1]), (uint32_t)dst));
       }
     }
-    cluster_arrive_release();
-    cluster_wait_acquire();
+    mbar_wait_cluster(&xb[1], 0);
   }
   trace_mark(s.trace, 12);
   // TopK_k under (score desc, id asc) (R7): rank this CTA's slice against all M scores
@@ -418,13 +426,10 @@ __global__ void __launch_bounds__((kMaxStages + 1) * 32, 1) cstep_kernel(const C
       for (int o = sub >> 1; o > 0; o >>= 1) rank += __shfl_xor_sync(0xffffffffu, rank, o);
       if (act && rank < s.k)
         for (int dst = part; dst < Q; dst += sub)
-          asm volatile("st.shared::cluster.u8 [%0], %1;" ::"r"(mapa_u32(smem_u32(selb + m), (uint32_t)dst)),
-                       "r"(1u)
-                       : "memory");
+          st_async_u32(mapa_u32(smem_u32(selb + m), (uint32_t)dst), 1u, mapa_u32(smem_u32(&xb[2]), (uint32_t)dst));
     }
   }
-  cluster_arrive_release();
-  cluster_wait_acquire();
+  mbar_wait_cluster(&xb[2], 0);
   trace_mark(s.trace, 13);
   {
     const int Mr = (M + 31) & ~31;
