@@ -149,6 +149,7 @@ __device__ __forceinline__ void trace_mark(unsigned long long* t, int slot) {
       uint32_t sm;
       asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
       t[blockIdx.x * 64 + 31] = sm + 1u;  // trace slot 31: SM id + 1
+      t[blockIdx.x * 64 + 30] = blockDim.x;  // trace slot 30: threads per CTA
     }
   }
 }

@@ -50,6 +50,7 @@ struct CStepArgs {
                              // written (the merger zeroes them after reading)
   unsigned* ctr;             // unused (the merger polls the records)
   unsigned long long* trace;
+  int variant;  // debug A/B switches (DS_CSTEP_VARIANT, read once); none defined at present
 };
 
 // Shared-memory carve-up (inside HeadSmem.extra).
@@ -453,10 +454,56 @@ __global__ void __launch_bounds__((kMaxStages + 1) * 32, 1) cstep_kernel(const C
       wsum[warp] = se;
     }
   }
-  for (int r = threadIdx.x; r < K; r += blockDim.x) out[r] = 0ull;
   __syncthreads();
   trace_mark(s.trace, 5);
-  if (cid == 0 && q == 0) {  // the caller's copies of scores / selection / offsets (S3 outputs)
+  if (a.pdl) pdl_launch_dependents();
+  const int G = (int)gridDim.x, g = (int)blockIdx.x, rec = 2 + K;
+  // CTA record = (max, sum exp) of the CTA's logits + its K best keys, sorted.  One pass, no further
+  // block barrier: thread i ranks warp-list entry i against all S K entries (keys are distinct;
+  // 0 = empty) and writes it to its rank if that is < K; the ranks >= the number of valid keys are
+  // padding (1, below every key: a key's low word ~id has bit 31 set).  Warp S (the producer, idle
+  // now) folds the S warp (max, sum) pairs: max as an order-preserving integer, sums by a fixed xor
+  // tree (R19).  Record words are never 0, so the merger polls the data itself: no fence, no ticket.
+  {
+    unsigned long long* my = s.crec + (size_t)g * rec;
+    const int n = S * K, nr = S * 32;  // the consumer warps rank; warp S folds (max, sum)
+    int P = 1;                         // lanes per key (a power of two: shallower loops)
+    while (P < 8 && n * (P * 2) <= nr) P <<= 1;
+    if (threadIdx.x < (unsigned)nr)
+      for (int v0 = 0; v0 < n * P; v0 += nr) {  // uniform trip count: every lane shuffles
+        const int v = v0 + threadIdx.x, i = v / P, part = v % P;
+        const bool act = i < n;
+        const unsigned long long x = act ? wl[i] : 0ull;
+        int rk = 0, nv = 0;
+        if (act)
+#pragma unroll 4
+          for (int j = part; j < n; j += P) {
+            const unsigned long long y = wl[j];
+            rk += y > x;
+            nv += y != 0ull;
+          }
+        for (int o = P >> 1; o > 0; o >>= 1) {
+          rk += __shfl_xor_sync(0xffffffffu, rk, o);
+          nv += __shfl_xor_sync(0xffffffffu, nv, o);
+        }
+        if (act && part == 0) {
+          if (x != 0ull && rk < K) my[2 + rk] = x;
+          if (i < K && i >= nv) my[2 + i] = 1ull;  // padding (R17)
+          if (i == 0) my[1] = (unsigned long long)min(nv, K) + 1ull;
+        }
+      }
+    if (warp == S) {
+      const bool has = lane < S;
+      const float mw = has ? wm[lane] : -INFINITY;
+      const uint32_t mk = __reduce_max_sync(0xffffffffu, mw > -INFINITY ? ord_key(mw) : 0u);
+      const float Mx = mk ? __uint_as_float((mk & 0x80000000u) ? (mk & 0x7fffffffu) : ~mk) : -INFINITY;
+      const float sum = warp_sum(has && mw > -INFINITY ? wsum[lane] * expf(mw - Mx) : 0.f);
+      if (lane == 0)
+        my[0] = (unsigned long long)__float_as_uint(Mx) | ((unsigned long long)__float_as_uint(sum) << 32);
+    }
+  }
+  trace_mark(s.trace, 9);
+  if (g == G - 1) {  // the caller's copies of scores / selection / offsets (S3 outputs), off the merger CTA
     emit_fast(mask, M, offs, sel_s, cnt_s, sloff_s, tmp);
     __syncthreads();
     const int cnt = *cnt_s;
@@ -467,85 +514,34 @@ __global__ void __launch_bounds__((kMaxStages + 1) * 32, 1) cstep_kernel(const C
     for (int i = threadIdx.x; i <= cnt; i += blockDim.x) s.sloff_out[i] = sloff_s[i];
     if (threadIdx.x == 0) *s.cnt_out = cnt;
   }
-  if (a.pdl) pdl_launch_dependents();
-  const int G = (int)gridDim.x, g = (int)blockIdx.x, rec = 2 + K;
-  // CTA record = (max, sum) of its logits + its best min(nc, K) candidates for the global top-K.
-  // Candidates: the warp-list entries >= Tb, Tb = max(best K-th entry of a warp list, K-th best warp
-  // head) — both have K keys above them, so Tb <= the CTA's (and the grid's) K-th best.  Record words
-  // are never 0 (padding = 1, below every key: a key's low word ~id has bit 31 set), so the merger
-  // polls the data itself: no fence, no ticket.
-  unsigned long long* Tb_s = reinterpret_cast<unsigned long long*>(misc + 8);  // misc[8..9]
-  if (threadIdx.x < (unsigned)S) {  // K-th best warp head (heads: entry 0 of each sorted list)
-    const unsigned long long h = wl[threadIdx.x * K];
-    int rank = 0;
-    for (int w2 = 0; w2 < S; ++w2) rank += wl[w2 * K] > h;
-    unsigned long long t = wl[threadIdx.x * K + K - 1];
-    if (h != 0ull && rank == K - 1) t = max(t, h);
-    if (t != 0ull) atomicMax(Tb_s, t);
-  } else if (threadIdx.x == 32 * ((S + 31) / 32)) {  // (max, sum exp) of the warps, in warp order
-    float M = -INFINITY;
-    for (int w2 = 0; w2 < S; ++w2) M = fmaxf(M, wm[w2]);
-    float sum = 0.f;
-    if (M > -INFINITY)
-      for (int w2 = 0; w2 < S; ++w2)
-        if (wm[w2] > -INFINITY) sum += wsum[w2] * expf(wm[w2] - M);
-    reinterpret_cast<float*>(misc)[4] = M;
-    reinterpret_cast<float*>(misc)[5] = sum;
-  }
-  __syncthreads();
-  {
-    const unsigned long long Tb = Tb_s[0];
-    unsigned long long* cand = wl + S * K;  // scratch after the lists (X.wl holds 2 S K keys)
-    const int n = S * K;
-    for (int i0 = 0; i0 < n; i0 += blockDim.x) {
-      const int i = i0 + threadIdx.x;
-      const unsigned long long x = i < n ? wl[i] : 0ull;
-      const bool keep = x != 0ull && x >= Tb;
-      const uint32_t bal = __ballot_sync(0xffffffffu, keep);
-      int base = 0;
-      if (lane == 0 && bal) base = atomicAdd(&misc[3], __popc(bal));
-      base = __shfl_sync(0xffffffffu, base, 0);
-      if (keep) cand[base + __popc(bal & ((1u << lane) - 1u))] = x;
-    }
-    __syncthreads();
-    const int nc = misc[3];
-    unsigned long long* my = s.crec + (size_t)g * rec;
-    for (int r = nc + threadIdx.x; r < K; r += blockDim.x) my[2 + r] = 1ull;  // padding
-    for (int t = threadIdx.x; t < nc; t += blockDim.x) {  // rank (keys are distinct), sorted record
-      const unsigned long long x = cand[t];
-      int rank = 0;
-#pragma unroll 4
-      for (int j = 0; j < nc; ++j) rank += cand[j] > x;
-      if (rank < K) my[2 + rank] = x;
-    }
-    if (threadIdx.x == 0) {
-      const float M = reinterpret_cast<float*>(misc)[4], sum = reinterpret_cast<float*>(misc)[5];
-      my[0] = (unsigned long long)__float_as_uint(M) | ((unsigned long long)__float_as_uint(sum) << 32);
-      my[1] = (unsigned long long)min(nc, K) + 1ull;
-    }
-  }
-  trace_mark(s.trace, 9);
   if (g != 0) return;
 
-  // Merger (CTA 0): wait for every record word to land, then every global top-K member is among the
-  // records' candidates (it passed its CTA's bound); keep those >= T2 = the K-th best record head,
-  // rank them; lse over the G (max, sum) pairs in CTA order.  Scratch: the ring.
-  const int GK2 = (G * K + 1) & ~1;
+  // Merger (CTA 0).  (1) every thread polls record words (coalesced) until they land, staging them
+  // in shared memory (record heads also contiguously) and folding max m_g as an order-preserving
+  // integer.  (2) thread g ranks head g among the G heads: with r_g heads above it, key j of record
+  // g has at least r_g + j keys above it (records are sorted), so only keys j < K - r_g can be in
+  // the global top-K (every global top-K member is in its CTA's record) — at most K (K + 1) / 2
+  // candidates; the same threads form the lse partials s_g e^{m_g - M} (fixed xor trees, R19).
+  // (3) thread per candidate: rank, outputs.  Two block barriers.  Scratch: the ring.
   unsigned long long* fk = reinterpret_cast<unsigned long long*>(c.ring);  // [G][K]
-  unsigned long long* fsurv = fk + GK2;                                    // [G*K]
-  float* fm = reinterpret_cast<float*>(fsurv + GK2);                       // [G]
+  unsigned long long* fsurv = fk + (size_t)G * K;                          // [G*K]
+  const int G4 = (G + 3) & ~3;
+  uint32_t* hh = reinterpret_cast<uint32_t*>(fsurv + (((size_t)G * K + 1) & ~(size_t)1));  // [G4] heads' high words (16 B aligned)
+  int* fc = reinterpret_cast<int*>(hh + G4);                               // [G] valid keys per record
+  float* fm = reinterpret_cast<float*>(fc + G);                            // [G]
   float* fs = fm + G;                                                      // [G]
-  float* wpart = fs + G;                                                   // [32] warp maxima, sums
-  int* nsh = reinterpret_cast<int*>(wpart + 64);                           // [0] count, [2..3] T2
-  unsigned long long* T2s = reinterpret_cast<unsigned long long*>(nsh + 2);
+  float* wps = fs + G;                                                     // [32] warp partial sums
+  unsigned* sh = reinterpret_cast<unsigned*>(wps + 32);                    // [0] count [1] max key
   if (threadIdx.x == 0) {
-    nsh[0] = 0;
-    nsh[1] = 0;
-    *T2s = 0ull;
+    sh[0] = 0u;
+    sh[1] = 0u;
   }
+  for (int i = G + threadIdx.x; i < G4; i += blockDim.x) hh[i] = 0u;
+  __syncthreads();
   {
     constexpr int kB = 8;
     const int nrec = G * rec, nt = blockDim.x;
+    unsigned mymk = 0u;
     for (int i0 = threadIdx.x; i0 < nrec; i0 += kB * nt) {
       unsigned long long v[kB];
 #pragma unroll
@@ -557,76 +553,84 @@ __global__ void __launch_bounds__((kMaxStages + 1) * 32, 1) cstep_kernel(const C
         if (i < nrec) {
           const int gg = i / rec, f = i - gg * rec;
           if (f == 0) {
-            fm[gg] = __uint_as_float((uint32_t)v[u]);
+            const float m = __uint_as_float((uint32_t)v[u]);
+            fm[gg] = m;
             fs[gg] = __uint_as_float((uint32_t)(v[u] >> 32));
-          } else if (f >= 2) {
+            if (m > -INFINITY) mymk = max(mymk, ord_key(m));
+          } else if (f == 1) {
+            fc[gg] = (int)v[u] - 1;
+          } else {
             fk[gg * K + f - 2] = v[u];
+            if (f == 2) hh[gg] = v[u] > 1ull ? (uint32_t)(v[u] >> 32) : 0u;
           }
         }
       }
     }
+    mymk = __reduce_max_sync(0xffffffffu, mymk);
+    if (lane == 0 && mymk) atomicMax(&sh[1], mymk);
   }
   __syncthreads();
   trace_mark(s.trace, 14);
-  // T2 = the best of the per-warp K-th best record heads (records are sorted; each warp's K-th best
-  // of its 32 heads has K distinct keys above it); max score as an order-preserving integer
+  const uint32_t Mk = sh[1];
+  const float Mx = Mk ? __uint_as_float((Mk & 0x80000000u) ? (Mk & 0x7fffffffu) : ~Mk) : -INFINITY;
   {
-    const int t = threadIdx.x;
-    const unsigned long long h = t < G ? fk[t * K] : 0ull;
-    if (t - lane < G) {  // warps holding heads: rank among the warp's 32 lanes by shuffles
-      int rank = 0;
-#pragma unroll
-      for (int j = 0; j < 32; ++j) rank += __shfl_sync(0xffffffffu, h, j) > h;
-      if (h > 1ull && rank == K - 1) atomicMax(T2s, h);
-      const uint32_t mk = (t < G && fm[t] > -INFINITY) ? ord_key(fm[t]) : 0u;
-      const uint32_t wmk = __reduce_max_sync(0xffffffffu, mk);
-      if (lane == 0 && wmk) atomicMax(reinterpret_cast<unsigned*>(nsh + 1), wmk);
+    float part = 0.f;
+    for (int t = threadIdx.x; t < G; t += blockDim.x) {
+      // r = heads with a strictly larger logit (<= heads above head t: a valid count)
+      const uint32_t h = hh[t];
+      const uint4* h4 = reinterpret_cast<const uint4*>(hh);
+      int r = 0;
+#pragma unroll 4
+      for (int j = 0; j < G4 / 4; ++j) {
+        const uint4 q = h4[j];
+        r += (int)(q.x > h) + (int)(q.y > h) + (int)(q.z > h) + (int)(q.w > h);
+      }
+      const int ne = min(K - r, fc[t]);
+      if (ne > 0) {
+        const int base = (int)atomicAdd(&sh[0], (unsigned)ne);
+        for (int j = 0; j < ne; ++j) fsurv[base + j] = fk[t * K + j];
+      }
+      if (fm[t] > -INFINITY) part += fs[t] * expf(fm[t] - Mx);
     }
+    part = warp_sum(part);  // sum_g s_g e^{m_g - M}: xor tree per warp, then the warps in order
+    if (lane == 0) wps[warp] = part;
   }
   __syncthreads();
   trace_mark(s.trace, 15);
-  const uint32_t Mk = reinterpret_cast<const unsigned*>(nsh)[1];
-  const float Mx = Mk ? __uint_as_float((Mk & 0x80000000u) ? (Mk & 0x7fffffffu) : ~Mk) : -INFINITY;
-  {
-    const unsigned long long Tfin = *T2s;
-    const int n = G * K;
-    for (int i0 = 0; i0 < n; i0 += blockDim.x) {
-      const int i = i0 + threadIdx.x;
-      const unsigned long long x = i < n ? fk[i] : 0ull;
-      const bool keep = x > 1ull && x >= Tfin;
-      const uint32_t bal = __ballot_sync(0xffffffffu, keep);
-      int base = 0;
-      if (lane == 0 && bal) base = atomicAdd(nsh, __popc(bal));
-      base = __shfl_sync(0xffffffffu, base, 0);
-      if (keep) fsurv[base + __popc(bal & ((1u << lane) - 1u))] = x;
-    }
-    float part = 0.f;  // sum_g s_g e^{m_g - M}: xor tree per warp, then the warps in order
-    for (int t = threadIdx.x; t < G; t += blockDim.x)
-      if (fm[t] > -INFINITY) part += fs[t] * expf(fm[t] - Mx);
-    part = warp_sum(part);
-    if (lane == 0) wpart[32 + warp] = part;
+  const int ns = (int)sh[0];
+  if (s.trace && threadIdx.x == 0) {
+    s.trace[24] = ns;
+    s.trace[25] = Mk;
   }
-  __syncthreads();
-  const int ns = *nsh;
-  for (int t = threadIdx.x; t < ns; t += blockDim.x) {
-    const unsigned long long x = fsurv[t];
-    int rank = 0;
-#pragma unroll 8
-    for (int j = 0; j < ns; ++j) rank += fsurv[j] > x;
-    if (rank < K) out[rank] = x;
-  }
-  __syncthreads();
-  float sum = 0.f;
-  for (int w2 = 0; w2 < nwarps; ++w2) sum += wpart[32 + w2];
   const bool ok = Mx > -INFINITY;
+  float sum = 0.f;
+  for (int w2 = 0; w2 < nwarps; ++w2) sum += wps[w2];
   const float lse = ok ? Mx + logf(sum) : __int_as_float(0x7fc00000);
-  for (int r = threadIdx.x; r < K; r += blockDim.x) {
-    const unsigned long long x = out[r];
-    const bool v = ok && x > 1ull;
-    const float z = v ? key_value(x) : -INFINITY;
-    a.top_ids[r] = v ? key_id(x) : -1;
-    a.top_logits[r] = z;
-    a.top_logp[r] = v ? z - lse : -INFINITY;
+  {
+    int P = 1;  // lanes per candidate
+    while (P < 8 && ns * (P * 2) <= (int)blockDim.x) P <<= 1;
+    const int nrk = ((int)blockDim.x / 32) * 32;
+    for (int v0 = 0; v0 < ns * P; v0 += nrk) {  // uniform trip count: every lane shuffles
+      const int v = v0 + threadIdx.x, i = v / P, part = v % P;
+      const bool act = i < ns;
+      const unsigned long long x = act ? fsurv[i] : 0ull;
+      int rk = 0;
+      if (act)
+#pragma unroll 4
+        for (int j = part; j < ns; j += P) rk += fsurv[j] > x;
+      for (int o = P >> 1; o > 0; o >>= 1) rk += __shfl_xor_sync(0xffffffffu, rk, o);
+      if (act && part == 0 && rk < K) {
+        const float z = key_value(x);
+        a.top_ids[rk] = key_id(x);
+        a.top_logits[rk] = z;
+        a.top_logp[rk] = z - lse;
+      }
+    }
+  }
+  for (int r = ns + threadIdx.x; r < K; r += blockDim.x) {  // fewer valid keys than K: padding (R17)
+    a.top_ids[r] = -1;
+    a.top_logits[r] = -INFINITY;
+    a.top_logp[r] = -INFINITY;
   }
   if (threadIdx.x == 0) a.lse[0] = lse;
   trace_mark(s.trace, 7);
@@ -726,7 +730,7 @@ static bool cstep_plan(const ds_clusters* c, const ds_router* r, int B, int k_t,
   }
   // the last CTA merges the G records inside its ring
   const size_t G = (size_t)C * Q;
-  if (G * (16 * k_t + 8) + 512 > (size_t)p->hp.stages * p->hp.stage_bytes) return false;
+  if (G * (16 * k_t + 20) + 1024 > (size_t)p->hp.stages * p->hp.stage_bytes) return false;
   p->total = 256 + align_up(G * (2 + k_t) * sizeof(unsigned long long), 256);
   return true;
 }
@@ -792,6 +796,13 @@ cudaError_t launch_cstep(const ds_clusters* c, const ds_router* r, const void* h
   s.crec = reinterpret_cast<unsigned long long*>(w8 + 256);
   s.ctr = reinterpret_cast<unsigned*>(w8);
   s.trace = debug_trace();
+  {
+    static const int variant = [] {
+      const char* v = getenv("DS_CSTEP_VARIANT");
+      return v && v[0] ? atoi(v) : 0;
+    }();
+    s.variant = variant;
+  }
   return c->dtype == DS_BF16 ? launch_cstep_t<__nv_bfloat16>(s, p.smem, p.Q, p.C, st, pdl)
                              : launch_cstep_t<float>(s, p.smem, p.Q, p.C, st, pdl);
 }

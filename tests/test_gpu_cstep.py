@@ -36,7 +36,8 @@ def _setup(V, d, M, h_r, dtype, regime, seed_part=2):
 
 @pytest.mark.parametrize("Q", ["16", "8", "4", "2", "0"])
 @pytest.mark.parametrize("dtype,h_r,k_t", [("bf16", 16, 8), ("f32", 16, 1), ("bf16", 0, 32), ("f32", 8, 32)])
-def test_cluster_step_exact_bit_exact(Q, dtype, h_r, k_t, monkeypatch):
+@pytest.mark.parametrize("k_max,k_min", [(16, 4), (40, 33)])  # k <= 32 and k > 32 up to k = M
+def test_cluster_step_exact_bit_exact(Q, dtype, h_r, k_t, k_max, k_min, monkeypatch):
     monkeypatch.setenv("DS_CLUSTER_Q", Q)
     D = _dyn()
     V, d, M = 7919, 384, 40     # prime V, ragged clusters, M not a multiple of Q
@@ -46,9 +47,9 @@ def test_cluster_step_exact_bit_exact(Q, dtype, h_r, k_t, monkeypatch):
     assert st.launches == 1
     for t in range(4):
         hp, e, hn = S.step_inputs(1, d, t, dtype, "exact", h_r=h_r)
-        st(hp.to(DEV), e.to(DEV), hn.to(DEV), t=t, k_max=16, k_min=4)
+        st(hp.to(DEV), e.to(DEV), hn.to(DEV), t=t, k_max=k_max, k_min=k_min)
         torch.cuda.synchronize()
-        ref = O.draft_step(part, ro, Wo, f64(hp), f64(e), f64(hn), t, 16, 4, k_t)[0]
+        ref = O.draft_step(part, ro, Wo, f64(hp), f64(e), f64(hn), t, k_max, k_min, k_t)[0]
         assert np.array_equal(st.scores[0].cpu().numpy(), ref["scores"].astype(np.float32)), "scores"
         cnt = st.sel_count[0].item()
         assert st.sel[0, :cnt].cpu().tolist() == ref["sel"].tolist()
