@@ -50,6 +50,7 @@ struct CStepArgs {
                              // written (the merger zeroes them after reading)
   unsigned* ctr;             // unused (the merger polls the records)
   unsigned long long* trace;
+  int xs_slot;  // ring slot holding [h_prev ‖ e] (-1: a separate shared-memory region)
   int variant;  // debug A/B switches (DS_CSTEP_VARIANT, read once); none defined at present
 };
 
@@ -57,7 +58,9 @@ struct CStepArgs {
 struct CExtra {
   uint32_t xs, p1, a1, sc, w2s, b1s, b2s, offs, selb, xb, mask, sel, sloff, cnt, tmp, wm, ws, wl, surv, out, misc, total;
 };
-__host__ __device__ inline CExtra cstep_extra(int d, int esz, int M, int h_r, int rows1, int Q, int K, int S, int C) {
+// xs_in_ring: [h_prev ‖ e] lives in a ring slot after the router rows (free until streaming starts)
+__host__ __device__ inline CExtra cstep_extra(int d, int esz, int M, int h_r, int rows1, int Q, int K, int S, int C,
+                                             int xs_in_ring) {
   CExtra X;
   uint32_t o = 0;
   auto take = [&](uint32_t bytes) {
@@ -67,7 +70,7 @@ __host__ __device__ inline CExtra cstep_extra(int d, int esz, int M, int h_r, in
   };
   const int U = (rows1 + Q - 1) / Q;
   const int Ms = h_r > 0 ? (M + Q - 1) / Q : 0;
-  X.xs = take(2u * d * esz);
+  X.xs = take(xs_in_ring ? 0u : 2u * d * esz);
   X.p1 = take(4u * 2 * U);
   X.a1 = take(4u * (h_r > 0 ? h_r : 1));
   X.sc = take(4u * ((M + 3) & ~3));
@@ -252,9 +255,9 @@ __global__ void __launch_bounds__((kMaxStages + 1) * 32, 1) cstep_kernel(const C
   const int Q = (int)cluster_nctarank(), q = (int)cluster_ctarank();
   const int cid = (int)cluster_id_x(), C = (int)cluster_count_x();
   const int M = a.M, d = a.d, K = a.k_t, S = a.stages;
-  const CExtra X = cstep_extra(d, (int)sizeof(T), M, s.h_r, s.rows1, Q, K, S, C);
+  const CExtra X = cstep_extra(d, (int)sizeof(T), M, s.h_r, s.rows1, Q, K, S, C, s.xs_slot >= 0);
   uint8_t* ex = c.extra;
-  T* xs = reinterpret_cast<T*>(ex + X.xs);
+  T* xs = reinterpret_cast<T*>(s.xs_slot >= 0 ? c.ring + (size_t)s.xs_slot * a.stage_bytes : ex + X.xs);
   float* p1 = reinterpret_cast<float*>(ex + X.p1);
   float* a1 = reinterpret_cast<float*>(ex + X.a1);
   float* sc = reinterpret_cast<float*>(ex + X.sc);
@@ -696,7 +699,7 @@ static int max_clusters(int Q) {
 
 struct CStepPlan {
   HeadPlan hp;
-  int Q, C, extra, rows1;
+  int Q, C, extra, rows1, xs_slot;
   size_t smem, total;
 };
 
@@ -711,16 +714,25 @@ static bool cstep_plan(const ds_clusters* c, const ds_router* r, int B, int k_t,
   p->C = C;
   p->rows1 = r->h_r > 0 ? r->h_r : r->M;
   const int esz = c->dtype == DS_BF16 ? 2 : 4;
-  const int x0 = (int)cstep_extra(c->d, esz, c->M, r->h_r, p->rows1, Q, k_t, kMaxStages, C).total;
+  const int x0 = (int)cstep_extra(c->d, esz, c->M, r->h_r, p->rows1, Q, k_t, kMaxStages, C, 0).total;
   if (!head_plan_ex(c, 1, k_t, max_shortlist, x0, 1, &p->hp, C * Q)) return false;
   // logits never touch shared memory here (online per-warp state): no per-CTA logit buffer, and
   // the freed bytes go back to the ring
   p->hp.lcap = 0;
   const int smax = max_smem_optin();
-  for (int st = kMaxStages; st >= 2; --st) {
-    const int xb = (int)cstep_extra(c->d, esz, c->M, r->h_r, p->rows1, Q, k_t, st, C).total;
+  // router rows per CTA occupy ring slots [0, n1); [h_prev ‖ e] takes the next slot(s) if free
+  const int n1 = (2 * ((p->rows1 + Q - 1) / Q) + p->hp.stage_rows - 1) / p->hp.stage_rows;
+  const int xs_slots = (int)((2 * (size_t)c->d * esz + p->hp.stage_bytes - 1) / p->hp.stage_bytes);
+  // at most 11 ring slots: measured at Llama-3 (k = 32,32,8x6), us/step by slots 8..12 =
+  // 24.3, 23.8, 23.4, 22.9, 23.4 (scripts/variants.sh DS_CSTEP_STAGES=n)
+  const char* sv = getenv("DS_CSTEP_STAGES");
+  const int smax_st = sv && sv[0] ? std::max(2, std::min(kMaxStages, atoi(sv))) : std::min(kMaxStages, 11);
+  for (int st = smax_st; st >= 2; --st) {
+    const int alias = n1 + xs_slots <= st;
+    const int xb = (int)cstep_extra(c->d, esz, c->M, r->h_r, p->rows1, Q, k_t, st, C, alias).total;
     const size_t sm = head_smem(st, p->hp.stage_bytes, 1, c->d, esz, 0, xb).total;
     if (sm <= (size_t)smax) {
+      p->xs_slot = alias ? n1 : -1;
       p->hp.stages = st;
       p->extra = xb;
       p->smem = sm;
@@ -793,6 +805,7 @@ cudaError_t launch_cstep(const ds_clusters* c, const ds_router* r, const void* h
   s.rows1 = p.rows1;
   s.k = k;
   s.extra_bytes = p.extra;
+  s.xs_slot = p.xs_slot;
   s.crec = reinterpret_cast<unsigned long long*>(w8 + 256);
   s.ctr = reinterpret_cast<unsigned*>(w8);
   s.trace = debug_trace();
