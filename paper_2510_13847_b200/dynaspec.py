@@ -462,6 +462,19 @@ class DraftStep:
                                        int(self.shared), ctypes.byref(self._o), self.ws_head.ptr(),
                                        self.ws_head.nbytes, _stream(stream)), "dynaspec_step_head")
 
+    def bind_outputs(self, top_ids=None, top_logp=None):
+        """Write the token top-k ids / log-probs into caller tensors (contiguous (B, k_t) int32 /
+        float32 on the step's device, e.g. slices of one buffer read back with a single copy)."""
+        for name, t, dt in (("top_ids", top_ids, torch.int32), ("top_logp", top_logp, torch.float32)):
+            if t is None:
+                continue
+            if t.dtype != dt or tuple(t.shape) != (self.B, self.k_t) or not t.is_contiguous():
+                raise ValueError(f"{name}: need a contiguous ({self.B}, {self.k_t}) {dt} tensor")
+            setattr(self, name, t)
+        self._o.top_ids = _ptr(self.top_ids)
+        self._o.top_logp = _ptr(self.top_logp)
+        return self
+
     def outputs(self):
         return {k: getattr(self, k) for k in ("scores", "sel", "sel_count", "sl_offsets", "top_ids", "top_logits",
                                                "top_logp", "lse", "z")}
