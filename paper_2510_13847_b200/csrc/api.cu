@@ -190,12 +190,25 @@ ds_status dynaspec_select(const float* scores, int32_t B, const ds_clusters* c, 
   return err == cudaSuccess ? DS_OK : DS_ERR_CUDA;
 }
 
+// Offset (from the head region) of the head-only cluster kernel's records: after every other head
+// kernel's scratch, so their partials never leave non-zero words where the records are polled.
+static HeadPlan pmax0(const ds_clusters* c, int32_t B, int32_t k_t) {
+  HeadPlan p = {};
+  head_plan(c, B, k_t, 0, &p);
+  return p;
+}
+
+static size_t head_rec_offset(const ds_clusters* c, int32_t B, int32_t k_t, const HeadPlan& pmax) {
+  return align_up(std::max(std::max(pmax.part_bytes, tc_head_part_bytes(c, B, k_t)), tc_batched_ws_bytes(c, B, k_t)),
+                  256);
+}
+
 size_t dynaspec_head_forward_ws(const ds_clusters* c, int32_t B, int32_t k_t) {
   HeadPlan p;
   if (!c || B < 1 || k_t < 1 || k_t > kMaxKt) return 0;
   if (!head_plan(c, B, k_t, 0, &p)) return 0;
-  return ws_layout(0, std::max(std::max(p.part_bytes, tc_head_part_bytes(c, B, k_t)),
-                               tc_batched_ws_bytes(c, B, k_t))).total;
+  // + a dedicated tail for the head-only cluster kernel's records (must stay zero between calls)
+  return ws_layout(0, head_rec_offset(c, B, k_t, p) + (B == 1 ? cstep_head_rec_bytes(c, k_t) : 0)).total;
 }
 
 ds_status dynaspec_head_forward(const ds_clusters* c, const void* h_new, int32_t B, const int32_t* sel,
@@ -226,6 +239,12 @@ ds_status dynaspec_head_forward(const ds_clusters* c, const void* h_new, int32_t
     err = launch_tc_head(c, h_new, B, sel, sel_count, sl_offsets, k_t, max_shortlist, top_ids, top_logits,
                          top_logp, lse, z_out, z_stride, reinterpret_cast<float*>(w8 + L.head),
                          reinterpret_cast<unsigned*>(w8 + L.counters), (cudaStream_t)stream, false);
+  } else if (B == 1 && !shared && cstep_head_supported(c, k_t, max_shortlist) &&
+             ws_bytes >= L.head + head_rec_offset(c, B, k_t, pmax0(c, B, k_t)) + cstep_head_rec_bytes(c, k_t)) {
+    // one CTA per SM streaming chunk c of the shortlist on CTA c mod G, per-warp online (max, sum, top-k)
+    const size_t off = L.head + head_rec_offset(c, B, k_t, pmax0(c, B, k_t));
+    err = launch_cstep_head(c, h_new, sel, sel_count, sl_offsets, k_t, max_shortlist, top_ids, top_logits, top_logp,
+                            lse, z_out, z_stride, w8 + off, (cudaStream_t)stream);
   } else {
     err = launch_head(c, p, h_new, B, sel, sel_count, sl_offsets, shared ? 1 : 0, k_t, max_shortlist, top_ids,
                       top_logits, top_logp, lse, z_out, z_stride, reinterpret_cast<float*>(w8 + L.head),
@@ -383,8 +402,7 @@ size_t dynaspec_draft_step_ws(const ds_clusters* c, const ds_router* r, int32_t 
   const size_t meta = meta_plan(r, B).part_bytes;
   const size_t scores = (size_t)B * r->M * sizeof(float);
   return std::max(ws_layout(align_up(meta, 256) + align_up(scores, 256),
-                            std::max(std::max(p.part_bytes, tc_head_part_bytes(c, B, k_t)),
-                                     tc_batched_ws_bytes(c, B, k_t))).total,
+                            head_rec_offset(c, B, k_t, p) + (B == 1 ? cstep_head_rec_bytes(c, k_t) : 0)).total,
                   step_ws_bytes(c, r, B, k_t));
 }
 
@@ -484,6 +502,11 @@ ds_status dynaspec_draft_step(const ds_clusters* c, const ds_router* r, const vo
     err = launch_tc_head(c, h_new, B, out->sel, out->sel_count, out->sl_offsets, k_t, ms, out->top_ids,
                          out->top_logits, out->top_logp, out->lse, out->z_out, out->z_stride,
                          reinterpret_cast<float*>(w8 + L.head), counters, sd, !two_streams && head_begin == nullptr);
+  } else if (B == 1 && !shared && cstep_head_supported(c, k_t, ms) &&
+             ws_bytes >= L.head + head_rec_offset(c, B, k_t, pmax) + cstep_head_rec_bytes(c, k_t)) {
+    err = launch_cstep_head(c, h_new, out->sel, out->sel_count, out->sl_offsets, k_t, ms, out->top_ids,
+                            out->top_logits, out->top_logp, out->lse, out->z_out, out->z_stride,
+                            w8 + L.head + head_rec_offset(c, B, k_t, pmax), sd);
   } else {
     err = launch_head(c, p, h_new, B, out->sel, out->sel_count, out->sl_offsets, shared ? 1 : 0, k_t, ms,
                       out->top_ids, out->top_logits, out->top_logp, out->lse, out->z_out, out->z_stride,

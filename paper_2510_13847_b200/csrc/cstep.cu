@@ -51,6 +51,7 @@ struct CStepArgs {
   unsigned* ctr;             // unused (the merger polls the records)
   unsigned long long* trace;
   int xs_slot;  // ring slot holding [h_prev ‖ e] (-1: a separate shared-memory region)
+  int head_only;  // 1: S1-S3 ran elsewhere (dynaspec_step_route); the TopK comes from h.sel / h.sel_count
   int variant;  // debug A/B switches (DS_CSTEP_VARIANT, read once); none defined at present
 };
 
@@ -303,9 +304,26 @@ __global__ void __launch_bounds__((kMaxStages + 1) * 32, 1) cstep_kernel(const C
   }
   for (int m = threadIdx.x; m < M; m += blockDim.x) selb[m] = 0;
   if (threadIdx.x < 16) misc[threadIdx.x] = 0;
+  if (threadIdx.x < 32) mask[threadIdx.x] = 0u;
   __syncthreads();
   cluster_arrive_relaxed();  // paired with the wait before the first DSMEM store (barrier inits are fenced)
   trace_mark(s.trace, 0);
+  if (s.head_only) {
+    // S1-S3 ran on S_m (dynaspec_step_route): the TopK mask from the selection in global memory
+    if (warp == S && lane == 0) {
+      mbar_arrive_expect_tx(xbar, hb);
+      bulk_g2s(c.hs, a.h, hb, xbar, policy_evict_first());
+    }
+    const int cnt = __ldg(a.sel_count);
+    for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
+      const int m = __ldg(a.sel + i);
+      atomicOr(&mask[m >> 5], 1u << (m & 31));
+    }
+    for (int m = threadIdx.x; m <= M; m += blockDim.x) offs[m] = __ldg(a.offsets + m);
+    cluster_wait_acquire();  // pairs the launch-time arrive (a one-CTA cluster: no peer)
+    mbar_wait(xbar, 0);
+    __syncthreads();
+  } else {
   if (warp == S) {
     if (lane == 0) {
       // router weights are constants: stream them before the PDL wait (W2 slice, then W1 rows)
@@ -443,14 +461,16 @@ __global__ void __launch_bounds__((kMaxStages + 1) * 32, 1) cstep_kernel(const C
     }
   }
   __syncthreads();
+  }
   fence_proxy_async_smem();  // the ring was read by generic loads (W1 rows) before TMA reuses it
   trace_mark(s.trace, 4);
   if (warp == S) {
-    cstep_produce<T>(a, c, mask, offs, (int)blockIdx.x, (int)gridDim.x, (uint32_t)n1);
+    cstep_produce<T>(a, c, mask, offs, (int)blockIdx.x, (int)gridDim.x, (uint32_t)(s.head_only ? 0 : n1));
   } else {  // logits folded into per-warp (m, s) + a sorted top-K list while the ring streams
     float m, se;
     unsigned long long mine;
-    cstep_consume<T>(a, c, warp, lane, n1 > warp ? (uint32_t)((n1 - 1 - warp) / S + 1) : 0u, m, se, mine);
+    const int it0 = s.head_only ? 0 : n1;
+    cstep_consume<T>(a, c, warp, lane, it0 > warp ? (uint32_t)((it0 - 1 - warp) / S + 1) : 0u, m, se, mine);
     if (lane < K) wl[warp * K + lane] = mine;
     if (lane == 0) {
       wm[warp] = m;
@@ -506,7 +526,7 @@ __global__ void __launch_bounds__((kMaxStages + 1) * 32, 1) cstep_kernel(const C
     }
   }
   trace_mark(s.trace, 9);
-  if (g == G - 1) {  // the caller's copies of scores / selection / offsets (S3 outputs), off the merger CTA
+  if (!s.head_only && g == G - 1) {  // the caller's copies of scores / selection / offsets (S3 outputs), off the merger CTA
     emit_fast(mask, M, offs, sel_s, cnt_s, sloff_s, tmp);
     __syncthreads();
     const int cnt = *cnt_s;
@@ -705,16 +725,19 @@ struct CStepPlan {
 
 static bool cstep_plan(const ds_clusters* c, const ds_router* r, int B, int k_t, int64_t max_shortlist, int shared,
                        CStepPlan* p) {
+  // r == nullptr: head-only launch (the selection comes from dynaspec_step_route): one CTA per SM,
+  // no cluster exchanges
   if (B != 1 || shared || k_t > kCStepMaxKt) return false;
-  const int Q = cluster_q();
-  if (Q < 2 || Q > 16) return false;
+  const int Q = r ? cluster_q() : 1;
+  if (r && (Q < 2 || Q > 16)) return false;
   const int C = max_clusters(Q);
   if (C < 1 || C * Q < 64) return false;  // too few SMs would stream the head slowly
   p->Q = Q;
   p->C = C;
-  p->rows1 = r->h_r > 0 ? r->h_r : r->M;
+  const int h_r = r ? r->h_r : 0;
+  p->rows1 = r ? (r->h_r > 0 ? r->h_r : r->M) : 0;
   const int esz = c->dtype == DS_BF16 ? 2 : 4;
-  const int x0 = (int)cstep_extra(c->d, esz, c->M, r->h_r, p->rows1, Q, k_t, kMaxStages, C, 0).total;
+  const int x0 = (int)cstep_extra(c->d, esz, c->M, h_r, p->rows1, Q, k_t, kMaxStages, C, 0).total;
   if (!head_plan_ex(c, 1, k_t, max_shortlist, x0, 1, &p->hp, C * Q)) return false;
   // logits never touch shared memory here (online per-warp state): no per-CTA logit buffer, and
   // the freed bytes go back to the ring
@@ -729,7 +752,7 @@ static bool cstep_plan(const ds_clusters* c, const ds_router* r, int B, int k_t,
   const int smax_st = sv && sv[0] ? std::max(2, std::min(kMaxStages, atoi(sv))) : std::min(kMaxStages, 11);
   for (int st = smax_st; st >= 2; --st) {
     const int alias = n1 + xs_slots <= st;
-    const int xb = (int)cstep_extra(c->d, esz, c->M, r->h_r, p->rows1, Q, k_t, st, C, alias).total;
+    const int xb = (int)cstep_extra(c->d, esz, c->M, h_r, p->rows1, Q, k_t, st, C, alias).total;
     const size_t sm = head_smem(st, p->hp.stage_bytes, 1, c->d, esz, 0, xb).total;
     if (sm <= (size_t)smax) {
       p->xs_slot = alias ? n1 : -1;
@@ -806,6 +829,7 @@ cudaError_t launch_cstep(const ds_clusters* c, const ds_router* r, const void* h
   s.k = k;
   s.extra_bytes = p.extra;
   s.xs_slot = p.xs_slot;
+  s.head_only = 0;
   s.crec = reinterpret_cast<unsigned long long*>(w8 + 256);
   s.ctr = reinterpret_cast<unsigned*>(w8);
   s.trace = debug_trace();
@@ -818,6 +842,42 @@ cudaError_t launch_cstep(const ds_clusters* c, const ds_router* r, const void* h
   }
   return c->dtype == DS_BF16 ? launch_cstep_t<__nv_bfloat16>(s, p.smem, p.Q, p.C, st, pdl)
                              : launch_cstep_t<float>(s, p.smem, p.Q, p.C, st, pdl);
+}
+
+// Head-only cluster-kernel launch (P:262-264 after S1-S3 on S_m): B = 1, the selection in sel /
+// sel_count (device), records in `rec` (zero-filled once; left zeroed).
+bool cstep_head_supported(const ds_clusters* c, int k_t, int64_t max_shortlist) {
+  CStepPlan p;
+  const char* v = getenv("DS_CSTEP_HEAD");
+  if (v && v[0] == '0') return false;
+  return cstep_plan(c, nullptr, 1, k_t, max_shortlist, 0, &p);
+}
+
+size_t cstep_head_rec_bytes(const ds_clusters* c, int k_t) {
+  CStepPlan p;
+  return cstep_plan(c, nullptr, 1, k_t, 0, 0, &p) ? p.total : 0;
+}
+
+cudaError_t launch_cstep_head(const ds_clusters* c, const void* h_new, const int32_t* sel, const int32_t* sel_count,
+                              const int32_t* sl_offsets, int k_t, int64_t max_shortlist, int32_t* top_ids,
+                              float* top_logits, float* top_logp, float* lse, float* z_out, int64_t z_stride,
+                              void* rec, cudaStream_t st) {
+  CStepPlan p;
+  if (!cstep_plan(c, nullptr, 1, k_t, max_shortlist, 0, &p)) return cudaErrorInvalidValue;
+  if ((reinterpret_cast<uintptr_t>(h_new) & 15u) != 0) return cudaErrorInvalidValue;
+  uint8_t* w8 = static_cast<uint8_t*>(rec);
+  CStepArgs s = {};
+  fill_head_args(s.h, c, p.hp, h_new, 0, 1, sel, sel_count, sl_offsets, 0, k_t, max_shortlist, top_ids, top_logits,
+                 top_logp, lse, z_out, z_stride, nullptr, reinterpret_cast<unsigned*>(w8), false);
+  s.k = 1;
+  s.extra_bytes = p.extra;
+  s.xs_slot = p.xs_slot;
+  s.head_only = 1;
+  s.crec = reinterpret_cast<unsigned long long*>(w8 + 256);
+  s.ctr = reinterpret_cast<unsigned*>(w8);
+  s.trace = debug_trace();
+  return c->dtype == DS_BF16 ? launch_cstep_t<__nv_bfloat16>(s, p.smem, p.Q, p.C, st, false)
+                             : launch_cstep_t<float>(s, p.smem, p.Q, p.C, st, false);
 }
 
 bool cstep_pointers_ok(const ds_router* r, const void* h_prev, const void* e, const void* h_new) {

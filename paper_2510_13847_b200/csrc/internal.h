@@ -75,6 +75,13 @@ cudaError_t launch_cstep(const ds_clusters* c, const ds_router* r, const void* h
                          float* top_logp, float* lse, float* z_out, int64_t z_stride, void* ws, cudaStream_t st,
                          bool pdl);
 
+bool cstep_head_supported(const ds_clusters* c, int k_t, int64_t max_shortlist);
+size_t cstep_head_rec_bytes(const ds_clusters* c, int k_t);
+cudaError_t launch_cstep_head(const ds_clusters* c, const void* h_new, const int32_t* sel, const int32_t* sel_count,
+                              const int32_t* sl_offsets, int k_t, int64_t max_shortlist, int32_t* top_ids,
+                              float* top_logits, float* top_logp, float* lse, float* z_out, int64_t z_stride,
+                              void* rec, cudaStream_t st);
+
 // ---- tcgen05 shared-shortlist head (tc_head.cu), bf16, R <= 64 rows sharing one shortlist
 bool tc_head_supported(const ds_clusters* c, int R, int k_t, int64_t max_shortlist);
 size_t tc_head_part_bytes(const ds_clusters* c, int R, int k_t);

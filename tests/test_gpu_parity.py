@@ -53,7 +53,9 @@ def _oracle_router(rt):
 
 # ------------------------------------------------------------------ golden worked example
 
-def test_e2e1_golden_on_gpu():
+@pytest.mark.parametrize("cstep_head", ["1", "0"])  # head-only cluster kernel (B = 1) or the grid head
+def test_e2e1_golden_on_gpu(cstep_head, monkeypatch):
+    monkeypatch.setenv("DS_CSTEP_HEAD", cstep_head)
     Dy = _dyn()
     d = 8  # pad the 2-D example with zero dimensions (kernels need d % 8 == 0); dot products unchanged
     W = torch.zeros((6, d), dtype=torch.float32)
@@ -108,7 +110,9 @@ def test_e2e1_golden_on_gpu():
 @pytest.mark.parametrize("fused", [True, False])
 @pytest.mark.parametrize("dtype", ["bf16", "f32"])
 @pytest.mark.parametrize("shared", [False, True])
-def test_exact_regime_pipeline(dtype, shared, fused):
+@pytest.mark.parametrize("cstep_head", ["1", "0"])  # head-only cluster kernel (B = 1) or the grid head
+def test_exact_regime_pipeline(dtype, shared, fused, cstep_head, monkeypatch):
+    monkeypatch.setenv("DS_CSTEP_HEAD", cstep_head)
     Dy = _dyn()
     V, d, M, h_r, B = 5003, 256, 24, 16, 3   # ragged V (prime), several tiles, ragged clusters
     W, rt, tau, part, c, r = _setup(V, d, M, h_r, dtype, "exact")
@@ -138,7 +142,9 @@ def test_exact_regime_pipeline(dtype, shared, fused):
                        st.lse[b].item(), ref[b]["z"], ref[b]["V_S"], k_t, torch.float32, exact=True)
 
 
-def test_exact_ties_injected():
+@pytest.mark.parametrize("cstep_head", ["1", "0"])  # head-only cluster kernel (B = 1) or the grid head
+def test_exact_ties_injected(cstep_head, monkeypatch):
+    monkeypatch.setenv("DS_CSTEP_HEAD", cstep_head)
     """Duplicated router rows (score ties -> lower cluster id) and duplicated W rows
     (logit ties -> lower token id), exact regime."""
     Dy = _dyn()
@@ -216,7 +222,9 @@ def test_random_regime_config(cfg, dtype, B, fused):
 
 @pytest.mark.parametrize("fused", [True, False])
 @pytest.mark.parametrize("positions", [(0, 2)])
-def test_llama3_full_size(positions, fused):
+@pytest.mark.parametrize("cstep_head", ["1", "0"])  # head-only cluster kernel (B = 1) or the grid head
+def test_llama3_full_size(positions, fused, cstep_head, monkeypatch):
+    monkeypatch.setenv("DS_CSTEP_HEAD", cstep_head)
     """BASELINE configs[2] at full size (V=128256, d=4096, M=256, bf16), the bench's launch
     configuration (two streams, B=1); every logit of V_S compared with the oracle."""
     Dy = _dyn()
