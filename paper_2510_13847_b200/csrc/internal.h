@@ -20,6 +20,7 @@ struct MetaPlan {
   int KC;       // K-chunk per split (elements of the 2d input)
   int KS;       // number of K splits
   int rows1;    // layer-1 output rows (h_r, or M for a linear router)
+  int RB;       // rows per layer-1 CTA (grid z = ceil(B / RB) row blocks)
   size_t part_bytes;
 };
 MetaPlan meta_plan(const ds_router* r, int B);

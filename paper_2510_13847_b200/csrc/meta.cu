@@ -54,10 +54,11 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(const float* __rest
 template <typename T>
 __global__ void __launch_bounds__(kMetaThreads) meta_l1_kernel(const T* __restrict__ W1, const T* __restrict__ h_prev,
                                                                const T* __restrict__ e, int B, int d, int rows1,
-                                                               int KC, float* __restrict__ part, int pdl) {
+                                                               int KC, int RB, float* __restrict__ part, int pdl) {
   constexpr int E = Elem<T>::kPer16B;
   extern __shared__ __align__(16) uint8_t msm[];
-  T* xs = reinterpret_cast<T*>(msm);  // [B][KC]
+  T* xs = reinterpret_cast<T*>(msm);  // [RB][KC]: rows [b0, b0 + nb) of this CTA's row block
+  const int b0 = blockIdx.z * RB, nb = min(RB, B - b0);
   const int dr = 2 * d;
   const int k0 = blockIdx.y * KC;
   const int kn = min(KC, dr - k0);
@@ -76,16 +77,16 @@ __global__ void __launch_bounds__(kMetaThreads) meta_l1_kernel(const T* __restri
   if (pdl) pdl_wait();
   // stage x = [h_prev || e][:, k0:k0+kn]; a 16-byte chunk never straddles h/e since d % E == 0
   const int cpr = kn / E;
-  for (int idx = threadIdx.x; idx < B * cpr; idx += blockDim.x) {
+  for (int idx = threadIdx.x; idx < nb * cpr; idx += blockDim.x) {
     const int b = idx / cpr, c = (idx - b * cpr) * E;
     const int k = k0 + c;
-    const T* src = k < d ? h_prev + (size_t)b * d + k : e + (size_t)b * d + (k - d);
+    const T* src = k < d ? h_prev + (size_t)(b0 + b) * d + k : e + (size_t)(b0 + b) * d + (k - d);
     *reinterpret_cast<uint4*>(xs + (size_t)b * KC + c) = *reinterpret_cast<const uint4*>(src);
   }
   __syncthreads();
   if (pdl) pdl_launch_dependents();
   if (u >= rows1) return;
-  for (int b = 0; b < B; ++b) {
+  for (int b = 0; b < nb; ++b) {
     float acc = 0.f;
 #pragma unroll
     for (int i = 0; i < kMaxChunks; ++i) {
@@ -99,7 +100,7 @@ __global__ void __launch_bounds__(kMetaThreads) meta_l1_kernel(const T* __restri
       }
     }
     acc = warp_sum(acc);
-    if (lane == 0) part[((size_t)blockIdx.y * B + b) * rows1 + u] = acc;
+    if (lane == 0) part[((size_t)blockIdx.y * B + b0 + b) * rows1 + u] = acc;
   }
 }
 
@@ -148,21 +149,20 @@ __global__ void __launch_bounds__(kMetaThreads) meta_l2_kernel(const float* __re
     emit_fast(mask, M, offs, sel + (size_t)b * M, sel_count + b, sl_off + (size_t)b * (M + 1), tmp);
     return;
   }
-  // shared mode: the last row-CTA (scores of every row are published) forms the union of the TopKs
+  // shared mode: every row-CTA publishes its TopK mask (workspace tail after the layer-1 partials);
+  // the last row-CTA ORs the B masks into the union and emits it (R9)
+  uint32_t* gmask = reinterpret_cast<uint32_t*>(const_cast<float*>(part) + (size_t)KS * B * rows1);
+  for (int w = threadIdx.x; w < words; w += blockDim.x) gmask[(size_t)b * (kMaxM / 32) + w] = mask[w];
   __syncthreads();
   if (threadIdx.x == 0) is_last = release_add(counter, 1u) == (unsigned)(gridDim.x - 1);
   __syncthreads();
   if (!is_last) return;
   if (threadIdx.x == 0) fence_acq_rel_gpu();
   __syncthreads();
-  for (int w = threadIdx.x; w < words; w += blockDim.x) acc[w] = 0u;
-  for (int r = 0; r < B; ++r) {
-    __syncthreads();
-    for (int m = threadIdx.x; m < M; m += blockDim.x) s[m] = __ldcg(scores + (size_t)r * M + m);
-    __syncthreads();
-    rank_mask(s, M, k_per_row ? k_per_row[r] : k, mask);
-    __syncthreads();
-    for (int w = threadIdx.x; w < words; w += blockDim.x) acc[w] |= mask[w];
+  for (int w = threadIdx.x; w < words; w += blockDim.x) {
+    uint32_t u = 0u;
+    for (int r = 0; r < B; ++r) u |= __ldcg(gmask + (size_t)r * (kMaxM / 32) + w);
+    acc[w] = u;
   }
   __syncthreads();
   emit_fast(acc, M, offs, sel, sel_count, sl_off, tmp);
@@ -182,8 +182,11 @@ MetaPlan meta_plan(const ds_router* r, int B) {
   while (KC > 32 * E && (size_t)B * KC * esz > 96 * 1024) KC /= 2;
   if (KC > dr) KC = ((dr + E - 1) / E) * E;
   p.KC = KC;
+  // rows per layer-1 CTA (x staging <= 96 KB); more rows -> more row blocks (grid z)
+  p.RB = std::max(1, std::min(B, (int)((96 * 1024) / ((size_t)KC * esz))));
   p.KS = (dr + KC - 1) / KC;
-  p.part_bytes = (size_t)p.KS * B * p.rows1 * sizeof(float);
+  // layer-1 partials, then (shared mode) the rows' TopK masks
+  p.part_bytes = (size_t)p.KS * B * p.rows1 * sizeof(float) + (size_t)B * (kMaxM / 32) * sizeof(uint32_t);
   return p;
 }
 
@@ -193,7 +196,7 @@ static cudaError_t launch_meta_t(const ds_router* r, const void* h_prev, const v
                                  const int32_t* k_per_row, int shared, int32_t* sel, int32_t* sel_count,
                                  int32_t* sl_offsets, cudaStream_t st, bool pdl) {
   const MetaPlan p = meta_plan(r, B);
-  const size_t smem1 = (size_t)B * p.KC * sizeof(T);
+  const size_t smem1 = (size_t)p.RB * p.KC * sizeof(T);
   if (smem1 > 48 * 1024) {
     cudaError_t ea = cudaFuncSetAttribute(meta_l1_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1);
     if (ea != cudaSuccess) return ea;
@@ -203,7 +206,7 @@ static cudaError_t launch_meta_t(const ds_router* r, const void* h_prev, const v
   attr[0].val.programmaticStreamSerializationAllowed = 1;
 
   cudaLaunchConfig_t c1 = {};
-  c1.gridDim = dim3((p.rows1 + kMetaUnitsPerCTA - 1) / kMetaUnitsPerCTA, p.KS);
+  c1.gridDim = dim3((p.rows1 + kMetaUnitsPerCTA - 1) / kMetaUnitsPerCTA, p.KS, (B + p.RB - 1) / p.RB);
   c1.blockDim = dim3(kMetaThreads);
   c1.dynamicSmemBytes = smem1;
   c1.stream = st;
@@ -211,7 +214,7 @@ static cudaError_t launch_meta_t(const ds_router* r, const void* h_prev, const v
   c1.numAttrs = pdl ? 1 : 0;
   cudaError_t err = cudaLaunchKernelEx(&c1, meta_l1_kernel<T>, static_cast<const T*>(r->W1),
                                        static_cast<const T*>(h_prev), static_cast<const T*>(e), B, r->d, p.rows1,
-                                       p.KC, part, pdl ? 1 : 0);
+                                       p.KC, p.RB, part, pdl ? 1 : 0);
   if (err != cudaSuccess) return err;
   cudaLaunchConfig_t c2 = {};
   c2.gridDim = dim3(B);

@@ -41,6 +41,7 @@ struct TcArgs {
   int32_t tmem_cols;
   int32_t online;   // 1: per-row running (max, sum, top-k) per tile instead of on-chip logit buffers
   const uint32_t* rowmask;  // nullable [nrows][32]: clusters each row selected (per-row batched mode)
+  unsigned long long* trace;  // opt-in phase trace (dynaspec_debug_set_trace)
 };
 
 struct TcSmem {
@@ -142,6 +143,7 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
 
 // ------------------------------------------------------------------ kernel
 __global__ void __launch_bounds__(kTcThreads, 1) tc_head_kernel(const __grid_constant__ CUtensorMap tmW,
+                                                                const __grid_constant__ CUtensorMap tmW128,
                                                                 const __grid_constant__ CUtensorMap tmH,
                                                                 const TcArgs t) {
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -182,6 +184,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_head_kernel(const __grid_con
     }
     fence_mbar_init();
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmW)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmW128)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmH)) : "memory");
   }
   if (warp == 1) {  // TMEM accumulators: 2 x N fp32 columns, owned (and freed) by warp 1
@@ -190,6 +193,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_head_kernel(const __grid_con
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
+  trace_mark(t.trace, 0);
   if (a.pdl) pdl_wait();
   head_segments(a, c);
   tc_fence_before();
@@ -228,6 +232,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_head_kernel(const __grid_con
   const int nboxes = c.misc[1];
   const int ntiles = nboxes > 0 ? (nboxes + kTcBoxes - 1) / kTcBoxes : 0;
   const uint32_t S = (uint32_t)t.S;
+  trace_mark(t.trace, 1);
+  if (t.trace && threadIdx.x == 0) t.trace[blockIdx.x * 64 + 29] = (unsigned long long)ntiles;
 
   if (warp == 0) {
     if (lane == 0 && ntiles > 0) {
@@ -235,17 +241,26 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_head_kernel(const __grid_con
       uint32_t it = 0;
       for (int tile = 0; tile < ntiles; ++tile) {
         const int b0 = tile * kTcBoxes, b1 = min(nboxes, b0 + kTcBoxes);
+        // a tile of 8 full, consecutive 16-row boxes (inside one cluster run: most tiles) is one
+        // 128-row box: the same swizzled shared-memory image with 8x fewer TMA operations
+        bool contig = b1 - b0 == kTcBoxes;
+        for (int b = b0; contig && b < b1; ++b)
+          contig = boxes[b].z == kTcBoxRows && boxes[b].x == boxes[b0].x + (b - b0) * kTcBoxRows;
         const uint32_t bytes = (uint32_t)(b1 - b0) * kTcBoxRows * kTcK * 2 + (uint32_t)t.N * kTcK * 2;
         for (int kc = 0; kc < t.kchunks; ++kc, ++it) {
           const uint32_t s = it % S;
           mbar_wait(&empty[s], ((it / S) & 1u) ^ 1u);
           mbar_arrive_expect_tx(&full[s], bytes);
-          for (int b = b0; b < b1; ++b)
-            tma_load_2d(sa + (size_t)s * kTcABytes + (size_t)(b - b0) * kTcBoxRows * 128, &tmW, kc * kTcK,
-                        boxes[b].x, &full[s], pol_w);
+          if (contig)
+            tma_load_2d(sa + (size_t)s * kTcABytes, &tmW128, kc * kTcK, boxes[b0].x, &full[s], pol_w);
+          else
+            for (int b = b0; b < b1; ++b)
+              tma_load_2d(sa + (size_t)s * kTcABytes + (size_t)(b - b0) * kTcBoxRows * 128, &tmW, kc * kTcK,
+                          boxes[b].x, &full[s], pol_w);
           tma_load_2d(sb + (size_t)s * t.N * 128, &tmH, kc * kTcK, 0, &full[s], pol_h);
         }
       }
+      trace_mark_w(t.trace, 2);
     }
   } else if (warp == 1) {
     if (lane == 0 && ntiles > 0) {
@@ -271,6 +286,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_head_kernel(const __grid_con
         }
         tc_commit(&tfull[buf]);  // accumulator complete
       }
+      trace_mark_w(t.trace, 3);
     }
     __syncwarp();
   } else if (!t.online) {
@@ -313,6 +329,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_head_kernel(const __grid_con
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[buf]);
     }
+    if (warp == 2) trace_mark_w(t.trace, 4);
   } else {
     // online epilogue: stage the tile's logits (masked to each row's own clusters), then warp
     // ew = warp - 2 folds rows ew, ew + 4, ... into their running (max, sum exp) and top-k_t.
@@ -332,10 +349,14 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_head_kernel(const __grid_con
       runs[i] = 0.f;
     }
     named_bar_sync(2, 128);
+    long long cw = 0, cs = 0, cr = 0;
     for (int tile = 0; tile < ntiles; ++tile) {
       const int buf = tile & 1;
+      const long long q0 = clock64();
       mbar_wait(&tfull[buf], ((uint32_t)tile >> 1) & 1u);
       tc_fence_after();
+      const long long q1 = clock64();
+      cw += q1 - q0;
       const int bi = tile * kTcBoxes + row / kTcBoxRows, r = row % kTcBoxRows;
       bool valid = false;
       int tok = INT_MAX, cl = 0;
@@ -366,11 +387,19 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_head_kernel(const __grid_con
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[buf]);
       named_bar_sync(2, 128);
+      const long long q2 = clock64();
+      cs += q2 - q1;
       const int cur = tile & 1, nxt = cur ^ 1;
       for (int rr = ew; rr < nr; rr += 4) {
         const float* zr = stage + rr * 128;
-        float m, se;
-        warp_lse_items(zr, 128, m, se);
+        // tile (max, sum exp) of the row: max as one order-preserving integer reduction, then one
+        // exp per logit against it and a fixed xor tree (R19); masked logits are -inf (exp = 0)
+        const float x0 = zr[lane], x1 = zr[lane + 32], x2 = zr[lane + 64], x3 = zr[lane + 96];
+        const uint32_t km = max(max(ord_key(x0), ord_key(x1)), max(ord_key(x2), ord_key(x3)));
+        const uint32_t Km = __reduce_max_sync(0xffffffffu, km);
+        const float m = __uint_as_float((Km & 0x80000000u) ? (Km & 0x7fffffffu) : ~Km);
+        float se = 0.f;
+        if (m != -INFINITY) se = warp_sum((expf(x0 - m) + expf(x1 - m)) + (expf(x2 - m) + expf(x3 - m)));
         if (lane == 0) {
           float M0 = runm[rr], S0 = runs[rr];
           lse_combine(M0, S0, m, se);
@@ -379,6 +408,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_head_kernel(const __grid_con
         }
         const float2* lc = lst + ((size_t)cur * nr + rr) * K;
         float2* ln = lst + ((size_t)nxt * nr + rr) * K;
+        // a tile logit can enter the row's top-K only if >= its current K-th value (-inf: not full)
+        if (m == -INFINITY || m < lc[K - 1].x) {
+          for (int qq = lane; qq < K; qq += 32) ln[qq] = lc[qq];
+          __syncwarp();
+          continue;
+        }
         const int nsv = warp_topk(
             128 + K, K,
             [&](int i, float& v, int& id) {
@@ -395,6 +430,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_head_kernel(const __grid_con
         __syncwarp();
       }
       named_bar_sync(2, 128);
+      cr += clock64() - q2;
+    }
+    if (t.trace && threadIdx.x == 64) {
+      t.trace[blockIdx.x * 64 + 20] = cw;
+      t.trace[blockIdx.x * 64 + 21] = cs;
+      t.trace[blockIdx.x * 64 + 22] = cr;
     }
     // per-CTA partial records [row][cta][rec]
     const int fin = ntiles & 1;  // buffer holding the latest lists
@@ -418,12 +459,15 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_head_kernel(const __grid_con
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(t.tmem_cols) : "memory");
   }
+  trace_mark(t.trace, 5);
   if (a.pdl) pdl_launch_dependents();
   if (!t.online) head_partials(a, c, t.S * kTcABytes);
+  trace_mark(t.trace, 6);
   const int j = head_ticket(a, c);
   if (j < 0) return;
   head_merge(a, c, t.S * kTcABytes, nullptr, 0, j, min(a.nrows, (int)gridDim.x));
   head_merge_done(a, 0);
+  trace_mark(t.trace, 7);
 }
 
 // Union of B rows' selections (one CTA): per-row cluster bit masks + the ascending union with
@@ -506,7 +550,7 @@ static bool tc_plan(const ds_clusters* c, int R, int k_t, int64_t max_shortlist,
   p->hp.part_bytes = (size_t)p->hp.G * R * p->hp.rec * sizeof(float);
   const int smax = max_smem_optin();
   p->S = 0;
-  for (int S = 8; S >= 3; --S) {
+  for (int S = 12; S >= 3; --S) {
     if (S * kTcABytes < merge_smem_bytes(p->hp.G, k_t, kTcThreads / 32) || p->hp.G > 32 * (kTcThreads / 32)) break;
     if ((int)tc_smem(S, p->N, R, p->hp.lcap, online, k_t).total <= smax) {
       p->S = S;
@@ -534,8 +578,8 @@ size_t tc_batched_ws_bytes(const ds_clusters* c, int B, int k_t) {
          align_up((size_t)(2 * c->M + 8) * 4, 256);
 }
 
-static cudaError_t launch_tc_kernel(const TcPlan& p, const CUtensorMap& mw, const CUtensorMap& mh, const TcArgs& t,
-                                    cudaStream_t st, bool pdl) {
+static cudaError_t launch_tc_kernel(const TcPlan& p, const CUtensorMap& mw, const CUtensorMap& mw128,
+                                    const CUtensorMap& mh, const TcArgs& t, cudaStream_t st, bool pdl) {
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(tc_head_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem_optin());
@@ -552,7 +596,7 @@ static cudaError_t launch_tc_kernel(const TcPlan& p, const CUtensorMap& mw, cons
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl ? 1 : 0;
-  return cudaLaunchKernelEx(&cfg, tc_head_kernel, mw, mh, t);
+  return cudaLaunchKernelEx(&cfg, tc_head_kernel, mw, mw128, mh, t);
 }
 
 cudaError_t launch_tc_batched(const ds_clusters* c, const void* h_new, int B, const int32_t* sel,
@@ -575,8 +619,10 @@ cudaError_t launch_tc_batched(const ds_clusters* c, const void* h_new, int B, co
                                       ucnt, usloff);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    CUtensorMap mw, mh;
+    CUtensorMap mw, mw128, mh;
     if (!make_map(&mw, c->W_perm, (uint64_t)c->V, (uint64_t)c->d, kTcBoxRows)) return cudaErrorInvalidValue;
+    if (!make_map(&mw128, c->W_perm, (uint64_t)c->V, (uint64_t)c->d, kTcBoxRows * kTcBoxes))
+      return cudaErrorInvalidValue;
     const void* h0 = static_cast<const uint8_t*>(h_new) + (size_t)r0 * c->d * esz;
     if (!make_map(&mh, h0, (uint64_t)nr, (uint64_t)c->d, (uint32_t)p.N)) return cudaErrorInvalidValue;
     TcArgs t;
@@ -590,7 +636,8 @@ cudaError_t launch_tc_batched(const ds_clusters* c, const void* h_new, int B, co
     t.tmem_cols = p.tmem_cols;
     t.online = 1;
     t.rowmask = rowmask;
-    e = launch_tc_kernel(p, mw, mh, t, st, false);
+    t.trace = debug_trace();
+    e = launch_tc_kernel(p, mw, mw128, mh, t, st, false);
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;
@@ -610,10 +657,14 @@ cudaError_t launch_tc_head(const ds_clusters* c, const void* h_new, int R, const
                            const int32_t* sel_count, const int32_t* sl_offsets, int k_t, int64_t max_shortlist,
                            int32_t* top_ids, float* top_logits, float* top_logp, float* lse, float* z_out,
                            int64_t z_stride, float* part, unsigned* counter, cudaStream_t st, bool pdl) {
+  // shared (tree) mode keeps the logits on chip for the per-CTA partial: at tree-depth shortlists a
+  // CTA holds 1-2 tiles, where the online per-tile epilogue measured slower (Qwen tree 89 vs 97 us)
   TcPlan p;
   if (!tc_plan(c, R, k_t, max_shortlist, &p)) return cudaErrorInvalidValue;
-  CUtensorMap mw, mh;
+  CUtensorMap mw, mw128, mh;
   if (!make_map(&mw, c->W_perm, (uint64_t)c->V, (uint64_t)c->d, kTcBoxRows)) return cudaErrorInvalidValue;
+  if (!make_map(&mw128, c->W_perm, (uint64_t)c->V, (uint64_t)c->d, kTcBoxRows * kTcBoxes))
+    return cudaErrorInvalidValue;
   if (!make_map(&mh, h_new, (uint64_t)R, (uint64_t)c->d, (uint32_t)p.N)) return cudaErrorInvalidValue;
   TcArgs t;
   fill_head_args(t.h, c, p.hp, h_new, 0, R, sel, sel_count, sl_offsets, 1, k_t, max_shortlist, top_ids, top_logits,
@@ -622,9 +673,10 @@ cudaError_t launch_tc_head(const ds_clusters* c, const void* h_new, int R, const
   t.S = p.S;
   t.kchunks = (c->d + kTcK - 1) / kTcK;
   t.tmem_cols = p.tmem_cols;
-  t.online = 0;
+  t.online = p.online;
   t.rowmask = nullptr;
-  return launch_tc_kernel(p, mw, mh, t, st, pdl);
+  t.trace = debug_trace();
+  return launch_tc_kernel(p, mw, mw128, mh, t, st, pdl);
 }
 
 }  // namespace ds

@@ -540,3 +540,23 @@ def test_frequency_heads_fr_and_pa_fr(dtype):
                 check_topk(out["top_ids"][b].cpu().numpy(), out["top_logits"][b].cpu().numpy(),
                            out["top_logp"][b].cpu().numpy(), out["lse"][b].item(), ref[b]["z"], ref[b]["V_S"], 8,
                            tdt)
+
+
+def test_router_many_rows_row_blocks():
+    """B = 512 rows (the Gemma config's batch on one GPU): the layer-1 router kernel stages x in
+    row blocks (grid z); scores and selections of sampled rows match the oracle."""
+    Dy = _dyn()
+    V, d, M, h_r, B = 20011, 512, 64, 32, 512
+    W, rt, tau, part, c, r = _setup(V, d, M, h_r, "bf16", "random")
+    hp, e, hn = S.step_inputs(B, d, 7, "bf16")
+    st = Dy.DraftStep(c, r, B, 8)
+    st(hp.to(DEV), e.to(DEV), hn.to(DEV), t=2, k_max=16, k_min=4)
+    torch.cuda.synchronize()
+    ro = _oracle_router(rt)
+    for b in (0, 1, 191, 192, 300, 511):
+        ref = O.draft_step(part, ro, Rows(W), f64(hp[b:b + 1]), f64(e[b:b + 1]), f64(hn[b:b + 1]), 2, 16, 4, 8)[0]
+        s_ref = ref["scores"]
+        assert np.max(np.abs(st.scores[b].cpu().numpy() - s_ref)) < 1e-3 * max(1.0, np.sqrt(np.mean(s_ref ** 2)))
+        if selection_certified(s_ref, ref["k"]):
+            cnt = st.sel_count[b].item()
+            assert st.sel[b, :cnt].cpu().tolist() == ref["sel"].tolist()
