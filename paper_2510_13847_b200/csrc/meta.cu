@@ -86,21 +86,51 @@ __global__ void __launch_bounds__(kMetaThreads) meta_l1_kernel(const T* __restri
   __syncthreads();
   if (pdl) pdl_launch_dependents();
   if (u >= rows1) return;
-  for (int b = 0; b < nb; ++b) {
-    float acc = 0.f;
+  float wf[kMaxChunks][E];
 #pragma unroll
-    for (int i = 0; i < kMaxChunks; ++i) {
-      const int c = lane * E + i * 32 * E;
-      if (c < kn) {
-        float wf[E], xf[E];
-        widen16(wv[i], wf, W1);
-        widen16(*reinterpret_cast<const uint4*>(xs + (size_t)b * KC + c), xf, W1);
+  for (int i = 0; i < kMaxChunks; ++i) widen16(wv[i], wf[i], W1);
+  // 8 rows at a time: lane partials, then one transpose-reduction (9 shuffles for 8 rows instead of
+  // 8 x 5): after it lane L holds row 4 b4 + 2 b3 + b2 (bits of L) summed over all 32 lanes
+  for (int bb = 0; bb < nb; bb += 8) {
+    float v[8];
 #pragma unroll
-        for (int j = 0; j < E; ++j) acc = fmaf(wf[j], xf[j], acc);
+    for (int q = 0; q < 8; ++q) {
+      float acc = 0.f;
+      if (bb + q < nb) {
+#pragma unroll
+        for (int i = 0; i < kMaxChunks; ++i) {
+          const int c = lane * E + i * 32 * E;
+          if (c < kn) {
+            float xf[E];
+            widen16(*reinterpret_cast<const uint4*>(xs + (size_t)(bb + q) * KC + c), xf, W1);
+#pragma unroll
+            for (int j = 0; j < E; ++j) acc = fmaf(wf[i][j], xf[j], acc);
+          }
+        }
       }
+      v[q] = acc;
     }
-    acc = warp_sum(acc);
-    if (lane == 0) part[((size_t)blockIdx.y * B + b0 + b) * rows1 + u] = acc;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const bool hi = lane & 16;
+      const float send = hi ? v[j] : v[j + 4], keep = hi ? v[j + 4] : v[j];
+      v[j] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+    }
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const bool hi = lane & 8;
+      const float send = hi ? v[j] : v[j + 2], keep = hi ? v[j + 2] : v[j];
+      v[j] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+    }
+    {
+      const bool hi = lane & 4;
+      const float send = hi ? v[0] : v[1], keep = hi ? v[1] : v[0];
+      v[0] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+    }
+    v[0] += __shfl_xor_sync(0xffffffffu, v[0], 2);
+    v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
+    const int q = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
+    if ((lane & 3) == 0 && bb + q < nb) part[((size_t)blockIdx.y * B + b0 + bb + q) * rows1 + u] = v[0];
   }
 }
 

@@ -484,10 +484,11 @@ __global__ void __launch_bounds__(256) union_kernel(const int32_t* __restrict__ 
   for (int i = threadIdx.x; i < 32 + B * 32; i += blockDim.x) us[i] = 0u;
   for (int m = threadIdx.x; m <= M; m += blockDim.x) offs[m] = offsets[m];
   __syncthreads();
-  for (int r = 0; r < B; ++r) {
-    const int n = cnt[r];
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
-      const int m = sel[(size_t)r * M + i];
+  // all rows at once (independent loads): entry i of row r for (r, i) in [0, B) x [0, M)
+  for (int idx = threadIdx.x; idx < B * M; idx += blockDim.x) {
+    const int r = idx / M, i = idx - r * M;
+    if (i < __ldg(cnt + r)) {
+      const int m = __ldg(sel + (size_t)r * M + i);
       atomicOr(&acc[m >> 5], 1u << (m & 31));
       atomicOr(&rm[r * 32 + (m >> 5)], 1u << (m & 31));
     }
