@@ -388,7 +388,8 @@ ds_status dynaspec_step_head(const ds_clusters* c, const void* h_new, int32_t B,
   const int32_t k = dynaspec_budget(t, k_max, k_min);
   if (k < 1 || k_max > c->M) return DS_ERR_INVALID_BUDGET;
   if (k_t < 1 || k_t > kMaxKt || (int64_t)k_t > (int64_t)k * c->min_size) return DS_ERR_INVALID_BUDGET;
-  const int64_t ms = shared ? c->V : dynaspec_max_shortlist(c, k);
+  // shared (tree) mode: the union of B rows' k clusters has at most min(M, B k) clusters
+  const int64_t ms = dynaspec_max_shortlist(c, shared ? (int32_t)std::min<int64_t>(c->M, (int64_t)B * k) : k);
   if (out->z_out && out->z_stride < ms) return DS_ERR_SHAPE;
   return dynaspec_head_forward(c, h_new, B, out->sel, out->sel_count, out->sl_offsets, shared, k_t, ms, out->top_ids,
                                out->top_logits, out->top_logp, out->lse, out->z_out, out->z_stride, ws, ws_bytes,
@@ -435,7 +436,8 @@ ds_status dynaspec_draft_step(const ds_clusters* c, const ds_router* r, const vo
   const int32_t k = dynaspec_budget(t, k_max, k_min);
   if (k < 1 || k_max > c->M) return DS_ERR_INVALID_BUDGET;
   if (k_t < 1 || k_t > kMaxKt || (int64_t)k_t > (int64_t)k * c->min_size) return DS_ERR_INVALID_BUDGET;
-  const int64_t ms = shared ? c->V : dynaspec_max_shortlist(c, k);
+  // shared (tree) mode: the union of B rows' k clusters has at most min(M, B k) clusters
+  const int64_t ms = dynaspec_max_shortlist(c, shared ? (int32_t)std::min<int64_t>(c->M, (int64_t)B * k) : k);
   if (out->z_out && out->z_stride < ms) return DS_ERR_SHAPE;
   const bool two_streams = s_meta != nullptr && s_meta != s_draft;
   if (two_streams && (!ev_fork || !ev_join)) return DS_ERR_SHAPE;
