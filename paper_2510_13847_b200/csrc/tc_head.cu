@@ -674,8 +674,18 @@ cudaError_t launch_tc_head(const ds_clusters* c, const void* h_new, int R, const
                            int64_t z_stride, float* part, unsigned* counter, cudaStream_t st, bool pdl) {
   // shared (tree) mode keeps the logits on chip for the per-CTA partial: at tree-depth shortlists a
   // CTA holds 1-2 tiles, where the online per-tile epilogue measured slower (Qwen tree 89 vs 97 us)
+  // Epilogue choice by the per-CTA logit bound lcap: <= 4 tiles keep the logits on chip for one
+  // per-CTA partial (Qwen tree depths: 94 vs 96 us online); more use the online per-tile running
+  // (max, sum, top-k) (dense k = M on the Qwen head: 255 vs 526+ us).  z_out needs the logits.
   TcPlan p;
-  if (!tc_plan(c, R, k_t, max_shortlist, &p)) return cudaErrorInvalidValue;
+  if (!tc_plan(c, R, k_t, max_shortlist, &p, 0)) return cudaErrorInvalidValue;
+  const char* ov = getenv("DS_TC_ONLINE");  // "0" / "1": force (tuning)
+  const bool force = ov && (ov[0] == '0' || ov[0] == '1');
+  const bool online = !z_out && (force ? ov[0] == '1' : p.hp.lcap > 4 * 128);
+  if (online) {
+    TcPlan po;
+    if (tc_plan(c, R, k_t, max_shortlist, &po, 1)) p = po;
+  }
   TcMaps mw;
   CUtensorMap mh;
   if (!make_maps(&mw, c)) return cudaErrorInvalidValue;

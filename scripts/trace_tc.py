@@ -36,7 +36,8 @@ for rep in range(reps + 2):
     torch.cuda.synchronize()
     for t in range(C.positions):
         D.debug_set_trace(bufs[t])
-        steps[t](*inp[t], t, C.k_max, C.k_min)
+        kmax = int(os.environ.get("KMAX", C.k_max))
+        steps[t](*inp[t], t, kmax, min(kmax, int(os.environ.get("KMIN", C.k_min))))
     D.debug_set_trace(None)
     torch.cuda.synchronize()
     if rep >= 2:
