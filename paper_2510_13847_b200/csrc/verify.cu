@@ -134,6 +134,54 @@ __device__ __forceinline__ void stream_segment(const T* __restrict__ l, const fl
   }
 }
 
+// bf16 lse of a warp segment, lean inner loop: 4 x 16 B per lane per batch (1024 logits per warp),
+// the next batch's loads in flight; the batch max by packed bf16x2 max (exact), then one
+// exp2 per logit against the running max in two independent sums.  ~4.5 instructions per logit
+// (the generic stream_segment path needs ~13).  Returns the first position it did not cover.
+__device__ __forceinline__ int lse_seg_bf16(const __nv_bfloat16* l, int lo, int hi, int lane, float& m, float& s) {
+  constexpr int U = 4, STEP = 32 * 8 * U;
+  const int nfull = (hi - lo) / STEP;
+  if (nfull <= 0) return lo;
+  const uint4* base = reinterpret_cast<const uint4*>(l + lo) + lane;
+  uint4 cur[U], nxt[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) cur[u] = __ldcs(base + u * 32);
+  for (int bt = 0; bt < nfull; ++bt) {
+    if (bt + 1 < nfull) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) nxt[u] = __ldcs(base + (size_t)(bt + 1) * (STEP / 8) + u * 32);
+    }
+    uint32_t w[4 * U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      w[4 * u] = cur[u].x;
+      w[4 * u + 1] = cur[u].y;
+      w[4 * u + 2] = cur[u].z;
+      w[4 * u + 3] = cur[u].w;
+    }
+    __nv_bfloat162 mx2 = *reinterpret_cast<const __nv_bfloat162*>(&w[0]);
+#pragma unroll
+    for (int i = 1; i < 4 * U; ++i) mx2 = __hmax2(mx2, *reinterpret_cast<const __nv_bfloat162*>(&w[i]));
+    const float mx = fmaxf(m, fmaxf(__low2float(mx2), __high2float(mx2)));
+    if (mx != -INFINITY) {
+      const float mxl = mx * kLog2e;
+      float acc0 = m == -INFINITY ? 0.f : s * ex2(fmaf(m, kLog2e, -mxl)), acc1 = 0.f;
+#pragma unroll
+      for (int i = 0; i < 4 * U; ++i) {
+        acc0 += ex2(fmaf(__uint_as_float(w[i] << 16), kLog2e, -mxl));
+        acc1 += ex2(fmaf(__uint_as_float(w[i] & 0xffff0000u), kLog2e, -mxl));
+      }
+      s = acc0 + acc1;
+      m = mx;
+    }
+    if (bt + 1 < nfull) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) cur[u] = nxt[u];
+    }
+  }
+  return lo + nfull * STEP;
+}
+
 // Warp-wide (max, sum) combine, every lane returns the result (fixed xor-tree order).
 __device__ __forceinline__ void warp_lse_pair(float& m, float& s) {
 #pragma unroll
@@ -215,7 +263,10 @@ __global__ void __launch_bounds__(kVT, 2) verify_lse_kernel(const VerifyArgs a) 
   const int lo = (int)min((int64_t)seg * L1, (int64_t)V), hi = min(V, lo + L1);
   constexpr int U = sizeof(T) == 2 ? 2 : 1;  // groups of 8 ids per lane per batch (2 batches in flight)
   float m = -INFINITY, s = 0.f;
-  stream_segment<T, U, false>(l, nullptr, lo, hi, lane, [&](float (&v)[U][8], float (&)[U][8]) {
+  int lo2 = lo;  // bf16 rows with 16-byte aligned segments: lean full batches, generic tail
+  if (sizeof(T) == 2 && ((reinterpret_cast<uintptr_t>(l + lo) & 15u) == 0))
+    lo2 = lse_seg_bf16(reinterpret_cast<const __nv_bfloat16*>(l), lo, hi, lane, m, s);
+  stream_segment<T, U, false>(l, nullptr, lo2, hi, lane, [&](float (&v)[U][8], float (&)[U][8]) {
     float mx = m;
 #pragma unroll
     for (int u = 0; u < U; ++u)
@@ -232,35 +283,48 @@ __global__ void __launch_bounds__(kVT, 2) verify_lse_kernel(const VerifyArgs a) 
       m = mx;
     }
   });
+  __shared__ float2 wpart[kVW];
   warp_lse_pair(m, s);
-  if (lane == 0) a.part[(size_t)row * a.s1 * kVW + seg] = make_float2(m, s);
+  if (a.s1 == 1) {  // the row is this CTA's alone: fold the warp partials in shared memory
+    if (lane == 0) wpart[warp] = make_float2(m, s);
+  } else if (lane == 0) {
+    a.part[(size_t)row * a.s1 * kVW + seg] = make_float2(m, s);
+  }
   if (cta == 0 && threadIdx.x == 32 && i < a.gamma) decision_inputs<T>(a, b, i);
   __syncthreads();
-  if (threadIdx.x == 0) {
+  if (a.s1 > 1) {
+    if (threadIdx.x == 0) {
+      fence_acq_rel_gpu();
+      sh[0] = atomicAdd(&a.ctr_row[row], 1u) == (unsigned)(a.s1 - 1);
+    }
+    __syncthreads();
+    if (!sh[0]) return;
     fence_acq_rel_gpu();
-    sh[0] = atomicAdd(&a.ctr_row[row], 1u) == (unsigned)(a.s1 - 1);
   }
-  __syncthreads();
-  if (!sh[0]) return;
-  fence_acq_rel_gpu();
   if (warp == 0) {
     const int np = a.s1 * kVW;  // <= 512: 16 independent loads per lane
     float M = -INFINITY, S = 0.f;
-    for (int h = 0; h < np; h += 8 * 32) {  // 8 independent loads per lane per round
-      float2 pp[8];
+    if (a.s1 == 1) {
+      const float2 pp = lane < kVW ? wpart[lane] : make_float2(-INFINITY, 0.f);
+      lse_combine(M, S, pp.x, pp.y);
+    } else {
+      for (int h = 0; h < np; h += 8 * 32) {  // 8 independent loads per lane per round
+        float2 pp[8];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const int c = h + k * 32 + lane;
-        pp[k] = c < np ? __ldcg(&a.part[(size_t)row * np + c]) : make_float2(-INFINITY, 0.f);
+        for (int k = 0; k < 8; ++k) {
+          const int c = h + k * 32 + lane;
+          pp[k] = c < np ? __ldcg(&a.part[(size_t)row * np + c]) : make_float2(-INFINITY, 0.f);
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) lse_combine(M, S, pp[k].x, pp[k].y);
       }
-#pragma unroll
-      for (int k = 0; k < 8; ++k) lse_combine(M, S, pp[k].x, pp[k].y);
     }
     warp_lse_pair(M, S);
     if (lane == 0) {
       const float lse = M + logf(S);
       a.lse_p[row] = lse;
       if (i < a.gamma) {  // Eq. 3: accept iff u < p(x) / q(x)
+        if (a.s1 == 1) fence_acq_rel_gpu();  // thread 32's rowrec store, ordered by the barrier
         const float4 r = __ldcg(&a.rowrec[row]);
         const float p = expf(r.x - lse), q = expf(r.y);
         a.rowflag[row] = r.w == 0.f ? -1 : (r.z < p / q ? 1 : 0);
