@@ -25,8 +25,10 @@ __device__ __forceinline__ void wait(uint64_t* b, uint32_t par) {
 constexpr int S = 8, STAGE = 16384, D = 3584, KCH = D / 64;
 
 // mode 0: row-major map, box (64, 128) at (kc*64, tile*128); mode 1: blocked map, box (64, 128) at
-// (0, (tile*KCH + kc)*128); mode 2: 1-D bulk copies of 16 KB of consecutive rows
-__global__ void __launch_bounds__(64, 1) k(const __grid_constant__ CUtensorMap m, const char* raw, int mode,
+// (0, (tile*KCH + kc)*128); mode 2: 1-D bulk copies of 16 KB of consecutive rows; mode 3 (tree
+// head): per K chunk 4 boxes of 16 rows (64-row tile, 16-row map) + one 16 x 64 box of H (hmap)
+__global__ void __launch_bounds__(64, 1) k(const __grid_constant__ CUtensorMap m, const __grid_constant__ CUtensorMap m16,
+                                           const __grid_constant__ CUtensorMap hm, const char* raw, int mode,
                                            int tiles_per_cta, float* sink) {
   extern __shared__ __align__(1024) char sm[];
   __shared__ __align__(8) uint64_t full[S];
@@ -37,6 +39,25 @@ __global__ void __launch_bounds__(64, 1) k(const __grid_constant__ CUtensorMap m
   __syncthreads();
   if (threadIdx.x != 0) return;
   const int nops = mode == 2 ? tiles_per_cta * 128 * D * 2 / STAGE : tiles_per_cta * KCH;
+  if (mode == 3) {  // one 64-row tile per CTA: KCH stages of 4 x 2 KB + 2 KB (H)
+    for (int c = 0; c < KCH; ++c) {
+      const int s = c % S;
+      if (c >= S) wait(&full[s], ((c / S) - 1) & 1);
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su(&full[s])), "r"(5 * 2048) : "memory");
+      for (int b = 0; b < 5; ++b) {
+        const CUtensorMap* mp = b < 4 ? &m16 : &hm;
+        const int y = b < 4 ? blockIdx.x * 64 + b * 16 : 0;
+        asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+            "[%4];" ::"r"(su(sm + s * STAGE + b * 2048)),
+            "l"(reinterpret_cast<uint64_t>(mp)), "r"(c * 64), "r"(y), "r"(su(&full[s]))
+            : "memory");
+      }
+    }
+    for (int c = KCH > S ? KCH - S : 0; c < KCH; ++c) wait(&full[c % S], (c / S) & 1);
+    sink[blockIdx.x] = sm[5];
+    return;
+  }
   for (int c = 0; c < nops; ++c) {
     const int s = c % S;
     if (c >= S) wait(&full[s], ((c / S) - 1) & 1);
@@ -75,7 +96,17 @@ int main() {
   cudaDriverEntryPointQueryResult q;
   cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fp, cudaEnableDefault, &q);
   EncodeFn enc = (EncodeFn)fp;
-  CUtensorMap mrow, mblk;
+  CUtensorMap mrow, mblk, m16, hmap;
+  {
+    const cuuint64_t dims[2] = {D, rows};
+    const cuuint64_t str[1] = {D * 2};
+    const cuuint32_t box[2] = {64, 16}, es[2] = {1, 1};
+    enc(&m16, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, w, dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    const cuuint64_t hd[2] = {D, 16};
+    enc(&hmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, w, hd, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  }
   {
     const cuuint64_t dims[2] = {D, rows};
     const cuuint64_t str[1] = {D * 2};
@@ -91,16 +122,17 @@ int main() {
         CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   }
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, S * STAGE);
-  const char* names[] = {"row-major, K-chunk boxes (tc_head)", "K-blocked copy, 16 KB boxes", "1-D bulk, whole rows"};
+  const char* names[] = {"row-major, K-chunk boxes (tc_head)", "K-blocked copy, 16 KB boxes", "1-D bulk, whole rows",
+                         "tree: 64-row tile, 4x16-row boxes + H, 1 tile"};
   cudaEvent_t a, b;
   cudaEventCreate(&a);
   cudaEventCreate(&b);
-  for (int mode = 0; mode < 3; ++mode) {
+  for (int mode = 0; mode < 4; ++mode) {
     float best = 1e9f;
     for (int rep = 0; rep < 5; ++rep) {
       cudaMemset(flush, rep, 512 << 20);
       cudaEventRecord(a);
-      k<<<G, 64, S * STAGE>>>(mode == 1 ? mblk : mrow, w, mode, tiles_per_cta, sink);
+      k<<<G, 64, S * STAGE>>>(mode == 1 ? mblk : mrow, m16, hmap, w, mode, tiles_per_cta, sink);
       cudaEventRecord(b);
       cudaEventSynchronize(b);
       float ms;
@@ -108,7 +140,8 @@ int main() {
       best = ms < best ? ms : best;
     }
     cudaError_t e = cudaGetLastError();
-    printf("%-40s %8.1f us  %7.0f GB/s  %s\n", names[mode], best * 1e3, bytes / (best * 1e-3) / 1e9,
+    const double by = mode == 3 ? (double)G * KCH * 5 * 2048 : (double)bytes;
+    printf("%-46s %8.1f us  %7.0f GB/s  %s\n", names[mode], best * 1e3, by / (best * 1e-3) / 1e9,
            cudaGetErrorString(e));
   }
   return 0;
