@@ -31,6 +31,12 @@ __device__ __forceinline__ void widen16(const uint4& v, float* out, const float*
   out[3] = __uint_as_float(v.w);
 }
 
+// Order-preserving map float -> uint32 (larger float => larger key); -0 folded into +0 (R23).
+__device__ __forceinline__ uint32_t ord_key(float x) {
+  const uint32_t u = __float_as_uint(x + 0.0f);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+
 // ------------------------------------------------------------------ warp reductions
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll

@@ -475,20 +475,57 @@ __device__ inline void merge_finish(const HeadArgs& a, const HeadCtx& c, int G, 
   trace_mark(trace, 17);
   const bool ok = valid_row && mx > -INFINITY;
   const float lse = ok ? mx + logf(S) : __int_as_float(0x7fc00000);
-  // candidates in rank-major order: the first G items are the heads of the G sorted lists
-  block_topk(
-      G * K, K, [&](int e, float& v, int& id) { v = cv[e]; id = ci[e]; },
-      [&](int rank, float v, int id) {
-        if (a.record_out) {
-          a.record_out[(size_t)r * rec + 2 + 2 * rank] = v;
-          a.record_out[(size_t)r * rec + 3 + 2 * rank] = __int_as_float(id);
-        } else {
-          a.top_ids[(size_t)r * K + rank] = ok ? id : -1;
-          a.top_logits[(size_t)r * K + rank] = ok ? v : -INFINITY;
-          a.top_logp[(size_t)r * K + rank] = ok ? v - lse : -INFINITY;
+  auto emit = [&](int rank, float v, int id) {
+    if (a.record_out) {
+      a.record_out[(size_t)r * rec + 2 + 2 * rank] = v;
+      a.record_out[(size_t)r * rec + 3 + 2 * rank] = __int_as_float(id);
+    } else {
+      a.top_ids[(size_t)r * K + rank] = ok ? id : -1;
+      a.top_logits[(size_t)r * K + rank] = ok ? v : -INFINITY;
+      a.top_logp[(size_t)r * K + rank] = ok ? v - lse : -INFINITY;
+    }
+  };
+  if (G * (K - 1) < K * (K + 1) / 2) {  // few lists (cross-rank merge): the generic pruned top-k
+    block_topk(
+        G * K, K, [&](int e, float& v, int& id) { v = cv[e]; id = ci[e]; }, emit, sv, si, c.misc + 8);
+  } else {
+    // Candidates (rank-major staging: entry j of list g at [j * G + g], lists sorted): with r_g list
+    // heads strictly above head g, entry j of list g has >= r_g + j entries beating it, so only
+    // j < K - r_g can be in the top-K — at most K (K + 1) / 2 (+ ties) candidates, ranked once.
+    // Head values as order-preserving integers in the tail of sv (candidates use its front).
+    uint32_t* hk = reinterpret_cast<uint32_t*>(sv + (size_t)G * K - G);
+    int* ncand = c.misc + 9;
+    if (tid == 0) *ncand = 0;
+    for (int g = tid; g < G; g += nt) hk[g] = cv[g] == -INFINITY ? 0u : ord_key(cv[g]);
+    __syncthreads();
+    for (int g = tid; g < G; g += nt) {
+      const uint32_t h = hk[g];
+      if (h == 0u) continue;  // empty list
+      int rg = 0;
+#pragma unroll 8
+      for (int q = 0; q < G; ++q) rg += hk[q] > h;
+      int ne = 0;
+      while (ne < K - rg && cv[ne * G + g] != -INFINITY) ++ne;
+      if (ne > 0) {
+        const int base = atomicAdd(ncand, ne);
+        for (int j = 0; j < ne; ++j) {
+          sv[base + j] = cv[j * G + g];
+          si[base + j] = ci[j * G + g];
         }
-      },
-      sv, si, c.misc + 8);
+      }
+    }
+    __syncthreads();
+    const int nc = *ncand;
+    for (int e = tid; e < nc; e += nt) {
+      const float v = sv[e];
+      const int id = si[e];
+      int rk = 0;
+      for (int f = 0; f < nc; ++f) rk += beats(sv[f], si[f], v, id);
+      if (rk < K) emit(rk, v, id);
+    }
+    if (tid == 0) c.misc[8] = min(nc, K);
+    __syncthreads();
+  }
   trace_mark(trace, 19);
   const int nvalid = c.misc[8];
   for (int q = nvalid + tid; q < K; q += nt) {

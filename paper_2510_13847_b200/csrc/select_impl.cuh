@@ -24,11 +24,7 @@ namespace ds {
 
 // ---------------------------------------------------------------- fast variants (fused step)
 
-// Order-preserving map float -> uint32 (larger float => larger key); -0 folded into +0 (R23).
-__device__ __forceinline__ uint32_t ord_key(float x) {
-  const uint32_t u = __float_as_uint(x + 0.0f);
-  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
-}
+// ord_key (order-preserving float -> uint32): common.cuh
 
 // One thread per score: s[m] = W2[m] . a1 + b2[m].  Thread m walks its 16-byte chunks starting at
 // chunk (m mod chunks), so the 8 threads of an LDS.128 phase hit 8 different bank groups.

@@ -472,7 +472,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_head_kernel(const __grid_con
   trace_mark(t.trace, 6);
   const int j = head_ticket(a, c);
   if (j < 0) return;
-  head_merge(a, c, t.S * kTcABytes, nullptr, 0, j, min(a.nrows, (int)gridDim.x));
+  head_merge(a, c, t.S * kTcABytes, t.trace, 0, j, min(a.nrows, (int)gridDim.x));
   head_merge_done(a, 0);
   trace_mark(t.trace, 7);
 }

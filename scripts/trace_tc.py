@@ -57,3 +57,12 @@ for t in range(C.positions):
     print(f"t={t} tiles/CTA max {int(a[0, :, 29].max())}: " + " ".join(line))
 print("online epilogue cycles per CTA (median over CTAs, last rep): wait, stage, rows:",
       [np.median(ns[-1, t, :, 20:23], axis=0).astype(int).tolist() for t in range(C.positions)])
+# merge phases of the merging CTAs (marks 6 partials, 16 staged, 17 lse, 19 top-k, 20 row done)
+for t in range(C.positions):
+    a = ns[-1, t]
+    mcta = np.where(a[:, 16] > 0)[0]
+    if len(mcta):
+        d = lambda x, y: np.median(a[mcta, y] - a[mcta, x]) / 1e3
+        print(f"t={t} merge CTAs {len(mcta)}: partials->staged {d(6,16):.2f} staged->lse {d(16,17):.2f} "
+              f"lse->topk {d(17,19):.2f} topk->done {d(19,20):.2f} us; last partial -> first staged "
+              f"{(a[mcta,16].min() - a[:,6].max())/1e3:.2f} us")
