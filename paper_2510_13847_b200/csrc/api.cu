@@ -239,7 +239,7 @@ ds_status dynaspec_head_forward(const ds_clusters* c, const void* h_new, int32_t
     err = launch_tc_head(c, h_new, B, sel, sel_count, sl_offsets, k_t, max_shortlist, top_ids, top_logits,
                          top_logp, lse, z_out, z_stride, reinterpret_cast<float*>(w8 + L.head),
                          reinterpret_cast<unsigned*>(w8 + L.counters), (cudaStream_t)stream, false);
-  } else if (B == 1 && !shared && cstep_head_supported(c, k_t, max_shortlist) &&
+  } else if (B == 1 && cstep_head_supported(c, k_t, max_shortlist) &&  // one row: shared == per-row
              ws_bytes >= L.head + head_rec_offset(c, B, k_t, pmax0(c, B, k_t)) + cstep_head_rec_bytes(c, k_t)) {
     // one CTA per SM streaming chunk c of the shortlist on CTA c mod G, per-warp online (max, sum, top-k)
     const size_t off = L.head + head_rec_offset(c, B, k_t, pmax0(c, B, k_t));
