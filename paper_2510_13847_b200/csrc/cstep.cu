@@ -52,7 +52,6 @@ struct CStepArgs {
   unsigned long long* trace;
   int xs_slot;  // ring slot holding [h_prev ‖ e] (-1: a separate shared-memory region)
   int head_only;  // 1: S1-S3 ran elsewhere (dynaspec_step_route); the TopK comes from h.sel / h.sel_count
-  int variant;  // debug A/B switches (DS_CSTEP_VARIANT, read once); none defined at present
 };
 
 // Shared-memory carve-up (inside HeadSmem.extra).
@@ -833,13 +832,6 @@ cudaError_t launch_cstep(const ds_clusters* c, const ds_router* r, const void* h
   s.crec = reinterpret_cast<unsigned long long*>(w8 + 256);
   s.ctr = reinterpret_cast<unsigned*>(w8);
   s.trace = debug_trace();
-  {
-    static const int variant = [] {
-      const char* v = getenv("DS_CSTEP_VARIANT");
-      return v && v[0] ? atoi(v) : 0;
-    }();
-    s.variant = variant;
-  }
   return c->dtype == DS_BF16 ? launch_cstep_t<__nv_bfloat16>(s, p.smem, p.Q, p.C, st, pdl)
                              : launch_cstep_t<float>(s, p.smem, p.Q, p.C, st, pdl);
 }
