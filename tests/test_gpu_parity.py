@@ -301,7 +301,9 @@ def test_k_equals_M_is_dense():
         assert abs(out["lse"][b].item() - dense[b]["lse"]) <= 2e-2
 
 
-def test_edge_cases_small_clusters_padding_and_singletons():
+@pytest.mark.parametrize("cstep_head", ["1", "0"])  # head-only cluster kernel (B = 1) or the grid head
+def test_edge_cases_small_clusters_padding_and_singletons(cstep_head, monkeypatch):
+    monkeypatch.setenv("DS_CSTEP_HEAD", cstep_head)
     Dy = _dyn()
     V, d, M = 40, 8, 20
     W = S.lm_head(V, d, 3, "f32", "exact")
@@ -560,3 +562,34 @@ def test_router_many_rows_row_blocks():
         if selection_certified(s_ref, ref["k"]):
             cnt = st.sel_count[b].item()
             assert st.sel[b, :cnt].cpu().tolist() == ref["sel"].tolist()
+
+
+@pytest.mark.parametrize("online", ["1", "0"])
+def test_tc_head_shared_online_epilogue_exact(online, monkeypatch):
+    """Tree rows on the tensor cores without z_out and a per-CTA logit bound above 4 tiles: the
+    online per-tile (max, sum, top-k) epilogue (and, forced off, the on-chip partial) give the
+    oracle's top ids / logits exactly and its lse (exact regime)."""
+    Dy = _dyn()
+    monkeypatch.setenv("DS_DISABLE_TC", "0")
+    monkeypatch.setenv("DS_TC_ONLINE", online)
+    V, d, M, R, kt = 80021, 256, 24, 10, 8
+    q = max(1, min(127, int((2 ** 21 / d) ** 0.5)))
+    W = S.lm_head(V, d, 0, "bf16", "exact", q=q)
+    tau, part = _partition(V, M)
+    c = Dy.Clusters.from_tau(W.to(DEV), torch.as_tensor(tau, dtype=torch.int32, device=DEV), M)
+    hn = S.hidden(R, d, 13, "bf16", "exact", q=q)
+    rng = np.random.default_rng(5)
+    for k in (3, M):
+        sel = np.sort(rng.choice(M, k, replace=False)).astype(np.int32)
+        selt = torch.zeros((1, M), dtype=torch.int32)
+        selt[0, :k] = torch.as_tensor(sel)
+        off = torch.zeros((1, M + 1), dtype=torch.int32)
+        off[0, :k + 1] = torch.as_tensor(O.shortlist_offsets(sel, part["offsets"]), dtype=torch.int32)
+        cnt = torch.tensor([k], dtype=torch.int32)
+        out = Dy.head_forward(c, hn.to(DEV), selt.to(DEV), cnt.to(DEV), off.to(DEV), kt, shared=True)
+        V_S = O.shortlist(sel, part["perm"], part["offsets"])
+        zref = O.head(f64(hn), f64(W), V_S)
+        for r in range(R):
+            check_topk(out["top_ids"][r].cpu().numpy(), out["top_logits"][r].cpu().numpy(),
+                       out["top_logp"][r].cpu().numpy(), out["lse"][r].item(), zref[r], V_S, kt, torch.float32,
+                       exact=True)
