@@ -56,7 +56,7 @@ struct CStepArgs {
 
 // Shared-memory carve-up (inside HeadSmem.extra).
 struct CExtra {
-  uint32_t xs, p1, a1, sc, w2s, b1s, b2s, offs, selb, xb, mask, sel, sloff, cnt, tmp, wm, ws, wl, surv, out, misc, total;
+  uint32_t xs, p1, a1, sc, w2s, b1s, b2s, offs, selb, xb, mask, sel, sloff, cnt, tmp, wm, ws, wl, total;
 };
 // xs_in_ring: [h_prev ‖ e] lives in a ring slot after the router rows (free until streaming starts)
 __host__ __device__ inline CExtra cstep_extra(int d, int esz, int M, int h_r, int rows1, int Q, int K, int S, int C,
@@ -88,9 +88,6 @@ __host__ __device__ inline CExtra cstep_extra(int d, int esz, int M, int h_r, in
   X.wm = take(4u * S);
   X.ws = take(4u * S);
   X.wl = take(16u * S * K);
-  X.surv = take(8u * S * K);
-  X.out = take(8u * K);
-  X.misc = take(64);
   X.total = o;
   return X;
 }
@@ -275,9 +272,6 @@ __global__ void __launch_bounds__((kMaxStages + 1) * 32, 1) cstep_kernel(const C
   float* wm = reinterpret_cast<float*>(ex + X.wm);
   float* wsum = reinterpret_cast<float*>(ex + X.ws);
   unsigned long long* wl = reinterpret_cast<unsigned long long*>(ex + X.wl);
-  unsigned long long* surv = reinterpret_cast<unsigned long long*>(ex + X.surv);
-  unsigned long long* out = reinterpret_cast<unsigned long long*>(ex + X.out);
-  int* misc = reinterpret_cast<int*>(ex + X.misc);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
   uint64_t* xbar = c.full + 2 * kMaxStages;  // spare barrier slots: x + h_new, W2 slice
   uint64_t* wbar = xbar + 1;
@@ -302,7 +296,6 @@ __global__ void __launch_bounds__((kMaxStages + 1) * 32, 1) cstep_kernel(const C
     fence_mbar_init();
   }
   for (int m = threadIdx.x; m < M; m += blockDim.x) selb[m] = 0;
-  if (threadIdx.x < 16) misc[threadIdx.x] = 0;
   if (threadIdx.x < 32) mask[threadIdx.x] = 0u;
   __syncthreads();
   cluster_arrive_relaxed();  // paired with the wait before the first DSMEM store (barrier inits are fenced)
