@@ -538,8 +538,8 @@ __global__ void __launch_bounds__((kMaxStages + 1) * 32, 1) cstep_kernel(const C
   // the global top-K (every global top-K member is in its CTA's record) — at most K (K + 1) / 2
   // candidates; the same threads form the lse partials s_g e^{m_g - M} (fixed xor trees, R19).
   // (3) thread per candidate: rank, outputs.  Two block barriers.  Scratch: the ring.
-  unsigned long long* fk = reinterpret_cast<unsigned long long*>(c.ring);  // [G][K]
-  unsigned long long* fsurv = fk + (size_t)G * K;                          // [G*K]
+  unsigned long long* raw = reinterpret_cast<unsigned long long*>(c.ring);  // [G][rec] the records
+  unsigned long long* fsurv = raw + (size_t)G * rec;                       // [G*K] candidates
   const int G4 = (G + 3) & ~3;
   uint32_t* hh = reinterpret_cast<uint32_t*>(fsurv + (((size_t)G * K + 1) & ~(size_t)1));  // [G4] heads' high words (16 B aligned)
   int* fc = reinterpret_cast<int*>(hh + G4);                               // [G] valid keys per record
@@ -552,34 +552,31 @@ __global__ void __launch_bounds__((kMaxStages + 1) * 32, 1) cstep_kernel(const C
     sh[1] = 0u;
   }
   for (int i = G + threadIdx.x; i < G4; i += blockDim.x) hh[i] = 0u;
-  __syncthreads();
-  {
+  {  // (1a) stage the record words as they land (coalesced; small code: the fields are decoded once below)
     constexpr int kB = 8;
     const int nrec = G * rec, nt = blockDim.x;
-    unsigned mymk = 0u;
     for (int i0 = threadIdx.x; i0 < nrec; i0 += kB * nt) {
       unsigned long long v[kB];
 #pragma unroll
       for (int u = 0; u < kB; ++u) v[u] = i0 + u * nt < nrec ? __ldcg(s.crec + i0 + u * nt) : 1ull;
 #pragma unroll
       for (int u = 0; u < kB; ++u) {
-        const int i = i0 + u * nt;
-        while (v[u] == 0ull) v[u] = ld_relaxed_u64(s.crec + i);  // not written yet: poll L2 (asm volatile)
-        if (i < nrec) {
-          const int gg = i / rec, f = i - gg * rec;
-          if (f == 0) {
-            const float m = __uint_as_float((uint32_t)v[u]);
-            fm[gg] = m;
-            fs[gg] = __uint_as_float((uint32_t)(v[u] >> 32));
-            if (m > -INFINITY) mymk = max(mymk, ord_key(m));
-          } else if (f == 1) {
-            fc[gg] = (int)v[u] - 1;
-          } else {
-            fk[gg * K + f - 2] = v[u];
-            if (f == 2) hh[gg] = v[u] > 1ull ? (uint32_t)(v[u] >> 32) : 0u;
-          }
-        }
+        while (v[u] == 0ull) v[u] = ld_relaxed_u64(s.crec + i0 + u * nt);  // not written yet: poll L2
+        if (i0 + u * nt < nrec) raw[i0 + u * nt] = v[u];
       }
+    }
+  }
+  __syncthreads();
+  {  // (1b) thread g: record g's (max, sum), valid count, head; the max over records
+    unsigned mymk = 0u;
+    for (int g2 = threadIdx.x; g2 < G; g2 += blockDim.x) {
+      const unsigned long long w0 = raw[(size_t)g2 * rec], hd = raw[(size_t)g2 * rec + 2];
+      const float m = __uint_as_float((uint32_t)w0);
+      fm[g2] = m;
+      fs[g2] = __uint_as_float((uint32_t)(w0 >> 32));
+      fc[g2] = (int)raw[(size_t)g2 * rec + 1] - 1;
+      hh[g2] = hd > 1ull ? (uint32_t)(hd >> 32) : 0u;
+      if (m > -INFINITY) mymk = max(mymk, ord_key(m));
     }
     mymk = __reduce_max_sync(0xffffffffu, mymk);
     if (lane == 0 && mymk) atomicMax(&sh[1], mymk);
@@ -603,7 +600,7 @@ __global__ void __launch_bounds__((kMaxStages + 1) * 32, 1) cstep_kernel(const C
       const int ne = min(K - r, fc[t]);
       if (ne > 0) {
         const int base = (int)atomicAdd(&sh[0], (unsigned)ne);
-        for (int j = 0; j < ne; ++j) fsurv[base + j] = fk[t * K + j];
+        for (int j = 0; j < ne; ++j) fsurv[base + j] = raw[(size_t)t * rec + 2 + j];
       }
       if (fm[t] > -INFINITY) part += fs[t] * expf(fm[t] - Mx);
     }
@@ -613,10 +610,6 @@ __global__ void __launch_bounds__((kMaxStages + 1) * 32, 1) cstep_kernel(const C
   __syncthreads();
   trace_mark(s.trace, 15);
   const int ns = (int)sh[0];
-  if (s.trace && threadIdx.x == 0) {
-    s.trace[24] = ns;
-    s.trace[25] = Mk;
-  }
   const bool ok = Mx > -INFINITY;
   float sum = 0.f;
   for (int w2 = 0; w2 < nwarps; ++w2) sum += wps[w2];
@@ -757,7 +750,7 @@ static bool cstep_plan(const ds_clusters* c, const ds_router* r, int B, int k_t,
   }
   // the last CTA merges the G records inside its ring
   const size_t G = (size_t)C * Q;
-  if (G * (16 * k_t + 20) + 1024 > (size_t)p->hp.stages * p->hp.stage_bytes) return false;
+  if (G * (8 * (2 + k_t) + 8 * k_t + 20) + 1024 > (size_t)p->hp.stages * p->hp.stage_bytes) return false;
   p->total = 256 + align_up(G * (2 + k_t) * sizeof(unsigned long long), 256);
   return true;
 }
