@@ -484,6 +484,8 @@ __global__ void __launch_bounds__(256) union_kernel(const int32_t* __restrict__ 
                                                     uint32_t* __restrict__ rowmask, int32_t* usel, int32_t* ucnt,
                                                     int32_t* usloff) {
   extern __shared__ __align__(16) uint32_t us[];
+  pdl_wait();                 // the rows' selections come from the router (or the previous batch's head)
+  pdl_launch_dependents();    // the head kernel may start its prologue; it waits for this grid
   uint32_t* acc = us;                                   // [32]
   uint32_t* rm = us + 32;                               // [B][32]
   int32_t* offs = reinterpret_cast<int32_t*>(rm + B * 32);  // [M+1]
@@ -630,9 +632,18 @@ cudaError_t launch_tc_batched(const ds_clusters* c, const void* h_new, int B, co
     int32_t* ucnt = usel + c->M;
     int32_t* usloff = ucnt + 4;
     const size_t usm = (size_t)(32 + nr * 32) * 4 + (size_t)(2 * c->M + 1) * 4;
-    union_kernel<<<1, 256, usm, st>>>(sel + (size_t)r0 * c->M, sel_count + r0, nr, c->M, c->offsets, rowmask, usel,
-                                      ucnt, usloff);
-    cudaError_t e = cudaGetLastError();
+    cudaLaunchConfig_t uc = {};
+    uc.gridDim = dim3(1);
+    uc.blockDim = dim3(256);
+    uc.dynamicSmemBytes = usm;
+    uc.stream = st;
+    cudaLaunchAttribute ua[1];
+    ua[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    ua[0].val.programmaticStreamSerializationAllowed = 1;
+    uc.attrs = ua;
+    uc.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&uc, union_kernel, sel + (size_t)r0 * c->M, sel_count + r0, nr, c->M,
+                                       (const int32_t*)c->offsets, rowmask, usel, ucnt, usloff);
     if (e != cudaSuccess) return e;
     TcMaps mw;
     CUtensorMap mh;
@@ -642,7 +653,7 @@ cudaError_t launch_tc_batched(const ds_clusters* c, const void* h_new, int B, co
     TcArgs t;
     fill_head_args(t.h, c, p.hp, h0, 0, nr, usel, ucnt, usloff, 1, k_t, 0, top_ids + (size_t)r0 * k_t,
                    top_logits + (size_t)r0 * k_t, top_logp + (size_t)r0 * k_t, lse + r0, nullptr, 0, part, counter,
-                   false);
+                   true);
     t.h.h = h0;
     t.N = p.N;
     t.S = p.S;
@@ -652,7 +663,7 @@ cudaError_t launch_tc_batched(const ds_clusters* c, const void* h_new, int B, co
     t.rowmask = rowmask;
     t.trace = debug_trace();
     t.box_cap = p.box_cap;
-    e = launch_tc_kernel(p, mw, mh, t, st, false);
+    e = launch_tc_kernel(p, mw, mh, t, st, true);  // PDL after the union kernel
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;
