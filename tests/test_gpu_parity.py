@@ -593,3 +593,41 @@ def test_tc_head_shared_online_epilogue_exact(online, monkeypatch):
             check_topk(out["top_ids"][r].cpu().numpy(), out["top_logits"][r].cpu().numpy(),
                        out["top_logp"][r].cpu().numpy(), out["lse"][r].item(), zref[r], V_S, kt, torch.float32,
                        exact=True)
+
+
+def test_gemma3_batched_full_size_sampled_rows(monkeypatch):
+    """Gemma-3 head at full size (V 262144, d 5376, M 512, h_r 256) and the bench's batch (B = 64
+    independent rows -> router + union + batched tcgen05 head), k = 16 (t = 2): sampled rows
+    against the oracle (scores, selection, shortlist offsets, top-k, lse)."""
+    Dy = _dyn()
+    monkeypatch.setenv("DS_DISABLE_TC", "0")
+    C = S.CONFIGS["gemma3"]
+    B, t = 64, 2
+    W = S.lm_head(C.V, C.d, 0, "bf16", device=DEV)
+    tau = S.random_partition(C.V, C.M, 2)
+    perm, off = O.layout(tau, C.M)
+    part = {"perm": perm, "offsets": off}
+    c = Dy.Clusters.from_tau(W, torch.as_tensor(tau, dtype=torch.int32, device=DEV), C.M)
+    rt = S.router(C.d, C.h_r, C.M, 1, "bf16")
+    r = Dy.Router(*[x.to(DEV) for x in rt])
+    st = Dy.DraftStep(c, r, B, C.k_t)
+    hp, e, hn = S.step_inputs(B, C.d, t, "bf16")
+    st(hp.to(DEV), e.to(DEV), hn.to(DEV), t=t, k_max=C.k_max, k_min=C.k_min)
+    torch.cuda.synchronize()
+    Wo, ro = Rows(W), _oracle_router(rt)
+    for b in (0, 37, 63):
+        ref = O.draft_step(part, ro, Wo, f64(hp[b:b + 1]), f64(e[b:b + 1]), f64(hn[b:b + 1]), t, C.k_max, C.k_min,
+                           C.k_t)[0]
+        s_ref = ref["scores"]
+        assert np.max(np.abs(st.scores[b].cpu().numpy() - s_ref)) < 1e-3 * max(1.0, np.sqrt(np.mean(s_ref ** 2)))
+        cnt = st.sel_count[b].item()
+        sel = np.array(st.sel[b, :cnt].cpu().tolist())
+        if selection_certified(s_ref, ref["k"]):
+            assert sel.tolist() == ref["sel"].tolist()
+            rb = ref
+        else:
+            rb = O.draft_step(part, ro, Wo, f64(hp[b:b + 1]), f64(e[b:b + 1]), f64(hn[b:b + 1]), t, C.k_max,
+                              C.k_min, C.k_t, sel_override=[sel])[0]
+        assert st.sl_offsets[b, :cnt + 1].cpu().tolist() == rb["sl_offsets"].tolist()
+        check_topk(st.top_ids[b].cpu().numpy(), st.top_logits[b].cpu().numpy(), st.top_logp[b].cpu().numpy(),
+                   st.lse[b].item(), rb["z"], rb["V_S"], C.k_t, torch.bfloat16)
