@@ -567,6 +567,8 @@ __global__ void __launch_bounds__((kMaxStages + 1) * 32, 1) cstep_kernel(const C
     }
   }
   __syncthreads();
+  // every record word is in shared memory: zero them for the next launch now (off the output path)
+  for (int i = threadIdx.x; i < G * rec; i += blockDim.x) s.crec[i] = 0ull;
   {  // (1b) thread g: record g's (max, sum), valid count, head; the max over records
     unsigned mymk = 0u;
     for (int g2 = threadIdx.x; g2 < G; g2 += blockDim.x) {
@@ -642,7 +644,6 @@ __global__ void __launch_bounds__((kMaxStages + 1) * 32, 1) cstep_kernel(const C
   }
   if (threadIdx.x == 0) a.lse[0] = lse;
   trace_mark(s.trace, 7);
-  for (int i = threadIdx.x; i < G * rec; i += blockDim.x) s.crec[i] = 0ull;  // ready for the next launch
 }
 
 // ------------------------------------------------------------------ host side
