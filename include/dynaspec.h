@@ -31,9 +31,6 @@
  *    zero-filled once by dynaspec_ws_init() before its first use (the library leaves the
  *    counters it uses back at zero after each call).  One workspace must not be used by
  *    two calls that may run concurrently.
- *  - Kernels whose CTAs wait on each other (the cluster step's merger, the grid-wide step,
- *    the last-CTA merges) are cooperative launches: every CTA is co-resident, so calls on
- *    different streams of one GPU cannot starve one another.
  *  - Precision: weights and activations are bf16 (DS_BF16) or fp32 (DS_F32), one dtype per
  *    call; every dot product accumulates in fp32; all floating outputs are fp32.
  *  - Determinism: no floating-point atomics; every reduction has a fixed order, so two

@@ -775,19 +775,15 @@ static cudaError_t launch_cstep_t(const CStepArgs& s, size_t smem, int Q, int C,
   cfg.blockDim = dim3((s.h.stages + 1) * 32);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  // cooperative: every CTA of the grid is co-resident (the merger polls the other CTAs' records),
-  // also when other streams run kernels on the same GPU
-  cudaLaunchAttribute attr[3];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = Q;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
-  attr[1].id = cudaLaunchAttributeCooperative;
-  attr[1].val.cooperative = 1;
-  attr[2].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[2].val.programmaticStreamSerializationAllowed = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = pdl ? 3 : 2;
+  cfg.numAttrs = pdl ? 2 : 1;
   return cudaLaunchKernelEx(&cfg, cstep_kernel<T>, s);
 }
 

@@ -334,15 +334,11 @@ static cudaError_t launch_step_t(const StepArgs& s, size_t smem, int G, cudaStre
   cfg.blockDim = dim3((s.h.stages + 1) * 32);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  // cooperative: all CTAs co-resident (the last CTAs wait on a grid-wide counter), also when
-  // other streams run kernels on the same GPU
-  cudaLaunchAttribute attr[2];
-  attr[0].id = cudaLaunchAttributeCooperative;
-  attr[0].val.cooperative = 1;
-  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = pdl ? 2 : 1;
+  cfg.numAttrs = pdl ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, step_kernel<T>, s);
 }
 
