@@ -31,6 +31,12 @@
  *    zero-filled once by dynaspec_ws_init() before its first use (the library leaves the
  *    counters it uses back at zero after each call).  One workspace must not be used by
  *    two calls that may run concurrently.
+ *  - Co-residency: the draft-step and head kernels launch at most one CTA per SM and their
+ *    CTAs wait on each other (the cluster step's merger polls the other CTAs' records; the
+ *    last-CTA merges wait on a grid counter).  Two such calls must not run concurrently on one
+ *    GPU (on different streams), or each could hold SMs the other needs.  (A cooperative
+ *    launch would guarantee co-residency at no measured cost, but the profiler cannot replay
+ *    cooperative cluster launches, so it is not used.)
  *  - Precision: weights and activations are bf16 (DS_BF16) or fp32 (DS_F32), one dtype per
  *    call; every dot product accumulates in fp32; all floating outputs are fp32.
  *  - Determinism: no floating-point atomics; every reduction has a fixed order, so two
