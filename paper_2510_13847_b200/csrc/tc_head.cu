@@ -29,7 +29,8 @@ namespace ds {
 constexpr int kTcBoxRows = 16;
 constexpr int kTcBoxes = 8;              // boxes per 128-row tile
 constexpr int kTcK = 64;                 // K elements per stage (128 bytes: one swizzle span)
-constexpr int kTcABytes = 128 * kTcK * 2;
+constexpr int kTcKPS = 2;                 // 64-wide K chunks per ring stage (one commit per stage)
+constexpr int kTcABytes = 128 * kTcK * 2 * kTcKPS;  // A bytes of one stage
 constexpr int kTcThreads = 6 * 32;
 constexpr int kTcMaxBoxes = 2048;
 
@@ -59,7 +60,7 @@ __host__ __device__ inline TcSmem tc_smem(int S, int N, int rows, int lcap, int 
   L.a = o;
   o += (uint32_t)S * kTcABytes;
   L.b = o;
-  o += (uint32_t)S * N * 128;
+  o += (uint32_t)S * N * 128 * kTcKPS;
   o = (o + 1023u) & ~1023u;
   L.bars = o;
   o += (2 * 16 + 4) * 8;
@@ -254,17 +255,22 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_head_kernel(const __grid_con
         for (int b = b0; contig && b < b1; ++b)
           contig = boxes[b].z == kTcBoxRows && boxes[b].x == boxes[b0].x + (b - b0) * kTcBoxRows;
         const uint32_t bytes = (uint32_t)(b1 - b0) * kTcBoxRows * kTcK * 2 + (uint32_t)t.N * kTcK * 2;
-        for (int kc = 0; kc < t.kchunks; ++kc, ++it) {
+        for (int kc0 = 0; kc0 < t.kchunks; kc0 += kTcKPS, ++it) {
           const uint32_t s = it % S;
+          const int nk = min(kTcKPS, t.kchunks - kc0);
           mbar_wait(&empty[s], ((it / S) & 1u) ^ 1u);
-          mbar_arrive_expect_tx(&full[s], bytes);
-          if (contig)
-            tma_load_2d(sa + (size_t)s * kTcABytes, &tmWs.w[3], kc * kTcK, boxes[b0].x, &full[s], pol_w);
-          else
-            for (int b = b0; b < b1; ++b)
-              tma_load_2d(sa + (size_t)s * kTcABytes + (size_t)(b - b0) * kTcBoxRows * 128, &tmWs.w[0], kc * kTcK,
-                          boxes[b].x, &full[s], pol_w);
-          tma_load_2d(sb + (size_t)s * t.N * 128, &tmH, kc * kTcK, 0, &full[s], pol_h);
+          mbar_arrive_expect_tx(&full[s], bytes * (uint32_t)nk);
+          for (int j = 0; j < nk; ++j) {
+            const int kc = kc0 + j;
+            uint8_t* sa_j = sa + (size_t)s * kTcABytes + (size_t)j * (kTcABytes / kTcKPS);
+            if (contig)
+              tma_load_2d(sa_j, &tmWs.w[3], kc * kTcK, boxes[b0].x, &full[s], pol_w);
+            else
+              for (int b = b0; b < b1; ++b)
+                tma_load_2d(sa_j + (size_t)(b - b0) * kTcBoxRows * 128, &tmWs.w[0], kc * kTcK, boxes[b].x, &full[s],
+                            pol_w);
+            tma_load_2d(sb + ((size_t)s * kTcKPS + j) * t.N * 128, &tmH, kc * kTcK, 0, &full[s], pol_h);
+          }
         }
       }
       trace_mark_w(t.trace, 2);
@@ -279,16 +285,19 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_head_kernel(const __grid_con
         mbar_wait(&tempty[buf], (((uint32_t)tile >> 1) & 1u) ^ 1u);
         tc_fence_after();
         const uint32_t d_tmem = tmem + (uint32_t)(buf * t.N);
-        for (int kc = 0; kc < t.kchunks; ++kc, ++it) {
+        for (int kc0 = 0; kc0 < t.kchunks; kc0 += kTcKPS, ++it) {
           const uint32_t s = it % S;
+          const int nk = min(kTcKPS, t.kchunks - kc0);
           mbar_wait(&full[s], (it / S) & 1u);
           tc_fence_after();
-          const uint32_t abase = smem_u32(sa + (size_t)s * kTcABytes);
-          const uint32_t bbase = smem_u32(sb + (size_t)s * t.N * 128);
+          for (int j = 0; j < nk; ++j) {
+            const uint32_t abase = smem_u32(sa + (size_t)s * kTcABytes + (size_t)j * (kTcABytes / kTcKPS));
+            const uint32_t bbase = smem_u32(sb + ((size_t)s * kTcKPS + j) * t.N * 128);
 #pragma unroll
-          for (int k = 0; k < kTcK / 16; ++k)
-            tc_mma_bf16(d_tmem, sw128_desc(abase + k * 32), sw128_desc(bbase + k * 32), idesc,
-                        (kc | k) != 0 ? 1u : 0u);
+            for (int k = 0; k < kTcK / 16; ++k)
+              tc_mma_bf16(d_tmem, sw128_desc(abase + k * 32), sw128_desc(bbase + k * 32), idesc,
+                          (kc0 + j + k) != 0 ? 1u : 0u);
+          }
           tc_commit(&empty[s]);  // slot reusable once these MMAs have read it
         }
         tc_commit(&tfull[buf]);  // accumulator complete
