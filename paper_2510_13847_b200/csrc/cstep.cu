@@ -650,7 +650,10 @@ __global__ void __launch_bounds__((kMaxStages + 1) * 32, 1) cstep_kernel(const C
 
 // Cluster size: DS_CLUSTER_Q (0 disables the cluster step), default 16 (non-portable; one cluster
 // per GPC).  Clusters per launch: the hardware's co-residency limit at one CTA per SM.
-static int cluster_q() {
+// Cluster size: DS_CLUSTER_Q if set (0 disables the cluster step; 1: every CTA evaluates the whole
+// router alone, no exchanges — measured slower even for the Tiny router, 16.96 vs 14.56 us, the
+// 148 CTAs each pulling W1 from L2), default 16 (each CTA holds 1/16 of W1).
+static int cluster_q(const ds_clusters*, const ds_router*) {
   const char* v = getenv("DS_CLUSTER_Q");
   if (v && v[0]) return atoi(v);
   return 16;
@@ -714,8 +717,8 @@ static bool cstep_plan(const ds_clusters* c, const ds_router* r, int B, int k_t,
   // r == nullptr: head-only launch (the selection comes from dynaspec_step_route): one CTA per SM,
   // no cluster exchanges
   if (B != 1 || shared || k_t > kCStepMaxKt) return false;
-  const int Q = r ? cluster_q() : 1;
-  if (r && (Q < 2 || Q > 16)) return false;
+  const int Q = r ? cluster_q(c, r) : 1;
+  if (r && (Q < 1 || Q > 16)) return false;
   const int C = max_clusters(Q);
   if (C < 1 || C * Q < 64) return false;  // too few SMs would stream the head slowly
   p->Q = Q;

@@ -34,7 +34,7 @@ def _setup(V, d, M, h_r, dtype, regime, seed_part=2):
     return W, rt, {"perm": perm, "offsets": off}, c, r
 
 
-@pytest.mark.parametrize("Q", ["16", "8", "4", "2", "0"])
+@pytest.mark.parametrize("Q", ["16", "8", "4", "2", "1", "0"])
 @pytest.mark.parametrize("dtype,h_r,k_t", [("bf16", 16, 8), ("f32", 16, 1), ("bf16", 0, 32), ("f32", 8, 32)])
 @pytest.mark.parametrize("k_max,k_min", [(16, 4), (40, 33)])  # k <= 32 and k > 32 up to k = M
 def test_cluster_step_exact_bit_exact(Q, dtype, h_r, k_t, k_max, k_min, monkeypatch):
