@@ -32,11 +32,13 @@
  *    counters it uses back at zero after each call).  One workspace must not be used by
  *    two calls that may run concurrently.
  *  - Co-residency: the draft-step and head kernels launch at most one CTA per SM and their
- *    CTAs wait on each other (the cluster step's merger polls the other CTAs' records; the
- *    last-CTA merges wait on a grid counter).  Two such calls must not run concurrently on one
- *    GPU (on different streams), or each could hold SMs the other needs.  (A cooperative
- *    launch would guarantee co-residency at no measured cost, but the profiler cannot replay
- *    cooperative cluster launches, so it is not used.)
+ *    CTAs wait on each other (the single-row steps poll published words and records; the
+ *    last-CTA merges wait on a grid counter).  A concurrent kernel that keeps SMs busy delays
+ *    them; the single-row step kernels bound every wait (2 s) and then raise
+ *    DS_ERR_DEVICE_TIMEOUT in the workspace error word (dynaspec_ws_error) instead of hanging.
+ *  - Workspace layout: the first 112 KB of every workspace are a fixed prefix (counters, the
+ *    device error word, the polled-record regions of the single-row step kernels, written by no
+ *    other kernel), so one workspace may serve any sequence of calls on one stream.
  *  - Precision: weights and activations are bf16 (DS_BF16) or fp32 (DS_F32), one dtype per
  *    call; every dot product accumulates in fp32; all floating outputs are fp32.
  *  - Determinism: no floating-point atomics; every reduction has a fixed order, so two
@@ -72,7 +74,9 @@ typedef enum {
   DS_ERR_EMPTY_SHORTLIST = 8,       /* a cluster would be empty (SPEC EmptyShortlist) */
   DS_ERR_WORKSPACE = 9,             /* workspace NULL or smaller than the *_ws() size */
   DS_ERR_CUDA = 10,                 /* a CUDA runtime error while launching */
-  DS_ERR_UNSUPPORTED = 11           /* shape outside what the kernels support (e.g. d % 8 != 0) */
+  DS_ERR_UNSUPPORTED = 11,          /* shape outside what the kernels support (e.g. d % 8 != 0) */
+  DS_ERR_DEVICE_TIMEOUT = 12        /* (device error word) a CTA of a single-row step kernel waited > 2 s for
+                                       another CTA of its grid: SMs held by a concurrent kernel; outputs invalid */
 } ds_status;
 
 typedef enum { DS_BF16 = 0, DS_F32 = 1 } ds_dtype;
@@ -137,6 +141,11 @@ int64_t dynaspec_max_shortlist(const ds_clusters* c, int32_t k);
 
 /* Zero-fill a workspace (once, before its first use). */
 ds_status dynaspec_ws_init(void* ws, size_t ws_bytes, ds_stream_t stream);
+
+/* Data-dependent device errors raised after a call returned are written to the workspace's error
+ * word (today: DS_ERR_DEVICE_TIMEOUT from a bounded inter-CTA wait).  Copies it to *code_host
+ * (DS_OK if none) and clears it.  SYNCHRONISES `stream`. */
+ds_status dynaspec_ws_error(void* ws, size_t ws_bytes, int32_t* code_host, ds_stream_t stream);
 
 /* ---------------------------------------------------------------- S0: offline partition */
 

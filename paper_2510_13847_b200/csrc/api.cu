@@ -71,7 +71,7 @@ struct WsLayout {
 static WsLayout ws_layout(size_t meta_bytes, size_t head_bytes) {
   WsLayout L;
   L.counters = 0;
-  L.meta = 256;
+  L.meta = kWsFixed;  // after the counters and the polled-record regions (internal.h)
   L.head = align_up(L.meta + meta_bytes, 256);
   L.total = align_up(L.head + head_bytes, 256);
   return L;
@@ -97,6 +97,7 @@ const char* dynaspec_status_string(ds_status s) {
     case DS_ERR_WORKSPACE: return "workspace missing or too small";
     case DS_ERR_CUDA: return "CUDA error";
     case DS_ERR_UNSUPPORTED: return "unsupported shape";
+    case DS_ERR_DEVICE_TIMEOUT: return "device timeout: a CTA waited > 2 s for its grid (SMs held by a concurrent kernel)";
   }
   return "unknown status";
 }
@@ -122,6 +123,17 @@ int64_t dynaspec_max_shortlist(const ds_clusters* c, int32_t k) {
 ds_status dynaspec_ws_init(void* ws, size_t ws_bytes, ds_stream_t stream) {
   if (!ws || ws_bytes < 256) return DS_ERR_WORKSPACE;
   return cudaMemsetAsync(ws, 0, ws_bytes, (cudaStream_t)stream) == cudaSuccess ? DS_OK : DS_ERR_CUDA;
+}
+
+ds_status dynaspec_ws_error(void* ws, size_t ws_bytes, int32_t* code_host, ds_stream_t stream) {
+  if (!ws || ws_bytes < kWsFixed || !code_host) return DS_ERR_WORKSPACE;
+  unsigned v = 0;
+  uint8_t* w = static_cast<uint8_t*>(ws) + kWsErrorWord;
+  if (cudaMemcpyAsync(&v, w, 4, cudaMemcpyDeviceToHost, (cudaStream_t)stream) != cudaSuccess) return DS_ERR_CUDA;
+  if (cudaMemsetAsync(w, 0, 4, (cudaStream_t)stream) != cudaSuccess) return DS_ERR_CUDA;
+  if (cudaStreamSynchronize((cudaStream_t)stream) != cudaSuccess) return DS_ERR_CUDA;
+  *code_host = (int32_t)v;
+  return DS_OK;
 }
 
 size_t dynaspec_layout_ws(int64_t V, int32_t M) { return layout_ws_bytes(V, M); }
@@ -190,25 +202,17 @@ ds_status dynaspec_select(const float* scores, int32_t B, const ds_clusters* c, 
   return err == cudaSuccess ? DS_OK : DS_ERR_CUDA;
 }
 
-// Offset (from the head region) of the head-only cluster kernel's records: after every other head
-// kernel's scratch, so their partials never leave non-zero words where the records are polled.
-static HeadPlan pmax0(const ds_clusters* c, int32_t B, int32_t k_t) {
-  HeadPlan p = {};
-  head_plan(c, B, k_t, 0, &p);
-  return p;
-}
-
-static size_t head_rec_offset(const ds_clusters* c, int32_t B, int32_t k_t, const HeadPlan& pmax) {
-  return align_up(std::max(std::max(pmax.part_bytes, tc_head_part_bytes(c, B, k_t)), tc_batched_ws_bytes(c, B, k_t)),
-                  256);
+// Head scratch for B rows: the largest of the head kernels' partials (the single-row step kernels'
+// records live in the fixed prefix, internal.h).
+static size_t head_scratch(const ds_clusters* c, int32_t B, int32_t k_t, const HeadPlan& pmax) {
+  return std::max(std::max(pmax.part_bytes, tc_head_part_bytes(c, B, k_t)), tc_batched_ws_bytes(c, B, k_t));
 }
 
 size_t dynaspec_head_forward_ws(const ds_clusters* c, int32_t B, int32_t k_t) {
   HeadPlan p;
   if (!c || B < 1 || k_t < 1 || k_t > kMaxKt) return 0;
   if (!head_plan(c, B, k_t, 0, &p)) return 0;
-  // + a dedicated tail for the head-only cluster kernel's records (must stay zero between calls)
-  return ws_layout(0, head_rec_offset(c, B, k_t, p) + (B == 1 ? cstep_head_rec_bytes(c, k_t) : 0)).total;
+  return ws_layout(0, head_scratch(c, B, k_t, p)).total;
 }
 
 ds_status dynaspec_head_forward(const ds_clusters* c, const void* h_new, int32_t B, const int32_t* sel,
@@ -239,12 +243,13 @@ ds_status dynaspec_head_forward(const ds_clusters* c, const void* h_new, int32_t
     err = launch_tc_head(c, h_new, B, sel, sel_count, sl_offsets, k_t, max_shortlist, top_ids, top_logits,
                          top_logp, lse, z_out, z_stride, reinterpret_cast<float*>(w8 + L.head),
                          reinterpret_cast<unsigned*>(w8 + L.counters), (cudaStream_t)stream, false);
-  } else if (B == 1 && cstep_head_supported(c, k_t, max_shortlist) &&  // one row: shared == per-row
-             ws_bytes >= L.head + head_rec_offset(c, B, k_t, pmax0(c, B, k_t)) + cstep_head_rec_bytes(c, k_t)) {
-    // one CTA per SM streaming chunk c of the shortlist on CTA c mod G, per-warp online (max, sum, top-k)
-    const size_t off = L.head + head_rec_offset(c, B, k_t, pmax0(c, B, k_t));
+  } else if (B == 1 && gstep_supported(c, nullptr, 1, k_t, 0) && (reinterpret_cast<uintptr_t>(h_new) & 15u) == 0) {
+    // one row (shared == per-row): one CTA per SM streams chunk c of the shortlist on CTA c mod G
+    err = launch_gstep_head(c, h_new, sel, sel_count, sl_offsets, k_t, max_shortlist, top_ids, top_logits, top_logp,
+                            lse, z_out, ws, (cudaStream_t)stream);
+  } else if (B == 1 && cstep_head_supported(c, k_t, max_shortlist)) {
     err = launch_cstep_head(c, h_new, sel, sel_count, sl_offsets, k_t, max_shortlist, top_ids, top_logits, top_logp,
-                            lse, z_out, z_stride, w8 + off, (cudaStream_t)stream);
+                            lse, z_out, z_stride, ws, (cudaStream_t)stream);
   } else {
     err = launch_head(c, p, h_new, B, sel, sel_count, sl_offsets, shared ? 1 : 0, k_t, max_shortlist, top_ids,
                       top_logits, top_logp, lse, z_out, z_stride, reinterpret_cast<float*>(w8 + L.head),
@@ -402,8 +407,7 @@ size_t dynaspec_draft_step_ws(const ds_clusters* c, const ds_router* r, int32_t 
   if (!head_plan(c, B, k_t, 0, &p)) return 0;
   const size_t meta = meta_plan(r, B).part_bytes;
   const size_t scores = (size_t)B * r->M * sizeof(float);
-  return std::max(ws_layout(align_up(meta, 256) + align_up(scores, 256),
-                            head_rec_offset(c, B, k_t, p) + (B == 1 ? cstep_head_rec_bytes(c, k_t) : 0)).total,
+  return std::max(ws_layout(align_up(meta, 256) + align_up(scores, 256), head_scratch(c, B, k_t, p)).total,
                   step_ws_bytes(c, r, B, k_t));
 }
 
@@ -471,6 +475,9 @@ ds_status dynaspec_draft_step(const ds_clusters* c, const ds_router* r, const vo
   if (tc && ws_bytes < ws_layout(align_up(meta_bytes, 256) + align_up(score_bytes, 256),
                                  tc_head_part_bytes(c, B, k_t)).total)
     return DS_ERR_WORKSPACE;
+  if (tcb && ws_bytes < ws_layout(align_up(meta_bytes, 256) + align_up(score_bytes, 256),
+                                  tc_batched_ws_bytes(c, B, k_t)).total)
+    return DS_ERR_WORKSPACE;  // checked before anything is enqueued
   uint8_t* w8 = static_cast<uint8_t*>(ws);
   unsigned* counters = reinterpret_cast<unsigned*>(w8 + L.counters);
   float* meta_part = reinterpret_cast<float*>(w8 + L.meta);
@@ -495,20 +502,19 @@ ds_status dynaspec_draft_step(const ds_clusters* c, const ds_router* r, const vo
   const unsigned evflags = cap == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : cudaEventRecordDefault;
   if (head_begin && cudaEventRecordWithFlags((cudaEvent_t)head_begin, sd, evflags) != cudaSuccess) return DS_ERR_CUDA;
   if (tcb) {
-    if (ws_bytes < ws_layout(align_up(meta_bytes, 256) + align_up(score_bytes, 256),
-                             tc_batched_ws_bytes(c, B, k_t)).total)
-      return DS_ERR_WORKSPACE;
     err = launch_tc_batched(c, h_new, B, out->sel, out->sel_count, k_t, out->top_ids, out->top_logits,
                             out->top_logp, out->lse, w8 + L.head, counters, sd);
   } else if (tc) {
     err = launch_tc_head(c, h_new, B, out->sel, out->sel_count, out->sl_offsets, k_t, ms, out->top_ids,
                          out->top_logits, out->top_logp, out->lse, out->z_out, out->z_stride,
                          reinterpret_cast<float*>(w8 + L.head), counters, sd, !two_streams && head_begin == nullptr);
-  } else if (B == 1 && !shared && cstep_head_supported(c, k_t, ms) &&
-             ws_bytes >= L.head + head_rec_offset(c, B, k_t, pmax) + cstep_head_rec_bytes(c, k_t)) {
+  } else if (B == 1 && !shared && gstep_supported(c, nullptr, 1, k_t, 0) &&
+             (reinterpret_cast<uintptr_t>(h_new) & 15u) == 0) {
+    err = launch_gstep_head(c, h_new, out->sel, out->sel_count, out->sl_offsets, k_t, ms, out->top_ids,
+                            out->top_logits, out->top_logp, out->lse, out->z_out, ws, sd);
+  } else if (B == 1 && !shared && cstep_head_supported(c, k_t, ms)) {
     err = launch_cstep_head(c, h_new, out->sel, out->sel_count, out->sl_offsets, k_t, ms, out->top_ids,
-                            out->top_logits, out->top_logp, out->lse, out->z_out, out->z_stride,
-                            w8 + L.head + head_rec_offset(c, B, k_t, pmax), sd);
+                            out->top_logits, out->top_logp, out->lse, out->z_out, out->z_stride, ws, sd);
   } else {
     err = launch_head(c, p, h_new, B, out->sel, out->sel_count, out->sl_offsets, shared ? 1 : 0, k_t, ms,
                       out->top_ids, out->top_logits, out->top_logp, out->lse, out->z_out, out->z_stride,

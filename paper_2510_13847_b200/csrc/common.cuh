@@ -149,8 +149,8 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
 // Opt-in phase trace (dynaspec_debug_set_trace): [cta][slot] nanosecond timestamps.
 __device__ __forceinline__ void trace_mark(unsigned long long* t, int slot) {
   if (t != nullptr && threadIdx.x == 0) {
+    t[blockIdx.x * 64 + 32 + slot] = clock64();  // SM clock first: the %globaltimer read is not free
     t[blockIdx.x * 64 + slot] = globaltimer_ns();
-    t[blockIdx.x * 64 + 32 + slot] = clock64();
     if (slot == 0) {
       uint32_t sm;
       asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
@@ -521,5 +521,18 @@ __device__ __forceinline__ void cluster_arrive_release() {
 }
 __device__ __forceinline__ void cluster_wait_acquire() {
   asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+}  // namespace ds
+
+namespace ds {
+// 64-bit store visible at GPU scope (one word: value and its "written" tag land together).
+__device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+// 16-byte read-only global load (inputs that no kernel writes while this one runs).
+__device__ __forceinline__ uint4 ld_nc_v4(const void* p) {
+  uint4 v;
+  asm volatile("ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+  return v;
 }
 }  // namespace ds

@@ -28,6 +28,7 @@
 #include "head_impl.cuh"
 #include "internal.h"
 #include "select_impl.cuh"
+#include "keys.cuh"
 
 namespace ds {
 
@@ -90,41 +91,6 @@ __host__ __device__ inline CExtra cstep_extra(int d, int esz, int M, int h_r, in
   X.wl = take(16u * S * K);
   X.total = o;
   return X;
-}
-
-// ---------------------------------------------------------------- total order as one 64-bit key
-// key = ord_key(z) << 32 | ~id: a larger key is a larger logit, or an equal logit with a lower
-// token id (R7, R23: -0 folded into +0).  0 is below every valid key (padding).
-__device__ __forceinline__ unsigned long long tok_key(float z, int id) {
-  return ((unsigned long long)ord_key(z) << 32) | (unsigned long long)(~(uint32_t)id);
-}
-__device__ __forceinline__ float key_value(unsigned long long k) {
-  const uint32_t u = (uint32_t)(k >> 32);
-  return __uint_as_float((u & 0x80000000u) ? (u & 0x7fffffffu) : ~u);
-}
-__device__ __forceinline__ int key_id(unsigned long long k) { return (int)(~(uint32_t)k); }
-
-// Warp-distributed sorted list (lane r < K holds the r-th best key; 0 = empty).  `kth` mirrors
-// lane K-1's entry, so a candidate that cannot enter costs one compare.
-__device__ __forceinline__ void list_insert(unsigned long long& mine, unsigned long long& kth, unsigned long long x,
-                                            int K, int lane) {
-  if (x <= kth) return;  // warp-uniform
-  const uint32_t lanes = K >= 32 ? 0xffffffffu : ((1u << K) - 1u);
-  const int pos = __popc(__ballot_sync(0xffffffffu, mine > x) & lanes);
-  const unsigned long long up = __shfl_up_sync(0xffffffffu, mine, 1);
-  if (lane > pos) mine = up;
-  else if (lane == pos) mine = x;
-  kth = __shfl_sync(0xffffffffu, mine, K - 1);
-}
-
-// Online softmax accumulation of one logit (warp-uniform state).
-__device__ __forceinline__ void lse_push(float& m, float& s, float z) {
-  if (z > m) {
-    s = s * expf(m - z) + 1.f;
-    m = z;
-  } else {
-    s += expf(z - m);
-  }
 }
 
 // Two staged rows against two (possibly different) vectors: lane-parallel fp32 partials + warp
@@ -755,7 +721,8 @@ static bool cstep_plan(const ds_clusters* c, const ds_router* r, int B, int k_t,
   // the last CTA merges the G records inside its ring
   const size_t G = (size_t)C * Q;
   if (G * (8 * (2 + k_t) + 8 * k_t + 20) + 1024 > (size_t)p->hp.stages * p->hp.stage_bytes) return false;
-  p->total = 256 + align_up(G * (2 + k_t) * sizeof(unsigned long long), 256);
+  if (G * (2 + k_t) * sizeof(unsigned long long) > kWsGstepRec - kWsCstepRec) return false;  // the record region
+  p->total = kWsFixed;
   return true;
 }
 
@@ -819,7 +786,7 @@ cudaError_t launch_cstep(const ds_clusters* c, const ds_router* r, const void* h
   s.extra_bytes = p.extra;
   s.xs_slot = p.xs_slot;
   s.head_only = 0;
-  s.crec = reinterpret_cast<unsigned long long*>(w8 + 256);
+  s.crec = reinterpret_cast<unsigned long long*>(w8 + kWsCstepRec);
   s.ctr = reinterpret_cast<unsigned*>(w8);
   s.trace = debug_trace();
   return c->dtype == DS_BF16 ? launch_cstep_t<__nv_bfloat16>(s, p.smem, p.Q, p.C, st, pdl)
@@ -843,11 +810,11 @@ size_t cstep_head_rec_bytes(const ds_clusters* c, int k_t) {
 cudaError_t launch_cstep_head(const ds_clusters* c, const void* h_new, const int32_t* sel, const int32_t* sel_count,
                               const int32_t* sl_offsets, int k_t, int64_t max_shortlist, int32_t* top_ids,
                               float* top_logits, float* top_logp, float* lse, float* z_out, int64_t z_stride,
-                              void* rec, cudaStream_t st) {
+                              void* ws, cudaStream_t st) {
   CStepPlan p;
   if (!cstep_plan(c, nullptr, 1, k_t, max_shortlist, 0, &p)) return cudaErrorInvalidValue;
   if ((reinterpret_cast<uintptr_t>(h_new) & 15u) != 0) return cudaErrorInvalidValue;
-  uint8_t* w8 = static_cast<uint8_t*>(rec);
+  uint8_t* w8 = static_cast<uint8_t*>(ws);
   CStepArgs s = {};
   fill_head_args(s.h, c, p.hp, h_new, 0, 1, sel, sel_count, sl_offsets, 0, k_t, max_shortlist, top_ids, top_logits,
                  top_logp, lse, z_out, z_stride, nullptr, reinterpret_cast<unsigned*>(w8), false);
@@ -855,7 +822,7 @@ cudaError_t launch_cstep_head(const ds_clusters* c, const void* h_new, const int
   s.extra_bytes = p.extra;
   s.xs_slot = p.xs_slot;
   s.head_only = 1;
-  s.crec = reinterpret_cast<unsigned long long*>(w8 + 256);
+  s.crec = reinterpret_cast<unsigned long long*>(w8 + kWsCstepRec);
   s.ctr = reinterpret_cast<unsigned*>(w8);
   s.trace = debug_trace();
   return c->dtype == DS_BF16 ? launch_cstep_t<__nv_bfloat16>(s, p.smem, p.Q, p.C, st, false)

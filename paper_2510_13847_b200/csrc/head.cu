@@ -48,6 +48,16 @@ int max_smem_optin() {
   return v;
 }
 
+cudaError_t configure_max_smem(const void* fn, int* done) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (done[dev]) return cudaSuccess;
+  const cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem_optin());
+  if (e == cudaSuccess) done[dev] = 1;
+  return e;
+}
+
 bool head_plan_ex(const ds_clusters* c, int B, int k_t, int64_t max_shortlist, int extra, int max_rows,
                   HeadPlan* p, int G) {
   const int esz = c->dtype == DS_BF16 ? 2 : 4;
@@ -128,12 +138,10 @@ void fill_head_args(HeadArgs& a, const ds_clusters* c, const HeadPlan& p, const 
 
 template <typename T>
 static cudaError_t launch_head_t(const HeadArgs& a, size_t smem, int G, cudaStream_t st, bool pdl) {
-  static bool configured = false;  // idempotent attribute set
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(head_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         max_smem_optin());
+  static int configured[64] = {0};  // the attribute is per device
+  {
+    cudaError_t e = configure_max_smem(reinterpret_cast<const void*>(head_kernel<T>), configured);
     if (e != cudaSuccess) return e;
-    configured = true;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(G);

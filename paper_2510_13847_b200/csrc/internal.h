@@ -11,6 +11,16 @@ constexpr int kMaxM = 1024;      // largest cluster count the select kernels sup
 constexpr int kMaxMHost = kMaxM;
 constexpr int kMaxKt = 64;       // largest token budget k_t
 
+// Workspace prefix shared by every entry point (fixed offsets, so one workspace can serve any mix
+// of calls): [0, 256) counters (left at zero by every kernel) with the device error word at 252;
+// the polled-record regions of the single-row step kernels (0 = "not written yet", re-zeroed by
+// their mergers, written by no other kernel); per-call scratch from kWsFixed on.
+constexpr size_t kWsErrorWord = 252;
+constexpr size_t kWsCstepRec = 256;                      // cluster step: [G][2 + k_t] u64 (<= 48 KB)
+constexpr size_t kWsGstepRec = kWsCstepRec + 48 * 1024;  // grid step:    [G][2 + k_t] u64 (<= 48 KB)
+constexpr size_t kWsGstepUnits = kWsGstepRec + 48 * 1024;  // grid step: [rows1] u64 layer-1 units (<= 4 KB)
+constexpr size_t kWsFixed = 112 * 1024;
+
 int num_sms();
 unsigned long long* debug_trace();   // device buffer set by dynaspec_debug_set_trace, or nullptr                 // SM count of the current device (cached per device)
 size_t align_up(size_t x, size_t a);
@@ -51,6 +61,8 @@ bool head_plan(const ds_clusters* c, int B, int k_t, int64_t max_shortlist, Head
 bool head_plan_ex(const ds_clusters* c, int B, int k_t, int64_t max_shortlist, int extra_smem, int max_rows,
                   HeadPlan* p, int G = 0 /* CTAs per launch; 0 = one per SM */);
 int max_smem_optin();
+// cudaFuncAttributeMaxDynamicSharedMemorySize = max_smem_optin() for `fn`, once per device (done: [64]).
+cudaError_t configure_max_smem(const void* fn, int* done);
 cudaError_t launch_head(const ds_clusters* c, const HeadPlan& p, const void* h_new, int B, const int32_t* sel,
                         const int32_t* sel_count, const int32_t* sl_offsets, int shared, int k_t,
                         int64_t max_shortlist, int32_t* top_ids, float* top_logits, float* top_logp,
@@ -82,6 +94,18 @@ cudaError_t launch_cstep_head(const ds_clusters* c, const void* h_new, const int
                               const int32_t* sl_offsets, int k_t, int64_t max_shortlist, int32_t* top_ids,
                               float* top_logits, float* top_logp, float* lse, float* z_out, int64_t z_stride,
                               void* rec, cudaStream_t st);
+
+// ---- grid draft step (gstep.cu): B = 1, router units spread over every CTA, no clusters, no counters
+bool gstep_supported(const ds_clusters* c, const ds_router* r /* nullptr: head only */, int B, int k_t, int shared);
+bool gstep_pointers_ok(const ds_router* r, const void* h_prev, const void* e, const void* h_new);
+cudaError_t launch_gstep(const ds_clusters* c, const ds_router* r, const void* h_prev, const void* e,
+                         const void* h_new, int k, int k_t, int64_t max_shortlist, float* scores, int32_t* sel,
+                         int32_t* sel_count, int32_t* sl_offsets, int32_t* top_ids, float* top_logits,
+                         float* top_logp, float* lse, float* z_out, void* ws, cudaStream_t st, bool pdl);
+cudaError_t launch_gstep_head(const ds_clusters* c, const void* h_new, const int32_t* sel, const int32_t* sel_count,
+                              const int32_t* sl_offsets, int k_t, int64_t max_shortlist, int32_t* top_ids,
+                              float* top_logits, float* top_logp, float* lse, float* z_out, void* ws,
+                              cudaStream_t st);
 
 // ---- tcgen05 shared-shortlist head (tc_head.cu), bf16, R <= 64 rows sharing one shortlist
 bool tc_head_supported(const ds_clusters* c, int R, int k_t, int64_t max_shortlist);

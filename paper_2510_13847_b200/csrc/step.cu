@@ -295,7 +295,7 @@ static bool step_plan(const ds_clusters* c, const ds_router* r, int B, int k_t, 
   p->scores_bytes = align_up((size_t)B * r->M * sizeof(float), 256);
   p->mask_bytes = align_up((size_t)B * 32 * sizeof(uint32_t), 256);
   p->head_bytes = align_up(p->hp.part_bytes, 256);
-  p->total = 256 + p->mpart_bytes + p->scores_bytes + p->mask_bytes + p->head_bytes;
+  p->total = kWsFixed + p->mpart_bytes + p->scores_bytes + p->mask_bytes + p->head_bytes;
   const size_t w2 = r->h_r > 0 ? (size_t)r->M * r->h_r * esz : 0;
   p->w2_bytes = (w2 > 0 && w2 % 16 == 0 && w2 <= (size_t)p->hp.stages * p->hp.stage_bytes) ? (int)w2 : 0;
   return true;
@@ -315,19 +315,15 @@ static size_t grid_step_ws(const ds_clusters* c, const ds_router* r, int B, int 
 }
 
 size_t step_ws_bytes(const ds_clusters* c, const ds_router* r, int B, int k_t) {
-  const size_t g = grid_step_ws(c, r, B, k_t);
-  if (g == 0) return 0;
-  return g + cstep_ws_bytes(c, r, B, k_t);
+  return grid_step_ws(c, r, B, k_t);  // the single-row step kernels use the fixed prefix (internal.h)
 }
 
 template <typename T>
 static cudaError_t launch_step_t(const StepArgs& s, size_t smem, int G, cudaStream_t st, bool pdl) {
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e =
-        cudaFuncSetAttribute(step_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem_optin());
+  static int configured[64] = {0};  // the attribute is per device
+  {
+    cudaError_t e = configure_max_smem(reinterpret_cast<const void*>(step_kernel<T>), configured);
     if (e != cudaSuccess) return e;
-    configured = true;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(G);
@@ -347,19 +343,22 @@ cudaError_t launch_step(const ds_clusters* c, const ds_router* r, const void* h_
                         int32_t* sel, int32_t* sel_count, int32_t* sl_offsets, int32_t* top_ids, float* top_logits,
                         float* top_logp, float* lse, float* z_out, int64_t z_stride, void* ws, cudaStream_t st,
                         bool pdl) {
-  // B = 1: the cluster step (cstep.cu) needs no grid-wide barrier before the head streams
+  // B = 1: the grid step (gstep.cu: router units over every CTA, no clusters) or, for shapes it does
+  // not cover, the cluster step (cstep.cu); neither needs a grid-wide barrier before the head streams
+  if (gstep_supported(c, r, B, k_t, shared) && gstep_pointers_ok(r, h_prev, e, h_new))
+    return launch_gstep(c, r, h_prev, e, h_new, k, k_t, max_shortlist, scores, sel, sel_count, sl_offsets, top_ids,
+                        top_logits, top_logp, lse, z_out, ws, st, pdl);
   if (cstep_supported(c, r, B, k_t, shared, max_shortlist) && cstep_pointers_ok(r, h_prev, e, h_new))
     return launch_cstep(c, r, h_prev, e, h_new, k, k_t, max_shortlist, scores, sel, sel_count, sl_offsets, top_ids,
-                        top_logits, top_logp, lse, z_out, z_stride,
-                        static_cast<uint8_t*>(ws) + grid_step_ws(c, r, B, k_t), st, pdl);
+                        top_logits, top_logp, lse, z_out, z_stride, ws, st, pdl);
   StepPlan p;
   if (!step_plan(c, r, B, k_t, max_shortlist, shared, &p)) return cudaErrorInvalidValue;
   uint8_t* w8 = static_cast<uint8_t*>(ws);
   unsigned* ctr = reinterpret_cast<unsigned*>(w8);
-  float* mpart = reinterpret_cast<float*>(w8 + 256);
-  float* sc = scores ? scores : reinterpret_cast<float*>(w8 + 256 + p.mpart_bytes);
-  uint32_t* maskbuf = reinterpret_cast<uint32_t*>(w8 + 256 + p.mpart_bytes + p.scores_bytes);
-  float* hpart = reinterpret_cast<float*>(w8 + 256 + p.mpart_bytes + p.scores_bytes + p.mask_bytes);
+  float* mpart = reinterpret_cast<float*>(w8 + kWsFixed);
+  float* sc = scores ? scores : reinterpret_cast<float*>(w8 + kWsFixed + p.mpart_bytes);
+  uint32_t* maskbuf = reinterpret_cast<uint32_t*>(w8 + kWsFixed + p.mpart_bytes + p.scores_bytes);
+  float* hpart = reinterpret_cast<float*>(w8 + kWsFixed + p.mpart_bytes + p.scores_bytes + p.mask_bytes);
   StepArgs s;
   fill_head_args(s.h, c, p.hp, h_new, 0, B, sel, sel_count, sl_offsets, shared, k_t, max_shortlist, top_ids,
                  top_logits, top_logp, lse, z_out, z_stride, hpart, ctr, pdl);

@@ -606,11 +606,10 @@ static bool make_maps(TcMaps* m, const ds_clusters* c) {
 
 static cudaError_t launch_tc_kernel(const TcPlan& p, const TcMaps& mw, const CUtensorMap& mh, const TcArgs& t,
                                     cudaStream_t st, bool pdl) {
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(tc_head_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem_optin());
+  static int configured[64] = {0};  // the attribute is per device
+  {
+    cudaError_t e = configure_max_smem(reinterpret_cast<const void*>(tc_head_kernel), configured);
     if (e != cudaSuccess) return e;
-    configured = true;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(p.hp.G);

@@ -22,7 +22,7 @@ STATUS = {
     0: "DS_OK", 1: "DS_ERR_SHAPE", 2: "DS_ERR_DTYPE", 3: "DS_ERR_INVALID_BUDGET",
     4: "DS_ERR_INVALID_CLUSTER_COUNT", 5: "DS_ERR_INVALID_CLUSTER_ID", 6: "DS_ERR_INVALID_TOKEN",
     7: "DS_ERR_DEGENERATE_COLUMN", 8: "DS_ERR_EMPTY_SHORTLIST", 9: "DS_ERR_WORKSPACE", 10: "DS_ERR_CUDA",
-    11: "DS_ERR_UNSUPPORTED",
+    11: "DS_ERR_UNSUPPORTED", 12: "DS_ERR_DEVICE_TIMEOUT",
 }
 
 
@@ -61,6 +61,7 @@ def _load():
         "dynaspec_budget": (c_int32, [c_int32, c_int32, c_int32]),
         "dynaspec_max_shortlist": (c_int64, [POINTER(DsClusters), c_int32]),
         "dynaspec_ws_init": (c_int32, [P, c_size_t, P]),
+        "dynaspec_ws_error": (c_int32, [P, c_size_t, P, P]),
         "dynaspec_build_clusters_ws": (c_size_t, [c_int64, c_int32, c_int32]),
         "dynaspec_build_clusters": (c_int32, [P, c_int32, c_int64, c_int32, c_int32, c_uint64, c_int32, P, P, P, P,
                                               P, P, P, P, c_size_t, P]),
@@ -104,7 +105,7 @@ def _load():
 _lib = _load()
 
 EXPORTED = [
-    "dynaspec_status_string", "dynaspec_budget", "dynaspec_max_shortlist", "dynaspec_ws_init",
+    "dynaspec_status_string", "dynaspec_budget", "dynaspec_max_shortlist", "dynaspec_ws_init", "dynaspec_ws_error",
     "dynaspec_build_clusters_ws", "dynaspec_build_clusters", "dynaspec_layout_ws", "dynaspec_layout",
     "dynaspec_meta_score_ws", "dynaspec_meta_score", "dynaspec_select", "dynaspec_head_forward_ws",
     "dynaspec_head_forward", "dynaspec_draft_step_ws", "dynaspec_draft_step", "dynaspec_draft_step_launches",
@@ -163,6 +164,14 @@ class Workspace:
 
     def ptr(self):
         return _ptr(self.buf)
+
+    def error(self, stream=None):
+        """Read and clear the device error word (dynaspec_ws_error; synchronises the stream).
+        Returns the status name, "DS_OK" if no kernel raised one."""
+        code = c_int32(0)
+        _check(_lib.dynaspec_ws_error(self.ptr(), self.nbytes, ctypes.cast(ctypes.pointer(code), c_void_p),
+                                      _stream(stream)), "dynaspec_ws_error")
+        return STATUS.get(code.value, str(code.value))
 
     def ensure(self, nbytes):
         if nbytes > self.nbytes:

@@ -15,6 +15,14 @@ from synth import inputs as S
 from tests.parity import Rows, check_topk, f64, selection_certified
 
 pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(autouse=True)
+def _cluster_step_only(monkeypatch):
+    """These tests exercise cstep.cu: keep the grid step (gstep.cu) out of the dispatch."""
+    monkeypatch.setenv("DS_GSTEP", "0")
+
+
 DEV = "cuda"
 
 
