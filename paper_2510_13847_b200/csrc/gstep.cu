@@ -53,12 +53,13 @@ constexpr int kGRows2 = 16;              // layer-2 rows per warp (M <= 256), 2 
                                          //   h_r <= 128 (bf16) / 64 (fp32)
 constexpr int kGMaxM = kGWarps * kGRows2;
 constexpr int kGHeadsPerLane = 5;       // merger: record headers per polling lane (G <= 160)
-constexpr int kGKeyWarps = 8;            // TopK: warps holding <= 32 scores each (M <= 256)
+constexpr int kGKeyWarps = 8;
+constexpr int kGTailPerCta = 2;          // run-time-claimed tail chunks per streaming CTA            // TopK: warps holding <= 32 scores each (M <= 256)
 constexpr int kGMaxKt = 32;              // one list entry per lane
 constexpr unsigned long long kSpinNs = 2000000000ull;
 
 struct GSmem {
-  uint32_t ring, bars, info, hs, a1, sc, b2s, offs, mask, thr, wc, surv, wl, wm, wsum, wn, misc, red, total;
+  uint32_t ring, bars, info, hs, a1, sc, b2s, offs, cch, ctab, mask, thr, wc, surv, wl, wm, wsum, wn, misc, red, total;
 };
 
 __host__ __device__ inline GSmem gstep_smem(int S, int stage_bytes, int d, int esz, int M, int rows1, int K) {
@@ -78,6 +79,8 @@ __host__ __device__ inline GSmem gstep_smem(int S, int stage_bytes, int d, int e
   L.sc = take(4u * M, 16);
   L.b2s = take(4u * M, 16);
   L.offs = take(4u * (M + 1), 16);
+  L.cch = take(4u * M, 16);
+  L.ctab = take(16u * M, 16);
   L.mask = take(4u * (kGMaxM / 32), 16);
   L.thr = take(8u * kGWarps, 8);  // per-warp thresholds, then survivor bits
   L.wc = take(4u * kGWarps, 4);
@@ -123,6 +126,7 @@ struct GStepArgs {
   unsigned long long* aslot;  // [rows1] published layer-1 units (0 = not yet)
   unsigned long long* rec;    // [G][2 + k_t] per-CTA records (0 = not yet)
   unsigned* err;              // workspace error word (DS_ERR_DEVICE_TIMEOUT)
+  unsigned* claim;            // tail-chunk claim counter (0 between launches; the merger resets it)
   unsigned long long* trace;
   GSmem L;                    // shared-memory carve-up (host-computed)
 };
@@ -131,19 +135,47 @@ struct GStepArgs {
 // t0: the spin's start; on timeout the workspace error word is raised, *dead is set (later polls
 // return at once) and 0 is returned.
 __device__ __noinline__ unsigned long long poll_slow(const unsigned long long* p, unsigned long long t0, unsigned* err,
-                                                     volatile int* dead) {
-  // back off between probes: every CTA polls the same few lines, and a tight spin would queue the
-  // publishers' stores behind the polling loads in those L2 slices
+                                                     volatile int* dead, unsigned sleep_ns) {
+  // sleep_ns > 0 backs off between probes: when every CTA polls the same few lines, a tight spin
+  // would queue the publishers' stores behind the polling loads in those L2 slices.  A single
+  // polling warp (the merger) spins.
   for (unsigned n = 1;; ++n) {
     const unsigned long long v = ld_relaxed_u64(p);
     if (v != 0ull) return v;
-    __nanosleep(64);
+    if (sleep_ns) __nanosleep(sleep_ns);
     if ((n & 63u) == 0u) {
       if (*dead) return 0ull;
       if (globaltimer_ns() - t0 > kSpinNs) {
         atomicExch(err, (unsigned)DS_ERR_DEVICE_TIMEOUT);
         *dead = 1;
         return 0ull;
+      }
+    }
+  }
+}
+
+// Poll N words per lane until all are non-zero, every round issuing the loads of all pending words
+// at once (one round trip per round, not per word).  v[i] holds the first probe's value (1 = no word).
+template <int N>
+__device__ __forceinline__ void poll_words(const unsigned long long* const (&p)[N], unsigned long long (&v)[N],
+                                           unsigned long long t0, unsigned* err, volatile int* dead, unsigned sleep_ns) {
+  uint32_t pend = 0;
+#pragma unroll
+  for (int i = 0; i < N; ++i) pend |= (v[i] == 0ull ? 1u : 0u) << i;
+  for (unsigned n = 1; pend; ++n) {
+    if (sleep_ns) __nanosleep(sleep_ns);
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+      if ((pend >> i) & 1u) v[i] = ld_relaxed_u64(p[i]);
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+      if (v[i] != 0ull) pend &= ~(1u << i);
+    if ((n & 63u) == 0u && pend) {
+      if (*dead) return;
+      if (globaltimer_ns() - t0 > kSpinNs) {
+        atomicExch(err, (unsigned)DS_ERR_DEVICE_TIMEOUT);
+        *dead = 1;
+        return;
       }
     }
   }
@@ -344,42 +376,65 @@ __device__ DS_GSTEP_NOINLINE void topk_mask(const float* sc, int M, int k, int k
 }
 
 // ---------------------------------------------------------------- gathered head
-// Producer lane: chunk c of the virtual shortlist (<= R whole rows inside one cluster) -> CTA c mod G.
-// info = (-, virtual shortlist position, rows, first W_perm row).
+// Producer lane.  Chunk c of the virtual shortlist = <= R whole W_perm rows inside one cluster, in
+// shortlist order (selected clusters ascending, R8).  The first Ns chunks are static: chunk c goes to
+// streaming CTA c mod Gs (the whole grid sweeps one window of the shortlist at a time).  The last D
+// (~2 per CTA) are claimed at run time, one atomicAdd each, so the SMs that stream faster take more
+// of the tail (per-SM HBM throughput varies by ~20%; a static split made the last CTA finish ~2 us
+// after the median at k = 8).  Claims are issued while >= 10 slots are still in flight, so their
+// round trip is hidden.  info = (-, virtual shortlist position, rows, first W_perm row).
 template <typename T>
 __device__ __noinline__ void gstep_produce(const GStepArgs& a, uint8_t* ring, uint64_t* full, uint64_t* empty,
-                                           int4* info, const uint32_t* mask, const int32_t* offs, bool stream) {
-  // the merger CTA (the last) streams nothing: chunk c -> CTA c mod (G - 1)
-  const int g = blockIdx.x, G = gridDim.x - 1;
-  if (g >= G) stream = false;
+                                           int4* info, const uint32_t* mask, const int32_t* offs, const int32_t* cch,
+                                           int nchunks, bool stream, int4* ctab) {
+  const int g = blockIdx.x, Gs = gridDim.x - 1;  // the merger CTA (the last) streams nothing
+  if (g >= Gs) stream = false;
   const uint64_t pol = policy_evict_first();
   const uint32_t rowbytes = (uint32_t)a.d * (uint32_t)sizeof(T);
   const uint8_t* W = static_cast<const uint8_t*>(a.W);
   const uint32_t S = (uint32_t)a.stages;
   const int R = a.stage_rows;
   uint32_t sl = 0, ph = 0;  // ring slot and phase (no divisions)
+  auto issue = [&](int vp, int n, int row) {
+    mbar_wait(&empty[sl], ph ^ 1u);
+    info[sl] = make_int4(0, vp, n, row);
+    mbar_arrive_expect_tx(&full[sl], (uint32_t)n * rowbytes);
+    bulk_g2s(ring + (size_t)sl * a.stage_bytes, W + (size_t)row * rowbytes, (uint32_t)n * rowbytes, &full[sl], pol);
+    if (++sl == S) {
+      sl = 0;
+      ph ^= 1u;
+    }
+  };
+  const long long N = nchunks;
+  const long long D = stream ? min(N / 4, (long long)Gs * kGTailPerCta) : 0;
+  const long long Ns = N - D;
+  int nsel = 0;
   long long vpos = 0, cb = 0, cn = g;
   const int words = (a.M + 31) >> 5;
   for (int w = 0; stream && w < words; ++w) {
     for (uint32_t bits = mask[w]; bits; bits &= bits - 1u) {
       const int m = (w << 5) + __ffs(bits) - 1;
       const int beg = offs[m], sz = offs[m + 1] - beg;
-      const long long nch = (sz + R - 1) / R;
-      for (; cn < cb + nch; cn += G) {
+      const int nch = cch[m];
+      ctab[nsel++] = make_int4((int)cb, (int)vpos, beg, sz);
+      for (; cn < cb + nch && cn < Ns; cn += Gs) {
         const int j0 = (int)(cn - cb) * R;
-        const int n = min(R, sz - j0);
-        mbar_wait(&empty[sl], ph ^ 1u);
-        info[sl] = make_int4(0, (int)(vpos + j0), n, beg + j0);
-        mbar_arrive_expect_tx(&full[sl], (uint32_t)n * rowbytes);
-        bulk_g2s(ring + (size_t)sl * a.stage_bytes, W + (size_t)(beg + j0) * rowbytes, (uint32_t)n * rowbytes,
-                 &full[sl], pol);
-        if (++sl == S) {
-          sl = 0;
-          ph ^= 1u;
-        }
+        issue((int)vpos + j0, min(R, sz - j0), beg + j0);
       }
       cb += nch;
       vpos += sz;
+    }
+  }
+  if (D > 0) {
+    unsigned* claim = a.claim;
+    int ci = 0;  // claims only increase: a forward cursor over the cluster table
+    for (;;) {
+      const long long c = Ns + (long long)atomicAdd(claim, 1u);
+      if (c >= N) break;
+      while (ci + 1 < nsel && ctab[ci + 1].x <= c) ++ci;
+      const int4 t = ctab[ci];
+      const int j0 = (int)(c - t.x) * R;
+      issue(t.y + j0, min(R, t.w - j0), t.z + j0);
     }
   }
 #pragma unroll 1
@@ -514,16 +569,16 @@ __device__ DS_GSTEP_NOINLINE void gstep_merge(const GStepArgs& a, uint8_t* ring,
   int* wq = reinterpret_cast<int*>(wps + kGWarps);                      // [16] keys each threshold bounds
   int* ncand = wq + kGWarps;
   const int nrec = G * rec;
-  if (warp == 0) {  // first word of every record (written with its keys): one warp, backoff
+  if (warp == 0) {  // first word of every record (written with its keys): one warp, all probes in flight
     unsigned long long v[kGHeadsPerLane];
+    const unsigned long long* pw[kGHeadsPerLane];
 #pragma unroll
     for (int i = 0; i < kGHeadsPerLane; ++i) {
       const int r = lane + 32 * i;
-      v[i] = r < G ? ld_relaxed_u64(a.rec + (size_t)r * rec) : 1ull;
+      pw[i] = a.rec + (size_t)(r < G ? r : 0) * rec;
+      v[i] = r < G ? ld_relaxed_u64(pw[i]) : 1ull;
     }
-#pragma unroll
-    for (int i = 0; i < kGHeadsPerLane; ++i)
-      if (v[i] == 0ull) poll_slow(a.rec + (size_t)(lane + 32 * i) * rec, t_spin, a.err, dead);
+    poll_words<kGHeadsPerLane>(pw, v, t_spin, a.err, dead, 0);
   }
   __syncthreads();
   {  // all loads in flight first, then spin only on the words that had not landed
@@ -540,7 +595,7 @@ __device__ DS_GSTEP_NOINLINE void gstep_merge(const GStepArgs& a, uint8_t* ring,
     trace_mark(a.trace, 15);
 #pragma unroll 1
     for (int i = tid; i < nrec; i += kGThreads)
-      if (raw[i] == 0ull) raw[i] = poll_slow(a.rec + i, t_spin, a.err, dead);
+      if (raw[i] == 0ull) raw[i] = poll_slow(a.rec + i, t_spin, a.err, dead, 0);
   }
   if (tid == 0) *ncand = 0;
   __syncthreads();
@@ -616,6 +671,7 @@ __device__ DS_GSTEP_NOINLINE void gstep_merge(const GStepArgs& a, uint8_t* ring,
 #pragma unroll 4
   for (int i = tid; i < nrec; i += kGThreads) a.rec[i] = 0ull;
   if (!a.head_only && tid < a.rows1) a.aslot[tid] = 0ull;  // rows1 <= blockDim
+  if (tid == 0) *a.claim = 0u;  // every producer has claimed past the end (its record exists)
 }
 
 template <typename T>
@@ -636,6 +692,7 @@ __global__ void __launch_bounds__(kGThreads, 1) gstep_kernel(const __grid_consta
   float* sc = reinterpret_cast<float*>(smem + L.sc);
   float* b2s = reinterpret_cast<float*>(smem + L.b2s);
   int32_t* offs = reinterpret_cast<int32_t*>(smem + L.offs);
+  int32_t* cch = reinterpret_cast<int32_t*>(smem + L.cch);  // chunks per cluster
   uint32_t* mask = reinterpret_cast<uint32_t*>(smem + L.mask);
   unsigned long long* wl = reinterpret_cast<unsigned long long*>(smem + L.wl);
   float* wm = reinterpret_cast<float*>(smem + L.wm);
@@ -689,7 +746,8 @@ __global__ void __launch_bounds__(kGThreads, 1) gstep_kernel(const __grid_consta
     }
   }
   if (tid <= M) offs[tid] = __ldg(a.offsets + tid);
-  __syncthreads();  // barrier inits, mask / misc zeroed, offsets staged
+  if (tid < M) cch[tid] = (__ldg(a.offsets + tid + 1) - __ldg(a.offsets + tid) + a.stage_rows - 1) / a.stage_rows;
+  __syncthreads();  // barrier inits, mask / misc zeroed, offsets and chunk counts staged
 
   if (a.pdl) pdl_wait();
   trace_mark(a.trace, 1);
@@ -736,18 +794,18 @@ __global__ void __launch_bounds__(kGThreads, 1) gstep_kernel(const __grid_consta
 #pragma unroll 1
       for (int u0 = 0; u0 < a.rows1; u0 += 128) {
         unsigned long long v[4];
+        const unsigned long long* pw[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           const int u = u0 + lane + 32 * i;
-          v[i] = u < a.rows1 ? ld_relaxed_u64(a.aslot + u) : 1ull;
+          pw[i] = a.aslot + (u < a.rows1 ? u : 0);
+          v[i] = u < a.rows1 ? ld_relaxed_u64(pw[i]) : 1ull;
         }
+        poll_words<4>(pw, v, t_spin, a.err, dead, 32);
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           const int u = u0 + lane + 32 * i;
-          if (u < a.rows1) {
-            if (v[i] == 0ull) v[i] = poll_slow(a.aslot + u, t_spin, a.err, dead);
-            a1[u] = __uint_as_float((uint32_t)v[i]);
-          }
+          if (u < a.rows1) a1[u] = __uint_as_float((uint32_t)v[i]);
         }
       }
     }
@@ -785,7 +843,16 @@ __global__ void __launch_bounds__(kGThreads, 1) gstep_kernel(const __grid_consta
 
   // ---- gathered head + per-warp epilogue state
   if (warp == kGProducer) {
-    if (lane == 0) gstep_produce<T>(a, ring, full, empty, info, mask, offs, stream);
+    int nl = 0;  // total chunks of the shortlist: the producer warp sums the selected clusters' counts
+#pragma unroll 1
+    for (int w = 0; w < ((M + 31) >> 5); ++w) {
+      const int m = (w << 5) + lane;
+      if (m < M && ((mask[w] >> lane) & 1u)) nl += cch[m];
+    }
+    const int nchunks = (int)__reduce_add_sync(0xffffffffu, (unsigned)nl);
+    if (lane == 0)
+      gstep_produce<T>(a, ring, full, empty, info, mask, offs, cch, nchunks, stream,
+                       reinterpret_cast<int4*>(smem + L.ctab));
   } else if (warp < S) {
     float m, se;
     unsigned long long mine;
@@ -837,7 +904,9 @@ static bool gstep_plan(const ds_clusters* c, const ds_router* r, int k_t, GStepP
     if ((size_t)2 * c->d * esz > (size_t)kGXChunks * kGThreads * 16) return false;
   }
   const int rowb = c->d * esz;
-  p->stage_rows = std::max(1, kStageTarget / rowb);
+  const char* skb = getenv("DS_GSTEP_STAGE_KB");  // ring slot size (tuning knob; default 16 KB)
+  const int target = skb && skb[0] ? std::max(4, std::min(64, atoi(skb))) * 1024 : kStageTarget;
+  p->stage_rows = std::max(1, target / rowb);
   p->stage_bytes = p->stage_rows * rowb;
   const int smax = max_smem_optin();
   const size_t fixed = gstep_smem(0, p->stage_bytes, c->d, esz, c->M, std::max(p->rows1, 1), k_t).total + 1024;
@@ -912,6 +981,7 @@ static void fill_common(GStepArgs& a, const ds_clusters* c, const GStepPlan& p, 
   a.rec = reinterpret_cast<unsigned long long*>(w8 + kWsGstepRec);
   a.aslot = reinterpret_cast<unsigned long long*>(w8 + kWsGstepUnits);
   a.err = reinterpret_cast<unsigned*>(w8 + kWsErrorWord);
+  a.claim = reinterpret_cast<unsigned*>(w8 + kWsGstepClaim);
   a.trace = debug_trace();
   a.L = gstep_smem(p.S, p.stage_bytes, c->d, c->dtype == DS_BF16 ? 2 : 4, c->M, std::max(p.rows1, 1), k_t);
   a.kpw = (c->M + kGKeyWarps - 1) / kGKeyWarps;

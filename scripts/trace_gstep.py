@@ -61,6 +61,20 @@ for rep in range(5):
     tot.append(e0.elapsed_time(e1) * 1e3 / C.positions)
 print(f"{cfg}: us per step (events, traced) {np.round(tot, 2)}")
 t_prev_end = None
+ends = []
+for t in range(C.positions):
+    a = bufs[t].view(G, 64).cpu().numpy().astype(np.float64)[:, :32]
+    p1 = a[:, 1][a[:, 1] > 0]
+    mg = int(np.argmax(a[:, 9]))
+    ends.append((p1.min(), p1.max(), a[:, 9].max(), a[:, 5][a[:, 5] > 0].min(), a[:, 6].max(), a[:, 7].max(),
+                 a[mg, 15], a[mg, 8], a[mg, 10], a[mg, 11]))
+print("per step (us): pdl release (first..last CTA) -> mask | -> streamed (last) | -> last record | -> outputs | -> next pdl")
+for t in range(C.positions):
+    p0, p1, out, mk, sd, rc, mi, mr, mf, mc = ends[t]
+    nxt = ends[t + 1][0] if t + 1 < C.positions else float("nan")
+    print(f"  t={t}: pdl spread {1e-3 * (p1 - p0):.2f} | mask {1e-3 * (mk - p0):.2f} | streamed {1e-3 * (sd - p0):.2f} | "
+          f"record {1e-3 * (rc - p0):.2f} | merger: headers+issued {1e-3 * (mi - p0):.2f} staged {1e-3 * (mr - p0):.2f} "
+          f"fields {1e-3 * (mf - p0):.2f} cands {1e-3 * (mc - p0):.2f} | out {1e-3 * (out - p0):.2f} | next pdl {1e-3 * (nxt - p0):.2f}")
 for t in range(C.positions):
     a = bufs[t].view(G, 64).cpu().numpy().astype(np.float64)[:, :32]
     t0 = a[:, 0][a[:, 0] > 0].min()
