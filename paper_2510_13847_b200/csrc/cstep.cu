@@ -272,10 +272,13 @@ __global__ void __launch_bounds__((kMaxStages + 1) * 32, 1) cstep_kernel(const C
       mbar_arrive_expect_tx(xbar, hb);
       bulk_g2s(c.hs, a.h, hb, xbar, policy_evict_first());
     }
+    // a row whose |V_S| exceeds max_shortlist is not computed (dynaspec.h): an empty mask streams
+    // nothing, so the merger emits ids -1 and lse NaN
     const int cnt = __ldg(a.sel_count);
-    for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
+    const bool fits = cnt >= 1 && cnt <= M && (long long)__ldg(a.sl_off + cnt) <= a.max_shortlist;
+    for (int i = threadIdx.x; fits && i < cnt; i += blockDim.x) {
       const int m = __ldg(a.sel + i);
-      atomicOr(&mask[m >> 5], 1u << (m & 31));
+      if (m >= 0 && m < M) atomicOr(&mask[m >> 5], 1u << (m & 31));
     }
     for (int m = threadIdx.x; m <= M; m += blockDim.x) offs[m] = __ldg(a.offsets + m);
     cluster_wait_acquire();  // pairs the launch-time arrive (a one-CTA cluster: no peer)

@@ -120,6 +120,7 @@ struct GStepArgs {
   float* z_out;             // nullable: z over V_S in shortlist order
   int64_t max_shortlist;
   int32_t M, d, h_r, rows1, k, k_t, stages, stage_rows, stage_bytes, head_only, pdl;
+  int32_t tail;                 // 1: run-time-claimed tail chunks (DS_GSTEP_TAIL=1)
   int32_t kpw, q_sel, q_merge;  // TopK launch constants: keys per warp, per-warp / record-warp ranks
   int32_t lgK;                  // ceil(log2(k_t + 1)): binary-search steps over a k_t-entry list
   uint32_t kdiv;                // ceil(2^32 / k_t): tid / k_t as one multiply-high
@@ -378,10 +379,9 @@ __device__ DS_GSTEP_NOINLINE void topk_mask(const float* sc, int M, int k, int k
 // ---------------------------------------------------------------- gathered head
 // Producer lane.  Chunk c of the virtual shortlist = <= R whole W_perm rows inside one cluster, in
 // shortlist order (selected clusters ascending, R8).  The first Ns chunks are static: chunk c goes to
-// streaming CTA c mod Gs (the whole grid sweeps one window of the shortlist at a time).  The last D
-// (~2 per CTA) are claimed at run time, one atomicAdd each, so the SMs that stream faster take more
-// of the tail (per-SM HBM throughput varies by ~20%; a static split made the last CTA finish ~2 us
-// after the median at k = 8).  Claims are issued while >= 10 slots are still in flight, so their
+// streaming CTA c mod Gs (the whole grid sweeps one window of the shortlist at a time).  With
+// a.tail, the last D (~2 per CTA) are claimed at run time, one atomicAdd each, so the SMs that
+// stream faster take more of the tail; claims are issued while the ring is still full, so their
 // round trip is hidden.  info = (-, virtual shortlist position, rows, first W_perm row).
 template <typename T>
 __device__ __noinline__ void gstep_produce(const GStepArgs& a, uint8_t* ring, uint64_t* full, uint64_t* empty,
@@ -406,7 +406,9 @@ __device__ __noinline__ void gstep_produce(const GStepArgs& a, uint8_t* ring, ui
     }
   };
   const long long N = nchunks;
-  const long long D = stream ? min(N / 4, (long long)Gs * kGTailPerCta) : 0;
+  // Off by default: which CTA sums a tail chunk then depends on timing, so the fp32 lse partials are
+  // grouped differently from run to run (R19 asks for identical bytes); ids and logits are unaffected.
+  const long long D = (stream && a.tail) ? min(N / 4, (long long)Gs * kGTailPerCta) : 0;
   const long long Ns = N - D;
   int nsel = 0;
   long long vpos = 0, cb = 0, cn = g;
@@ -982,6 +984,8 @@ static void fill_common(GStepArgs& a, const ds_clusters* c, const GStepPlan& p, 
   a.aslot = reinterpret_cast<unsigned long long*>(w8 + kWsGstepUnits);
   a.err = reinterpret_cast<unsigned*>(w8 + kWsErrorWord);
   a.claim = reinterpret_cast<unsigned*>(w8 + kWsGstepClaim);
+  const char* tl = getenv("DS_GSTEP_TAIL");
+  a.tail = tl && tl[0] == '1' ? 1 : 0;
   a.trace = debug_trace();
   a.L = gstep_smem(p.S, p.stage_bytes, c->d, c->dtype == DS_BF16 ? 2 : 4, c->M, std::max(p.rows1, 1), k_t);
   a.kpw = (c->M + kGKeyWarps - 1) / kGKeyWarps;

@@ -83,6 +83,17 @@ def test_forgy_distinct():
         assert len(set(ids.tolist())) == M and ids.min() >= 0 and ids.max() < V
 
 
+def test_forgy_hand_draw():
+    """R12 step 2 by hand from the published splitmix64 reference vector (seed 0):
+    r0 = 16294208416658607535 (0xE220A8397B1DCDAF): r0 mod 10 = 5 (last digit) -> swap a[0], a[5];
+    r1 = 7960286522194355700: digit sum 90, so r1 mod 9 = 0 -> j = 1, no swap;
+    r2 = 487617019471545679: 679 mod 8 = 7 -> j = 2 + 7 = 9 -> swap a[2], a[9].
+    a = [0..9] becomes [5, 1, 9, ...]: the first M = 3 entries are the Forgy ids."""
+    assert O.forgy_init(10, 3, 0).tolist() == [5, 1, 9]
+    assert O.forgy_init(10, 1, 0).tolist() == [5]
+    assert O.forgy_init(10, 2, 0).tolist() == [5, 1]
+
+
 def _W_e2e():
     return np.array(GOLD["W_rows"], dtype=np.float64)
 
@@ -320,6 +331,34 @@ def test_k_equals_M_is_dense():
         assert abs(o["lse"] - dn["lse"]) < 1e-12
         z_at = dn["z"][o["V_S"]]
         assert np.allclose(o["z"], z_at, atol=1e-12)
+
+
+def test_shared_mode_hand_example():
+    """R9 (one index set I for all rows of a depth) by hand.  M = 5 clusters of one
+    token each (tau = id), k = 2:
+      row 0 scores [5, 4, 1, 0, 0] -> TopK {0, 1};  row 1 [0, 1, 9, 8, 0] -> {2, 3};
+      row 2 [3, 3, 3, 0, 0] -> ties, lower id first (R7) -> {0, 1}.
+    Shared selection = ascending union [0, 1, 2, 3]; every row's logits, lse and top ids range over
+    tokens 0..3 (not over its own clusters only): W rows e_0..e_4 of R^5 give z_r = h_r[0..3]."""
+    s = np.array([[5, 4, 1, 0, 0], [0, 1, 9, 8, 0], [3, 3, 3, 0, 0]], dtype=np.float64)
+    assert O.select_shared(s, 2).tolist() == [0, 1, 2, 3]
+    assert O.select(s[2], 2).tolist() == [0, 1]
+    part = {"perm": np.arange(5), "offsets": np.arange(6)}
+    W = np.eye(5)
+    # a linear router that reproduces the scores: s = W1 [h_prev || e] + b1 with W1 = 0, b1 per row is
+    # not expressible (b1 is shared), so feed the rows through h_prev with W1 = [I | 0]
+    W1 = np.hstack([np.eye(5), np.zeros((5, 5))])
+    router = (W1, np.zeros(5), None, None)
+    h_new = np.array([[1.0, 0, 0, 0, 7.0], [0, 2.0, 0, 0, 0], [0, 0, 0, 3.0, 0]])
+    out = O.draft_step(part, router, W, s, np.zeros_like(s), h_new, t=0, k_max=2, k_min=1, k_t=2, shared=True)
+    for r, o in enumerate(out):
+        assert o["V_S"].tolist() == [0, 1, 2, 3]
+        z = h_new[r, :4]
+        assert np.array_equal(o["z"], z)                      # token 4 (z = 7 in row 0) is not in I
+        assert abs(o["lse"] - math.log(np.exp(z).sum())) < 1e-12
+    assert out[0]["top_ids"].tolist() == [0, 1]               # z = [1, 0, 0, 0]: then id order
+    assert out[1]["top_ids"].tolist() == [1, 0]
+    assert out[2]["top_ids"].tolist() == [3, 0]
 
 
 def test_shared_mode_union():
