@@ -554,6 +554,97 @@ __device__ __noinline__ void gstep_emit_selection(const GStepArgs& a, const uint
   }
 }
 
+// Merge of the G staged records raw[G][2 + K] (every thread of the CTA): lse = M + log sum_g s_g
+// e^{m_g - M}, as per-warp partials relative to the warp's max (fixed xor trees) combined by one
+// fixed tree (R19); top-K: each record warp finds its min(q, n_w)-th best head (REDUX rounds) and
+// every key with a high word >= the smallest of those is a candidate (>= K keys are, and every key
+// above a candidate is one); candidates (prefixes of the sorted records) are compacted and
+// rank-counted.  Scratch after the records in raw.
+__device__ DS_GSTEP_NOINLINE void gstep_merge_compute(const GStepArgs& a, unsigned long long* raw, int G, bool ok_in) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int K = a.k_t, rec = 2 + K;
+  unsigned long long* cand = raw + (size_t)G * rec;                     // [G*K]
+  uint32_t* wthr = reinterpret_cast<uint32_t*>(cand + (size_t)G * K);  // [16] per-warp q-th heads
+  uint32_t* wmx = wthr + kGWarps;                                       // [16] per-warp max logit keys
+  float* wps = reinterpret_cast<float*>(wmx + kGWarps);                 // [16] per-warp lse partials
+  int* wq = reinterpret_cast<int*>(wps + kGWarps);                      // [16] keys each threshold bounds
+  int* ncand = wq + kGWarps;
+  // thread g: record g (G <= blockDim: one CTA per SM)
+  const bool has = tid < G;
+  const unsigned long long w0 = has ? raw[(size_t)tid * rec] : 0ull;
+  const float mg = has ? __uint_as_float((uint32_t)w0) : -INFINITY;
+  const float sg = __uint_as_float((uint32_t)(w0 >> 32));
+  const int cg = has ? (int)raw[(size_t)tid * rec + 1] - 1 : 0;
+  const unsigned long long hd = has ? raw[(size_t)tid * rec + 2] : 0ull;
+  const uint32_t hk = (cg > 0 && hd > 1ull) ? (uint32_t)(hd >> 32) : 0u;
+  {
+    const uint32_t mk = __reduce_max_sync(0xffffffffu, mg > -INFINITY ? ord_key(mg) : 0u);
+    const float Mw = mk ? __uint_as_float((mk & 0x80000000u) ? (mk & 0x7fffffffu) : ~mk) : -INFINITY;
+    const float part = warp_sum(mg > -INFINITY ? sg * expf(mg - Mw) : 0.f);
+    // this warp's min(q, n_w)-th best head (n_w: its non-empty records)
+    const int qq = min(a.q_merge, __popc(__ballot_sync(0xffffffffu, hk != 0u)));
+    uint32_t v = hk, tq = 0xffffffffu;
+    for (int it = 0; it < qq; ++it) {
+      tq = __reduce_max_sync(0xffffffffu, v);
+      const uint32_t b = __ballot_sync(0xffffffffu, v == tq);
+      if (lane == __ffs(b) - 1) v = 0u;
+    }
+    if (lane == 0) {
+      wmx[warp] = mk;
+      wps[warp] = part;
+      wthr[warp] = tq;
+      wq[warp] = qq;
+    }
+    if (tid == 0) *ncand = 0;
+  }
+  __syncthreads();
+  trace_mark(a.trace, 10);
+  const uint32_t wk = lane < kGWarps ? wmx[lane] : 0u;
+  const uint32_t Mk = __reduce_max_sync(0xffffffffu, wk);
+  const float Mx = Mk ? __uint_as_float((Mk & 0x80000000u) ? (Mk & 0x7fffffffu) : ~Mk) : -INFINITY;
+  // the warps' thresholds bound >= sum of their qq keys from below: valid if that is >= K
+  const unsigned nq = __reduce_add_sync(0xffffffffu, lane < kGWarps ? (unsigned)wq[lane] : 0u);
+  const uint32_t T = (int)nq >= K ? __reduce_min_sync(0xffffffffu, lane < kGWarps ? wthr[lane] : 0xffffffffu) : 0u;
+  if (has) {
+    int c = cg;  // record keys with a high word >= T: a prefix of the sorted record
+    if (T > 0u) {
+      c = 0;
+      while (c < cg && (uint32_t)(raw[(size_t)tid * rec + 2 + c] >> 32) >= T) ++c;
+    }
+    if (c > 0) {
+      const int base = atomicAdd(ncand, c);
+#pragma unroll 1
+      for (int j = 0; j < c; ++j) cand[base + j] = raw[(size_t)tid * rec + 2 + j];
+    }
+  }
+  // lse, meanwhile (every thread, same fixed tree): the warp partials rescaled to the global max
+  float wt = 0.f;
+  if (wk != 0u) {
+    const float Mw = __uint_as_float((wk & 0x80000000u) ? (wk & 0x7fffffffu) : ~wk);
+    wt = wps[lane] * expf(Mw - Mx);
+  }
+  const float sum = warp_sum(wt);
+  const bool ok = ok_in && Mx > -INFINITY;
+  const float lse = ok ? Mx + logf(sum) : __int_as_float(0x7fc00000);
+  __syncthreads();
+  trace_mark(a.trace, 11);
+  const int ns = *ncand;
+  if (a.trace != nullptr && tid == 0) a.trace[blockIdx.x * 64 + 29] = (unsigned long long)ns;  // candidates
+  rank_keys(cand, ns, K, kGThreads, [&](int rk, unsigned long long x) {
+    const float z = key_value(x);
+    a.top_ids[rk] = ok ? key_id(x) : -1;
+    a.top_logits[rk] = ok ? z : -INFINITY;
+    a.top_logp[rk] = ok ? z - lse : -INFINITY;
+  });
+  if (tid >= min(ns, K) && tid < K) {  // fewer valid keys than K: padding (R17)
+    a.top_ids[tid] = -1;
+    a.top_logits[tid] = -INFINITY;
+    a.top_logp[tid] = -INFINITY;
+  }
+  if (tid == 0) a.lse[0] = lse;
+  trace_mark(a.trace, 9);
+}
+
 // Merger (CTA 0): stage the G records as their words land; thread g decodes record g.  lse = M + log
 // sum_g s_g e^{m_g - M} (per-warp xor trees, then one fixed tree over the warps, R19).  Top-K: each
 // record warp finds its q-th best head (q = ceil(K / record warps), REDUX rounds); every key with a
@@ -563,13 +654,7 @@ __device__ DS_GSTEP_NOINLINE void gstep_merge(const GStepArgs& a, uint8_t* ring,
                                          volatile int* dead) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int G = gridDim.x, K = a.k_t, rec = 2 + K;
-  unsigned long long* raw = reinterpret_cast<unsigned long long*>(ring);  // [G][rec]
-  unsigned long long* cand = raw + (size_t)G * rec;                       // [G*K]
-  uint32_t* wthr = reinterpret_cast<uint32_t*>(cand + (size_t)G * K);    // [16] per-warp q-th heads
-  uint32_t* wmx = wthr + kGWarps;                                         // [16] per-warp max logit keys
-  float* wps = reinterpret_cast<float*>(wmx + kGWarps);                   // [16] per-warp lse partials
-  int* wq = reinterpret_cast<int*>(wps + kGWarps);                      // [16] keys each threshold bounds
-  int* ncand = wq + kGWarps;
+  unsigned long long* raw = reinterpret_cast<unsigned long long*>(ring);  // [G][rec] staged records
   const int nrec = G * rec;
   if (warp == 0) {  // first word of every record (written with its keys): one warp, all probes in flight
     unsigned long long v[kGHeadsPerLane];
@@ -599,81 +684,15 @@ __device__ DS_GSTEP_NOINLINE void gstep_merge(const GStepArgs& a, uint8_t* ring,
     for (int i = tid; i < nrec; i += kGThreads)
       if (raw[i] == 0ull) raw[i] = poll_slow(a.rec + i, t_spin, a.err, dead, 0);
   }
-  if (tid == 0) *ncand = 0;
   __syncthreads();
   trace_mark(a.trace, 8);
-  const bool ok_all = *dead == 0;
-  // thread g: record g (G <= blockDim: one CTA per SM)
-  const bool has = tid < G;
-  const unsigned long long w0 = has ? raw[(size_t)tid * rec] : 0ull;
-  const float mg = has ? __uint_as_float((uint32_t)w0) : -INFINITY;
-  const float sg = __uint_as_float((uint32_t)(w0 >> 32));
-  const int cg = has ? (int)raw[(size_t)tid * rec + 1] - 1 : 0;
-  const unsigned long long hd = has ? raw[(size_t)tid * rec + 2] : 0ull;
-  const uint32_t hk = (cg > 0 && hd > 1ull) ? (uint32_t)(hd >> 32) : 0u;
-  const int q = a.q_merge;  // ceil(K / record warps), from the host
-  {
-    const uint32_t mk = __reduce_max_sync(0xffffffffu, mg > -INFINITY ? ord_key(mg) : 0u);
-    // this warp's min(q, n_w)-th best head (n_w: its non-empty records)
-    const int qq = min(q, __popc(__ballot_sync(0xffffffffu, hk != 0u)));
-    uint32_t v = hk, tq = 0xffffffffu;
-    for (int it = 0; it < qq; ++it) {
-      tq = __reduce_max_sync(0xffffffffu, v);
-      const uint32_t b = __ballot_sync(0xffffffffu, v == tq);
-      if (lane == __ffs(b) - 1) v = 0u;
-    }
-    if (lane == 0) {
-      wmx[warp] = mk;
-      wthr[warp] = tq;
-      wq[warp] = qq;
-    }
-  }
-  __syncthreads();
-  trace_mark(a.trace, 10);
-  const uint32_t Mk = __reduce_max_sync(0xffffffffu, lane < kGWarps ? wmx[lane] : 0u);
-  const float Mx = Mk ? __uint_as_float((Mk & 0x80000000u) ? (Mk & 0x7fffffffu) : ~Mk) : -INFINITY;
-  // the warps' thresholds bound >= sum of their qq keys from below: valid if that is >= K
-  const unsigned nq = __reduce_add_sync(0xffffffffu, lane < kGWarps ? (unsigned)wq[lane] : 0u);
-  const uint32_t T = (int)nq >= K ? __reduce_min_sync(0xffffffffu, lane < kGWarps ? wthr[lane] : 0xffffffffu) : 0u;
-  {
-    const float part = warp_sum(has && mg > -INFINITY ? sg * expf(mg - Mx) : 0.f);
-    if (lane == 0) wps[warp] = part;
-    int c = 0;  // record keys with a high word >= T: a prefix of the sorted record
-    if (has && T > 0u)
-      while (c < cg && (uint32_t)(raw[(size_t)tid * rec + 2 + c] >> 32) >= T) ++c;
-    else if (has)
-      c = cg;
-    if (c > 0) {
-      const int base = atomicAdd(ncand, c);
-#pragma unroll 1
-      for (int j = 0; j < c; ++j) cand[base + j] = raw[(size_t)tid * rec + 2 + j];
-    }
-  }
-  __syncthreads();
-  trace_mark(a.trace, 11);
-  const int ns = *ncand;
-  const bool ok = ok_all && stream && Mx > -INFINITY;
-  const float sum = warp_sum(lane < kGWarps ? wps[lane] : 0.f);  // one fixed tree over the warps (R19)
-  const float lse = ok ? Mx + logf(sum) : __int_as_float(0x7fc00000);
-  rank_keys(cand, ns, K, kGThreads, [&](int rk, unsigned long long x) {
-    const float z = key_value(x);
-    a.top_ids[rk] = ok ? key_id(x) : -1;
-    a.top_logits[rk] = ok ? z : -INFINITY;
-    a.top_logp[rk] = ok ? z - lse : -INFINITY;
-  });
-  if (tid >= min(ns, K) && tid < K) {  // fewer valid keys than K: padding (R17)
-    a.top_ids[tid] = -1;
-    a.top_logits[tid] = -INFINITY;
-    a.top_logp[tid] = -INFINITY;
-  }
-  if (tid == 0) a.lse[0] = lse;
-  trace_mark(a.trace, 9);
   // every word is staged and every CTA has read the unit words (its record exists only after its
-  // poll): zero both for the next launch
+  // poll): zero both for the next launch (the stores drain while the merge computes)
 #pragma unroll 4
   for (int i = tid; i < nrec; i += kGThreads) a.rec[i] = 0ull;
   if (!a.head_only && tid < a.rows1) a.aslot[tid] = 0ull;  // rows1 <= blockDim
   if (tid == 0) *a.claim = 0u;  // every producer has claimed past the end (its record exists)
+  gstep_merge_compute(a, raw, G, *dead == 0 && stream);
 }
 
 template <typename T>

@@ -5,6 +5,7 @@
 // nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -o phase_bench phase_bench.cu
 #include <cstdio>
 #include <algorithm>
+#include <cstring>
 #include <functional>
 #include <vector>
 
@@ -89,6 +90,21 @@ __global__ void __launch_bounds__(512, 1) k_record(const unsigned long long* lis
   }
 }
 
+__global__ void __launch_bounds__(512, 1) k_merge(GStepArgs a, const unsigned long long* recs, int G,
+                                                  unsigned long long* cyc) {
+  extern __shared__ __align__(16) unsigned long long raw[];
+  const int tid = threadIdx.x, rec = 2 + a.k_t;
+  for (int r = 0; r < R; ++r) {
+    for (int i = tid; i < G * rec; i += blockDim.x) raw[i] = recs[i];
+    __syncthreads();
+    const unsigned long long t0 = clock64();
+    gstep_merge_compute(a, raw, G, true);
+    __syncthreads();
+    const unsigned long long t1 = clock64();
+    if (tid == 0) cyc[r] = t1 - t0;
+  }
+}
+
 static double median(std::vector<unsigned long long> v) {
   std::sort(v.begin(), v.end());
   return (double)v[v.size() / 2];
@@ -160,6 +176,46 @@ int main() {
   int bad = 0;
   for (int r = 0; r < K; ++r) bad += hr[2 + r] != all[r];
   printf("  record check: %d wrong of %d (count word %llu)\n", bad, K, hr[1]);
+  }
+  {  // merger compute: G = 147 records of K = 8 keys
+    const int G = 147, K = 8, rec = 2 + K;
+    std::vector<unsigned long long> h((size_t)G * rec);
+    unsigned y = 777;
+    for (int g = 0; g < G; ++g) {
+      float m = 10.f + (float)(g % 13) * 0.01f;
+      unsigned mb;
+      memcpy(&mb, &m, 4);
+      float sm = 3.f;
+      unsigned sb;
+      memcpy(&sb, &sm, 4);
+      h[(size_t)g * rec] = (unsigned long long)mb | ((unsigned long long)sb << 32);
+      h[(size_t)g * rec + 1] = K + 1;
+      unsigned hi = 0xc1000000u + (unsigned)(g * 7919 % 100000);
+      for (int j = 0; j < K; ++j) {
+        y = y * 1664525u + 1013904223u;
+        hi -= 20000u + (y >> 18);
+        h[(size_t)g * rec + 2 + j] = ((unsigned long long)hi << 32) | (0xffffffffu - (unsigned)(g * K + j));
+      }
+    }
+    unsigned long long *dr;
+    cudaMalloc(&dr, h.size() * 8);
+    cudaMemcpy(dr, h.data(), h.size() * 8, cudaMemcpyHostToDevice);
+    GStepArgs m = {};
+    m.k_t = K;
+    m.q_merge = (K + 4) / 5;
+    int* oi;
+    float* of;
+    cudaMalloc(&oi, 64 * 4);
+    cudaMalloc(&of, 3 * 64 * 4);
+    m.top_ids = oi;
+    m.top_logits = of;
+    m.top_logp = of + 64;
+    m.lse = of + 128;
+    const size_t sm = (size_t)G * rec * 8 + (size_t)G * K * 8 + 1024;
+    cudaFuncSetAttribute(k_merge, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    for (int rep = 0; rep < 2; ++rep) k_merge<<<1, 512, sm>>>(m, dr, G, cyc);
+    cudaDeviceSynchronize();
+    printf("merge_compute G=147 K=8 (+ barrier): %.0f cycles/call\n", median({cyc, cyc + R}));
   }
   cudaError_t e = cudaGetLastError();
   printf("status: %s\n", cudaGetErrorString(e));

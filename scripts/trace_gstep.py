@@ -72,7 +72,8 @@ print("per step (us): pdl release (first..last CTA) -> mask | -> streamed (last)
 for t in range(C.positions):
     p0, p1, out, mk, sd, rc, mi, mr, mf, mc = ends[t]
     nxt = ends[t + 1][0] if t + 1 < C.positions else float("nan")
-    print(f"  t={t}: pdl spread {1e-3 * (p1 - p0):.2f} | mask {1e-3 * (mk - p0):.2f} | streamed {1e-3 * (sd - p0):.2f} | "
+    print(f"  t={t}: merger candidates {int(bufs[t].view(G, 64)[:, 29].max().item())} |"
+          f" pdl spread {1e-3 * (p1 - p0):.2f} | mask {1e-3 * (mk - p0):.2f} | streamed {1e-3 * (sd - p0):.2f} | "
           f"record {1e-3 * (rc - p0):.2f} | merger: headers+issued {1e-3 * (mi - p0):.2f} staged {1e-3 * (mr - p0):.2f} "
           f"fields {1e-3 * (mf - p0):.2f} cands {1e-3 * (mc - p0):.2f} | out {1e-3 * (out - p0):.2f} | next pdl {1e-3 * (nxt - p0):.2f}")
 for t in range(C.positions):
