@@ -136,6 +136,11 @@ const char* dynaspec_status_string(ds_status s);
  * Returns -1 if t < 0, k_min < 1 or k_max < k_min. */
 int32_t dynaspec_budget(int32_t t, int32_t k_max, int32_t k_min);
 
+/* PA-FR position-aware frequency budget (App. A.1): K_fr(t) = K_max for t in {0,1},
+ * floor(K_max / (t + 1)) for t >= 2, clamped below by 1 (reading R26).  Returns -1 if t < 0 or
+ * K_max < 1. */
+int32_t dynaspec_pa_fr_budget(int32_t t, int32_t K_max);
+
 /* Upper bound on |V_S| for k selected clusters of one row: min(V, k * max_size). */
 int64_t dynaspec_max_shortlist(const ds_clusters* c, int32_t k);
 
@@ -315,6 +320,16 @@ ds_status dynaspec_head_partial(const ds_clusters* c, const void* h_new, int32_t
  * defines them (softmax over the union of the ranks' shortlists).  G <= 64. */
 ds_status dynaspec_merge_records(const float* records, int32_t G, int32_t B, int32_t k_t, int32_t* top_ids,
                                  float* top_logits, float* top_logp, float* lse, ds_stream_t stream);
+
+/* ---------------------------------------------------------------- static frequency heads (NEXT-3) */
+
+/* Row gather out[i] = W[ids[i]] for i < n (W [V][d] of dtype, out [n][d]; device pointers): the
+ * frequency-ordered copy of W_LM that FR-Spec / PA-FR heads stream as one contiguous prefix
+ * (App. A.1; ids = pi_f, tokens by descending corpus count, R26).  Errors: DS_ERR_SHAPE,
+ * DS_ERR_DTYPE, DS_ERR_UNSUPPORTED (d * sizeof(dtype) not a multiple of 16).  The ids are not
+ * range-checked on the device (an id outside [0, V) is a precondition violation). */
+ds_status dynaspec_gather_rows(const void* W, int32_t dtype, int64_t V, int32_t d, const int32_t* ids, int64_t n,
+                               void* out, ds_stream_t stream);
 
 /* ---------------------------------------------------------------- lossless verification (NEXT-4) */
 

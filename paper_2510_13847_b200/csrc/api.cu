@@ -114,6 +114,23 @@ int32_t dynaspec_budget(int32_t t, int32_t k_max, int32_t k_min) {
   return k > k_min ? k : k_min;
 }
 
+int32_t dynaspec_pa_fr_budget(int32_t t, int32_t K_max) {
+  if (t < 0 || K_max < 1) return -1;
+  if (t <= 1) return K_max;
+  const int32_t k = K_max / (t + 1);
+  return k > 1 ? k : 1;
+}
+
+ds_status dynaspec_gather_rows(const void* W, int32_t dtype, int64_t V, int32_t d, const int32_t* ids, int64_t n,
+                               void* out, ds_stream_t stream) {
+  if (!W || !ids || !out || V < 1 || d < 1 || n < 0) return DS_ERR_SHAPE;
+  if (!dtype_ok(dtype)) return DS_ERR_DTYPE;
+  const size_t rowb = (size_t)d * (dtype == DS_BF16 ? 2 : 4);
+  if (rowb % 16 != 0) return DS_ERR_UNSUPPORTED;
+  if (n == 0) return DS_OK;
+  return launch_gather_rows(W, rowb, ids, n, out, (cudaStream_t)stream) == cudaSuccess ? DS_OK : DS_ERR_CUDA;
+}
+
 int64_t dynaspec_max_shortlist(const ds_clusters* c, int32_t k) {
   if (!c || k < 1) return 0;
   const int64_t b = (int64_t)k * c->max_size;

@@ -147,6 +147,9 @@ cudaError_t launch_verify(const void* p_logits, int dtype, int64_t V, int B, int
 cudaError_t launch_shortlist_ids(const ds_clusters* c, int rows, const int32_t* sel, const int32_t* cnt,
                                  const int32_t* sl_off, int64_t stride, int32_t* ids, cudaStream_t st);
 
+// ---- row gather (layout.cu): out[i] = W[ids[i]], rows of rowb bytes (a multiple of 16)
+cudaError_t launch_gather_rows(const void* W, size_t rowb, const int32_t* ids, int64_t n, void* out, cudaStream_t st);
+
 // ---- offline partition (build.cu)
 size_t build_ws_bytes(int64_t V, int d, int M);
 size_t layout_ws_bytes(int64_t V, int M);

@@ -63,6 +63,12 @@ __global__ void gather_rows_kernel(const uint8_t* __restrict__ W, const int32_t*
   }
 }
 
+cudaError_t launch_gather_rows(const void* W, size_t rowb, const int32_t* ids, int64_t n, void* out, cudaStream_t st) {
+  gather_rows_kernel<<<num_sms() * 8, 256, 0, st>>>(static_cast<const uint8_t*>(W), ids, n, (int)rowb,
+                                                   static_cast<uint8_t*>(out));
+  return cudaGetLastError();
+}
+
 size_t layout_ws_bytes(int64_t V, int M) {
   (void)V;
   return align_up((size_t)(M + 1) * sizeof(int32_t), 256) + 256;

@@ -59,6 +59,8 @@ def _load():
     sig = {
         "dynaspec_status_string": (ctypes.c_char_p, [c_int32]),
         "dynaspec_budget": (c_int32, [c_int32, c_int32, c_int32]),
+        "dynaspec_pa_fr_budget": (c_int32, [c_int32, c_int32]),
+        "dynaspec_gather_rows": (c_int32, [P, c_int32, c_int64, c_int32, P, c_int64, P, P]),
         "dynaspec_max_shortlist": (c_int64, [POINTER(DsClusters), c_int32]),
         "dynaspec_ws_init": (c_int32, [P, c_size_t, P]),
         "dynaspec_ws_error": (c_int32, [P, c_size_t, P, P]),
@@ -105,7 +107,8 @@ def _load():
 _lib = _load()
 
 EXPORTED = [
-    "dynaspec_status_string", "dynaspec_budget", "dynaspec_max_shortlist", "dynaspec_ws_init", "dynaspec_ws_error",
+    "dynaspec_status_string", "dynaspec_budget", "dynaspec_pa_fr_budget", "dynaspec_gather_rows",
+    "dynaspec_max_shortlist", "dynaspec_ws_init", "dynaspec_ws_error",
     "dynaspec_build_clusters_ws", "dynaspec_build_clusters", "dynaspec_layout_ws", "dynaspec_layout",
     "dynaspec_meta_score_ws", "dynaspec_meta_score", "dynaspec_select", "dynaspec_head_forward_ws",
     "dynaspec_head_forward", "dynaspec_draft_step_ws", "dynaspec_draft_step", "dynaspec_draft_step_launches",
@@ -500,7 +503,9 @@ class FrequencyHead:
         _need_cuda(W)
         self.V, self.d = W.shape
         self.perm = torch.as_tensor(pi_f, dtype=torch.int32, device=W.device).contiguous()
-        self.W_freq = W.index_select(0, self.perm.long()).contiguous()
+        self.W_freq = torch.empty_like(W)  # W_freq[i] = W[pi_f[i]] (dynaspec_gather_rows)
+        _check(_lib.dynaspec_gather_rows(_ptr(W.contiguous()), _DTYPE[W.dtype], self.V, self.d, _ptr(self.perm),
+                                         self.V, _ptr(self.W_freq), _stream()), "dynaspec_gather_rows")
         self._views = {}
 
     def _view(self, K):
@@ -530,8 +535,12 @@ class FrequencyHead:
 
 
 def pa_fr_budget(t, K_max):
-    """K_fr(t) = K_max for t < 2, else max(1, floor(K_max / (t + 1))) (App. A.1, P:404-410)."""
-    return K_max if t < 2 else max(1, K_max // (t + 1))
+    """K_fr(t) = K_max for t < 2, else max(1, floor(K_max / (t + 1))) (App. A.1, P:404-410):
+    dynaspec_pa_fr_budget."""
+    k = _lib.dynaspec_pa_fr_budget(int(t), int(K_max))
+    if k < 1:
+        raise ValueError("pa_fr_budget: t >= 0 and K_max >= 1 required")
+    return k
 
 
 # ---------------------------------------------------------------------------- verification (NEXT-4)

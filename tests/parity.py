@@ -13,6 +13,13 @@ from oracle import dynaspec_oracle as O
 
 BF16_TOL = 2e-2
 F32_REL = 1e-5
+# Router scores: fp32 accumulation of d_r = 2d products against the fp64 oracle.
+# measured max |s_f32 - s_f64| = 3.9e-7 at Llama-3 shape (score rms 0.70); 1e-5 rms leaves ~18x.
+SCORE_REL = 1e-5
+
+
+def score_tol(s_ref):
+    return SCORE_REL * float(np.sqrt(np.mean(np.asarray(s_ref, dtype=np.float64) ** 2)))
 
 
 class Rows:

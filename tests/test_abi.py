@@ -43,10 +43,21 @@ def test_budget_agrees_with_oracle_exhaustively():
                 assert D.budget(t, kmax, kmin) == O.budget(t, kmax, kmin)
 
 
+def test_pa_fr_budget_matches_paper_and_oracle():
+    """K_fr(t) (App. A.1): K_max at t = 0, 1; floor(K_max / (t + 1)) after, >= 1 (R26)."""
+    from oracle import dynaspec_oracle as O
+    from paper_2510_13847_b200 import dynaspec as D
+    assert [D.pa_fr_budget(t, 32768) for t in range(6)] == [32768, 32768, 10922, 8192, 6553, 5461]
+    for K in (1, 2, 7, 1000, 32768):
+        for t in range(0, 30):
+            assert D.pa_fr_budget(t, K) == O.budget_pa_fr(t, K)
+    assert D.lib().dynaspec_pa_fr_budget(-1, 4) == -1 and D.lib().dynaspec_pa_fr_budget(0, 0) == -1
+
+
 def test_status_strings_and_sync_validation():
     from paper_2510_13847_b200 import dynaspec as D
     lib = D.lib()
-    for code in range(12):
+    for code in range(13):
         assert lib.dynaspec_status_string(code)
     # NULL pointers / bad sizes are rejected synchronously, before any CUDA call
     c = D.DsClusters(100, 16, 4, 0, 1, 30, None, None, None, None)

@@ -13,7 +13,7 @@ import torch
 
 from oracle import dynaspec_oracle as O
 from synth import inputs as S
-from tests.parity import Rows, check_topk, f64, selection_certified
+from tests.parity import Rows, check_topk, f64, score_tol, selection_certified
 
 pytestmark = pytest.mark.gpu
 
@@ -199,7 +199,7 @@ def test_random_regime_config(cfg, dtype, B, fused):
         s_gpu = st.scores.cpu().numpy()
         for b in range(B):
             s_ref = ref[b]["scores"]
-            assert np.max(np.abs(s_gpu[b] - s_ref)) < 1e-3 * max(1.0, np.sqrt(np.mean(s_ref ** 2)))
+            assert np.max(np.abs(s_gpu[b] - s_ref)) <= score_tol(s_ref)
             cnt = st.sel_count[b].item()
             sel_gpu = np.array(st.sel[b, :cnt].cpu().tolist())
             if selection_certified(s_ref, ref[b]["k"]):
@@ -558,7 +558,7 @@ def test_router_many_rows_row_blocks():
     for b in (0, 1, 191, 192, 300, 511):
         ref = O.draft_step(part, ro, Rows(W), f64(hp[b:b + 1]), f64(e[b:b + 1]), f64(hn[b:b + 1]), 2, 16, 4, 8)[0]
         s_ref = ref["scores"]
-        assert np.max(np.abs(st.scores[b].cpu().numpy() - s_ref)) < 1e-3 * max(1.0, np.sqrt(np.mean(s_ref ** 2)))
+        assert np.max(np.abs(st.scores[b].cpu().numpy() - s_ref)) <= score_tol(s_ref)
         if selection_certified(s_ref, ref["k"]):
             cnt = st.sel_count[b].item()
             assert st.sel[b, :cnt].cpu().tolist() == ref["sel"].tolist()
@@ -619,7 +619,7 @@ def test_gemma3_batched_full_size_sampled_rows(monkeypatch):
         ref = O.draft_step(part, ro, Wo, f64(hp[b:b + 1]), f64(e[b:b + 1]), f64(hn[b:b + 1]), t, C.k_max, C.k_min,
                            C.k_t)[0]
         s_ref = ref["scores"]
-        assert np.max(np.abs(st.scores[b].cpu().numpy() - s_ref)) < 1e-3 * max(1.0, np.sqrt(np.mean(s_ref ** 2)))
+        assert np.max(np.abs(st.scores[b].cpu().numpy() - s_ref)) <= score_tol(s_ref)
         cnt = st.sel_count[b].item()
         sel = np.array(st.sel[b, :cnt].cpu().tolist())
         if selection_certified(s_ref, ref["k"]):
