@@ -276,6 +276,12 @@ ds_status dynaspec_step_head(const ds_clusters* c, const void* h_new, int32_t B,
 int32_t dynaspec_draft_step_launches(const ds_clusters* c, const ds_router* r, int32_t B, int32_t k_t,
                                      int32_t shared, int32_t two_streams);
 
+/* Name of the dominant kernel one dynaspec_draft_step runs for this shape (for measurement
+ * bookkeeping: the kernel a roofline is quoted on).  Static string, never NULL ("?" on bad
+ * arguments).  Assumes 16-byte aligned inputs (the unaligned fallbacks are not named). */
+const char* dynaspec_draft_step_kernel(const ds_clusters* c, const ds_router* r, int32_t B, int32_t k_t,
+                                       int32_t shared, int32_t two_streams);
+
 /* ---------------------------------------------------------------- draft tree (Alg. 1 lines 12-18) */
 
 /* One step of the draft-tree bookkeeping for R current beams (R = 1 at j = 0):

@@ -440,6 +440,25 @@ int32_t dynaspec_draft_step_launches(const ds_clusters* c, const ds_router* r, i
   return 2 + p.launches;  // meta layer 1, meta layer 2 (+select), head chunks
 }
 
+const char* dynaspec_draft_step_kernel(const ds_clusters* c, const ds_router* r, int32_t B, int32_t k_t,
+                                       int32_t shared, int32_t two_streams) {
+  HeadPlan p;
+  if (!c || !r || !head_plan(c, B, k_t, 0, &p)) return "?";
+  const int64_t ms = shared ? c->V : 0;
+  if (use_tc_head(c, B, k_t, shared, ms)) return "ds::tc_head_kernel (tcgen05, shared shortlist)";
+  if (use_tc_batched(c, B, k_t, shared, false)) return "ds::tc_head_kernel (tcgen05, batched rows over the union)";
+  if (!two_streams && step_supported(c, r, B, k_t, shared, 0)) {
+    if (gstep_supported(c, r, B, k_t, shared))
+      return "ds::gstep_kernel (grid step: router units over all CTAs + select + gathered head + epilogue, one launch)";
+    if (cstep_supported(c, r, B, k_t, shared, 0))
+      return "ds::cstep_kernel (cluster step: router per 16-CTA cluster + select + gathered head + epilogue, one launch)";
+    return "ds::step_kernel (router + select + gathered head + epilogue, one launch)";
+  }
+  if (B == 1 && !shared && gstep_supported(c, nullptr, 1, k_t, 0)) return "ds::gstep_kernel (head only, after the router on S_m)";
+  if (B == 1 && !shared && cstep_head_supported(c, k_t, 0)) return "ds::cstep_kernel (head only, after the router on S_m)";
+  return "ds::head_kernel (gathered head + epilogue, after the router on S_m)";
+}
+
 ds_status dynaspec_draft_step(const ds_clusters* c, const ds_router* r, const void* h_prev, const void* e,
                               const void* h_new, int32_t B, int32_t t, int32_t k_max, int32_t k_min, int32_t k_t,
                               int32_t shared, const ds_step_outputs* out, void* ws, size_t ws_bytes,

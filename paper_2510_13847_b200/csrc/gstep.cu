@@ -54,12 +54,11 @@ constexpr int kGRows2 = 16;              // layer-2 rows per warp (M <= 256), 2 
 constexpr int kGMaxM = kGWarps * kGRows2;
 constexpr int kGHeadsPerLane = 5;       // merger: record headers per polling lane (G <= 160)
 constexpr int kGKeyWarps = 8;
-constexpr int kGTailPerCta = 2;          // run-time-claimed tail chunks per streaming CTA            // TopK: warps holding <= 32 scores each (M <= 256)
 constexpr int kGMaxKt = 32;              // one list entry per lane
 constexpr unsigned long long kSpinNs = 2000000000ull;
 
 struct GSmem {
-  uint32_t ring, bars, info, hs, a1, sc, b2s, offs, cch, ctab, mask, thr, wc, surv, wl, wm, wsum, wn, misc, red, total;
+  uint32_t ring, bars, info, hs, a1, sc, b2s, offs, cch, mask, thr, wc, surv, wl, wm, wsum, wn, misc, red, total;
 };
 
 __host__ __device__ inline GSmem gstep_smem(int S, int stage_bytes, int d, int esz, int M, int rows1, int K) {
@@ -80,7 +79,6 @@ __host__ __device__ inline GSmem gstep_smem(int S, int stage_bytes, int d, int e
   L.b2s = take(4u * M, 16);
   L.offs = take(4u * (M + 1), 16);
   L.cch = take(4u * M, 16);
-  L.ctab = take(16u * M, 16);
   L.mask = take(4u * (kGMaxM / 32), 16);
   L.thr = take(8u * kGWarps, 8);  // per-warp thresholds, then survivor bits
   L.wc = take(4u * kGWarps, 4);
@@ -119,15 +117,13 @@ struct GStepArgs {
   float* lse;
   float* z_out;             // nullable: z over V_S in shortlist order
   int64_t max_shortlist;
-  int32_t M, d, h_r, rows1, k, k_t, stages, stage_rows, stage_bytes, head_only, pdl;
-  int32_t tail;                 // 1: run-time-claimed tail chunks (DS_GSTEP_TAIL=1)
+  int32_t V, M, d, h_r, rows1, k, k_t, stages, stage_rows, stage_bytes, head_only, pdl;
   int32_t kpw, q_sel, q_merge;  // TopK launch constants: keys per warp, per-warp / record-warp ranks
   int32_t lgK;                  // ceil(log2(k_t + 1)): binary-search steps over a k_t-entry list
   uint32_t kdiv;                // ceil(2^32 / k_t): tid / k_t as one multiply-high
   unsigned long long* aslot;  // [rows1] published layer-1 units (0 = not yet)
   unsigned long long* rec;    // [G][2 + k_t] per-CTA records (0 = not yet)
   unsigned* err;              // workspace error word (DS_ERR_DEVICE_TIMEOUT)
-  unsigned* claim;            // tail-chunk claim counter (0 between launches; the merger resets it)
   unsigned long long* trace;
   GSmem L;                    // shared-memory carve-up (host-computed)
 };
@@ -377,68 +373,91 @@ __device__ DS_GSTEP_NOINLINE void topk_mask(const float* sc, int M, int k, int k
 }
 
 // ---------------------------------------------------------------- gathered head
-// Producer lane.  Chunk c of the virtual shortlist = <= R whole W_perm rows inside one cluster, in
-// shortlist order (selected clusters ascending, R8).  The first Ns chunks are static: chunk c goes to
-// streaming CTA c mod Gs (the whole grid sweeps one window of the shortlist at a time).  With
-// a.tail, the last D (~2 per CTA) are claimed at run time, one atomicAdd each, so the SMs that
-// stream faster take more of the tail; claims are issued while the ring is still full, so their
-// round trip is hidden.  info = (-, virtual shortlist position, rows, first W_perm row).
+// Chunks of the virtual shortlist, in shortlist order (selected clusters ascending, R8): chunk c =
+// <= R whole W_perm rows inside one cluster; chunk c goes to streaming CTA c mod Gs (the whole grid
+// sweeps one window of the shortlist at a time).  A resumable walk over this CTA's chunks.
+struct ChunkWalk {
+  const uint32_t* mask;
+  const int32_t* offs;
+  const int32_t* cch;
+  int words, R, Gs;
+  int w, beg, sz, nch;
+  uint32_t bits;
+  long long cb, vpos, cn;
+  bool live;
+  __device__ void init(const uint32_t* mask_, const int32_t* offs_, const int32_t* cch_, int M, int R_, int g, int Gs_) {
+    mask = mask_;
+    offs = offs_;
+    cch = cch_;
+    words = (M + 31) >> 5;
+    R = R_;
+    Gs = Gs_;
+    w = 0;
+    bits = mask[0];
+    cb = 0;
+    vpos = 0;
+    cn = g;
+    live = false;
+    beg = sz = nch = 0;
+  }
+  // next chunk of this CTA: (virtual position, rows, first W_perm row); false at the end
+  __device__ __forceinline__ bool next(int& vp, int& n, int& row) {
+    for (;;) {
+      if (live && cn < cb + nch) {
+        const int j0 = (int)(cn - cb) * R;
+        vp = (int)vpos + j0;
+        n = min(R, sz - j0);
+        row = beg + j0;
+        cn += Gs;
+        return true;
+      }
+      if (live) {
+        cb += nch;
+        vpos += sz;
+      }
+      while (bits == 0u) {
+        if (++w >= words) return false;
+        bits = mask[w];
+      }
+      const int m = (w << 5) + __ffs(bits) - 1;
+      bits &= bits - 1u;
+      beg = offs[m];
+      sz = offs[m + 1] - beg;
+      nch = cch[m];
+      live = true;
+    }
+  }
+};
+
+// Producer lane: the CTA's chunks through the TMA bulk-copy ring (info = (-, virtual shortlist
+// position, rows, first W_perm row)).  (Requesting the chunks that wait for a slot into L2 ahead of
+// time with cp.async.bulk.prefetch.L2 measured slower: 20.1 -> 23.9 us per step.)
 template <typename T>
 __device__ __noinline__ void gstep_produce(const GStepArgs& a, uint8_t* ring, uint64_t* full, uint64_t* empty,
                                            int4* info, const uint32_t* mask, const int32_t* offs, const int32_t* cch,
-                                           int nchunks, bool stream, int4* ctab) {
+                                           bool stream) {
   const int g = blockIdx.x, Gs = gridDim.x - 1;  // the merger CTA (the last) streams nothing
-  if (g >= Gs) stream = false;
   const uint64_t pol = policy_evict_first();
   const uint32_t rowbytes = (uint32_t)a.d * (uint32_t)sizeof(T);
   const uint8_t* W = static_cast<const uint8_t*>(a.W);
   const uint32_t S = (uint32_t)a.stages;
-  const int R = a.stage_rows;
   uint32_t sl = 0, ph = 0;  // ring slot and phase (no divisions)
-  auto issue = [&](int vp, int n, int row) {
-    mbar_wait(&empty[sl], ph ^ 1u);
-    info[sl] = make_int4(0, vp, n, row);
-    mbar_arrive_expect_tx(&full[sl], (uint32_t)n * rowbytes);
-    bulk_g2s(ring + (size_t)sl * a.stage_bytes, W + (size_t)row * rowbytes, (uint32_t)n * rowbytes, &full[sl], pol);
-    if (++sl == S) {
-      sl = 0;
-      ph ^= 1u;
-    }
-  };
-  const long long N = nchunks;
-  // Off by default: which CTA sums a tail chunk then depends on timing, so the fp32 lse partials are
-  // grouped differently from run to run (R19 asks for identical bytes); ids and logits are unaffected.
-  const long long D = (stream && a.tail) ? min(N / 4, (long long)Gs * kGTailPerCta) : 0;
-  const long long Ns = N - D;
-  int nsel = 0;
-  long long vpos = 0, cb = 0, cn = g;
-  const int words = (a.M + 31) >> 5;
-  for (int w = 0; stream && w < words; ++w) {
-    for (uint32_t bits = mask[w]; bits; bits &= bits - 1u) {
-      const int m = (w << 5) + __ffs(bits) - 1;
-      const int beg = offs[m], sz = offs[m + 1] - beg;
-      const int nch = cch[m];
-      ctab[nsel++] = make_int4((int)cb, (int)vpos, beg, sz);
-      for (; cn < cb + nch && cn < Ns; cn += Gs) {
-        const int j0 = (int)(cn - cb) * R;
-        issue((int)vpos + j0, min(R, sz - j0), beg + j0);
+  if (stream && g < Gs) {
+    ChunkWalk is;
+    is.init(mask, offs, cch, a.M, a.stage_rows, g, Gs);
+    int vp, n, row;
+    while (is.next(vp, n, row)) {
+      mbar_wait(&empty[sl], ph ^ 1u);
+      info[sl] = make_int4(0, vp, n, row);
+      mbar_arrive_expect_tx(&full[sl], (uint32_t)n * rowbytes);
+      bulk_g2s(ring + (size_t)sl * a.stage_bytes, W + (size_t)row * rowbytes, (uint32_t)n * rowbytes, &full[sl], pol);
+      if (++sl == S) {
+        sl = 0;
+        ph ^= 1u;
       }
-      cb += nch;
-      vpos += sz;
     }
   }
-  if (D > 0) {
-    unsigned* claim = a.claim;
-    int ci = 0;  // claims only increase: a forward cursor over the cluster table
-    for (;;) {
-      const long long c = Ns + (long long)atomicAdd(claim, 1u);
-      if (c >= N) break;
-      while (ci + 1 < nsel && ctab[ci + 1].x <= c) ++ci;
-      const int4 t = ctab[ci];
-      const int j0 = (int)(c - t.x) * R;
-      issue(t.y + j0, min(R, t.w - j0), t.z + j0);
-    }
-  }
+  trace_mark_w(a.trace, 18);  // last chunk issued
 #pragma unroll 1
   for (uint32_t j = 0; j < S; ++j) {  // one end-of-stream marker per slot
     mbar_wait(&empty[sl], ph ^ 1u);
@@ -463,6 +482,7 @@ __device__ __forceinline__ void gstep_consume(const GStepArgs& a, const uint8_t*
   mine = 0ull;
   for (uint32_t k = 0;; ++k) {
     mbar_wait(&full[w], k & 1u);
+    if (k == 0 && w == 0) trace_mark_w(a.trace, 12);  // first chunk of slot 0 landed
     const int4 inf = info[w];
     if (inf.z < 0) break;
     const T* st = reinterpret_cast<const T*>(ring + (size_t)w * a.stage_bytes);
@@ -691,7 +711,6 @@ __device__ DS_GSTEP_NOINLINE void gstep_merge(const GStepArgs& a, uint8_t* ring,
 #pragma unroll 4
   for (int i = tid; i < nrec; i += kGThreads) a.rec[i] = 0ull;
   if (!a.head_only && tid < a.rows1) a.aslot[tid] = 0ull;  // rows1 <= blockDim
-  if (tid == 0) *a.claim = 0u;  // every producer has claimed past the end (its record exists)
   gstep_merge_compute(a, raw, G, *dead == 0 && stream);
 }
 
@@ -864,16 +883,7 @@ __global__ void __launch_bounds__(kGThreads, 1) gstep_kernel(const __grid_consta
 
   // ---- gathered head + per-warp epilogue state
   if (warp == kGProducer) {
-    int nl = 0;  // total chunks of the shortlist: the producer warp sums the selected clusters' counts
-#pragma unroll 1
-    for (int w = 0; w < ((M + 31) >> 5); ++w) {
-      const int m = (w << 5) + lane;
-      if (m < M && ((mask[w] >> lane) & 1u)) nl += cch[m];
-    }
-    const int nchunks = (int)__reduce_add_sync(0xffffffffu, (unsigned)nl);
-    if (lane == 0)
-      gstep_produce<T>(a, ring, full, empty, info, mask, offs, cch, nchunks, stream,
-                       reinterpret_cast<int4*>(smem + L.ctab));
+    if (lane == 0) gstep_produce<T>(a, ring, full, empty, info, mask, offs, cch, stream);
   } else if (warp < S) {
     float m, se;
     unsigned long long mine;
@@ -911,6 +921,7 @@ static bool gstep_plan(const ds_clusters* c, const ds_router* r, int k_t, GStepP
   const char* off = getenv("DS_GSTEP");
   if (off && off[0] == '0') return false;
   if (k_t < 1 || k_t > kGMaxKt || c->M > kGMaxM) return false;
+  if ((reinterpret_cast<uintptr_t>(c->perm) & 15u) != 0 || c->V > (int64_t)0x7fffffff) return false;  // perm windows
   const int esz = c->dtype == DS_BF16 ? 2 : 4;
   const int G = gstep_grid();
   if (G > 32 * kGHeadsPerLane) return false;
@@ -992,6 +1003,7 @@ static void fill_common(GStepArgs& a, const ds_clusters* c, const GStepPlan& p, 
   a.lse = lse;
   a.z_out = z_out;
   a.max_shortlist = max_shortlist > 0 ? std::min<int64_t>(max_shortlist, c->V) : c->V;
+  a.V = (int32_t)c->V;
   a.M = c->M;
   a.d = c->d;
   a.k_t = k_t;
@@ -1002,9 +1014,6 @@ static void fill_common(GStepArgs& a, const ds_clusters* c, const GStepPlan& p, 
   a.rec = reinterpret_cast<unsigned long long*>(w8 + kWsGstepRec);
   a.aslot = reinterpret_cast<unsigned long long*>(w8 + kWsGstepUnits);
   a.err = reinterpret_cast<unsigned*>(w8 + kWsErrorWord);
-  a.claim = reinterpret_cast<unsigned*>(w8 + kWsGstepClaim);
-  const char* tl = getenv("DS_GSTEP_TAIL");
-  a.tail = tl && tl[0] == '1' ? 1 : 0;
   a.trace = debug_trace();
   a.L = gstep_smem(p.S, p.stage_bytes, c->d, c->dtype == DS_BF16 ? 2 : 4, c->M, std::max(p.rows1, 1), k_t);
   a.kpw = (c->M + kGKeyWarps - 1) / kGKeyWarps;

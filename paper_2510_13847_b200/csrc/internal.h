@@ -19,7 +19,6 @@ constexpr size_t kWsErrorWord = 252;
 constexpr size_t kWsCstepRec = 256;                      // cluster step: [G][2 + k_t] u64 (<= 48 KB)
 constexpr size_t kWsGstepRec = kWsCstepRec + 48 * 1024;  // grid step:    [G][2 + k_t] u64 (<= 48 KB)
 constexpr size_t kWsGstepUnits = kWsGstepRec + 48 * 1024;  // grid step: [rows1] u64 layer-1 units (<= 4 KB)
-constexpr size_t kWsGstepClaim = kWsGstepUnits + 4 * 1024;  // grid step: tail-chunk claim counter (u32)
 constexpr size_t kWsFixed = 112 * 1024;
 
 int num_sms();

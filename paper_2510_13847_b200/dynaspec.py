@@ -96,6 +96,8 @@ def _load():
                                             P, P, P, c_size_t, P]),
         "dynaspec_draft_step_launches": (c_int32, [POINTER(DsClusters), POINTER(DsRouter), c_int32, c_int32,
                                                    c_int32, c_int32]),
+        "dynaspec_draft_step_kernel": (ctypes.c_char_p, [POINTER(DsClusters), POINTER(DsRouter), c_int32, c_int32,
+                                                         c_int32, c_int32]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -112,6 +114,7 @@ EXPORTED = [
     "dynaspec_build_clusters_ws", "dynaspec_build_clusters", "dynaspec_layout_ws", "dynaspec_layout",
     "dynaspec_meta_score_ws", "dynaspec_meta_score", "dynaspec_select", "dynaspec_head_forward_ws",
     "dynaspec_head_forward", "dynaspec_draft_step_ws", "dynaspec_draft_step", "dynaspec_draft_step_launches",
+    "dynaspec_draft_step_kernel",
     "dynaspec_debug_set_trace", "dynaspec_restrict_selection", "dynaspec_head_partial", "dynaspec_merge_records",
     "dynaspec_tree_step", "dynaspec_tree_rerank", "dynaspec_step_route", "dynaspec_step_head",
     "dynaspec_shortlist_ids", "dynaspec_verify_ws", "dynaspec_verify_chain",
@@ -445,6 +448,8 @@ class DraftStep:
         self.ev_join = make_event() if two_streams else None
         self.launches = _lib.dynaspec_draft_step_launches(clusters.struct(), router.struct(), B, k_t, int(shared),
                                                           int(two_streams))
+        self.kernel = _lib.dynaspec_draft_step_kernel(clusters.struct(), router.struct(), B, k_t, int(shared),
+                                                      int(two_streams)).decode()
 
     def __call__(self, h_prev, e, h_new, t, k_max, k_min, head_events=None, stream=None):
         sd = _stream(stream)

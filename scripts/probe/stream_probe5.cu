@@ -1,0 +1,127 @@
+// stream_probe.cu — how fast can G CTAs (one per SM) stream B bytes of contiguous HBM into shared
+// memory with a TMA bulk-copy ring, chunk c -> CTA c mod G (the grid-step assignment)?  In-kernel
+// %globaltimer: start = min over CTAs of the first issue, end = max over CTAs of the last landing.
+// Sizes 8 MB .. 1 GB, ring S x CH bytes.  Cold L2 (a 512 MB memset before each launch).
+// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o stream_probe stream_probe.cu
+#include <cstdio>
+#include <cstdint>
+#include <vector>
+#include <algorithm>
+#include <cuda_runtime.h>
+
+__device__ __forceinline__ unsigned long long gt() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+__global__ void __launch_bounds__(64, 1) k_stream(const char* src, long long nbytes, int S, int CH,
+                                                  unsigned long long* ts, int consume, const long long* ctab) {
+  extern __shared__ __align__(1024) char sm[];
+  __shared__ __align__(8) unsigned long long full[48];
+  const int G = gridDim.x, g = blockIdx.x;
+  const long long nch = nbytes / CH;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < S; ++i)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((unsigned)__cvta_generic_to_shared(&full[i])));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  unsigned long long t0 = gt();
+  if (consume & 1) {
+    for (long long c = g; c < nch; c += G)
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src + c * CH), "r"(CH) : "memory");
+  }
+  long long it = 0;
+  const long long c_lo = (consume & 2) ? nch * g / G : g, c_hi = (consume & 2) ? nch * (g + 1) / G : nch;
+  const long long c_step = (consume & 2) ? 1 : G;
+  for (long long c = c_lo; c < c_hi; c += c_step, ++it) {
+    const int s = (int)(it % S);
+    const unsigned bar = (unsigned)__cvta_generic_to_shared(&full[s]);
+    if (it >= S) {
+      unsigned ok = 0;
+      const unsigned par = (unsigned)(((it / S) - 1) & 1);
+      while (!ok)
+        asm volatile("{.reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0,1,0,p;}"
+                     : "=r"(ok) : "r"(bar), "r"(par) : "memory");
+    }
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(CH) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     (unsigned)__cvta_generic_to_shared(sm + s * CH)),
+                 "l"(src + (ctab ? ctab[c] : c * CH)), "r"(CH), "r"(bar)
+                 : "memory");
+  }
+  for (long long j = (it > S ? it - S : 0); j < it; ++j) {
+    const unsigned bar = (unsigned)__cvta_generic_to_shared(&full[j % S]);
+    unsigned ok = 0;
+    const unsigned par = (unsigned)((j / S) & 1);
+    while (!ok)
+      asm volatile("{.reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0,1,0,p;}"
+                   : "=r"(ok) : "r"(bar), "r"(par) : "memory");
+  }
+  ts[2 * g] = t0;
+  ts[2 * g + 1] = gt();
+  (void)consume;
+}
+
+__global__ void k_read(const int4* p, long long n, int* sink) {
+  int4 acc = make_int4(0, 0, 0, 0);
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    int4 v = p[i];
+    acc.x ^= v.x; acc.y ^= v.y; acc.z ^= v.z; acc.w ^= v.w;
+  }
+  if ((acc.x ^ acc.y ^ acc.z ^ acc.w) == 0x12345678) sink[0] = 1;
+}
+
+int main() {
+  int G0 = 0;
+  cudaDeviceGetAttribute(&G0, cudaDevAttrMultiProcessorCount, 0);
+  char* src;
+  const size_t big = 1ull << 30;
+  cudaMalloc(&src, big);
+  cudaMemset(src, 1, big);
+  char* flush;
+  cudaMalloc(&flush, 512ull << 20);
+  unsigned long long* ts;
+  cudaMallocManaged(&ts, 2 * 256 * 8);
+  cudaFuncSetAttribute(k_stream, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  struct Cfg { int G, S, CH; };
+  const Cfg cfgs[] = {{G0 - 1, 12, 16384}};
+  char* cleanbuf; cudaMalloc(&cleanbuf, 512ull << 20); cudaMemset(cleanbuf, 3, 512ull << 20);
+  int* sink; cudaMalloc(&sink, 64);
+  long long* ctab; cudaMallocManaged(&ctab, sizeof(long long) * 65536);
+  {
+    unsigned long long x = 12345;
+    int sel[256]; for (int i = 0; i < 256; ++i) sel[i] = i;
+    for (int i = 255; i > 0; --i) { x = x * 6364136223846793005ull + 1442695040888963407ull; int j = (int)((x >> 33) % (i + 1)); int t = sel[i]; sel[i] = sel[j]; sel[j] = t; }
+    int cnt = 0; int ids[256];
+    for (int i = 0; i < 256; ++i) if (sel[i] < 250) ids[cnt++] = sel[i];
+    std::sort(ids, ids + 64);
+    for (int c = 0; c < 64 * 256; ++c) ctab[c] = (long long)ids[c / 256] * (4ll << 20) + (long long)(c % 256) * 16384;
+  }
+  const long long sizes[] = {8ll << 20, 32ll << 20, 128ll << 20};
+  for (int mode : {8, 24})
+  for (const Cfg& c : cfgs) {
+    for (long long B : sizes) {
+      std::vector<double> r;
+      for (int rep = 0; rep < 5; ++rep) {
+        cudaMemset(flush, rep, 512ull << 20);
+        if (mode >= 4) k_read<<<G0 * 4, 512>>>((const int4*)cleanbuf, (mode >= 8 ? (512ll << 20) : (256ll << 20)) / 16, sink);
+        k_stream<<<c.G, 64, (size_t)c.S * c.CH>>>(src, B, c.S, c.CH, ts, mode & 15, (mode & 16) ? ctab : nullptr);
+        cudaDeviceSynchronize();
+        unsigned long long a = ~0ull, b = 0;
+        for (int g = 0; g < c.G; ++g) {
+          a = std::min(a, ts[2 * g]);
+          b = std::max(b, ts[2 * g + 1]);
+        }
+        r.push_back((double)B / (double)(b - a));  // bytes per ns = GB/s
+      }
+      std::sort(r.begin(), r.end());
+      printf("mode=%d G=%3d S=%2d CH=%5d  %5lld MB: %6.0f GB/s  (%.2f us)\n", mode, c.G, c.S, c.CH, B >> 20, r[2],
+             (double)B / r[2] * 1e-3);
+    }
+  }
+  printf("status %s\n", cudaGetErrorString(cudaGetLastError()));
+  return 0;
+}

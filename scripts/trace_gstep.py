@@ -25,7 +25,9 @@ r = D.Router(*[x.to(dev) for x in S.router(C.d, C.h_r, C.M, 1, "bf16")])
 steps = [D.DraftStep(c, r, 1, C.k_t) for _ in range(C.positions)]
 G = torch.cuda.get_device_properties(0).multi_processor_count
 bufs = [torch.zeros(G * 64, dtype=torch.int64, device=dev) for _ in range(C.positions)]
-flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from bench import L2Flush  # noqa: E402
+flush = L2Flush(dev)
 names = ["start", "pdl", "L1pub", "a_in", "layer2", "mask", "streamed", "record", "recs_in", "out", "M:fields", "M:cands",
          "-", "tk:thr", "tk:surv", "M:issued"]
 inp = [[x.to(dev) for x in S.step_inputs(1, C.d, t, "bf16")] for t in range(C.positions)]
@@ -98,6 +100,12 @@ for t in range(C.positions):
     m0 = int(np.argmax(a[:, 9]))
     mseq = [7, 15, 8, 10, 11, 9]
     print("  merger CTA cycles:", {f"{names[i]}->{names[j]}": int(cy[m0, j] - cy[m0, i]) for i, j in zip(mseq, mseq[1:])})
+    ok2 = (a[:, 5] > 0) & (a[:, 12] > 0) & (a[:, 18] > 0)
+    if ok2.any():
+        q = lambda v: np.round(1e-3 * np.percentile(v, [0, 50, 90, 100]), 2)
+        print("  per CTA (us, p0/p50/p90/max): mask->1st landed", q(a[ok2, 12] - a[ok2, 5]),
+              "| mask->last issued", q(a[ok2, 18] - a[ok2, 5]), "| mask->streamed", q(a[ok2, 6] - a[ok2, 5]),
+              "| mask skew", q(a[ok2, 5] - a[ok2, 5].min()))
     st0, st1 = a[:, 5][a[:, 5] > 0].min(), a[:, 6][a[:, 6] > 0].max()
     print(f"  streaming: {rows * C.d * 2 / (st1 - st0):.0f} GB/s over [first mask, last streamed]")
     t_prev_end = a[:, 9][a[:, 9] > 0].max()

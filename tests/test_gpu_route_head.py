@@ -1,0 +1,102 @@
+"""NEXT-2 split of one draft step through the C ABI: dynaspec_step_route
+(router + TopK + offsets, Alg. 1 line 8) on a side stream S_m while a stand-in drafter core runs on
+S_d, the event join ("sync S_m, S_d", Alg. 1 line 10), then dynaspec_step_head (gathered head +
+log-softmax + top-k_t, lines 10-11) on S_d -- compared with the oracle's draft step."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import dynaspec_oracle as O
+from synth import inputs as S
+from tests.parity import Rows, check_topk, f64, score_tol, selection_certified
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda"
+
+
+def _run_split(Dy, st, hp, e, hn, t, k_max, k_min):
+    """route on S_m || a core stand-in on S_d (it writes h_new), join, head on S_d."""
+    cur = torch.cuda.current_stream()
+    s_meta = torch.cuda.Stream()
+    ev_f, ev_j = torch.cuda.Event(), torch.cuda.Event()
+    h_new = torch.empty_like(hn)
+    ev_f.record(cur)
+    s_meta.wait_event(ev_f)
+    st.route(hp, e, t, k_max, k_min, s_meta)
+    h_new.copy_(hn * 1.0)          # the caller's drafter core on S_d produces the head input
+    ev_j.record(s_meta)
+    cur.wait_event(ev_j)
+    st.head(h_new, t, k_max, k_min, cur)
+
+
+@pytest.mark.parametrize("dtype,shared,B", [("bf16", False, 1), ("f32", False, 1), ("bf16", False, 3),
+                                            ("bf16", True, 3)])
+def test_route_head_exact_regime(dtype, shared, B):
+    """Exact regime (every fp32 sum exact): scores, selection, offsets, every logit and the top-k
+    are bit-exact against the oracle."""
+    from paper_2510_13847_b200 import dynaspec as Dy
+    V, d, M, h_r, k_t = 5003, 256, 24, 16, 8
+    W = S.lm_head(V, d, 0, dtype, "exact")
+    rt = S.router(d, h_r, M, 1, dtype, "exact")
+    tau = S.random_partition(V, M, 2)
+    perm, off = O.layout(tau, M)
+    part = {"perm": perm, "offsets": off}
+    c = Dy.Clusters.from_tau(W.to(DEV), torch.as_tensor(tau, dtype=torch.int32, device=DEV), M)
+    r = Dy.Router(*[x.to(DEV) for x in rt])
+    st = Dy.DraftStep(c, r, B, k_t, shared=shared, z_out=True)
+    Wo, ro = Rows(W), tuple(f64(x) for x in rt)
+    for t in range(4):
+        hp, e, hn = S.step_inputs(B, d, t, dtype, "exact", h_r=h_r)
+        _run_split(Dy, st, hp.to(DEV), e.to(DEV), hn.to(DEV), t, 8, 2)
+        torch.cuda.synchronize()
+        ref = O.draft_step(part, ro, Wo, f64(hp), f64(e), f64(hn), t, 8, 2, k_t, shared=shared)
+        sc = st.scores.cpu().numpy()
+        for b in range(B):
+            assert np.array_equal(sc[b], ref[b]["scores"].astype(np.float32))
+        for b in range(1 if shared else B):
+            cnt = st.sel_count[b].item()
+            assert st.sel[b, :cnt].cpu().tolist() == ref[b]["sel"].tolist()
+            assert st.sl_offsets[b, :cnt + 1].cpu().tolist() == ref[b]["sl_offsets"].tolist()
+        for b in range(B):
+            n = len(ref[b]["V_S"])
+            assert np.array_equal(st.z[b, :n].cpu().numpy(), ref[b]["z"].astype(np.float32))
+            check_topk(st.top_ids[b].cpu().numpy(), st.top_logits[b].cpu().numpy(), st.top_logp[b].cpu().numpy(),
+                       st.lse[b].item(), ref[b]["z"], ref[b]["V_S"], k_t, torch.float32, exact=True)
+
+
+@pytest.mark.parametrize("B", [1, 4])
+def test_route_head_llama3_random(B):
+    """Llama-3 head at full size (V 128256, d 4096, M 256, bf16), random regime, the bench's
+    NEXT-2 launch configuration: scores within 1e-5 rms, selections bit-exact when certified,
+    every shortlist logit within 2e-2, top-k valid."""
+    from paper_2510_13847_b200 import dynaspec as Dy
+    C = S.CONFIGS["llama3"]
+    W = S.lm_head(C.V, C.d, 0, "bf16")
+    rt = S.router(C.d, C.h_r, C.M, 1, "bf16")
+    tau = S.random_partition(C.V, C.M, 2)
+    perm, off = O.layout(tau, C.M)
+    part = {"perm": perm, "offsets": off}
+    c = Dy.Clusters.from_tau(W.to(DEV), torch.as_tensor(tau, dtype=torch.int32, device=DEV), C.M)
+    r = Dy.Router(*[x.to(DEV) for x in rt])
+    st = Dy.DraftStep(c, r, B, C.k_t, z_out=True)
+    Wo, ro = Rows(W), tuple(f64(x) for x in rt)
+    for t in (0, 3):
+        hp, e, hn = S.step_inputs(B, C.d, t, "bf16")
+        _run_split(Dy, st, hp.to(DEV), e.to(DEV), hn.to(DEV), t, C.k_max, C.k_min)
+        torch.cuda.synchronize()
+        ref = O.draft_step(part, ro, Wo, f64(hp), f64(e), f64(hn), t, C.k_max, C.k_min, C.k_t)
+        for b in range(B):
+            rb = ref[b]
+            assert np.max(np.abs(st.scores[b].cpu().numpy() - rb["scores"])) <= score_tol(rb["scores"])
+            cnt = st.sel_count[b].item()
+            sel = st.sel[b, :cnt].cpu().numpy()
+            if selection_certified(rb["scores"], rb["k"]):
+                assert sel.tolist() == rb["sel"].tolist()
+            else:
+                rb = O.draft_step(part, ro, Wo, f64(hp[b:b + 1]), f64(e[b:b + 1]), f64(hn[b:b + 1]), t, C.k_max,
+                                  C.k_min, C.k_t, sel_override=[sel])[0]
+            assert st.sl_offsets[b, :cnt + 1].cpu().tolist() == rb["sl_offsets"].tolist()
+            n = len(rb["V_S"])
+            assert np.max(np.abs(st.z[b, :n].cpu().numpy().astype(np.float64) - rb["z"])) <= 2e-2
+            check_topk(st.top_ids[b].cpu().numpy(), st.top_logits[b].cpu().numpy(), st.top_logp[b].cpu().numpy(),
+                       st.lse[b].item(), rb["z"], rb["V_S"], C.k_t, torch.bfloat16)
