@@ -41,6 +41,16 @@ bool use_tc_batched(const ds_clusters* c, int B, int k_t, int shared, bool z_out
   return !shared && !z_out && c->dtype == DS_BF16 && B >= 8 && tc_batched_supported(c, B, k_t);
 }
 
+// Many independent rows in bf16: the grouped cluster-major head (gh.cu) reads every selected cluster
+// block once for all the rows that chose it.  DS_GH_MIN_ROWS (default 8) is the smallest batch.
+bool use_gh(const ds_clusters* c, int B, int k_t, int shared, bool z_out, int kmax) {
+  const char* off = getenv("DS_DISABLE_TC");
+  if (off && off[0] == '1') return false;
+  const char* mr = getenv("DS_GH_MIN_ROWS");
+  const int min_rows = mr && mr[0] ? atoi(mr) : 8;
+  return !shared && !z_out && c->dtype == DS_BF16 && B >= std::max(2, min_rows) && gh_supported(c, B, k_t, kmax);
+}
+
 static bool dtype_ok(int dt) { return dt == DS_BF16 || dt == DS_F32; }
 
 static ds_status check_clusters(const ds_clusters* c) {
@@ -222,7 +232,9 @@ ds_status dynaspec_select(const float* scores, int32_t B, const ds_clusters* c, 
 // Head scratch for B rows: the largest of the head kernels' partials (the single-row step kernels'
 // records live in the fixed prefix, internal.h).
 static size_t head_scratch(const ds_clusters* c, int32_t B, int32_t k_t, const HeadPlan& pmax) {
-  return std::max(std::max(pmax.part_bytes, tc_head_part_bytes(c, B, k_t)), tc_batched_ws_bytes(c, B, k_t));
+  const size_t gh = gh_supported(c, B, k_t, c->M) ? gh_ws_bytes(c, B, k_t, c->M) : 0;
+  return std::max(std::max(std::max(pmax.part_bytes, tc_head_part_bytes(c, B, k_t)), tc_batched_ws_bytes(c, B, k_t)),
+                  gh);
 }
 
 size_t dynaspec_head_forward_ws(const ds_clusters* c, int32_t B, int32_t k_t) {
@@ -251,7 +263,11 @@ ds_status dynaspec_head_forward(const ds_clusters* c, const void* h_new, int32_t
   if (!ws || ws_bytes < L.total) return DS_ERR_WORKSPACE;
   uint8_t* w8 = static_cast<uint8_t*>(ws);
   cudaError_t err;
-  if (use_tc_batched(c, B, k_t, shared, z_out != nullptr)) {
+  if (use_gh(c, B, k_t, shared, z_out != nullptr, c->M)) {
+    if (ws_bytes < ws_layout(0, gh_ws_bytes(c, B, k_t, c->M)).total) return DS_ERR_WORKSPACE;
+    err = launch_gh(c, h_new, B, sel, sel_count, k_t, c->M, top_ids, top_logits, top_logp, lse, w8 + L.head,
+                    (cudaStream_t)stream);
+  } else if (use_tc_batched(c, B, k_t, shared, z_out != nullptr)) {
     if (ws_bytes < ws_layout(0, tc_batched_ws_bytes(c, B, k_t)).total) return DS_ERR_WORKSPACE;
     err = launch_tc_batched(c, h_new, B, sel, sel_count, k_t, top_ids, top_logits, top_logp, lse, w8 + L.head,
                             reinterpret_cast<unsigned*>(w8 + L.counters), (cudaStream_t)stream);
@@ -434,6 +450,7 @@ int32_t dynaspec_draft_step_launches(const ds_clusters* c, const ds_router* r, i
   if (!c || !r || !head_plan(c, B, k_t, 0, &p)) return 0;
   const int64_t ms = shared ? c->V : 0;
   if (use_tc_head(c, B, k_t, shared, ms)) return 3;  // meta layer 1, meta layer 2 (+union), tcgen05 head
+  if (use_gh(c, B, k_t, shared, false, c->M)) return 5;  // meta x2, group, grouped tcgen05 head, merge
   if (use_tc_batched(c, B, k_t, shared, false))
     return 2 + 2 * ((B + 127) / 128);  // meta x2, then (union + tcgen05 head) per 128 rows
   if (!two_streams && step_supported(c, r, B, k_t, shared, 0)) return 1;  // fused single-stream step
@@ -446,6 +463,8 @@ const char* dynaspec_draft_step_kernel(const ds_clusters* c, const ds_router* r,
   if (!c || !r || !head_plan(c, B, k_t, 0, &p)) return "?";
   const int64_t ms = shared ? c->V : 0;
   if (use_tc_head(c, B, k_t, shared, ms)) return "ds::tc_head_kernel (tcgen05, shared shortlist)";
+  if (use_gh(c, B, k_t, shared, false, c->M))
+    return "ds::gh_head_kernel (tcgen05 grouped head: every selected cluster block once for the rows that chose it)";
   if (use_tc_batched(c, B, k_t, shared, false)) return "ds::tc_head_kernel (tcgen05, batched rows over the union)";
   if (!two_streams && step_supported(c, r, B, k_t, shared, 0)) {
     if (gstep_supported(c, r, B, k_t, shared))
@@ -482,8 +501,10 @@ ds_status dynaspec_draft_step(const ds_clusters* c, const ds_router* r, const vo
   const bool two_streams = s_meta != nullptr && s_meta != s_draft;
   if (two_streams && (!ev_fork || !ev_join)) return DS_ERR_SHAPE;
   const bool tc = use_tc_head(c, B, k_t, shared, ms);
-  const bool tcb = !tc && use_tc_batched(c, B, k_t, shared, out->z_out != nullptr);
-  const bool fused = !tc && !tcb && !two_streams && step_supported(c, r, B, k_t, shared, ms);
+  // supported-ness with kmax = M (what dynaspec_draft_step_ws sized the workspace for); launched with k
+  const bool gh = !tc && use_gh(c, B, k_t, shared, out->z_out != nullptr, c->M);
+  const bool tcb = !tc && !gh && use_tc_batched(c, B, k_t, shared, out->z_out != nullptr);
+  const bool fused = !tc && !tcb && !gh && !two_streams && step_supported(c, r, B, k_t, shared, ms);
   if (fused) {  // one persistent launch: router + select + head + epilogue (step.cu)
     const size_t need = step_ws_bytes(c, r, B, k_t);
     if (!ws || need == 0 || ws_bytes < need) return DS_ERR_WORKSPACE;
@@ -511,6 +532,9 @@ ds_status dynaspec_draft_step(const ds_clusters* c, const ds_router* r, const vo
   if (tc && ws_bytes < ws_layout(align_up(meta_bytes, 256) + align_up(score_bytes, 256),
                                  tc_head_part_bytes(c, B, k_t)).total)
     return DS_ERR_WORKSPACE;
+  if (gh && ws_bytes < ws_layout(align_up(meta_bytes, 256) + align_up(score_bytes, 256),
+                                 gh_ws_bytes(c, B, k_t, k)).total)
+    return DS_ERR_WORKSPACE;
   if (tcb && ws_bytes < ws_layout(align_up(meta_bytes, 256) + align_up(score_bytes, 256),
                                   tc_batched_ws_bytes(c, B, k_t)).total)
     return DS_ERR_WORKSPACE;  // checked before anything is enqueued
@@ -537,7 +561,10 @@ ds_status dynaspec_draft_step(const ds_clusters* c, const ds_router* r, const vo
   cudaStreamIsCapturing(sd, &cap);
   const unsigned evflags = cap == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : cudaEventRecordDefault;
   if (head_begin && cudaEventRecordWithFlags((cudaEvent_t)head_begin, sd, evflags) != cudaSuccess) return DS_ERR_CUDA;
-  if (tcb) {
+  if (gh) {
+    err = launch_gh(c, h_new, B, out->sel, out->sel_count, k_t, k, out->top_ids, out->top_logits, out->top_logp,
+                    out->lse, w8 + L.head, sd);
+  } else if (tcb) {
     err = launch_tc_batched(c, h_new, B, out->sel, out->sel_count, k_t, out->top_ids, out->top_logits,
                             out->top_logp, out->lse, w8 + L.head, counters, sd);
   } else if (tc) {

@@ -122,6 +122,13 @@ cudaError_t launch_tc_batched(const ds_clusters* c, const void* h_new, int B, co
                               const int32_t* sel_count, int k_t, int32_t* top_ids, float* top_logits,
                               float* top_logp, float* lse, void* ws, unsigned* counter, cudaStream_t st);
 bool use_tc_batched(const ds_clusters* c, int B, int k_t, int shared, bool z_out);
+// ---- grouped (cluster-major) tcgen05 head for many independent rows (gh.cu)
+bool gh_supported(const ds_clusters* c, int B, int k_t, int kmax);
+size_t gh_ws_bytes(const ds_clusters* c, int B, int k_t, int kmax);
+cudaError_t launch_gh(const ds_clusters* c, const void* h_new, int B, const int32_t* sel, const int32_t* sel_count,
+                      int k_t, int kmax, int32_t* top_ids, float* top_logits, float* top_logp, float* lse, void* ws,
+                      cudaStream_t st);
+bool use_gh(const ds_clusters* c, int B, int k_t, int shared, bool z_out, int kmax);
 
 // ---- cluster sharding (shard.cu)
 cudaError_t launch_restrict(const int32_t* sel, const int32_t* cnt, int rows, int M, const int32_t* offsets, int m_lo,

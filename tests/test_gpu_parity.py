@@ -493,15 +493,17 @@ def test_tc_batched_per_row_exact(B, monkeypatch):
     assert torch.equal(outs["tc"]["top_logits"], outs["cuda"]["top_logits"])
 
 
-def test_tc_batched_draft_step_llama3_b16(monkeypatch):
-    """Draft step at Llama-3 size with 16 independent rows (batched tcgen05 path) vs the oracle."""
+@pytest.mark.parametrize("gh", ["1", "0"])  # grouped cluster-major head (gh.cu) / union-batched tc_head
+def test_tc_batched_draft_step_llama3_b16(gh, monkeypatch):
+    """Draft step at Llama-3 size with 16 independent rows (tcgen05 paths) vs the oracle."""
     Dy = _dyn()
     monkeypatch.setenv("DS_DISABLE_TC", "0")
+    monkeypatch.setenv("DS_GH", gh)
     C = S.CONFIGS["llama3"]
     B = 16
     W, rt, tau, part, c, r = _setup(C.V, C.d, C.M, C.h_r, "bf16", "random")
     st = Dy.DraftStep(c, r, B, C.k_t)
-    assert st.launches == 4
+    assert st.launches == (5 if gh == "1" else 4)
     hp, e, hn = S.step_inputs(B, C.d, 2, "bf16")
     st(hp.to(DEV), e.to(DEV), hn.to(DEV), t=2, k_max=C.k_max, k_min=C.k_min)
     torch.cuda.synchronize()
