@@ -272,15 +272,16 @@ ds_status dynaspec_step_head(const ds_clusters* c, const void* h_new, int32_t B,
                              size_t ws_bytes, ds_stream_t s_draft);
 
 /* Number of kernel launches one dynaspec_draft_step enqueues (for launch accounting):
- * 1 for the fused single-stream step, 2 + head chunks for the two-stream path. */
+ * 1 for the fused single-stream step, 2 + head chunks for the two-stream path, 5 for the grouped
+ * tcgen05 head (router x2, grouping, head, merge).  z_out: whether the call passes out->z_out. */
 int32_t dynaspec_draft_step_launches(const ds_clusters* c, const ds_router* r, int32_t B, int32_t k_t,
-                                     int32_t shared, int32_t two_streams);
+                                     int32_t shared, int32_t two_streams, int32_t z_out);
 
 /* Name of the dominant kernel one dynaspec_draft_step runs for this shape (for measurement
  * bookkeeping: the kernel a roofline is quoted on).  Static string, never NULL ("?" on bad
  * arguments).  Assumes 16-byte aligned inputs (the unaligned fallbacks are not named). */
 const char* dynaspec_draft_step_kernel(const ds_clusters* c, const ds_router* r, int32_t B, int32_t k_t,
-                                       int32_t shared, int32_t two_streams);
+                                       int32_t shared, int32_t two_streams, int32_t z_out);
 
 /* ---------------------------------------------------------------- draft tree (Alg. 1 lines 12-18) */
 

@@ -48,7 +48,8 @@ bool use_gh(const ds_clusters* c, int B, int k_t, int shared, bool z_out, int km
   if (off && off[0] == '1') return false;
   const char* mr = getenv("DS_GH_MIN_ROWS");
   const int min_rows = mr && mr[0] ? atoi(mr) : 8;
-  return !shared && !z_out && c->dtype == DS_BF16 && B >= std::max(2, min_rows) && gh_supported(c, B, k_t, kmax);
+  // shared (tree) mode: every row streams the one union shortlist, >= 2 rows
+  return !z_out && c->dtype == DS_BF16 && B >= (shared ? 2 : std::max(2, min_rows)) && gh_supported(c, B, k_t, kmax);
 }
 
 static bool dtype_ok(int dt) { return dt == DS_BF16 || dt == DS_F32; }
@@ -263,9 +264,9 @@ ds_status dynaspec_head_forward(const ds_clusters* c, const void* h_new, int32_t
   if (!ws || ws_bytes < L.total) return DS_ERR_WORKSPACE;
   uint8_t* w8 = static_cast<uint8_t*>(ws);
   cudaError_t err;
-  if (use_gh(c, B, k_t, shared, z_out != nullptr, c->M)) {
+  if (!use_tc_head(c, B, k_t, shared, max_shortlist) && use_gh(c, B, k_t, shared, z_out != nullptr, c->M)) {
     if (ws_bytes < ws_layout(0, gh_ws_bytes(c, B, k_t, c->M)).total) return DS_ERR_WORKSPACE;
-    err = launch_gh(c, h_new, B, sel, sel_count, k_t, c->M, top_ids, top_logits, top_logp, lse, w8 + L.head,
+    err = launch_gh(c, h_new, B, sel, sel_count, shared, k_t, c->M, top_ids, top_logits, top_logp, lse, w8 + L.head,
                     (cudaStream_t)stream);
   } else if (use_tc_batched(c, B, k_t, shared, z_out != nullptr)) {
     if (ws_bytes < ws_layout(0, tc_batched_ws_bytes(c, B, k_t)).total) return DS_ERR_WORKSPACE;
@@ -445,27 +446,28 @@ size_t dynaspec_draft_step_ws(const ds_clusters* c, const ds_router* r, int32_t 
 }
 
 int32_t dynaspec_draft_step_launches(const ds_clusters* c, const ds_router* r, int32_t B, int32_t k_t,
-                                     int32_t shared, int32_t two_streams) {
+                                     int32_t shared, int32_t two_streams, int32_t z_out) {
   HeadPlan p;
   if (!c || !r || !head_plan(c, B, k_t, 0, &p)) return 0;
   const int64_t ms = shared ? c->V : 0;
   if (use_tc_head(c, B, k_t, shared, ms)) return 3;  // meta layer 1, meta layer 2 (+union), tcgen05 head
-  if (use_gh(c, B, k_t, shared, false, c->M)) return 5;  // meta x2, group, grouped tcgen05 head, merge
-  if (use_tc_batched(c, B, k_t, shared, false))
+  if (use_gh(c, B, k_t, shared, z_out != 0, c->M)) return 5;  // meta x2, group, grouped tcgen05 head, merge
+  if (use_tc_batched(c, B, k_t, shared, z_out != 0))
     return 2 + 2 * ((B + 127) / 128);  // meta x2, then (union + tcgen05 head) per 128 rows
   if (!two_streams && step_supported(c, r, B, k_t, shared, 0)) return 1;  // fused single-stream step
   return 2 + p.launches;  // meta layer 1, meta layer 2 (+select), head chunks
 }
 
 const char* dynaspec_draft_step_kernel(const ds_clusters* c, const ds_router* r, int32_t B, int32_t k_t,
-                                       int32_t shared, int32_t two_streams) {
+                                       int32_t shared, int32_t two_streams, int32_t z_out) {
   HeadPlan p;
   if (!c || !r || !head_plan(c, B, k_t, 0, &p)) return "?";
   const int64_t ms = shared ? c->V : 0;
   if (use_tc_head(c, B, k_t, shared, ms)) return "ds::tc_head_kernel (tcgen05, shared shortlist)";
-  if (use_gh(c, B, k_t, shared, false, c->M))
+  if (use_gh(c, B, k_t, shared, z_out != 0, c->M))
     return "ds::gh_head_kernel (tcgen05 grouped head: every selected cluster block once for the rows that chose it)";
-  if (use_tc_batched(c, B, k_t, shared, false)) return "ds::tc_head_kernel (tcgen05, batched rows over the union)";
+  if (use_tc_batched(c, B, k_t, shared, z_out != 0))
+    return "ds::tc_head_kernel (tcgen05, batched rows over the union)";
   if (!two_streams && step_supported(c, r, B, k_t, shared, 0)) {
     if (gstep_supported(c, r, B, k_t, shared))
       return "ds::gstep_kernel (grid step: router units over all CTAs + select + gathered head + epilogue, one launch)";
@@ -500,8 +502,10 @@ ds_status dynaspec_draft_step(const ds_clusters* c, const ds_router* r, const vo
   if (out->z_out && out->z_stride < ms) return DS_ERR_SHAPE;
   const bool two_streams = s_meta != nullptr && s_meta != s_draft;
   if (two_streams && (!ev_fork || !ev_join)) return DS_ERR_SHAPE;
+  // tree rows (shared): the shared-shortlist tcgen05 head (Qwen tree 90 vs 127 us per step with the
+  // grouped head, whose router / grouping / merge launches dominate at 10 rows); independent rows: the
+  // grouped head.  Supported-ness with kmax = M (what dynaspec_draft_step_ws sized the workspace for).
   const bool tc = use_tc_head(c, B, k_t, shared, ms);
-  // supported-ness with kmax = M (what dynaspec_draft_step_ws sized the workspace for); launched with k
   const bool gh = !tc && use_gh(c, B, k_t, shared, out->z_out != nullptr, c->M);
   const bool tcb = !tc && !gh && use_tc_batched(c, B, k_t, shared, out->z_out != nullptr);
   const bool fused = !tc && !tcb && !gh && !two_streams && step_supported(c, r, B, k_t, shared, ms);
@@ -562,7 +566,9 @@ ds_status dynaspec_draft_step(const ds_clusters* c, const ds_router* r, const vo
   const unsigned evflags = cap == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : cudaEventRecordDefault;
   if (head_begin && cudaEventRecordWithFlags((cudaEvent_t)head_begin, sd, evflags) != cudaSuccess) return DS_ERR_CUDA;
   if (gh) {
-    err = launch_gh(c, h_new, B, out->sel, out->sel_count, k_t, k, out->top_ids, out->top_logits, out->top_logp,
+    // shared (tree) mode: the union of the rows' k clusters has up to min(M, B k) clusters
+    const int kmax = shared ? (int)std::min<int64_t>(c->M, (int64_t)B * k) : k;
+    err = launch_gh(c, h_new, B, out->sel, out->sel_count, shared, k_t, kmax, out->top_ids, out->top_logits, out->top_logp,
                     out->lse, w8 + L.head, sd);
   } else if (tcb) {
     err = launch_tc_batched(c, h_new, B, out->sel, out->sel_count, k_t, out->top_ids, out->top_logits,

@@ -95,34 +95,81 @@ __device__ __forceinline__ void cp_async_wait() {
 }
 
 // ---------------------------------------------------------------------------- grouping
-// One CTA.  cnt_m = #rows that selected cluster m; CSR of (cluster -> rows); per-row record slots:
-// row b's records are [rowoff[b], rowoff[b + 1]) with, for its i-th selected cluster m_i, the
-// nparts(m_i) = ceil(|C_m| / 256) records of that cluster at rowoff[b] + sum_{i' < i} nparts(m_i').
+// One CTA.  The rows' selections are staged in shared memory (one coalesced pass; every later pass
+// reads them on chip), then: cnt_m = #rows that selected cluster m; the vocabulary tile T (256, or
+// 128 / 64 when the union is too small to give every SM two items); CSR of (cluster -> rows); per-row
+// record slots: row b's records are [rowoff[b], rowoff[b + 1]) with, for its i-th selected cluster
+// m_i, the nparts(m_i) = ceil(|C_m| / T) records of that cluster at rowoff[b] + sum_{i' < i} nparts.
+constexpr int kGhStageMax = 40 * 1024;  // staged selection entries (160 KB); larger batches read L2
+
 __global__ void __launch_bounds__(1024) gh_group_kernel(const int32_t* __restrict__ sel,
                                                         const int32_t* __restrict__ cnt, int B, int M,
+                                                        int shared, int kmax, int G,
                                                         const int32_t* __restrict__ offsets, int32_t* grp_rows,
                                                         int32_t* grp_rec, int32_t* rowoff, int4* items,
                                                         int32_t* nitems) {
-  __shared__ int cm[kGhMaxM], go[kGhMaxM + 1], cur[kGhMaxM], np[kGhMaxM], io[kGhMaxM + 1];
+  extern __shared__ __align__(16) int32_t stg[];  // [nsel rows][kmax] staged selections (when they fit)
+  __shared__ int cm[kGhMaxM], go[kGhMaxM + 1], cur[kGhMaxM], np[kGhMaxM], io[kGhMaxM + 1], csz[kGhMaxM];
   __shared__ int wsum[32];
+  __shared__ int red[3], tsel;
   pdl_wait();                // the selections come from the router kernel
   pdl_launch_dependents();   // the head kernel may run its prologue
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  const int nrows_sel = shared ? 1 : B;
+  const bool staged = (int64_t)nrows_sel * kmax <= kGhStageMax;
   for (int m = tid; m < M; m += blockDim.x) {
     cm[m] = 0;
     cur[m] = 0;
-    np[m] = (__ldg(offsets + m + 1) - __ldg(offsets + m) + kGhVoc - 1) / kGhVoc;
+    csz[m] = __ldg(offsets + m + 1) - __ldg(offsets + m);
+  }
+  if (tid < 3) red[tid] = 0;
+  if (staged) {
+#pragma unroll 4
+    for (int e = tid; e < nrows_sel * kmax; e += blockDim.x) {
+      const int r = e / kmax, i = e - r * kmax;
+      stg[e] = i < __ldg(cnt + r) ? __ldg(sel + (size_t)r * M + i) : -1;
+    }
   }
   __syncthreads();
-  // counts (warp per row) and each row's record count
-  for (int b = warp; b < B; b += nw) {
-    const int n = __ldg(cnt + b);
-    int nr = 0;
-    for (int i = lane; i < n; i += 32) {
-      const int m = __ldg(sel + (size_t)b * M + i);
-      atomicAdd(&cm[m], 1);
-      nr += np[m];
+  auto sel_at = [&](int r, int i) { return staged ? stg[r * kmax + i] : __ldg(sel + (size_t)r * M + i); };
+  // cluster counts: a shared selection is every row's (n_m = B for each union cluster)
+  if (shared) {
+    const int n = __ldg(cnt);
+    for (int i = tid; i < n; i += blockDim.x) cm[sel_at(0, i)] = B;
+  } else {
+    for (int b = warp; b < B; b += nw) {
+      const int n = __ldg(cnt + b);
+      for (int i = lane; i < n; i += 32) atomicAdd(&cm[sel_at(b, i)], 1);
     }
+  }
+  __syncthreads();
+  // vocabulary tile: the largest T in {256, 128, 64} giving >= 2 items per SM
+  {
+    int it[3] = {0, 0, 0};
+    for (int m = tid; m < M; m += blockDim.x)
+      if (cm[m] > 0) {
+        const int rb = (cm[m] + kGhRows - 1) / kGhRows;
+#pragma unroll
+        for (int j = 0; j < 3; ++j) it[j] += rb * ((csz[m] + (kGhVoc >> j) - 1) / (kGhVoc >> j));
+      }
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      const int v = (int)__reduce_add_sync(0xffffffffu, (unsigned)it[j]);
+      if (lane == 0 && v) atomicAdd(&red[j], v);
+    }
+  }
+  __syncthreads();
+  if (tid == 0) tsel = red[0] >= 2 * G ? kGhVoc : red[1] >= 2 * G ? kGhVoc / 2 : kGhVoc / 4;
+  __syncthreads();
+  const int T = tsel;
+  for (int m = tid; m < M; m += blockDim.x) np[m] = (csz[m] + T - 1) / T;
+  __syncthreads();
+  // each row's record count
+  for (int b = warp; b < B; b += nw) {
+    const int sb = shared ? 0 : b;
+    const int n = __ldg(cnt + sb);
+    int nr = 0;
+    for (int i = lane; i < n; i += 32) nr += np[sel_at(sb, i)];
     nr = (int)__reduce_add_sync(0xffffffffu, (unsigned)nr);
     if (lane == 0) rowoff[b + 1] = nr;
   }
@@ -172,11 +219,12 @@ __global__ void __launch_bounds__(1024) gh_group_kernel(const int32_t* __restric
   __syncthreads();
   // fill: warp per row; lane i's record base = rowoff[b] + prefix of nparts over the row's clusters
   for (int b = warp; b < B; b += nw) {
-    const int n = __ldg(cnt + b);
+    const int sb = shared ? 0 : b;
+    const int n = __ldg(cnt + sb);
     int base = rowoff[b];
     for (int i0 = 0; i0 < n; i0 += 32) {
       const int i = i0 + lane;
-      const int m = i < n ? __ldg(sel + (size_t)b * M + i) : 0;
+      const int m = i < n ? sel_at(sb, i) : 0;
       const int p = i < n ? np[m] : 0;
       int x = p;
 #pragma unroll
@@ -185,7 +233,7 @@ __global__ void __launch_bounds__(1024) gh_group_kernel(const int32_t* __restric
         if (lane >= o) x += y;
       }
       if (i < n) {
-        const int pos = go[m] + atomicAdd(&cur[m], 1);
+        const int pos = go[m] + (shared ? b : atomicAdd(&cur[m], 1));
         grp_rows[pos] = b;
         grp_rec[pos] = base + x - p;
       }
@@ -196,12 +244,12 @@ __global__ void __launch_bounds__(1024) gh_group_kernel(const int32_t* __restric
   for (int m = tid; m < M; m += blockDim.x) {
     const int n = cm[m];
     if (n == 0) continue;
-    const int beg = __ldg(offsets + m), sz = __ldg(offsets + m + 1) - beg;
+    const int beg = __ldg(offsets + m), sz = csz[m];
     const int nrb = (n + kGhRows - 1) / kGhRows;
     int it = io[m];
     for (int p = 0; p < np[m]; ++p)
       for (int rb = 0; rb < nrb; ++rb)
-        items[it++] = make_int4(beg + p * kGhVoc, min(kGhVoc, sz - p * kGhVoc) | (p << 16), go[m] + rb * kGhRows,
+        items[it++] = make_int4(beg + p * T, min(T, sz - p * T) | (p << 16), go[m] + rb * kGhRows,
                                 min(kGhRows, n - rb * kGhRows));
   }
 }
@@ -493,10 +541,14 @@ struct GhWs {
 static GhWs gh_ws(const ds_clusters* c, int B, int k_t, int kmax) {
   GhWs w;
   const int64_t P = (c->max_size + kGhVoc - 1) / kGhVoc;
-  w.max_recs_per_row = std::min<int64_t>((int64_t)kmax * P, (int64_t)kmax + (c->V + kGhVoc - 1) / kGhVoc);
+  // T = 256: <= min(k P, k + V / 256); T < 256 is chosen only when the 2T items number < 2 G, so a row
+  // has < 4 G + M records then
+  w.max_recs_per_row = std::max(std::min<int64_t>((int64_t)kmax * P, (int64_t)kmax + (c->V + kGhVoc - 1) / kGhVoc),
+                                std::min<int64_t>((int64_t)4 * num_sms() + c->M, (int64_t)kmax * ((c->max_size + 63) / 64)));
   const int64_t pairs = (int64_t)B * kmax;
-  w.max_items = std::min<int64_t>((int64_t)c->M * P, (int64_t)c->M + (c->V + kGhVoc - 1) / kGhVoc) *
-                ((B + kGhRows - 1) / kGhRows);
+  w.max_items = std::max(std::min<int64_t>((int64_t)c->M * P, (int64_t)c->M + (c->V + kGhVoc - 1) / kGhVoc) *
+                             ((B + kGhRows - 1) / kGhRows),
+                         (int64_t)4 * num_sms() + 2 * c->M);
   size_t o = 0;
   auto take = [&](size_t bytes) {
     const size_t at = o;
@@ -547,7 +599,7 @@ static cudaError_t launch_gh_head_t(const GhMaps& maps, const GhArgs& a, cudaStr
 }
 
 cudaError_t launch_gh(const ds_clusters* c, const void* h_new, int B, const int32_t* sel, const int32_t* sel_count,
-                      int k_t, int kmax, int32_t* top_ids, float* top_logits, float* top_logp, float* lse, void* ws,
+                      int shared, int k_t, int kmax, int32_t* top_ids, float* top_logits, float* top_logp, float* lse, void* ws,
                       cudaStream_t st) {
   if (!gh_supported(c, B, k_t, kmax)) return cudaErrorInvalidValue;
   const GhWs w = gh_ws(c, B, k_t, kmax);
@@ -563,12 +615,20 @@ cudaError_t launch_gh(const ds_clusters* c, const void* h_new, int B, const int3
   pdl[0].val.programmaticStreamSerializationAllowed = 1;
   {
     cudaLaunchConfig_t cfg = {};
+    const int nrs = shared ? 1 : B;
+    const size_t stg = (int64_t)nrs * kmax <= kGhStageMax ? (size_t)nrs * kmax * 4 : 0;
+    if (stg > 16 * 1024) {  // static arrays (~25 KB) + staged selections above the 48 KB default: opt in
+      cudaError_t e0 = cudaFuncSetAttribute(gh_group_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)stg);
+      if (e0 != cudaSuccess) return e0;
+    }
     cfg.gridDim = dim3(1);
     cfg.blockDim = dim3(1024);
+    cfg.dynamicSmemBytes = stg;
     cfg.stream = st;
     cfg.attrs = pdl;
     cfg.numAttrs = 1;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, gh_group_kernel, sel, sel_count, B, c->M, (const int32_t*)c->offsets,
+    cudaError_t e = cudaLaunchKernelEx(&cfg, gh_group_kernel, sel, sel_count, B, c->M, shared ? 1 : 0, kmax,
+                                       num_sms(), (const int32_t*)c->offsets,
                                        grp_rows, grp_rec, rowoff, items, nitems);
     if (e != cudaSuccess) return e;
   }

@@ -31,8 +31,13 @@ struct MetaPlan {
   int KS;       // number of K splits
   int rows1;    // layer-1 output rows (h_r, or M for a linear router)
   int RB;       // rows per layer-1 CTA (grid z = ceil(B / RB) row blocks)
+  int tc;       // 1: layer 1 on tcgen05 (meta_tc.cu), KS_tc splits of kc_per_tc 64-wide chunks
+  int KS_tc, kc_per_tc;
   size_t part_bytes;
 };
+bool meta_tc_plan(const ds_router* r, int B, int* KS, int* kc_per);
+cudaError_t launch_meta_tc_l1(const ds_router* r, const void* h_prev, const void* e, int B, float* part, int KS,
+                              int kc_per, cudaStream_t st, bool pdl);
 MetaPlan meta_plan(const ds_router* r, int B);
 // Enqueue layer 1 (split-K partials) and layer 2 + (optionally) selection.
 // sel == nullptr => scores only.
@@ -126,7 +131,7 @@ bool use_tc_batched(const ds_clusters* c, int B, int k_t, int shared, bool z_out
 bool gh_supported(const ds_clusters* c, int B, int k_t, int kmax);
 size_t gh_ws_bytes(const ds_clusters* c, int B, int k_t, int kmax);
 cudaError_t launch_gh(const ds_clusters* c, const void* h_new, int B, const int32_t* sel, const int32_t* sel_count,
-                      int k_t, int kmax, int32_t* top_ids, float* top_logits, float* top_logp, float* lse, void* ws,
+                      int shared, int k_t, int kmax, int32_t* top_ids, float* top_logits, float* top_logp, float* lse, void* ws,
                       cudaStream_t st);
 bool use_gh(const ds_clusters* c, int B, int k_t, int shared, bool z_out, int kmax);
 

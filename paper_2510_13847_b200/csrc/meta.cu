@@ -215,8 +215,14 @@ MetaPlan meta_plan(const ds_router* r, int B) {
   // rows per layer-1 CTA (x staging <= 96 KB); more rows -> more row blocks (grid z)
   p.RB = std::max(1, std::min(B, (int)((96 * 1024) / ((size_t)KC * esz))));
   p.KS = (dr + KC - 1) / KC;
+  // many bf16 rows: layer 1 on tcgen05 (meta_tc.cu) with its own split count
+  int ks_tc = 0, kcp = 0;
+  p.tc = meta_tc_plan(r, B, &ks_tc, &kcp) ? 1 : 0;
+  p.KS_tc = ks_tc;
+  p.kc_per_tc = kcp;
+  const int ks_max = std::max(p.KS, p.tc ? p.KS_tc : 0);
   // layer-1 partials, then (shared mode) the rows' TopK masks
-  p.part_bytes = (size_t)p.KS * B * p.rows1 * sizeof(float) + (size_t)B * (kMaxM / 32) * sizeof(uint32_t);
+  p.part_bytes = (size_t)ks_max * B * p.rows1 * sizeof(float) + (size_t)B * (kMaxM / 32) * sizeof(uint32_t);
   return p;
 }
 
@@ -235,6 +241,14 @@ static cudaError_t launch_meta_t(const ds_router* r, const void* h_prev, const v
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
 
+  int KS = p.KS;
+  const bool tc = p.tc && sizeof(T) == 2 && ((reinterpret_cast<uintptr_t>(h_prev) | reinterpret_cast<uintptr_t>(e) |
+                                              reinterpret_cast<uintptr_t>(r->W1)) & 15u) == 0;
+  if (tc) {
+    KS = p.KS_tc;
+    cudaError_t et = launch_meta_tc_l1(r, h_prev, e, B, part, p.KS_tc, p.kc_per_tc, st, pdl);
+    if (et != cudaSuccess) return et;
+  } else {
   cudaLaunchConfig_t c1 = {};
   c1.gridDim = dim3((p.rows1 + kMetaUnitsPerCTA - 1) / kMetaUnitsPerCTA, p.KS, (B + p.RB - 1) / p.RB);
   c1.blockDim = dim3(kMetaThreads);
@@ -246,13 +260,14 @@ static cudaError_t launch_meta_t(const ds_router* r, const void* h_prev, const v
                                        static_cast<const T*>(h_prev), static_cast<const T*>(e), B, r->d, p.rows1,
                                        p.KC, p.RB, part, pdl ? 1 : 0);
   if (err != cudaSuccess) return err;
+  }
   cudaLaunchConfig_t c2 = {};
   c2.gridDim = dim3(B);
   c2.blockDim = dim3(kMetaThreads);
   c2.stream = st;
   c2.attrs = attr;
   c2.numAttrs = 1;  // layer 2 always follows layer 1 in-stream
-  return cudaLaunchKernelEx(&c2, meta_l2_kernel<T>, (const float*)part, p.KS, B, p.rows1, r->b1,
+  return cudaLaunchKernelEx(&c2, meta_l2_kernel<T>, (const float*)part, KS, B, p.rows1, r->b1,
                             static_cast<const T*>(r->W2), r->b2, r->h_r, r->M, scores, offsets, k, k_per_row,
                             shared, sel, sel_count, sl_offsets, counter, 1);
 }

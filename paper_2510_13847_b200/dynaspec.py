@@ -95,9 +95,9 @@ def _load():
         "dynaspec_verify_chain": (c_int32, [P, c_int32, c_int64, c_int32, c_int32, P, P, c_int64, P, P, P, P, P, P,
                                             P, P, P, c_size_t, P]),
         "dynaspec_draft_step_launches": (c_int32, [POINTER(DsClusters), POINTER(DsRouter), c_int32, c_int32,
-                                                   c_int32, c_int32]),
+                                                   c_int32, c_int32, c_int32]),
         "dynaspec_draft_step_kernel": (ctypes.c_char_p, [POINTER(DsClusters), POINTER(DsRouter), c_int32, c_int32,
-                                                         c_int32, c_int32]),
+                                                         c_int32, c_int32, c_int32]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -447,9 +447,9 @@ class DraftStep:
         self.ev_fork = make_event() if two_streams else None
         self.ev_join = make_event() if two_streams else None
         self.launches = _lib.dynaspec_draft_step_launches(clusters.struct(), router.struct(), B, k_t, int(shared),
-                                                          int(two_streams))
+                                                          int(two_streams), int(bool(z_out)))
         self.kernel = _lib.dynaspec_draft_step_kernel(clusters.struct(), router.struct(), B, k_t, int(shared),
-                                                      int(two_streams)).decode()
+                                                      int(two_streams), int(bool(z_out))).decode()
 
     def __call__(self, h_prev, e, h_new, t, k_max, k_min, head_events=None, stream=None):
         sd = _stream(stream)

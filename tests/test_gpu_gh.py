@@ -141,3 +141,28 @@ def test_gh_full_size_sampled_rows(cfg, B, t):
         assert st.sl_offsets[b, :cnt + 1].cpu().tolist() == rb["sl_offsets"].tolist()
         check_topk(st.top_ids[b].cpu().numpy(), st.top_logits[b].cpu().numpy(), st.top_logp[b].cpu().numpy(),
                    st.lse[b].item(), rb["z"], rb["V_S"], C.k_t, torch.bfloat16)
+
+
+@pytest.mark.parametrize("B", [2, 3])
+def test_gh_shared_tree_rows_exact(B):
+    """Tree mode (R9: one index set for all rows of a depth) on the grouped head: every row streams
+    the one union selection; bit-exact top-k against the oracle over the union shortlist."""
+    Dy = _dyn()
+    V, d, M, k, k_t = 5003, 256, 24, 6, 8
+    W, tau, perm, off, c = _exact_setup(V, d, M)
+    hn = S.step_inputs(B, d, 2, "bf16", "exact")[2]
+    union = np.sort(np.random.default_rng(7).choice(M, size=k, replace=False)).astype(np.int32)
+    sel = np.zeros((1, M), dtype=np.int32)
+    sel[0, :k] = union
+    sl = np.zeros((1, M + 1), dtype=np.int32)
+    sl[0, :k + 1] = O.shortlist_offsets(union, off)
+    out = Dy.head_forward(c, hn.to(DEV), torch.as_tensor(sel, device=DEV),
+                          torch.tensor([k], dtype=torch.int32, device=DEV), torch.as_tensor(sl, device=DEV), k_t,
+                          shared=True)
+    torch.cuda.synchronize()
+    VS = O.shortlist(union, perm, off)
+    Wo = Rows(W)
+    for b in range(B):
+        z = O.head(f64(hn[b]), Wo, VS)[0]
+        check_topk(out["top_ids"][b].cpu().numpy(), out["top_logits"][b].cpu().numpy(),
+                   out["top_logp"][b].cpu().numpy(), out["lse"][b].item(), z, VS, k_t, torch.float32, exact=True)
