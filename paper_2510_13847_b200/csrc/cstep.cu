@@ -34,6 +34,21 @@ namespace ds {
 
 constexpr int kCStepMaxKt = 32;  // one list entry per lane
 
+// Poll a record word until it is non-zero.  Bounded: a record that has not landed 2 s after the merger
+// started (a CTA of this grid could not become resident, e.g. SMs held by a concurrent kernel) raises
+// DS_ERR_DEVICE_TIMEOUT in the workspace error word and returns a placeholder instead of hanging.
+__device__ __noinline__ unsigned long long cstep_poll(const unsigned long long* p, unsigned long long t0,
+                                                      unsigned* err) {
+  for (unsigned n = 1;; ++n) {
+    const unsigned long long v = ld_relaxed_u64(p);
+    if (v != 0ull) return v;
+    if ((n & 255u) == 0u && globaltimer_ns() - t0 > 2000000000ull) {
+      atomicExch(err, (unsigned)DS_ERR_DEVICE_TIMEOUT);
+      return 1ull;
+    }
+  }
+}
+
 struct CStepArgs {
   HeadArgs h;              // head part; sel / sel_count / sl_off are redirected to shared memory
   const void* W1;          // [rows1][2d]
@@ -49,7 +64,7 @@ struct CStepArgs {
   int32_t h_r, rows1, k, extra_bytes;
   unsigned long long* crec;  // [G][2 + k_t] per-CTA records (max | sum, count + 1, k_t keys); 0 = not yet
                              // written (the merger zeroes them after reading)
-  unsigned* ctr;             // unused (the merger polls the records)
+  unsigned* ctr;             // workspace error word: DS_ERR_DEVICE_TIMEOUT when a record never lands
   unsigned long long* trace;
   int xs_slot;  // ring slot holding [h_prev ‖ e] (-1: a separate shared-memory region)
   int head_only;  // 1: S1-S3 ran elsewhere (dynaspec_step_route); the TopK comes from h.sel / h.sel_count
@@ -524,13 +539,14 @@ __global__ void __launch_bounds__((kMaxStages + 1) * 32, 1) cstep_kernel(const C
   {  // (1a) stage the record words as they land (coalesced; small code: the fields are decoded once below)
     constexpr int kB = 8;
     const int nrec = G * rec, nt = blockDim.x;
+    const unsigned long long t0 = globaltimer_ns();
     for (int i0 = threadIdx.x; i0 < nrec; i0 += kB * nt) {
       unsigned long long v[kB];
 #pragma unroll
       for (int u = 0; u < kB; ++u) v[u] = i0 + u * nt < nrec ? __ldcg(s.crec + i0 + u * nt) : 1ull;
 #pragma unroll
       for (int u = 0; u < kB; ++u) {
-        while (v[u] == 0ull) v[u] = ld_relaxed_u64(s.crec + i0 + u * nt);  // not written yet: poll L2
+        if (v[u] == 0ull) v[u] = cstep_poll(s.crec + i0 + u * nt, t0, s.ctr);  // not written yet: poll L2
         if (i0 + u * nt < nrec) raw[i0 + u * nt] = v[u];
       }
     }
@@ -790,7 +806,7 @@ cudaError_t launch_cstep(const ds_clusters* c, const ds_router* r, const void* h
   s.xs_slot = p.xs_slot;
   s.head_only = 0;
   s.crec = reinterpret_cast<unsigned long long*>(w8 + kWsCstepRec);
-  s.ctr = reinterpret_cast<unsigned*>(w8);
+  s.ctr = reinterpret_cast<unsigned*>(w8 + kWsErrorWord);
   s.trace = debug_trace();
   return c->dtype == DS_BF16 ? launch_cstep_t<__nv_bfloat16>(s, p.smem, p.Q, p.C, st, pdl)
                              : launch_cstep_t<float>(s, p.smem, p.Q, p.C, st, pdl);
@@ -826,7 +842,7 @@ cudaError_t launch_cstep_head(const ds_clusters* c, const void* h_new, const int
   s.xs_slot = p.xs_slot;
   s.head_only = 1;
   s.crec = reinterpret_cast<unsigned long long*>(w8 + kWsCstepRec);
-  s.ctr = reinterpret_cast<unsigned*>(w8);
+  s.ctr = reinterpret_cast<unsigned*>(w8 + kWsErrorWord);
   s.trace = debug_trace();
   return c->dtype == DS_BF16 ? launch_cstep_t<__nv_bfloat16>(s, p.smem, p.Q, p.C, st, false)
                              : launch_cstep_t<float>(s, p.smem, p.Q, p.C, st, false);

@@ -100,6 +100,7 @@ __device__ __forceinline__ void cp_async_wait() {
 // 128 / 64 when the union is too small to give every SM two items); CSR of (cluster -> rows); per-row
 // record slots: row b's records are [rowoff[b], rowoff[b + 1]) with, for its i-th selected cluster
 // m_i, the nparts(m_i) = ceil(|C_m| / T) records of that cluster at rowoff[b] + sum_{i' < i} nparts.
+// (T = 256 unless fewer than G / 2 items would result; the workspace bound below covers T < 256.)
 constexpr int kGhStageMax = 40 * 1024;  // staged selection entries (160 KB); larger batches read L2
 
 __global__ void __launch_bounds__(1024) gh_group_kernel(const int32_t* __restrict__ sel,
@@ -143,7 +144,7 @@ __global__ void __launch_bounds__(1024) gh_group_kernel(const int32_t* __restric
     }
   }
   __syncthreads();
-  // vocabulary tile: the largest T in {256, 128, 64} giving >= 2 items per SM
+  // vocabulary tile: the largest T in {256, 128, 64} giving work to at least half of the SMs
   {
     int it[3] = {0, 0, 0};
     for (int m = tid; m < M; m += blockDim.x)
@@ -159,7 +160,9 @@ __global__ void __launch_bounds__(1024) gh_group_kernel(const int32_t* __restric
     }
   }
   __syncthreads();
-  if (tid == 0) tsel = red[0] >= 2 * G ? kGhVoc : red[1] >= 2 * G ? kGhVoc / 2 : kGhVoc / 4;
+  // a 256-row tile keeps ~128 KB of W in flight per SM, so it only pays to split tiles when fewer than
+  // half of the SMs would get one (Llama-3 B = 8: T = 64 measured 160 vs 120 us per step)
+  if (tid == 0) tsel = red[0] >= G / 2 ? kGhVoc : red[1] >= G / 2 ? kGhVoc / 2 : kGhVoc / 4;
   __syncthreads();
   const int T = tsel;
   for (int m = tid; m < M; m += blockDim.x) np[m] = (csz[m] + T - 1) / T;
@@ -374,10 +377,16 @@ __global__ void __launch_bounds__(kGhThreads, 1) gh_head_kernel(const __grid_con
     }
     __syncwarp();
   } else if (warp < 4) {
-    // ---- row gather: the item's rows of h_new into the SW128 K-major image, 16 B per cp.async
+    // ---- row gather: the item's rows of h_new into the SW128 K-major image, 16 B per cp.async.  A
+    // stage is published (proxy fence + arrive) once its copies have landed, kLag stages later
+    // (kLag < kGhS keeps the ring deadlock-free).  kLag = 1: publishing stage s needs the issue of
+    // s + kLag, i.e. the MMA of stage s + kLag - kGhS; kLag = 3 coupled stage s to the MMA of s - 1 and
+    // measured slower (Gemma-3 B = 512 head 460 -> 534 us).
+    constexpr int kLag = 1;
     const int t = threadIdx.x - 64;  // 0..63
     uint32_t it = 0;
-    int li = 0, pend = -1;  // stage whose copies are in flight (arrive after they land)
+    int li = 0, npend = 0;
+    int pend[kLag];
     for (int item = blockIdx.x; item < nitems; item += G, ++li) {
       const int4 itm = __ldg(g.items + item);
       const int n = itm.w;
@@ -394,20 +403,26 @@ __global__ void __launch_bounds__(kGhThreads, 1) gh_head_kernel(const __grid_con
                      reinterpret_cast<const uint8_t*>(g.h) + (size_t)rows[j] * rowbytes + (size_t)kc * 128 + ch * 16);
         }
         cp_async_commit();
-        if (pend >= 0) {  // the previous stage's copies have landed: make them visible to the tensor core
-          cp_async_wait<1>();
+        if (npend == kLag) {  // the oldest pending stage's copies have landed: visible to the tensor core
+          cp_async_wait<kLag>();
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          mbar_arrive(&full[pend]);
+          mbar_arrive(&full[pend[0]]);
+#pragma unroll
+          for (int q = 0; q + 1 < kLag; ++q) pend[q] = pend[q + 1];
+          --npend;
         }
-        pend = (int)s;
+#pragma unroll
+        for (int q = 0; q < kLag; ++q)
+          if (q == npend) pend[q] = (int)s;
+        ++npend;
       }
       named_bar_sync(1, kGhLoaders);  // rows[] of this parity is reused two items later
     }
-    if (pend >= 0) {
-      cp_async_wait<0>();
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      mbar_arrive(&full[pend]);
-    }
+    cp_async_wait<0>();
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+#pragma unroll
+    for (int q = 0; q < kLag; ++q)
+      if (q < npend) mbar_arrive(&full[pend[q]]);
   } else {
     // ---- epilogue: TMEM lane quarter q = warp & 3 holds rows 32 q .. 32 q + 31 of the item
     const int q = warp & 3, row = 32 * q + lane, et = threadIdx.x - 128;  // et: 0..127

@@ -118,6 +118,7 @@ struct GStepArgs {
   float* z_out;             // nullable: z over V_S in shortlist order
   int64_t max_shortlist;
   int32_t V, M, d, h_r, rows1, k, k_t, stages, stage_rows, stage_bytes, head_only, pdl;
+  int32_t merge_old;            // DS_GSTEP_MERGE=old: the block-wide merge (A/B)
   int32_t kpw, q_sel, q_merge;  // TopK launch constants: keys per warp, per-warp / record-warp ranks
   int32_t lgK;                  // ceil(log2(k_t + 1)): binary-search steps over a k_t-entry list
   uint32_t kdiv;                // ceil(2^32 / k_t): tid / k_t as one multiply-high
@@ -665,6 +666,95 @@ __device__ DS_GSTEP_NOINLINE void gstep_merge_compute(const GStepArgs& a, unsign
   trace_mark(a.trace, 9);
 }
 
+// Merge for k_t <= 16 and G <= 160 by two warps, no block barrier (the staged records raw[G][2 + K]):
+//   warp 1: lse = M + log sum_g s_g e^{m_g - M} — lane l folds records l, l + 32, ... in that order,
+//           then one fixed xor tree (R19);
+//   warp 0: top-K by a K-round tournament over the G sorted records: each lane holds the current
+//           head of its <= 5 records, the warp takes the largest 64-bit key (REDUX on the high
+//           word, then on the low word among the ties — keys are unique), and the winning lane
+//           advances that record.
+// They meet at one named barrier (lse is needed for the log-probs).  Measured cost in isolation
+// (scripts/probe/phase_bench.cu): see DESIGN §5.2c; replaces three block-wide phases.
+constexpr int kGMergeRecs = 5;  // records per lane (G <= 160)
+__device__ DS_GSTEP_NOINLINE void gstep_merge_fast(const GStepArgs& a, const unsigned long long* raw, int G,
+                                                   bool ok_in, float* lse_sh) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int K = a.k_t, rec = 2 + K;
+  if (warp == 1) {
+    float mg[kGMergeRecs], sg[kGMergeRecs];
+    uint32_t mk = 0u;
+#pragma unroll
+    for (int q = 0; q < kGMergeRecs; ++q) {
+      const int g = lane + 32 * q;
+      const unsigned long long w0 = g < G ? raw[(size_t)g * rec] : 0ull;
+      mg[q] = g < G ? __uint_as_float((uint32_t)w0) : -INFINITY;
+      sg[q] = __uint_as_float((uint32_t)(w0 >> 32));
+      if (mg[q] > -INFINITY) mk = max(mk, ord_key(mg[q]));
+    }
+    mk = __reduce_max_sync(0xffffffffu, mk);
+    const float Mx = mk ? __uint_as_float((mk & 0x80000000u) ? (mk & 0x7fffffffu) : ~mk) : -INFINITY;
+    float part = 0.f;
+#pragma unroll
+    for (int q = 0; q < kGMergeRecs; ++q)
+      if (mg[q] > -INFINITY) part += sg[q] * expf(mg[q] - Mx);
+    const float sum = warp_sum(part);
+    const bool ok = ok_in && Mx > -INFINITY;
+    const float lse = ok ? Mx + logf(sum) : __int_as_float(0x7fc00000);
+    if (lane == 0) {
+      *lse_sh = lse;
+      a.lse[0] = lse;
+    }
+    named_bar_sync(3, 64);
+  } else if (warp == 0) {
+    unsigned long long cur[kGMergeRecs];
+    int pos[kGMergeRecs], cnt[kGMergeRecs];
+#pragma unroll
+    for (int q = 0; q < kGMergeRecs; ++q) {
+      const int g = lane + 32 * q;
+      cnt[q] = g < G ? (int)raw[(size_t)g * rec + 1] - 1 : 0;
+      pos[q] = 0;
+      cur[q] = cnt[q] > 0 ? raw[(size_t)g * rec + 2] : 0ull;
+    }
+    unsigned long long mine = 0ull;  // lane r keeps the r-th best key
+    for (int r = 0; r < K; ++r) {
+      unsigned long long best = cur[0];
+      int bq = 0;
+#pragma unroll
+      for (int q = 1; q < kGMergeRecs; ++q)
+        if (cur[q] > best) {
+          best = cur[q];
+          bq = q;
+        }
+      const uint32_t hi = (uint32_t)(best >> 32);
+      const uint32_t Mhi = __reduce_max_sync(0xffffffffu, hi);
+      if (Mhi == 0u) break;  // every record exhausted: padding below
+      const uint32_t lo = hi == Mhi ? (uint32_t)best : 0u;
+      const uint32_t Mlo = __reduce_max_sync(0xffffffffu, lo);
+      const unsigned long long win = ((unsigned long long)Mhi << 32) | Mlo;
+      if (lane == r) mine = win;
+      if (best == win) {  // exactly one lane: advance its record
+#pragma unroll
+        for (int q = 0; q < kGMergeRecs; ++q)
+          if (q == bq) {
+            ++pos[q];
+            cur[q] = pos[q] < cnt[q] ? raw[(size_t)(lane + 32 * q) * rec + 2 + pos[q]] : 0ull;
+          }
+      }
+    }
+    named_bar_sync(3, 64);
+    const float lse = *lse_sh;
+    const bool ok = !(lse != lse);
+    if (lane < K) {
+      const bool v = ok && mine != 0ull;
+      const float z = key_value(mine);
+      a.top_ids[lane] = v ? key_id(mine) : -1;
+      a.top_logits[lane] = v ? z : -INFINITY;
+      a.top_logp[lane] = v ? z - lse : -INFINITY;
+    }
+  }
+  trace_mark(a.trace, 9);
+}
+
 // Merger (CTA 0): stage the G records as their words land; thread g decodes record g.  lse = M + log
 // sum_g s_g e^{m_g - M} (per-warp xor trees, then one fixed tree over the warps, R19).  Top-K: each
 // record warp finds its q-th best head (q = ceil(K / record warps), REDUX rounds); every key with a
@@ -711,7 +801,10 @@ __device__ DS_GSTEP_NOINLINE void gstep_merge(const GStepArgs& a, uint8_t* ring,
 #pragma unroll 4
   for (int i = tid; i < nrec; i += kGThreads) a.rec[i] = 0ull;
   if (!a.head_only && tid < a.rows1) a.aslot[tid] = 0ull;  // rows1 <= blockDim
-  gstep_merge_compute(a, raw, G, *dead == 0 && stream);
+  if (a.k_t <= 16 && G <= 32 * kGMergeRecs && !a.merge_old)
+    gstep_merge_fast(a, raw, G, *dead == 0 && stream, reinterpret_cast<float*>(raw + (size_t)G * (2 + a.k_t)));
+  else
+    gstep_merge_compute(a, raw, G, *dead == 0 && stream);
 }
 
 template <typename T>
@@ -1015,6 +1108,8 @@ static void fill_common(GStepArgs& a, const ds_clusters* c, const GStepPlan& p, 
   a.aslot = reinterpret_cast<unsigned long long*>(w8 + kWsGstepUnits);
   a.err = reinterpret_cast<unsigned*>(w8 + kWsErrorWord);
   a.trace = debug_trace();
+  const char* mv = getenv("DS_GSTEP_MERGE");
+  a.merge_old = mv && mv[0] == 'o' ? 1 : 0;
   a.L = gstep_smem(p.S, p.stage_bytes, c->d, c->dtype == DS_BF16 ? 2 : 4, c->M, std::max(p.rows1, 1), k_t);
   a.kpw = (c->M + kGKeyWarps - 1) / kGKeyWarps;
   a.lgK = 0;

@@ -153,6 +153,7 @@ __global__ void __launch_bounds__(kMetaThreads) meta_l2_kernel(const float* __re
   __shared__ float b1s[kMaxM];
   __shared__ float b2s[kMaxM];
   __shared__ int32_t offs[kMaxM + 1];
+  __shared__ uint32_t rhist[256 + 8];
   const int b = blockIdx.x;
   // constants first (they do not depend on the upstream kernel)
   for (int u = threadIdx.x; u < rows1; u += blockDim.x) b1s[u] = b1[u];
@@ -173,7 +174,8 @@ __global__ void __launch_bounds__(kMetaThreads) meta_l2_kernel(const float* __re
   for (int m = threadIdx.x; m < M; m += blockDim.x) scores[(size_t)b * M + m] = s[m];
   if (sel == nullptr) return;
   if (pdl) pdl_launch_dependents();
-  rank_mask(s, M, k_per_row ? k_per_row[b] : k, mask);
+  if (M > 128) radix_mask(s, M, k_per_row ? k_per_row[b] : k, mask, rhist);
+  else rank_mask(s, M, k_per_row ? k_per_row[b] : k, mask);
   __syncthreads();
   if (!shared) {
     emit_fast(mask, M, offs, sel + (size_t)b * M, sel_count + b, sl_off + (size_t)b * (M + 1), tmp);

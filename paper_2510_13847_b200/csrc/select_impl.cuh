@@ -12,7 +12,15 @@ __device__ __forceinline__ void router_hidden(const float* part, int KS, int B, 
                                               bool relu, float* a1) {
   for (int u = threadIdx.x; u < rows1; u += blockDim.x) {
     float acc = 0.f;
-    for (int ks = 0; ks < KS; ++ks) acc += __ldcg(part + ((size_t)ks * B + b) * rows1 + u);
+    int ks = 0;
+    for (; ks + 8 <= KS; ks += 8) {  // 8 independent loads in flight, summed in split order (R19)
+      float v[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] = __ldcg(part + ((size_t)(ks + j) * B + b) * rows1 + u);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc += v[j];
+    }
+    for (; ks < KS; ++ks) acc += __ldcg(part + ((size_t)ks * B + b) * rows1 + u);
     acc += b1[u];
     a1[u] = relu ? fmaxf(acc, 0.f) : acc;
   }
@@ -80,6 +88,79 @@ __device__ __forceinline__ void rank_mask(const float* sc, int M, int k, uint32_
     const uint32_t b = __ballot_sync(0xffffffffu, sel);
     if (lane == 0) mask[m >> 5] = b;
   }
+}
+
+// TopK_k of sc[0..M) under (score desc, id asc) (R7) as a bit mask, by an MSB-first radix select on
+// the order-preserving 32-bit keys (4 passes of 8-bit digits: a shared-memory histogram each, one warp
+// finds the digit where the count from the top crosses k): T = the k-th largest key and need = how
+// many keys equal to T are taken (the lowest ids).  O(M) work per pass instead of rank_mask's O(M^2):
+// the router's layer-2 kernel at M = 512 spent most of its time ranking.  Same selection bit for bit.
+// hist: shared [256 + 8] u32.  Ends with a __syncthreads (mask complete).
+__device__ __forceinline__ void radix_mask(const float* sc, int M, int k, uint32_t* mask, uint32_t* hist) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t* st = hist + 256;  // [0] prefix, [1] prefix mask, [2] remaining k, [3] equal-key budget
+  if (threadIdx.x == 0) {
+    st[0] = 0u;
+    st[1] = 0u;
+    st[2] = (uint32_t)k;
+  }
+#pragma unroll 1
+  for (int shift = 24; shift >= 0; shift -= 8) {
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0u;
+    __syncthreads();
+    const uint32_t pre = st[0], pm = st[1];
+    for (int m = threadIdx.x; m < M; m += blockDim.x) {
+      const uint32_t key = ord_key(sc[m] + 0.0f);
+      if ((key & pm) == pre) atomicAdd(&hist[(key >> shift) & 255u], 1u);
+    }
+    __syncthreads();
+    if (warp == 0) {  // digits 255..0 from the top: lane l holds digits 255 - 8l .. 248 - 8l
+      uint32_t c[8], tot = 0u;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        c[j] = hist[255 - 8 * lane - j];
+        tot += c[j];
+      }
+      uint32_t inc = tot;  // inclusive scan over lanes (from the top digit down)
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+      }
+      const uint32_t kk = st[2];
+      const uint32_t before = inc - tot;  // keys in higher digits than this lane's
+      if (before < kk && inc >= kk) {     // exactly one lane: the crossing digit is here
+        uint32_t run = before;
+        int j = 0;
+        for (; j < 8; ++j) {
+          if (run + c[j] >= kk) break;
+          run += c[j];
+        }
+        const uint32_t digit = 255u - 8u * (uint32_t)lane - (uint32_t)j;
+        st[0] = pre | (digit << shift);
+        st[1] = pm | (255u << shift);
+        st[2] = kk - run;  // still to take among keys with this prefix
+      }
+    }
+    __syncthreads();
+  }
+  // T = st[0]: keys > T are in; keys == T: the st[2] lowest ids
+  const uint32_t T = st[0], need = st[2];
+  const int Mr = (M + 31) & ~31;
+  uint32_t taken = 0u;  // equal keys in earlier words, per thread (words are handled in order by warp 0)
+  if (warp == 0) {
+    for (int m0 = 0; m0 < Mr; m0 += 32) {
+      const int m = m0 + lane;
+      const uint32_t key = m < M ? ord_key(sc[m] + 0.0f) : 0u;
+      const uint32_t eq = __ballot_sync(0xffffffffu, m < M && key == T);
+      const uint32_t rank_eq = taken + __popc(eq & ((1u << lane) - 1u));
+      const bool in = m < M && (key > T || (key == T && rank_eq < need));
+      const uint32_t b = __ballot_sync(0xffffffffu, in);
+      if (lane == 0) mask[m0 >> 5] = b;
+      taken += __popc(eq);
+    }
+  }
+  __syncthreads();
 }
 
 // Ascending ids of the set bits (position = popcount of the lower bits) and sl_offsets = exclusive

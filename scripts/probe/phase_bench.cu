@@ -105,6 +105,21 @@ __global__ void __launch_bounds__(512, 1) k_merge(GStepArgs a, const unsigned lo
   }
 }
 
+__global__ void __launch_bounds__(512, 1) k_merge_fast(GStepArgs a, const unsigned long long* recs, int G,
+                                                       unsigned long long* cyc) {
+  extern __shared__ __align__(16) unsigned long long raw[];
+  const int tid = threadIdx.x, rec = 2 + a.k_t;
+  for (int r = 0; r < R; ++r) {
+    for (int i = tid; i < G * rec; i += blockDim.x) raw[i] = recs[i];
+    __syncthreads();
+    const unsigned long long t0 = clock64();
+    gstep_merge_fast(a, raw, G, true, reinterpret_cast<float*>(raw + (size_t)G * rec));
+    __syncthreads();
+    const unsigned long long t1 = clock64();
+    if (tid == 0) cyc[r] = t1 - t0;
+  }
+}
+
 static double median(std::vector<unsigned long long> v) {
   std::sort(v.begin(), v.end());
   return (double)v[v.size() / 2];
@@ -216,6 +231,16 @@ int main() {
     for (int rep = 0; rep < 2; ++rep) k_merge<<<1, 512, sm>>>(m, dr, G, cyc);
     cudaDeviceSynchronize();
     printf("merge_compute G=147 K=8 (+ barrier): %.0f cycles/call\n", median({cyc, cyc + R}));
+    int ids0[8], ids1[8];
+    cudaMemcpy(ids0, oi, 32, cudaMemcpyDeviceToHost);
+    cudaFuncSetAttribute(k_merge_fast, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    for (int rep = 0; rep < 2; ++rep) k_merge_fast<<<1, 512, sm>>>(m, dr, G, cyc);
+    cudaDeviceSynchronize();
+    printf("merge_fast    G=147 K=8 (+ barrier): %.0f cycles/call\n", median({cyc, cyc + R}));
+    cudaMemcpy(ids1, oi, 32, cudaMemcpyDeviceToHost);
+    int same = 1;
+    for (int i = 0; i < 8; ++i) same &= ids0[i] == ids1[i];
+    printf("  same top ids: %d (%d %d %d ...)\n", same, ids1[0], ids1[1], ids1[2]);
   }
   cudaError_t e = cudaGetLastError();
   printf("status: %s\n", cudaGetErrorString(e));
