@@ -451,7 +451,8 @@ int32_t dynaspec_draft_step_launches(const ds_clusters* c, const ds_router* r, i
   if (!c || !r || !head_plan(c, B, k_t, 0, &p)) return 0;
   const int64_t ms = shared ? c->V : 0;
   if (use_tc_head(c, B, k_t, shared, ms)) return 3;  // meta layer 1, meta layer 2 (+union), tcgen05 head
-  if (use_gh(c, B, k_t, shared, z_out != 0, c->M)) return 5;  // meta x2, group, grouped tcgen05 head, merge
+  if (use_gh(c, B, k_t, shared, z_out != 0, c->M))  // meta x2, grouping (1 or 3), grouped tcgen05 head, merge
+    return gh_wide_grouping(B, shared) ? 7 : 5;
   if (use_tc_batched(c, B, k_t, shared, z_out != 0))
     return 2 + 2 * ((B + 127) / 128);  // meta x2, then (union + tcgen05 head) per 128 rows
   if (!two_streams && step_supported(c, r, B, k_t, shared, 0)) return 1;  // fused single-stream step

@@ -257,6 +257,135 @@ __global__ void __launch_bounds__(1024) gh_group_kernel(const int32_t* __restric
   }
 }
 
+// Large independent batches (B >= kGhWideRows rows, T = 256): the grouping as three
+// grid-wide kernels (the one-CTA kernel above spent 35 us on Gemma-3 B = 512, one SM working):
+//   gh_count_kernel  warp per row: n_m by global atomics, each row's record count (fixed T = 256)
+//   gh_scan_kernel   one CTA: scans of n_m (groups), items per cluster and rows' records; the items;
+//                    n_m and the fill cursors zeroed for the fill and the next call
+//   gh_fill_kernel   warp per row: CSR entries and record slots
+// cnt_g / cur_g: [M] ints in the per-call head scratch (cnt_g zeroed by a memset before the count kernel,
+// cur_g by the scan kernel before the fill).
+constexpr int kGhWideRows = 128;
+
+__global__ void __launch_bounds__(1024) gh_count_kernel(const int32_t* __restrict__ sel,
+                                                        const int32_t* __restrict__ cnt, int B, int M,
+                                                        const int32_t* __restrict__ offsets, int* cnt_g,
+                                                        int32_t* rowoff) {
+  pdl_wait();
+  pdl_launch_dependents();
+  const int lane = threadIdx.x & 31;
+  const int b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (b >= B) return;
+  const int n = __ldg(cnt + b);
+  int nr = 0;
+  for (int i = lane; i < n; i += 32) {
+    const int m = __ldg(sel + (size_t)b * M + i);
+    atomicAdd(cnt_g + m, 1);
+    nr += (__ldg(offsets + m + 1) - __ldg(offsets + m) + kGhVoc - 1) / kGhVoc;
+  }
+  nr = (int)__reduce_add_sync(0xffffffffu, (unsigned)nr);
+  if (lane == 0) rowoff[b + 1] = nr;
+}
+
+__global__ void __launch_bounds__(1024) gh_scan_kernel(int B, int M, const int32_t* __restrict__ offsets, int* cnt_g,
+                                                       int* cur_g, int32_t* go_g, int32_t* rowoff, int4* items,
+                                                       int32_t* nitems) {
+  __shared__ int cm[kGhMaxM], go[kGhMaxM + 1], io[kGhMaxM + 1];
+  __shared__ int wsum[32];
+  pdl_wait();
+  pdl_launch_dependents();
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  for (int m = tid; m < M; m += blockDim.x) {
+    cm[m] = __ldcg(cnt_g + m);
+    cur_g[m] = 0;  // the fill cursors
+  }
+  __syncthreads();
+  auto block_scan = [&](auto get, auto put, int n) {
+    int carry = 0;
+    for (int base = 0; base < n; base += blockDim.x) {
+      const int i = base + tid;
+      const int v = i < n ? get(i) : 0;
+      int x = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      if (lane == 31) wsum[warp] = x;
+      __syncthreads();
+      if (warp == 0) {
+        int s = lane < nw ? wsum[lane] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, s, o);
+          if (lane >= o) s += y;
+        }
+        wsum[lane] = s;
+      }
+      __syncthreads();
+      const int excl = carry + (warp > 0 ? wsum[warp - 1] : 0) + x - v;
+      if (i < n) put(i, excl);
+      const int tot = wsum[nw - 1];
+      __syncthreads();
+      carry += tot;
+    }
+    return carry;
+  };
+  auto np = [&](int m) { return (__ldg(offsets + m + 1) - __ldg(offsets + m) + kGhVoc - 1) / kGhVoc; };
+  const int tg = block_scan([&](int m) { return cm[m]; }, [&](int m, int e) { go[m] = e; }, M);
+  const int ti = block_scan([&](int m) { return cm[m] > 0 ? np(m) * ((cm[m] + kGhRows - 1) / kGhRows) : 0; },
+                            [&](int m, int e) { io[m] = e; }, M);
+  const int tr = block_scan([&](int b) { return __ldcg(rowoff + b + 1); }, [&](int b, int e) { rowoff[b] = e; }, B);
+  if (tid == 0) {
+    rowoff[B] = tr;
+    *nitems = ti;
+    go_g[M] = tg;
+  }
+  for (int m = tid; m < M; m += blockDim.x) {
+    go_g[m] = go[m];
+    const int n = cm[m];
+    if (n == 0) continue;
+    const int beg = __ldg(offsets + m), sz = __ldg(offsets + m + 1) - beg, P = np(m);
+    const int nrb = (n + kGhRows - 1) / kGhRows;
+    int it = io[m];
+    for (int p = 0; p < P; ++p)
+      for (int rb = 0; rb < nrb; ++rb)
+        items[it++] = make_int4(beg + p * kGhVoc, min(kGhVoc, sz - p * kGhVoc) | (p << 16), go[m] + rb * kGhRows,
+                                min(kGhRows, n - rb * kGhRows));
+  }
+}
+
+__global__ void __launch_bounds__(1024) gh_fill_kernel(const int32_t* __restrict__ sel,
+                                                       const int32_t* __restrict__ cnt, int B, int M,
+                                                       const int32_t* __restrict__ offsets, const int32_t* go_g,
+                                                       int* cur_g, const int32_t* rowoff, int32_t* grp_rows,
+                                                       int32_t* grp_rec) {
+  pdl_wait();
+  pdl_launch_dependents();
+  const int lane = threadIdx.x & 31;
+  const int b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (b >= B) return;
+  const int n = __ldg(cnt + b);
+  int base = __ldcg(rowoff + b);
+  for (int i0 = 0; i0 < n; i0 += 32) {
+    const int i = i0 + lane;
+    const int m = i < n ? __ldg(sel + (size_t)b * M + i) : 0;
+    const int p = i < n ? (__ldg(offsets + m + 1) - __ldg(offsets + m) + kGhVoc - 1) / kGhVoc : 0;
+    int x = p;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (i < n) {
+      const int pos = __ldcg(go_g + m) + atomicAdd(cur_g + m, 1);
+      grp_rows[pos] = b;
+      grp_rec[pos] = base + x - p;
+    }
+    base += __shfl_sync(0xffffffffu, x, 31);
+  }
+}
+
 // ---------------------------------------------------------------------------- head
 // Thread-local sorted top-K list in KMAX registers: slots [0, KMAX - K) hold ~0 sentinels (never
 // displaced), the K real entries (descending 64-bit keys, 0 = empty) are L[KMAX - K .. KMAX - 1], so
@@ -547,7 +676,7 @@ __global__ void __launch_bounds__(128) gh_merge_kernel(const float* __restrict__
 
 // ---------------------------------------------------------------------------- host
 struct GhWs {
-  size_t grp_rows, grp_rec, rowoff, items, nitems, recs, total;
+  size_t grp_rows, grp_rec, rowoff, items, nitems, cnt, cur, go, recs, total;
   int64_t max_recs_per_row, max_items;
 };
 
@@ -575,12 +704,17 @@ static GhWs gh_ws(const ds_clusters* c, int B, int k_t, int kmax) {
   w.rowoff = take((size_t)(B + 1) * 4);
   w.items = take((size_t)w.max_items * 16);
   w.nitems = take(16);
+  w.cnt = take((size_t)c->M * 4);  // per-cluster counts (zeroed by launch_gh), fill cursors, group offsets
+  w.cur = take((size_t)c->M * 4);
+  w.go = take((size_t)(c->M + 1) * 4);
   w.recs = take((size_t)B * w.max_recs_per_row * (2 + 2 * k_t) * 4);
   w.total = o;
   return w;
 }
 
 static size_t gh_merge_smem(int64_t G, int K) { return (size_t)(2 * G + 4 * G * K) * 4 + 64 * 4 + 16 * 4; }
+
+bool gh_wide_grouping(int B, int shared) { return !shared && B >= kGhWideRows; }
 
 bool gh_supported(const ds_clusters* c, int B, int k_t, int kmax) {
   const char* off = getenv("DS_GH");
@@ -628,7 +762,31 @@ cudaError_t launch_gh(const ds_clusters* c, const void* h_new, int B, const int3
   cudaLaunchAttribute pdl[1];
   pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   pdl[0].val.programmaticStreamSerializationAllowed = 1;
-  {
+  if (gh_wide_grouping(B, shared)) {
+    int* cnt_g = reinterpret_cast<int*>(w8 + w.cnt);
+    int* cur_g = reinterpret_cast<int*>(w8 + w.cur);
+    int32_t* go_g = reinterpret_cast<int32_t*>(w8 + w.go);
+    cudaLaunchConfig_t cfg = {};
+    cfg.blockDim = dim3(1024);
+    cfg.stream = st;
+    cfg.attrs = pdl;
+    cfg.numAttrs = 1;
+    cfg.gridDim = dim3((B + 31) / 32);
+    // the counters live in the per-call head scratch, which other head kernels also use: zero them here
+    cudaError_t e = cudaMemsetAsync(cnt_g, 0, (size_t)c->M * 4, st);
+    if (e != cudaSuccess) return e;
+    e = cudaLaunchKernelEx(&cfg, gh_count_kernel, sel, sel_count, B, c->M, (const int32_t*)c->offsets,
+                                       cnt_g, rowoff);
+    if (e != cudaSuccess) return e;
+    cfg.gridDim = dim3(1);
+    e = cudaLaunchKernelEx(&cfg, gh_scan_kernel, B, c->M, (const int32_t*)c->offsets, cnt_g, cur_g, go_g, rowoff,
+                           items, nitems);
+    if (e != cudaSuccess) return e;
+    cfg.gridDim = dim3((B + 31) / 32);
+    e = cudaLaunchKernelEx(&cfg, gh_fill_kernel, sel, sel_count, B, c->M, (const int32_t*)c->offsets,
+                           (const int32_t*)go_g, cur_g, (const int32_t*)rowoff, grp_rows, grp_rec);
+    if (e != cudaSuccess) return e;
+  } else {
     cudaLaunchConfig_t cfg = {};
     const int nrs = shared ? 1 : B;
     const size_t stg = (int64_t)nrs * kmax <= kGhStageMax ? (size_t)nrs * kmax * 4 : 0;

@@ -129,6 +129,7 @@ cudaError_t launch_tc_batched(const ds_clusters* c, const void* h_new, int B, co
 bool use_tc_batched(const ds_clusters* c, int B, int k_t, int shared, bool z_out);
 // ---- grouped (cluster-major) tcgen05 head for many independent rows (gh.cu)
 bool gh_supported(const ds_clusters* c, int B, int k_t, int kmax);
+bool gh_wide_grouping(int B, int shared);  // grouping by three grid-wide kernels instead of one CTA
 size_t gh_ws_bytes(const ds_clusters* c, int B, int k_t, int kmax);
 cudaError_t launch_gh(const ds_clusters* c, const void* h_new, int B, const int32_t* sel, const int32_t* sel_count,
                       int shared, int k_t, int kmax, int32_t* top_ids, float* top_logits, float* top_logp, float* lse, void* ws,

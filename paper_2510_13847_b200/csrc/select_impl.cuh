@@ -44,8 +44,33 @@ __device__ __forceinline__ void router_scores_thread(const T* W2, const float* a
   for (int m = threadIdx.x; m < M; m += blockDim.x) {
     const T* w = W2 + (size_t)m * h_r;
     float acc0 = 0.f, acc1 = 0.f;
-    int c = m % chunks;
-    for (int i = 0; i < chunks; ++i) {
+    const int c0 = m % chunks;
+    int i = 0;
+    for (; i + 8 <= chunks; i += 8) {  // 8 independent 16-byte loads in flight, then the FMAs in order
+      uint4 raw[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        int c = c0 + i + u;
+        c = c >= chunks ? c - chunks : c;
+        raw[u] = *reinterpret_cast<const uint4*>(w + c * E);
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        int c = c0 + i + u;
+        c = c >= chunks ? c - chunks : c;
+        float wf[E];
+        widen16(raw[u], wf, w);
+        const float* av = a1 + c * E;
+#pragma unroll
+        for (int j = 0; j < E; j += 2) {
+          acc0 = fmaf(wf[j], av[j], acc0);
+          acc1 = fmaf(wf[j + 1], av[j + 1], acc1);
+        }
+      }
+    }
+    for (; i < chunks; ++i) {
+      int c = c0 + i;
+      c = c >= chunks ? c - chunks : c;
       float wf[E];
       widen16(*reinterpret_cast<const uint4*>(w + c * E), wf, w);
       const float* av = a1 + c * E;
@@ -54,7 +79,6 @@ __device__ __forceinline__ void router_scores_thread(const T* W2, const float* a
         acc0 = fmaf(wf[j], av[j], acc0);
         acc1 = fmaf(wf[j + 1], av[j + 1], acc1);
       }
-      c = (c + 1 == chunks) ? 0 : c + 1;
     }
     sc[m] = (acc0 + acc1) + b2[m];
   }
