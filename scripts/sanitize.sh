@@ -7,7 +7,7 @@ cd "$(dirname "$0")/.."
 out=gpurun_out/sanitize
 mkdir -p $out
 : > $out/summary.txt
-for case in gstep gstep_head cstep step head tc_tree tc_batched verify build; do
+for case in ${SAN_CASES:-gstep gstep_head cstep step head tc_tree tc_batched gh gh_wide verify build}; do
   for tool in memcheck racecheck synccheck initcheck; do
     log=$out/${case}_${tool}.log
     start=$(date +%s)

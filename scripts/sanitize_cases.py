@@ -3,7 +3,8 @@ case under memcheck, racecheck, synccheck and initcheck).  Usage: sanitize_cases
 
 Cases: gstep (B = 1 grid step), gstep_head (head-only grid step), cstep (B = 1 cluster step),
 step (grid-wide fused step, B = 4), head (head_forward B = 3), tc_tree (tcgen05 shared head, 10 rows),
-tc_batched (tcgen05 batched head, 16 rows), verify (verify_chain), build (k-means build)."""
+tc_batched (tcgen05 batched head, 16 rows), gh (grouped tcgen05 head, 16 rows), gh_wide (160 rows:
+tcgen05 router layer 1 + grid-wide grouping + grouped head), verify (verify_chain), build (k-means build)."""
 import os
 import sys
 
@@ -22,8 +23,8 @@ c = D.Clusters.from_tau(W, tau, M)
 r = D.Router(*[x.to(dev) for x in S.router(d, h_r, M, 1, "bf16")])
 
 
-def steps(B, shared=False, two=False, n=3):
-    st = D.DraftStep(c, r, B, 4, shared=shared, two_streams=two, z_out=not shared)
+def steps(B, shared=False, two=False, n=3, z_out=None):
+    st = D.DraftStep(c, r, B, 4, shared=shared, two_streams=two, z_out=(not shared) if z_out is None else z_out)
     for t in range(n):
         hp, e, hn = [x.to(dev) for x in S.step_inputs(B, d, t, "bf16")]
         st(hp, e, hn, t, 8, 2)
@@ -53,6 +54,12 @@ elif case == "tc_tree":
     st = steps(10, shared=True)
 elif case == "tc_batched":
     st = steps(16)
+elif case == "gh":
+    st = steps(16, z_out=False)          # grouped cluster-major tcgen05 head, one-CTA grouping
+    assert st.kernel.startswith("ds::gh_head_kernel"), st.kernel
+elif case == "gh_wide":
+    st = steps(160, z_out=False, n=2)    # + router layer 1 on tcgen05 (B >= 32), grid-wide grouping
+    assert st.kernel.startswith("ds::gh_head_kernel") and st.launches == 7, (st.kernel, st.launches)
 elif case == "verify":
     B, gam, n_short = 4, 3, 64
     vi = S.verify_inputs(B, gam, 1024, n_short)
