@@ -55,6 +55,7 @@ struct GhArgs {
   const int32_t* grp_rec;    // [sum n_m] record index of the pair's first vocabulary tile
   float* recs;               // [records][2 + 2 k_t]
   int32_t d, kchunks, k_t;
+  int32_t dbg;  // DS_GH_DBG (timing experiments only; results wrong): 1 skip the MMAs, 2 skip the row gather
   unsigned long long* trace;
 };
 
@@ -495,10 +496,12 @@ __global__ void __launch_bounds__(kGhThreads, 1) gh_head_kernel(const __grid_con
           tc_fence_after();
           const uint32_t abase = smem_u32(sa + (size_t)s * kGhABytes);
           const uint32_t bbase = smem_u32(sb + (size_t)s * kGhBBytes);
+          if (!(g.dbg & 1)) {
 #pragma unroll
-          for (int k = 0; k < 4; ++k)
-            tc_mma_bf16(d_tmem, sw128_desc(abase + k * 32), sw128_desc(bbase + k * 32), idesc,
-                        (kc | k) != 0 ? 1u : 0u);
+            for (int k = 0; k < 4; ++k)
+              tc_mma_bf16(d_tmem, sw128_desc(abase + k * 32), sw128_desc(bbase + k * 32), idesc,
+                          (kc | k) != 0 ? 1u : 0u);
+          }
           tc_commit(&empty[s]);
         }
         tc_commit(&tfull[buf]);
@@ -506,52 +509,64 @@ __global__ void __launch_bounds__(kGhThreads, 1) gh_head_kernel(const __grid_con
     }
     __syncwarp();
   } else if (warp < 4) {
-    // ---- row gather: the item's rows of h_new into the SW128 K-major image, 16 B per cp.async.  A
-    // stage is published (proxy fence + arrive) once its copies have landed, kLag stages later
-    // (kLag < kGhS keeps the ring deadlock-free).  kLag = 1: publishing stage s needs the issue of
-    // s + kLag, i.e. the MMA of stage s + kLag - kGhS; kLag = 3 coupled stage s to the MMA of s - 1 and
-    // measured slower (Gemma-3 B = 512 head 460 -> 534 us).
-    constexpr int kLag = 1;
+    // ---- row gather: the item's rows of h_new into the SW128 K-major image, 16 B per cp.async.
+    // Every loader thread runs its own pipeline (no barrier between the 64 threads): thread t copies
+    // column chunk t & 7 of rows (t >> 3) + 8 u, so it needs only its own <= 16 row ids, loaded from
+    // global memory at each item start.  It issues a stage whenever the stage's slot is free and fewer
+    // than kPend stages are pending, and otherwise publishes its oldest pending stage (wait for those
+    // copies, proxy fence, arrive) — so up to kPend stages of row copies are in flight and a stage is
+    // published as soon as its copies have landed.  (Publishing stage s only after issuing s + 1 capped
+    // the gather at one stage per half L2 round trip, ~4.7 TB/s of W at Gemma-3 B = 512; waiting for
+    // s + 3 to issue coupled stage s to the MMA of s - 1: slower still.)
+    constexpr int kPend = kGhS - 1;
     const int t = threadIdx.x - 64;  // 0..63
-    uint32_t it = 0;
-    int li = 0, npend = 0;
-    int pend[kLag];
-    for (int item = blockIdx.x; item < nitems; item += G, ++li) {
-      const int4 itm = __ldg(g.items + item);
-      const int n = itm.w;
-      int32_t* rows = prow + (li & 1) * kGhRows;
-      for (int j = t; j < n; j += kGhLoaders) rows[j] = __ldg(g.grp_rows + itm.z + j);
-      named_bar_sync(1, kGhLoaders);
-      for (int kc = 0; kc < KC; ++kc, ++it) {
-        const uint32_t s = it % kGhS;
-        mbar_wait(&empty[s], ((it / kGhS) & 1u) ^ 1u);
-        uint8_t* dst = sa + (size_t)s * kGhABytes;
-        for (int c = t; c < n * 8; c += kGhLoaders) {
-          const int j = c >> 3, ch = c & 7;
-          cp_async16(dst + j * 128 + ((ch ^ (j & 7)) << 4),
-                     reinterpret_cast<const uint8_t*>(g.h) + (size_t)rows[j] * rowbytes + (size_t)kc * 128 + ch * 16);
+    const int r0 = t >> 3, cch = t & 7;
+    constexpr int kRowsPerThread = kGhRows / 8;
+    uint32_t it_i = 0, it_r = 0;  // stages issued / published by this thread
+    int item = blockIdx.x, kc = 0, n = 0;
+    int rid[kRowsPerThread];
+    const uint8_t* hb = reinterpret_cast<const uint8_t*>(g.h);
+    for (;;) {
+      const bool more = item < nitems;
+      if (more && it_i - it_r < (uint32_t)kPend &&
+          mbar_test_wait(&empty[it_i % kGhS], ((it_i / kGhS) & 1u) ^ 1u)) {
+        if (kc == 0) {  // item start: this thread's row ids
+          const int4 itm = __ldg(g.items + item);
+          n = itm.w;
+#pragma unroll
+          for (int u = 0; u < kRowsPerThread; ++u) {
+            const int j = r0 + 8 * u;
+            rid[u] = j < n ? __ldg(g.grp_rows + itm.z + j) : 0;
+          }
+        }
+        uint8_t* dst = sa + (size_t)(it_i % kGhS) * kGhABytes;
+#pragma unroll
+        for (int u = 0; u < kRowsPerThread; ++u) {
+          const int j = r0 + 8 * u;
+          if (j < n && !(g.dbg & 2))
+            cp_async16(dst + j * 128 + ((cch ^ (j & 7)) << 4), hb + (size_t)rid[u] * rowbytes + (size_t)kc * 128 + cch * 16);
         }
         cp_async_commit();
-        if (npend == kLag) {  // the oldest pending stage's copies have landed: visible to the tensor core
-          cp_async_wait<kLag>();
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          mbar_arrive(&full[pend[0]]);
-#pragma unroll
-          for (int q = 0; q + 1 < kLag; ++q) pend[q] = pend[q + 1];
-          --npend;
+        ++it_i;
+        if (++kc == KC) {
+          kc = 0;
+          item += G;
         }
-#pragma unroll
-        for (int q = 0; q < kLag; ++q)
-          if (q == npend) pend[q] = (int)s;
-        ++npend;
+      } else if (it_i != it_r) {  // publish the oldest pending stage once its copies have landed
+        switch (it_i - it_r) {
+          case 1: cp_async_wait<0>(); break;
+          case 2: cp_async_wait<1>(); break;
+          default: cp_async_wait<2>(); break;  // kPend = 3
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_arrive(&full[it_r % kGhS]);
+        ++it_r;
+      } else if (!more) {
+        break;
+      } else {  // nothing pending and the next slot busy: sleep on it
+        mbar_wait(&empty[it_i % kGhS], ((it_i / kGhS) & 1u) ^ 1u);
       }
-      named_bar_sync(1, kGhLoaders);  // rows[] of this parity is reused two items later
     }
-    cp_async_wait<0>();
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-#pragma unroll
-    for (int q = 0; q < kLag; ++q)
-      if (q < npend) mbar_arrive(&full[pend[q]]);
   } else {
     // ---- epilogue: TMEM lane quarter q = warp & 3 holds rows 32 q .. 32 q + 31 of the item
     const int q = warp & 3, row = 32 * q + lane, et = threadIdx.x - 128;  // et: 0..127
@@ -821,6 +836,8 @@ cudaError_t launch_gh(const ds_clusters* c, const void* h_new, int B, const int3
   a.kchunks = c->d / 64;
   a.k_t = k_t;
   a.trace = debug_trace();
+  const char* dv = getenv("DS_GH_DBG");
+  a.dbg = dv ? atoi(dv) : 0;
   cudaError_t e = k_t <= 8 ? launch_gh_head_t<8>(maps, a, st)
                   : k_t <= 16 ? launch_gh_head_t<16>(maps, a, st)
                               : launch_gh_head_t<32>(maps, a, st);
