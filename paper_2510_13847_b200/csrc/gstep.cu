@@ -118,7 +118,8 @@ struct GStepArgs {
   float* z_out;             // nullable: z over V_S in shortlist order
   int64_t max_shortlist;
   int32_t V, M, d, h_r, rows1, k, k_t, stages, stage_rows, stage_bytes, head_only, pdl;
-  int32_t merge_old;            // DS_GSTEP_MERGE=old: the block-wide merge (A/B)
+  int32_t merge_fast;           // DS_GSTEP_MERGE=fast: the two-warp tournament merge (A/B; same cost, and
+                                //   compute-sanitizer's synccheck flags its named barrier after the tournament)
   int32_t kpw, q_sel, q_merge;  // TopK launch constants: keys per warp, per-warp / record-warp ranks
   int32_t lgK;                  // ceil(log2(k_t + 1)): binary-search steps over a k_t-entry list
   uint32_t kdiv;                // ceil(2^32 / k_t): tid / k_t as one multiply-high
@@ -704,6 +705,7 @@ __device__ DS_GSTEP_NOINLINE void gstep_merge_fast(const GStepArgs& a, const uns
       *lse_sh = lse;
       a.lse[0] = lse;
     }
+    __syncwarp();
     named_bar_sync(3, 64);
   } else if (warp == 0) {
     unsigned long long cur[kGMergeRecs];
@@ -741,6 +743,7 @@ __device__ DS_GSTEP_NOINLINE void gstep_merge_fast(const GStepArgs& a, const uns
           }
       }
     }
+    __syncwarp();  // the tournament's winner-only updates leave the warp diverged: reconverge first
     named_bar_sync(3, 64);
     const float lse = *lse_sh;
     const bool ok = !(lse != lse);
@@ -801,7 +804,7 @@ __device__ DS_GSTEP_NOINLINE void gstep_merge(const GStepArgs& a, uint8_t* ring,
 #pragma unroll 4
   for (int i = tid; i < nrec; i += kGThreads) a.rec[i] = 0ull;
   if (!a.head_only && tid < a.rows1) a.aslot[tid] = 0ull;  // rows1 <= blockDim
-  if (a.k_t <= 16 && G <= 32 * kGMergeRecs && !a.merge_old)
+  if (a.k_t <= 16 && G <= 32 * kGMergeRecs && a.merge_fast)
     gstep_merge_fast(a, raw, G, *dead == 0 && stream, reinterpret_cast<float*>(raw + (size_t)G * (2 + a.k_t)));
   else
     gstep_merge_compute(a, raw, G, *dead == 0 && stream);
@@ -1109,7 +1112,7 @@ static void fill_common(GStepArgs& a, const ds_clusters* c, const GStepPlan& p, 
   a.err = reinterpret_cast<unsigned*>(w8 + kWsErrorWord);
   a.trace = debug_trace();
   const char* mv = getenv("DS_GSTEP_MERGE");
-  a.merge_old = mv && mv[0] == 'o' ? 1 : 0;
+  a.merge_fast = mv && mv[0] == 'f' ? 1 : 0;
   a.L = gstep_smem(p.S, p.stage_bytes, c->d, c->dtype == DS_BF16 ? 2 : 4, c->M, std::max(p.rows1, 1), k_t);
   a.kpw = (c->M + kGKeyWarps - 1) / kGKeyWarps;
   a.lgK = 0;

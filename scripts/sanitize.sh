@@ -8,7 +8,7 @@ out=gpurun_out/sanitize
 mkdir -p $out
 : > $out/summary.txt
 for case in ${SAN_CASES:-gstep gstep_head cstep step head tc_tree tc_batched gh gh_wide verify build}; do
-  for tool in memcheck racecheck synccheck initcheck; do
+  for tool in ${SAN_TOOLS:-memcheck racecheck synccheck initcheck}; do
     log=$out/${case}_${tool}.log
     start=$(date +%s)
     timeout ${SAN_TIMEOUT:-240} compute-sanitizer --tool $tool --error-exitcode 3 --print-limit 20 \
