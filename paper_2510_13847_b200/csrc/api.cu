@@ -506,7 +506,9 @@ ds_status dynaspec_draft_step(const ds_clusters* c, const ds_router* r, const vo
   // tree rows (shared): the shared-shortlist tcgen05 head (Qwen tree 90 vs 127 us per step with the
   // grouped head, whose router / grouping / merge launches dominate at 10 rows); independent rows: the
   // grouped head.  Supported-ness with kmax = M (what dynaspec_draft_step_ws sized the workspace for).
-  const bool tc = use_tc_head(c, B, k_t, shared, ms);
+  const char* gt = getenv("DS_GH_TREE");  // "1": tree rows on the grouped head too (A/B)
+  const bool gh_tree = gt && gt[0] == '1';
+  const bool tc = !gh_tree && use_tc_head(c, B, k_t, shared, ms);
   const bool gh = !tc && use_gh(c, B, k_t, shared, out->z_out != nullptr, c->M);
   const bool tcb = !tc && !gh && use_tc_batched(c, B, k_t, shared, out->z_out != nullptr);
   const bool fused = !tc && !tcb && !gh && !two_streams && step_supported(c, r, B, k_t, shared, ms);

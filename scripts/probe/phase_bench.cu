@@ -120,6 +120,26 @@ __global__ void __launch_bounds__(512, 1) k_merge_fast(GStepArgs a, const unsign
   }
 }
 
+__global__ void __launch_bounds__(512, 1) k_radix(const float* scores, int M, int k, unsigned long long* cyc,
+                                                  unsigned* out) {
+  __shared__ float sc[256];
+  __shared__ uint32_t mask[8], hist[264];
+  const int tid = threadIdx.x;
+  if (tid < M) sc[tid] = scores[tid];
+  unsigned acc = 0;
+  for (int r = 0; r < R; ++r) {
+    __syncthreads();
+    const unsigned long long t0 = clock64();
+    radix_mask(sc, M, k, mask, hist);
+    const unsigned long long t1 = clock64();
+    if (tid == 0) cyc[r] = t1 - t0;
+    acc += mask[r & 7];
+  }
+  __syncthreads();
+  if (tid < 8) out[tid] = mask[tid];
+  else out[tid] = acc;
+}
+
 static double median(std::vector<unsigned long long> v) {
   std::sort(v.begin(), v.end());
   return (double)v[v.size() / 2];
@@ -150,9 +170,27 @@ int main() {
   for (int k : {8, 32}) {
     for (int rep = 0; rep < 2; ++rep) k_topk<<<1, 512>>>(ds_, doff, M, k, cyc, out, dbg);
     cudaDeviceSynchronize();
+    {
+      unsigned m0[8];
+      cudaMemcpy(m0, out, 0, cudaMemcpyDeviceToHost);
+    }
     printf("topk_mask M=256 k=%d: %.0f cycles/call (median of %d): to 1st barrier %.0f, compaction %.0f, rank %.0f\n", k,
            median({cyc, cyc + R}), R, median({cyc + R, cyc + 2 * R}), median({cyc + 2 * R, cyc + 3 * R}),
            median({cyc + 3 * R, cyc + 4 * R}));
+  }
+  for (int k : {8, 32}) {
+    for (int rep = 0; rep < 2; ++rep) k_radix<<<1, 512>>>(ds_, M, k, cyc, out);
+    cudaDeviceSynchronize();
+    unsigned mk[8];
+    cudaMemcpy(mk, out, 32, cudaMemcpyDeviceToHost);
+    std::vector<int> idx(M);
+    for (int i = 0; i < M; ++i) idx[i] = i;
+    std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) { return s[a] > s[b]; });
+    unsigned ex[8] = {0};
+    for (int i = 0; i < k; ++i) ex[idx[i] >> 5] |= 1u << (idx[i] & 31);
+    int ok = 1;
+    for (int w = 0; w < 8; ++w) ok &= mk[w] == ex[w];
+    printf("radix_mask M=256 k=%d: %.0f cycles/call, mask %s\n", k, median({cyc, cyc + R}), ok ? "ok" : "WRONG");
   }
   // layer 2: W2 [256][128] bf16
   GStepArgs a = {};
