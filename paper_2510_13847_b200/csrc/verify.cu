@@ -570,6 +570,8 @@ struct VerifyLayout {
 // Splits: at most one wave of two 512-thread CTAs per SM over the rows of each pass, <= 32 CTAs per
 // row (<= 512 segments), warp segments >= 256 ids.
 static int verify_split(int64_t V, int rows) {
+  const char* ev = getenv("DS_VERIFY_SPLIT");  // tuning: CTAs per row
+  if (ev && ev[0]) return std::max(1, std::min(32, atoi(ev)));
   const int64_t want = 2 * (int64_t)num_sms() / rows;  // floor: never a partial second wave
   return (int)std::max<int64_t>(1, std::min<int64_t>(std::min<int64_t>(want, 32), V / (kVW * 256)));
 }
