@@ -104,6 +104,54 @@ __device__ __forceinline__ void cp_async_wait() {
 // (T = 256 unless fewer than G / 2 items would result; the workspace bound below covers T < 256.)
 constexpr int kGhStageMax = 40 * 1024;  // staged selection entries (160 KB); larger batches read L2
 
+// Items in descending tile-size order (counting sort on nv; ties in any order: an item's records do
+// not depend on the CTA that computes it), so gh_item's snake assignment (CTA b takes positions b,
+// 2G - 1 - b, 2G + b, ...) gives every CTA nearly the same W bytes: with cluster-major round-robin the
+// busiest CTA carried 1.15x (Gemma-3 B = 512) to 1.4x (Llama-3 B = 16-64) the mean.
+// bins: shared scratch of T + 1 ints.  The whole CTA calls it; cm / go are in shared memory.
+__device__ void gh_emit_items(int M, int T, const int32_t* __restrict__ offsets, const int* cm, const int* go,
+                              int4* items, int* bins) {
+  const int tid = threadIdx.x, lane = tid & 31;
+  for (int i = tid; i <= T; i += blockDim.x) bins[i] = 0;
+  __syncthreads();
+  for (int m = tid; m < M; m += blockDim.x) {
+    const int n = cm[m];
+    if (n == 0) continue;
+    const int sz = __ldg(offsets + m + 1) - __ldg(offsets + m), nrb = (n + kGhRows - 1) / kGhRows;
+    if (sz >= T) atomicAdd(&bins[T], (sz / T) * nrb);
+    if (sz % T) atomicAdd(&bins[sz % T], nrb);
+  }
+  __syncthreads();
+  if (tid < 32) {  // bins[nv] <- number of items with a larger tile (one warp, T + 1 <= 257 bins)
+    int carry = 0;
+    for (int base = T; base >= 0; base -= 32) {
+      const int nv = base - lane;
+      const int v = nv >= 0 ? bins[nv] : 0;
+      int x = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      if (nv >= 0) bins[nv] = carry + x - v;
+      carry += __shfl_sync(0xffffffffu, x, 31);
+    }
+  }
+  __syncthreads();
+  for (int m = tid; m < M; m += blockDim.x) {
+    const int n = cm[m];
+    if (n == 0) continue;
+    const int beg = __ldg(offsets + m), sz = __ldg(offsets + m + 1) - beg;
+    const int nrb = (n + kGhRows - 1) / kGhRows, P = (sz + T - 1) / T;
+    for (int p = 0; p < P; ++p) {
+      const int nv = min(T, sz - p * T);
+      for (int rb = 0; rb < nrb; ++rb)
+        items[atomicAdd(&bins[nv], 1)] = make_int4(beg + p * T, nv | (p << 16), go[m] + rb * kGhRows,
+                                                   min(kGhRows, n - rb * kGhRows));
+    }
+  }
+}
+
 __global__ void __launch_bounds__(1024) gh_group_kernel(const int32_t* __restrict__ sel,
                                                         const int32_t* __restrict__ cnt, int B, int M,
                                                         int shared, int kmax, int G,
@@ -244,18 +292,8 @@ __global__ void __launch_bounds__(1024) gh_group_kernel(const int32_t* __restric
       base += __shfl_sync(0xffffffffu, x, 31);
     }
   }
-  // items, cluster-major (W_perm address order): part p, row block rb
-  for (int m = tid; m < M; m += blockDim.x) {
-    const int n = cm[m];
-    if (n == 0) continue;
-    const int beg = __ldg(offsets + m), sz = csz[m];
-    const int nrb = (n + kGhRows - 1) / kGhRows;
-    int it = io[m];
-    for (int p = 0; p < np[m]; ++p)
-      for (int rb = 0; rb < nrb; ++rb)
-        items[it++] = make_int4(beg + p * T, min(T, sz - p * T) | (p << 16), go[m] + rb * kGhRows,
-                                min(kGhRows, n - rb * kGhRows));
-  }
+  // items: part p, row block rb of every selected cluster, largest tiles first
+  gh_emit_items(M, T, offsets, cm, go, items, io);
 }
 
 // Large independent batches (B >= kGhWideRows rows, T = 256): the grouping as three
@@ -342,18 +380,8 @@ __global__ void __launch_bounds__(1024) gh_scan_kernel(int B, int M, const int32
     *nitems = ti;
     go_g[M] = tg;
   }
-  for (int m = tid; m < M; m += blockDim.x) {
-    go_g[m] = go[m];
-    const int n = cm[m];
-    if (n == 0) continue;
-    const int beg = __ldg(offsets + m), sz = __ldg(offsets + m + 1) - beg, P = np(m);
-    const int nrb = (n + kGhRows - 1) / kGhRows;
-    int it = io[m];
-    for (int p = 0; p < P; ++p)
-      for (int rb = 0; rb < nrb; ++rb)
-        items[it++] = make_int4(beg + p * kGhVoc, min(kGhVoc, sz - p * kGhVoc) | (p << 16), go[m] + rb * kGhRows,
-                                min(kGhRows, n - rb * kGhRows));
-  }
+  for (int m = tid; m < M; m += blockDim.x) go_g[m] = go[m];
+  gh_emit_items(M, kGhVoc, offsets, cm, go, items, io);
 }
 
 __global__ void __launch_bounds__(1024) gh_fill_kernel(const int32_t* __restrict__ sel,
@@ -404,6 +432,11 @@ __device__ __forceinline__ void topk_insert(unsigned long long (&L)[KMAX], unsig
   }
 }
 
+// The j-th item of CTA b (items sorted by tile size, largest first): a snake over rounds of G items.
+__device__ __forceinline__ int gh_item(int j, int G) {
+  return j * G + ((j & 1) ? G - 1 - (int)blockIdx.x : (int)blockIdx.x);
+}
+
 template <int KMAX>
 __global__ void __launch_bounds__(kGhThreads, 1) gh_head_kernel(const __grid_constant__ GhMaps maps,
                                                                 const GhArgs g) {
@@ -446,6 +479,12 @@ __global__ void __launch_bounds__(kGhThreads, 1) gh_head_kernel(const __grid_con
   pdl_wait();  // items / row lists come from gh_group_kernel
   trace_mark(g.trace, 1);
   const int nitems = *g.nitems;
+  // this CTA's J items, processed from a per-CTA rotation so that at any moment the CTAs work on a mix
+  // of tile sizes (all CTAs on ragged tiles at once leave HBM idle while they wait on latency)
+  int J = 0;
+  while (gh_item(J, G) < nitems) ++J;
+  const int rot = J > 0 ? (int)blockIdx.x % J : 0;
+  auto order = [&](int li) { return li < J ? gh_item(li + rot < J ? li + rot : li + rot - J, G) : nitems; };
   const int KC = g.kchunks;
   const size_t rowbytes = (size_t)g.d * 2;
 
@@ -454,7 +493,7 @@ __global__ void __launch_bounds__(kGhThreads, 1) gh_head_kernel(const __grid_con
     if (lane == 0) {
       const uint64_t pol = policy_evict_first();
       uint32_t it = 0;
-      for (int item = blockIdx.x; item < nitems; item += G) {
+      for (int li = 0, item = order(0); item < nitems; item = order(++li)) {
         const int4 itm = __ldg(g.items + item);
         const int v0 = itm.x, nv = itm.y & 0xffff;
         const int nv8 = (nv + 7) & ~7;  // rows loaded (multiple of 8; the tail beyond nv is never read back)
@@ -480,7 +519,7 @@ __global__ void __launch_bounds__(kGhThreads, 1) gh_head_kernel(const __grid_con
     if (lane == 0) {
       uint32_t it = 0;
       int li = 0;
-      for (int item = blockIdx.x; item < nitems; item += G, ++li) {
+      for (int item = order(0); item < nitems; item = order(++li)) {
         const int4 itm = __ldg(g.items + item);
         const int nv = itm.y & 0xffff;
         const int N = (nv + 15) & ~15;
@@ -523,7 +562,7 @@ __global__ void __launch_bounds__(kGhThreads, 1) gh_head_kernel(const __grid_con
     const int r0 = t >> 3, cch = t & 7;
     constexpr int kRowsPerThread = kGhRows / 8;
     uint32_t it_i = 0, it_r = 0;  // stages issued / published by this thread
-    int item = blockIdx.x, kc = 0, n = 0;
+    int li = 0, item = order(0), kc = 0, n = 0;
     int rid[kRowsPerThread];
     const uint8_t* hb = reinterpret_cast<const uint8_t*>(g.h);
     for (;;) {
@@ -550,7 +589,7 @@ __global__ void __launch_bounds__(kGhThreads, 1) gh_head_kernel(const __grid_con
         ++it_i;
         if (++kc == KC) {
           kc = 0;
-          item += G;
+          item = order(++li);
         }
       } else if (it_i != it_r) {  // publish the oldest pending stage once its copies have landed
         switch (it_i - it_r) {
@@ -572,7 +611,7 @@ __global__ void __launch_bounds__(kGhThreads, 1) gh_head_kernel(const __grid_con
     const int q = warp & 3, row = 32 * q + lane, et = threadIdx.x - 128;  // et: 0..127
     const int K = g.k_t, rec = 2 + 2 * K;
     int li = 0;
-    for (int item = blockIdx.x; item < nitems; item += G, ++li) {
+    for (int item = order(0); item < nitems; item = order(++li)) {
       const int4 itm = __ldg(g.items + item);
       const int v0 = itm.x, nv = itm.y & 0xffff, part = itm.y >> 16, n = itm.w;
       const int buf = li & 1;

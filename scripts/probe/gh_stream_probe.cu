@@ -26,6 +26,51 @@ __device__ __forceinline__ void box(void* dst, const CUtensorMap* m, int x, int 
 constexpr int D = 5376, KCH = D / 64, STAGE = 32768;
 constexpr long long ROWS = 262144;
 
+__device__ __forceinline__ bool test(uint64_t* b, uint32_t par) {
+  uint32_t ok;
+  asm volatile("{.reg .pred p; mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0,1,0,p;}" : "=r"(ok) : "r"(su(b)), "r"(par) : "memory");
+  return ok;
+}
+__device__ __forceinline__ void spin(uint64_t* b, uint32_t par) { while (!test(b, par)) { } }
+
+// relay modes: warp 0 lane 0 = producer (waits empty[s]), warp 1 lane 0 = consumer (waits full[s], arrives empty[s])
+__global__ void __launch_bounds__(64, 1) krelay(const __grid_constant__ CUtensorMap m256, int S, int use_spin, float* sink) {
+  extern __shared__ __align__(1024) char sm[];
+  __shared__ __align__(8) uint64_t full[8], empty[8];
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < S; ++i) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su(&full[i])));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su(&empty[i])));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int G = gridDim.x;
+  const long long nst = 0;
+  (void)nst;
+  if (threadIdx.x == 0) {
+    long long c = 0;
+    for (int it = blockIdx.x; it < ROWS / 256; it += G)
+      for (int kc = 0; kc < KCH; ++kc, ++c) {
+        const int s = (int)(c % S);
+        const uint32_t par = (uint32_t)(((c / S) & 1) ^ 1);
+        if (use_spin) spin(&empty[s], par); else wait(&empty[s], par);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su(&full[s])), "r"(STAGE) : "memory");
+        box(sm + s * STAGE, &m256, kc * 64, it * 256, &full[s]);
+      }
+  } else if (threadIdx.x == 32) {
+    long long c = 0;
+    for (int it = blockIdx.x; it < ROWS / 256; it += G)
+      for (int kc = 0; kc < KCH; ++kc, ++c) {
+        const int s = (int)(c % S);
+        const uint32_t par = (uint32_t)((c / S) & 1);
+        if (use_spin) spin(&full[s], par); else wait(&full[s], par);
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su(&empty[s])) : "memory");
+      }
+    sink[blockIdx.x] = sm[5];
+  }
+}
+
 __global__ void __launch_bounds__(32, 1) k(const __grid_constant__ CUtensorMap m256, const __grid_constant__ CUtensorMap m64,
                                            const char* raw, int mode, int S, float* sink) {
   extern __shared__ __align__(1024) char sm[];
@@ -125,5 +170,23 @@ int main() {
     printf("%-34s %8.1f us  %7.0f GB/s  %s\n", names[i], best * 1e3, bytes / (best * 1e-3) / 1e9,
            cudaGetErrorString(cudaGetLastError()));
   }
+  cudaFuncSetAttribute(krelay, cudaFuncAttributeMaxDynamicSharedMemorySize, 6 * STAGE);
+  for (int S : {4, 6})
+    for (int sp : {0, 1}) {
+      float best = 1e9f;
+      for (int rep = 0; rep < 3; ++rep) {
+        cudaMemset(flush, rep, 512 << 20);
+        k_read<<<148 * 4, 512>>>((const int4*)clean, (512ll << 20) / 16, so);
+        cudaEventRecord(a);
+        krelay<<<148, 64, S * STAGE>>>(m256, S, sp, sink);
+        cudaEventRecord(b);
+        cudaEventSynchronize(b);
+        float ms;
+        cudaEventElapsedTime(&ms, a, b);
+        best = ms < best ? ms : best;
+      }
+      printf("relay (producer <- consumer thread) S=%d %s %8.1f us  %7.0f GB/s  %s\n", S, sp ? "test_wait spin" : "try_wait      ",
+             best * 1e3, bytes / (best * 1e-3) / 1e9, cudaGetErrorString(cudaGetLastError()));
+    }
   return 0;
 }
