@@ -119,6 +119,13 @@ cudaError_t launch_tc_head(const ds_clusters* c, const void* h_new, int R, const
                            const int32_t* sel_count, const int32_t* sl_offsets, int k_t, int64_t max_shortlist,
                            int32_t* top_ids, float* top_logits, float* top_logp, float* lse, float* z_out,
                            int64_t z_stride, float* part, unsigned* counter, cudaStream_t st, bool pdl);
+// ---- balanced tree head (th.cu): <= 16 rows sharing one shortlist, k_t <= 16 (dispatched by launch_tc_head)
+bool th_supported(const ds_clusters* c, int R, int k_t);
+size_t th_ws_bytes(const ds_clusters* c, int R, int k_t);
+cudaError_t launch_th(const ds_clusters* c, const void* h_new, int R, const int32_t* sel, const int32_t* sel_count,
+                      const int32_t* sl_offsets, int k_t, int64_t max_shortlist, int32_t* top_ids,
+                      float* top_logits, float* top_logp, float* lse, float* z_out, int64_t z_stride, void* ws,
+                      unsigned* counter, cudaStream_t st, bool pdl);
 bool use_tc_head(const ds_clusters* c, int B, int k_t, int shared, int64_t max_shortlist);
 // batched per-row rows (each with its own selection), streamed once as their union on tcgen05
 bool tc_batched_supported(const ds_clusters* c, int B, int k_t);

@@ -17,6 +17,14 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
       "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar)), "l"(policy)
       : "memory");
 }
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int x, int y, int z, uint64_t* bar,
+                                            uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint "
+      "[%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_commit(uint64_t* bar) {
@@ -75,6 +83,22 @@ inline bool make_map(CUtensorMap* m, const void* base, uint64_t rows, uint64_t d
   const cuuint32_t box[2] = {64u, box_rows};
   const cuuint32_t estr[2] = {1, 1};
   return f(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// [rows x d] bf16 viewed as (64 elements, rows, d / 64 K chunks): a box {64, box_rows, box_chunks}
+// lands as box_chunks K-chunk images of box_rows x 128 B (128B swizzle) — one TMA op loads several
+// K chunks of a row block, each row read as box_chunks x 128 contiguous bytes.  d % 64 == 0.
+inline bool make_map_kchunks(CUtensorMap* m, const void* base, uint64_t rows, uint64_t d, uint32_t box_rows,
+                             uint32_t box_chunks) {
+  EncodeTiledFn f = encode_fn();
+  if (!f || d % 64 != 0) return false;
+  const cuuint64_t dims[3] = {64, rows, d / 64};
+  const cuuint64_t strides[2] = {d * 2, 128};
+  const cuuint32_t box[3] = {64u, box_rows, box_chunks};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  return f(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }

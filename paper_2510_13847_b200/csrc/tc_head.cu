@@ -610,12 +610,12 @@ cudaError_t launch_tc_batched(const ds_clusters* c, const void* h_new, int B, co
 
 bool tc_head_supported(const ds_clusters* c, int R, int k_t, int64_t max_shortlist) {
   TcPlan p;
-  return tc_plan(c, R, k_t, max_shortlist, &p);
+  return th_supported(c, R, k_t) || tc_plan(c, R, k_t, max_shortlist, &p);
 }
 
 size_t tc_head_part_bytes(const ds_clusters* c, int R, int k_t) {
   TcPlan p;
-  return tc_plan(c, R, k_t, 0, &p) ? p.hp.part_bytes : 0;
+  return std::max(tc_plan(c, R, k_t, 0, &p) ? p.hp.part_bytes : (size_t)0, th_ws_bytes(c, R, k_t));
 }
 
 cudaError_t launch_tc_head(const ds_clusters* c, const void* h_new, int R, const int32_t* sel,
@@ -627,6 +627,10 @@ cudaError_t launch_tc_head(const ds_clusters* c, const void* h_new, int R, const
   // Epilogue choice by the per-CTA logit bound lcap: <= 4 tiles keep the logits on chip for one
   // per-CTA partial (Qwen tree depths: 94 vs 96 us online); more use the online per-tile running
   // (max, sum, top-k) (dense k = M on the Qwen head: 255 vs 526+ us).  z_out needs the logits.
+  // <= 16 tree rows: the balanced tree head (th.cu)
+  if (th_supported(c, R, k_t))
+    return launch_th(c, h_new, R, sel, sel_count, sl_offsets, k_t, max_shortlist, top_ids, top_logits, top_logp, lse,
+                     z_out, z_stride, part, counter, st, pdl);
   TcPlan p;
   if (!tc_plan(c, R, k_t, max_shortlist, &p, 0)) return cudaErrorInvalidValue;
   const char* ov = getenv("DS_TC_ONLINE");  // "0" / "1": force (tuning)

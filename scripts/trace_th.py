@@ -1,0 +1,60 @@
+"""Per-CTA phase marks of the balanced tree head (th.cu) over the Qwen tree cycle (L2 flushed before
+the cycle, depths back to back, as trace_tc.py).  Marks: 0 start (before the dependency wait),
+1 plan done, 2 streamed + TMEM drained, 3 merge start (merging CTAs), 4 done."""
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2510_13847_b200 import dynaspec as D  # noqa: E402
+from synth import inputs as S  # noqa: E402
+
+cfg = sys.argv[1] if len(sys.argv) > 1 else "qwen25"
+reps = int(os.environ.get("REPS", "10"))
+C = S.CONFIGS[cfg]
+dev = "cuda"
+W = S.lm_head(C.V, C.d, 0, "bf16", device=dev)
+tau = torch.as_tensor(S.random_partition(C.V, C.M, 2, zipf=0.0), dtype=torch.int32, device=dev)
+c = D.Clusters.from_tau(W, tau, C.M)
+r = D.Router(*[x.to(dev) for x in S.router(C.d, C.h_r, C.M, 1, "bf16")])
+steps = [D.DraftStep(c, r, C.B, C.k_t, shared=C.shared) for _ in range(C.positions)]
+G = torch.cuda.get_device_properties(0).multi_processor_count
+bufs = [torch.zeros(G * 64, dtype=torch.int64, device=dev) for _ in range(C.positions)]
+flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+inp = [[x.to(dev) for x in S.step_inputs(C.B, C.d, t, "bf16", sibling_eps=0.1)] for t in range(C.positions)]
+ns = np.zeros((reps, C.positions, G, 16))
+ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+tot = []
+for rep in range(reps + 2):
+    flush.zero_()
+    for bb in bufs:
+        bb.zero_()
+    torch.cuda.synchronize()
+    ev[0].record()
+    for t in range(C.positions):
+        D.debug_set_trace(bufs[t])
+        steps[t](*inp[t], t, C.k_max, C.k_min)
+    ev[1].record()
+    D.debug_set_trace(None)
+    torch.cuda.synchronize()
+    if rep >= 2:
+        tot.append(ev[0].elapsed_time(ev[1]) * 1e3 / C.positions)
+        for t in range(C.positions):
+            ns[rep - 2, t] = bufs[t].view(G, 64).cpu().numpy()[:, :16]
+print(f"us per step (traced, events): {np.median(tot):.1f}")
+for t in range(C.positions):
+    print(f"t={t} positions per CTA: max {int(ns[-1, t, :, 12].max())} median {int(np.median(ns[-1, t, :, 12]))}")
+names = {0: "start", 1: "plan", 5: "H", 6: "slot0", 7: "issued", 8: "mma_done", 2: "streamed", 10: "keys", 9: "records", 3: "merge0", 4: "done"}
+for t in range(C.positions):
+    a = ns[:, t]
+    t0 = np.where(a[:, :, 0] > 0, a[:, :, 0], np.inf).min(1)
+    line = []
+    for sl, nm in names.items():
+        x = a[:, :, sl]
+        if (x > 0).any():
+            mx = np.median([np.max(xx[xx > 0]) - tt for xx, tt in zip(x, t0) if (xx > 0).any()]) / 1e3
+            md = np.median([np.median(xx[xx > 0]) - tt for xx, tt in zip(x, t0) if (xx > 0).any()]) / 1e3
+            line.append(f"{nm}={mx:.2f}(med {md:.2f})")
+    print(f"t={t} k={steps[t].k if hasattr(steps[t], 'k') else ''}: " + " ".join(line))

@@ -394,11 +394,13 @@ def test_error_codes():
 
 # ------------------------------------------------------------------ tcgen05 shared-shortlist head (S5')
 
-@pytest.mark.parametrize("R,d", [(4, 256), (10, 200), (17, 512), (64, 128)])
-def test_tc_head_exact_bit_exact(R, d, monkeypatch):
+@pytest.mark.parametrize("th", ["1", "0"])  # balanced tree head (th.cu, R <= 16) / general tc_head
+@pytest.mark.parametrize("R,d", [(4, 256), (10, 200), (16, 128), (17, 512), (64, 128)])
+def test_tc_head_exact_bit_exact(R, d, th, monkeypatch):
     """Tree rows sharing one shortlist on the tensor cores: every logit bit-exact vs the oracle
     (exact regime keeps partial sums < 2^21 units), and identical to the CUDA-core path."""
     Dy = _dyn()
+    monkeypatch.setenv("DS_TH", th)
     V, M = 6007, 24
     q = max(1, min(127, int((2 ** 21 / d) ** 0.5)))
     W = S.lm_head(V, d, 0, "bf16", "exact", q=q)
@@ -431,10 +433,12 @@ def test_tc_head_exact_bit_exact(R, d, monkeypatch):
             assert outs["tc"]["top_ids"][r].cpu().tolist() == outs["cuda"]["top_ids"][r].cpu().tolist()
 
 
-def test_tc_head_random_regime_qwen_full_size(monkeypatch):
+@pytest.mark.parametrize("th", ["1", "0"])
+def test_tc_head_random_regime_qwen_full_size(th, monkeypatch):
     """Qwen-2.5 head at full size (V=151936, d=3584, M=256), 10 tree rows, tcgen05 vs oracle."""
     Dy = _dyn()
     monkeypatch.setenv("DS_DISABLE_TC", "0")
+    monkeypatch.setenv("DS_TH", th)
     C = S.CONFIGS["qwen25"]
     W, rt, tau, part, c, r = _setup(C.V, C.d, C.M, C.h_r, "bf16", "random")
     st = Dy.DraftStep(c, r, C.B, C.k_t, shared=True, z_out=True)
@@ -452,6 +456,52 @@ def test_tc_head_random_regime_qwen_full_size(monkeypatch):
         assert np.max(np.abs(z - ref[b]["z"])) <= 2e-2
         check_topk(st.top_ids[b].cpu().numpy(), st.top_logits[b].cpu().numpy(), st.top_logp[b].cpu().numpy(),
                    st.lse[b].item(), ref[b]["z"], ref[b]["V_S"], C.k_t, torch.bfloat16)
+
+
+@pytest.mark.parametrize("R,kt", [(4, 1), (16, 16), (7, 5)])
+def test_th_tree_head_ragged_exact(R, kt, monkeypatch):
+    """Balanced tree head (th.cu): clusters of every size mod 8 (1..37 rows: pieces ending inside an
+    8-row group, singletons, runs of adjacent selected clusters), k in {1, 3, M}; ids, logits and the
+    token order bit-exact against the oracle, lse within the exact-regime bound; a shortlist bound
+    below the union gives the documented sentinel (ids -1, lse NaN)."""
+    Dy = _dyn()
+    monkeypatch.setenv("DS_DISABLE_TC", "0")
+    monkeypatch.setenv("DS_TH", "1")
+    d, M = 192, 40
+    sizes = np.array([1 + (7 * m) % 37 for m in range(M)])
+    V = int(sizes.sum())
+    tau = np.repeat(np.arange(M), sizes)
+    np.random.default_rng(3).shuffle(tau)
+    tau = O.canonical_relabel(tau, M) if hasattr(O, "canonical_relabel") else tau
+    perm, offs = O.layout(tau, M)
+    part = {"perm": perm, "offsets": offs}
+    q = max(1, min(127, int((2 ** 21 / d) ** 0.5)))
+    W = S.lm_head(V, d, 0, "bf16", "exact", q=q)
+    c = Dy.Clusters.from_tau(W.to(DEV), torch.as_tensor(tau, dtype=torch.int32, device=DEV), M)
+    hn = S.hidden(R, d, 17, "bf16", "exact", q=q)
+    rng = np.random.default_rng(R + kt)
+    for k in (1, 3, M):
+        sel = np.sort(rng.choice(M, k, replace=False)).astype(np.int32)
+        if int(sizes[sel].sum()) < kt:
+            continue
+        selt = torch.zeros((1, M), dtype=torch.int32)
+        selt[0, :k] = torch.as_tensor(sel)
+        off = torch.zeros((1, M + 1), dtype=torch.int32)
+        off[0, :k + 1] = torch.as_tensor(O.shortlist_offsets(sel, part["offsets"]), dtype=torch.int32)
+        cnt = torch.tensor([k], dtype=torch.int32)
+        out = Dy.head_forward(c, hn.to(DEV), selt.to(DEV), cnt.to(DEV), off.to(DEV), kt, shared=True, z_out=True)
+        V_S = O.shortlist(sel, part["perm"], part["offsets"])
+        zref = O.head(f64(hn), f64(W), V_S)
+        n = len(V_S)
+        for r in range(R):
+            assert np.array_equal(out["z"][r, :n].cpu().numpy(), zref[r].astype(np.float32)), (R, kt, k, r)
+            check_topk(out["top_ids"][r].cpu().numpy(), out["top_logits"][r].cpu().numpy(),
+                       out["top_logp"][r].cpu().numpy(), out["lse"][r].item(), zref[r], V_S, kt, torch.float32,
+                       exact=True)
+        if n > kt:
+            out = Dy.head_forward(c, hn.to(DEV), selt.to(DEV), cnt.to(DEV), off.to(DEV), kt, shared=True,
+                                  max_shortlist=n - 1)
+            assert (out["top_ids"].cpu() == -1).all() and torch.isnan(out["lse"].cpu()).all()
 
 
 # ------------------------------------------------------------------ batched per-row rows on tcgen05 (K5/S5')
@@ -566,14 +616,15 @@ def test_router_many_rows_row_blocks():
             assert st.sel[b, :cnt].cpu().tolist() == ref["sel"].tolist()
 
 
-@pytest.mark.parametrize("online", ["1", "0"])
-def test_tc_head_shared_online_epilogue_exact(online, monkeypatch):
+@pytest.mark.parametrize("online,th", [("1", "0"), ("0", "0"), ("0", "1")])
+def test_tc_head_shared_online_epilogue_exact(online, th, monkeypatch):
     """Tree rows on the tensor cores without z_out and a per-CTA logit bound above 4 tiles: the
     online per-tile (max, sum, top-k) epilogue (and, forced off, the on-chip partial) give the
     oracle's top ids / logits exactly and its lse (exact regime)."""
     Dy = _dyn()
     monkeypatch.setenv("DS_DISABLE_TC", "0")
     monkeypatch.setenv("DS_TC_ONLINE", online)
+    monkeypatch.setenv("DS_TH", th)  # th.cu: several 128-row tiles per CTA (double-buffered TMEM)
     V, d, M, R, kt = 80021, 256, 24, 10, 8
     q = max(1, min(127, int((2 ** 21 / d) ** 0.5)))
     W = S.lm_head(V, d, 0, "bf16", "exact", q=q)
