@@ -144,7 +144,7 @@ __global__ void __launch_bounds__(kMetaThreads) meta_l2_kernel(const float* __re
                                                                const int32_t* __restrict__ offsets, int k,
                                                                const int32_t* __restrict__ k_per_row, int shared,
                                                                int32_t* sel, int32_t* sel_count, int32_t* sl_off,
-                                                               unsigned* counter, int pdl) {
+                                                               unsigned* counter, int pdl, unsigned long long* trace) {
   __shared__ __align__(16) float a1[kMaxM];
   __shared__ __align__(16) float s[kMaxM];
   __shared__ uint32_t mask[kMaxM / 32], acc[kMaxM / 32];
@@ -160,10 +160,19 @@ __global__ void __launch_bounds__(kMetaThreads) meta_l2_kernel(const float* __re
   for (int m = threadIdx.x; m < M; m += blockDim.x) b2s[m] = h_r > 0 ? b2[m] : 0.f;
   if (offsets)
     for (int m = threadIdx.x; m <= M; m += blockDim.x) offs[m] = offsets[m];
+  if (h_r > 0 && threadIdx.x == 0) {  // W2 into L2 while the upstream kernel finishes: slice b of B
+    const size_t bytes = (size_t)M * h_r * sizeof(T);
+    const size_t per = ((bytes + gridDim.x - 1) / gridDim.x + 15) & ~(size_t)15;
+    const size_t lo = (size_t)b * per;
+    if (lo < bytes) bulk_prefetch_l2(reinterpret_cast<const uint8_t*>(W2) + lo, (uint32_t)min(per, bytes - lo));
+  }
+  trace_mark(trace, 16);
   if (pdl) pdl_wait();
   __syncthreads();
+  trace_mark(trace, 17);
   router_hidden(part, KS, B, b, rows1, b1s, h_r > 0, a1);
   __syncthreads();
+  trace_mark(trace, 18);
   if (h_r > 0) {
     router_scores_thread<T>(W2, a1, b2s, M, h_r, s);
   } else {
@@ -174,9 +183,12 @@ __global__ void __launch_bounds__(kMetaThreads) meta_l2_kernel(const float* __re
   for (int m = threadIdx.x; m < M; m += blockDim.x) scores[(size_t)b * M + m] = s[m];
   if (sel == nullptr) return;
   if (pdl) pdl_launch_dependents();
-  if (M > 128) radix_mask(s, M, k_per_row ? k_per_row[b] : k, mask, rhist);
+  trace_mark(trace, 19);
+  // O(M^2 / threads) rank count up to M = 256 (one score per thread: 0.5 us); radix select above
+  if (M > 256) radix_mask(s, M, k_per_row ? k_per_row[b] : k, mask, rhist);
   else rank_mask(s, M, k_per_row ? k_per_row[b] : k, mask);
   __syncthreads();
+  trace_mark(trace, 20);
   if (!shared) {
     emit_fast(mask, M, offs, sel + (size_t)b * M, sel_count + b, sl_off + (size_t)b * (M + 1), tmp);
     return;
@@ -188,6 +200,7 @@ __global__ void __launch_bounds__(kMetaThreads) meta_l2_kernel(const float* __re
   __syncthreads();
   if (threadIdx.x == 0) is_last = release_add(counter, 1u) == (unsigned)(gridDim.x - 1);
   __syncthreads();
+  trace_mark(trace, 21);
   if (!is_last) return;
   if (threadIdx.x == 0) fence_acq_rel_gpu();
   __syncthreads();
@@ -199,6 +212,7 @@ __global__ void __launch_bounds__(kMetaThreads) meta_l2_kernel(const float* __re
   __syncthreads();
   emit_fast(acc, M, offs, sel, sel_count, sl_off, tmp);
   if (threadIdx.x == 0) *counter = 0u;
+  trace_mark(trace, 22);
 }
 
 // ------------------------------------------------------------------ host side
@@ -271,7 +285,7 @@ static cudaError_t launch_meta_t(const ds_router* r, const void* h_prev, const v
   c2.numAttrs = 1;  // layer 2 always follows layer 1 in-stream
   return cudaLaunchKernelEx(&c2, meta_l2_kernel<T>, (const float*)part, KS, B, p.rows1, r->b1,
                             static_cast<const T*>(r->W2), r->b2, r->h_r, r->M, scores, offsets, k, k_per_row,
-                            shared, sel, sel_count, sl_offsets, counter, 1);
+                            shared, sel, sel_count, sl_offsets, counter, 1, debug_trace());
 }
 
 cudaError_t launch_meta(const ds_router* r, const void* h_prev, const void* e, int B, float* scores, float* part,

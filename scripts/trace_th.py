@@ -24,7 +24,7 @@ G = torch.cuda.get_device_properties(0).multi_processor_count
 bufs = [torch.zeros(G * 64, dtype=torch.int64, device=dev) for _ in range(C.positions)]
 flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
 inp = [[x.to(dev) for x in S.step_inputs(C.B, C.d, t, "bf16", sibling_eps=0.1)] for t in range(C.positions)]
-ns = np.zeros((reps, C.positions, G, 16))
+ns = np.zeros((reps, C.positions, G, 32))
 ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
 tot = []
 for rep in range(reps + 2):
@@ -42,7 +42,7 @@ for rep in range(reps + 2):
     if rep >= 2:
         tot.append(ev[0].elapsed_time(ev[1]) * 1e3 / C.positions)
         for t in range(C.positions):
-            ns[rep - 2, t] = bufs[t].view(G, 64).cpu().numpy()[:, :16]
+            ns[rep - 2, t] = bufs[t].view(G, 64).cpu().numpy()[:, :32]
 print(f"us per step (traced, events): {np.median(tot):.1f}")
 for t in range(C.positions):
     print(f"t={t} positions per CTA: max {int(ns[-1, t, :, 12].max())} median {int(np.median(ns[-1, t, :, 12]))}")
@@ -58,3 +58,16 @@ for t in range(C.positions):
             md = np.median([np.median(xx[xx > 0]) - tt for xx, tt in zip(x, t0) if (xx > 0).any()]) / 1e3
             line.append(f"{nm}={mx:.2f}(med {md:.2f})")
     print(f"t={t} k={steps[t].k if hasattr(steps[t], 'k') else ''}: " + " ".join(line))
+
+# router layer 2 (meta_l2_kernel, one CTA per row; slots 16-22), relative to the th kernel's first start
+ln = {16: "l2start", 17: "l2wait", 18: "hidden", 19: "scores", 20: "topk", 21: "ticket", 22: "union"}
+for t in range(C.positions):
+    a = ns[:, t]
+    t0 = np.where(a[:, :, 0] > 0, a[:, :, 0], np.inf).min(1)
+    line = []
+    for sl, nm in ln.items():
+        x = a[:, :C.B, sl]
+        if (x > 0).any():
+            mx = np.median([np.max(xx[xx > 0]) - tt for xx, tt in zip(x, t0) if (xx > 0).any()]) / 1e3
+            line.append(f"{nm}={mx:.2f}")
+    print(f"t={t} router: " + " ".join(line))
