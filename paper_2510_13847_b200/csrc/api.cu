@@ -464,7 +464,9 @@ const char* dynaspec_draft_step_kernel(const ds_clusters* c, const ds_router* r,
   HeadPlan p;
   if (!c || !r || !head_plan(c, B, k_t, 0, &p)) return "?";
   const int64_t ms = shared ? c->V : 0;
-  if (use_tc_head(c, B, k_t, shared, ms)) return "ds::tc_head_kernel (tcgen05, shared shortlist)";
+  if (use_tc_head(c, B, k_t, shared, ms))
+    return th_supported(c, B, k_t) ? "ds::th_kernel (tcgen05 balanced tree head: one cluster per CTA, 3-D TMA boxes)"
+                                   : "ds::tc_head_kernel (tcgen05, shared shortlist)";
   if (use_gh(c, B, k_t, shared, z_out != 0, c->M))
     return "ds::gh_head_kernel (tcgen05 grouped head: every selected cluster block once for the rows that chose it)";
   if (use_tc_batched(c, B, k_t, shared, z_out != 0))

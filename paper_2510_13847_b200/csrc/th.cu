@@ -219,11 +219,11 @@ __global__ void __launch_bounds__(kThThreads, 1) th_kernel(const __grid_constant
   for (int i = tid; i <= M; i += kThThreads) soff[i] = __ldg(a.offsets + i);
   trace_mark(a.trace, 0);
   if (a.pdl) pdl_wait();
+  trace_mark(a.trace, 13);  // dependency released
   __syncthreads();  // barriers initialised
-  if (tid == 0) {   // H (produced upstream) as soon as the wait is over: one box per K chunk
+  if (tid == 0) {  // H (produced upstream) as soon as the wait is over: ONE 3-D box, all K chunks
     mbar_arrive_expect_tx(hbar, (uint32_t)a.kchunks * kThN * 128);
-    const uint64_t pol_h = policy_evict_last();
-    for (int kc = 0; kc < a.kchunks; ++kc) tma_load_2d(hs + (size_t)kc * kThN * 128, &tmH, kc * 64, 0, hbar, pol_h);
+    tma_load_3d(hs, &tmH, 0, 0, 0, hbar, policy_evict_last());
   }
   // the selection (count, ids, offsets) in one round of loads, whatever the count
   if (tid == 32) misc[7] = __ldcg(a.sel_count);
@@ -233,6 +233,7 @@ __global__ void __launch_bounds__(kThThreads, 1) th_kernel(const __grid_constant
     else sslo[i - M] = __ldcg(a.sl_off + (i - M));
   }
   __syncthreads();
+  trace_mark(a.trace, 14);  // selection staged
 
   // ---- plan (warp 0): this CTA's tiles.  Cluster i of the union (positions [so_i, so_i + n_i))
   // owns CTAs [s_i, s_(i+1)), s_i = round(G so_i / |V_S|); its 8-row groups are split evenly over
@@ -244,7 +245,7 @@ __global__ void __launch_bounds__(kThThreads, 1) th_kernel(const __grid_constant
     const int total = cnt > 0 ? sslo[cnt] : 0;
     const bool fits = cnt > 0 && cnt <= M && (a.max_shortlist <= 0 || (long long)total <= a.max_shortlist);
     const int ncl = fits ? cnt : 0;
-    const long long NU = total > 0 ? total : 1;
+    const unsigned NU = total > 0 ? (unsigned)total : 1u;  // 2 G |V_S| + |V_S| < 2^32 (host: V G < 2^30)
     int nt = 0, p0 = INT_MAX, p1 = 0;
     for (int i0 = 0; i0 < ncl; i0 += 32) {
       const int i = i0 + lane;
@@ -253,13 +254,13 @@ __global__ void __launch_bounds__(kThThreads, 1) th_kernel(const __grid_constant
         so = sslo[i];
         const int n = sslo[i + 1] - so;
         m = ssel[i];
-        const int si = (int)(((long long)G * so * 2 + NU) / (2 * NU));
-        const int sn = i + 1 < ncl ? (int)(((long long)G * sslo[i + 1] * 2 + NU) / (2 * NU)) : G;
+        const int si = (int)(((unsigned)G * (unsigned)so * 2u + NU) / (2u * NU));
+        const int sn = i + 1 < ncl ? (int)(((unsigned)G * (unsigned)sslo[i + 1] * 2u + NU) / (2u * NU)) : G;
         if (sn > si) {
           if (b >= si && b < sn) {
             const int c = sn - si, j = b - si, ng = (n + 7) >> 3;
-            r0 = min(n, 8 * (int)(((long long)j * ng) / c));
-            r1 = min(n, 8 * (int)(((long long)(j + 1) * ng) / c));
+            r0 = min(n, 8 * (int)(((unsigned)j * (unsigned)ng) / (unsigned)c));
+            r1 = min(n, 8 * (int)(((unsigned)(j + 1) * (unsigned)ng) / (unsigned)c));
           }
         } else if (min(si, G - 1) == b) {
           r1 = n;
@@ -598,7 +599,8 @@ static bool th_plan(const ds_clusters* c, int R, int k_t, ThPlan* p) {
   if (c->dtype != DS_BF16 || R < 1 || R > kThN || k_t < 1 || k_t > kThMaxKt || (c->d % 64) != 0) return false;
   if (c->M < 1 || c->M > kMaxM) return false;
   const int G = num_sms();
-  if (G > kThMaxG) return false;
+  if (G > kThMaxG || c->V * (int64_t)G >= (int64_t)1 << 30) return false;  // 32-bit CTA-range arithmetic
+  if ((c->d + 63) / 64 > 256) return false;                                   // H box: <= 256 K chunks
   const int kchunks = (c->d + 63) / 64;
   // union positions per CTA: a share of its big cluster (< 2 shares) + the small clusters rounded
   // to it (< 1 share) + up to 7 rows of group rounding; a share is |V_S| / G <= V / G
@@ -645,8 +647,9 @@ cudaError_t launch_th(const ds_clusters* c, const void* h_new, int R, const int3
     if (!make_map_kchunks(&mw.w[j], c->W_perm, (uint64_t)c->V, (uint64_t)c->d, (uint32_t)(8 * (j + 1)),
                           (uint32_t)th_cpc(8 * (j + 1))))
       return cudaErrorInvalidValue;
-  CUtensorMap mh;
-  if (!make_map(&mh, h_new, (uint64_t)R, (uint64_t)c->d, (uint32_t)kThN)) return cudaErrorInvalidValue;
+  CUtensorMap mh;  // H as (64, R rows, K chunks): one box {64, 16, kchunks} = the whole [chunk][16][128 B] image
+  if (!make_map_kchunks(&mh, h_new, (uint64_t)R, (uint64_t)c->d, (uint32_t)kThN, (uint32_t)((c->d + 63) / 64)))
+    return cudaErrorInvalidValue;
   uint8_t* w8 = static_cast<uint8_t*>(ws);
   ThArgs a;
   a.sel = sel;
