@@ -28,7 +28,8 @@ ns = np.zeros((reps, C.positions, G, 32))
 ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
 tot = []
 for rep in range(reps + 2):
-    flush.zero_()
+    if not os.environ.get("NOFLUSH"):
+        flush.zero_()
     for bb in bufs:
         bb.zero_()
     torch.cuda.synchronize()
@@ -46,7 +47,7 @@ for rep in range(reps + 2):
 print(f"us per step (traced, events): {np.median(tot):.1f}")
 for t in range(C.positions):
     print(f"t={t} positions per CTA: max {int(ns[-1, t, :, 12].max())} median {int(np.median(ns[-1, t, :, 12]))}")
-names = {0: "start", 1: "plan", 5: "H", 6: "slot0", 7: "issued", 8: "mma_done", 2: "streamed", 10: "keys", 9: "records", 3: "merge0", 4: "done"}
+names = {0: "start", 13: "released", 14: "sel", 1: "plan", 5: "H", 6: "slot0", 7: "issued", 8: "mma_done", 2: "streamed", 10: "keys", 9: "records", 3: "merge0", 4: "done"}
 for t in range(C.positions):
     a = ns[:, t]
     t0 = np.where(a[:, :, 0] > 0, a[:, :, 0], np.inf).min(1)
