@@ -680,6 +680,8 @@ cudaError_t launch_th(const ds_clusters* c, const void* h_new, int R, const int3
   a.lse = lse;
   a.counter = counter + 16;  // [16] arrivals, [17] finished mergers (no other kernel uses them)
   a.err = reinterpret_cast<unsigned*>(reinterpret_cast<uint8_t*>(counter) + kWsErrorWord);
+  const char* np_ = getenv("DS_TH_NOPDL");  // A/B: launch without programmatic dependent launch
+  if (np_ && np_[0] == '1') pdl = false;
   a.pdl = pdl ? 1 : 0;
   const char* dbg = getenv("DS_TH_DBG");
   a.dbg = dbg ? atoi(dbg) : 0;
@@ -697,7 +699,7 @@ cudaError_t launch_th(const ds_clusters* c, const void* h_new, int R, const int3
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl ? 1 : 0;
-  return cudaLaunchKernelEx(&cfg, th_kernel, mw, mh, a);
+  return cudaLaunchKernelEx(&cfg, th_kernel, mw, mh, a);  // (pdl false: plain stream order)
 }
 
 }  // namespace ds
