@@ -36,9 +36,10 @@
  *    last-CTA merges wait on a grid counter).  A concurrent kernel that keeps SMs busy delays
  *    them; the single-row step kernels bound every wait (2 s) and then raise
  *    DS_ERR_DEVICE_TIMEOUT in the workspace error word (dynaspec_ws_error) instead of hanging.
- *  - Workspace layout: the first 112 KB of every workspace are a fixed prefix (counters, the
- *    device error word, the polled-record regions of the single-row step kernels, written by no
- *    other kernel), so one workspace may serve any sequence of calls on one stream.
+ *  - Workspace layout: the first 132 KB of every workspace are a fixed prefix (counters, the
+ *    device error word, the polled-record / unit / mask words of the single-row step and
+ *    few-row router kernels, written by no other kernel), so one workspace may serve any
+ *    sequence of calls on one stream.
  *  - Precision: weights and activations are bf16 (DS_BF16) or fp32 (DS_F32), one dtype per
  *    call; every dot product accumulates in fp32; all floating outputs are fp32.
  *  - Determinism: no floating-point atomics; every reduction has a fixed order, so two

@@ -54,6 +54,19 @@ bool use_gh(const ds_clusters* c, int B, int k_t, int shared, bool z_out, int km
 
 static bool dtype_ok(int dt) { return dt == DS_BF16 || dt == DS_F32; }
 
+// S1 + S3/S4 for B rows: the few-row one-launch router (meta_rows.cu) when it applies, else the
+// split-K pair (meta.cu).  ws = the workspace base.
+static cudaError_t route_rows(const ds_router* r, const ds_clusters* c, const void* h_prev, const void* e, int B,
+                              float* scores, float* part, unsigned* counter, int k, int shared, int32_t* sel,
+                              int32_t* sel_count, int32_t* sl_offsets, void* ws, cudaStream_t st, bool pdl) {
+  const bool aligned = ((reinterpret_cast<uintptr_t>(h_prev) | reinterpret_cast<uintptr_t>(e) |
+                         reinterpret_cast<uintptr_t>(r->W1) | reinterpret_cast<uintptr_t>(r->W2)) & 15u) == 0;
+  if (aligned && meta_rows_supported(r, B, k, nullptr))
+    return launch_meta_rows(r, h_prev, e, B, scores, c->offsets, k, shared, sel, sel_count, sl_offsets, ws, st, pdl);
+  return launch_meta(r, h_prev, e, B, scores, part, counter, c->offsets, k, nullptr, shared, sel, sel_count,
+                     sl_offsets, st, pdl);
+}
+
 static ds_status check_clusters(const ds_clusters* c) {
   if (!c || !c->perm || !c->offsets || !c->W_perm) return DS_ERR_SHAPE;
   if (!dtype_ok(c->dtype)) return DS_ERR_DTYPE;
@@ -411,9 +424,9 @@ ds_status dynaspec_step_route(const ds_clusters* c, const ds_router* r, const vo
   if (!ws || ws_bytes < L.total) return DS_ERR_WORKSPACE;
   uint8_t* w8 = static_cast<uint8_t*>(ws);
   float* scores = out->scores ? out->scores : reinterpret_cast<float*>(w8 + L.meta + align_up(meta_bytes, 256));
-  return launch_meta(r, h_prev, e, B, scores, reinterpret_cast<float*>(w8 + L.meta),
-                     reinterpret_cast<unsigned*>(w8 + L.counters) + 1, c->offsets, k, nullptr, shared ? 1 : 0,
-                     out->sel, out->sel_count, out->sl_offsets, (cudaStream_t)s_meta, false) == cudaSuccess
+  return route_rows(r, c, h_prev, e, B, scores, reinterpret_cast<float*>(w8 + L.meta),
+                    reinterpret_cast<unsigned*>(w8 + L.counters) + 1, k, shared ? 1 : 0, out->sel, out->sel_count,
+                    out->sl_offsets, ws, (cudaStream_t)s_meta, false) == cudaSuccess
              ? DS_OK
              : DS_ERR_CUDA;
 }
@@ -450,13 +463,15 @@ int32_t dynaspec_draft_step_launches(const ds_clusters* c, const ds_router* r, i
   HeadPlan p;
   if (!c || !r || !head_plan(c, B, k_t, 0, &p)) return 0;
   const int64_t ms = shared ? c->V : 0;
-  if (use_tc_head(c, B, k_t, shared, ms)) return 3;  // meta layer 1, meta layer 2 (+union), tcgen05 head
-  if (use_gh(c, B, k_t, shared, z_out != 0, c->M))  // meta x2, grouping (1 or 3), grouped tcgen05 head, merge
-    return gh_wide_grouping(B, shared) ? 7 : 5;
+  // router: one launch (few rows, meta_rows.cu; 16-byte aligned inputs assumed) or layer 1 + layer 2
+  const int meta = meta_rows_supported(r, B, 1, nullptr) ? 1 : 2;
+  if (use_tc_head(c, B, k_t, shared, ms)) return meta + 1;  // router (+union), tcgen05 tree head
+  if (use_gh(c, B, k_t, shared, z_out != 0, c->M))  // router, grouping (1 or 3), grouped tcgen05 head, merge
+    return meta + (gh_wide_grouping(B, shared) ? 5 : 3);
   if (use_tc_batched(c, B, k_t, shared, z_out != 0))
-    return 2 + 2 * ((B + 127) / 128);  // meta x2, then (union + tcgen05 head) per 128 rows
+    return meta + 2 * ((B + 127) / 128);  // router, then (union + tcgen05 head) per 128 rows
   if (!two_streams && step_supported(c, r, B, k_t, shared, 0)) return 1;  // fused single-stream step
-  return 2 + p.launches;  // meta layer 1, meta layer 2 (+select), head chunks
+  return meta + p.launches;  // router (+select), head chunks
 }
 
 const char* dynaspec_draft_step_kernel(const ds_clusters* c, const ds_router* r, int32_t B, int32_t k_t,
@@ -558,8 +573,8 @@ ds_status dynaspec_draft_step(const ds_clusters* c, const ds_router* r, const vo
     if (cudaEventRecord((cudaEvent_t)ev_fork, sd) != cudaSuccess) return DS_ERR_CUDA;
     if (cudaStreamWaitEvent(sm, (cudaEvent_t)ev_fork, 0) != cudaSuccess) return DS_ERR_CUDA;
   }
-  cudaError_t err = launch_meta(r, h_prev, e, B, scores, meta_part, counters + 1, c->offsets, k, nullptr,
-                                shared ? 1 : 0, out->sel, out->sel_count, out->sl_offsets, sm, !two_streams);
+  cudaError_t err = route_rows(r, c, h_prev, e, B, scores, meta_part, counters + 1, k, shared ? 1 : 0, out->sel,
+                               out->sel_count, out->sl_offsets, ws, sm, !two_streams);
   if (err != cudaSuccess) return DS_ERR_CUDA;
   if (two_streams) {  // Alg. 1 line 10: "sync S_m, S_d"
     if (cudaEventRecord((cudaEvent_t)ev_join, sm) != cudaSuccess) return DS_ERR_CUDA;

@@ -1031,7 +1031,7 @@ static bool gstep_plan(const ds_clusters* c, const ds_router* r, int k_t, GStepP
     p->rows1 = r->h_r > 0 ? r->h_r : r->M;
     if (r->h_r > 0 && r->h_r > 64 * (esz == 2 ? 2 : 1)) return false;  // layer-2 register slice
     if (p->rows1 > kGUnits * G || p->rows1 > kGThreads) return false;  // one polled unit word per thread
-    if ((size_t)p->rows1 * 8 > kWsFixed - kWsGstepUnits) return false;
+    if ((size_t)p->rows1 * 8 > kWsRowsUnits - kWsGstepUnits) return false;
     if ((size_t)2 * c->d * esz > (size_t)kGXChunks * kGThreads * 16) return false;
   }
   const int rowb = c->d * esz;

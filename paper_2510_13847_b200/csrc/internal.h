@@ -19,7 +19,9 @@ constexpr size_t kWsErrorWord = 252;
 constexpr size_t kWsCstepRec = 256;                      // cluster step: [G][2 + k_t] u64 (<= 48 KB)
 constexpr size_t kWsGstepRec = kWsCstepRec + 48 * 1024;  // grid step:    [G][2 + k_t] u64 (<= 48 KB)
 constexpr size_t kWsGstepUnits = kWsGstepRec + 48 * 1024;  // grid step: [rows1] u64 layer-1 units (<= 4 KB)
-constexpr size_t kWsFixed = 112 * 1024;
+constexpr size_t kWsRowsUnits = 112 * 1024;                // few-row router: [16][h_r <= 128] u64 units
+constexpr size_t kWsRowsMasks = kWsRowsUnits + 16 * 1024;  // few-row router: [16][32] u64 TopK masks
+constexpr size_t kWsFixed = kWsRowsMasks + 4 * 1024;       // 132 KB
 
 int num_sms();
 unsigned long long* debug_trace();   // device buffer set by dynaspec_debug_set_trace, or nullptr                 // SM count of the current device (cached per device)
@@ -36,6 +38,12 @@ struct MetaPlan {
   size_t part_bytes;
 };
 bool meta_tc_plan(const ds_router* r, int B, int* KS, int* kc_per);
+// Few rows (2 <= B <= 16, bf16, h_r <= #SMs, M <= 256): router + TopK (+ union) in ONE launch over all
+// SMs (meta_rows.cu); ws = the workspace base (its unit / mask words live in the fixed prefix).
+bool meta_rows_supported(const ds_router* r, int B, int k, const int32_t* k_per_row);
+cudaError_t launch_meta_rows(const ds_router* r, const void* h_prev, const void* e, int B, float* scores,
+                             const int32_t* offsets, int k, int shared, int32_t* sel, int32_t* sel_count,
+                             int32_t* sl_offsets, void* ws, cudaStream_t st, bool pdl);
 cudaError_t launch_meta_tc_l1(const ds_router* r, const void* h_prev, const void* e, int B, float* part, int KS,
                               int kc_per, cudaStream_t st, bool pdl);
 MetaPlan meta_plan(const ds_router* r, int B);

@@ -24,7 +24,7 @@ G = torch.cuda.get_device_properties(0).multi_processor_count
 bufs = [torch.zeros(G * 64, dtype=torch.int64, device=dev) for _ in range(C.positions)]
 flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
 inp = [[x.to(dev) for x in S.step_inputs(C.B, C.d, t, "bf16", sibling_eps=0.1)] for t in range(C.positions)]
-ns = np.zeros((reps, C.positions, G, 32))
+ns = np.zeros((reps, C.positions, G, 64))
 ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
 tot = []
 for rep in range(reps + 2):
@@ -43,7 +43,7 @@ for rep in range(reps + 2):
     if rep >= 2:
         tot.append(ev[0].elapsed_time(ev[1]) * 1e3 / C.positions)
         for t in range(C.positions):
-            ns[rep - 2, t] = bufs[t].view(G, 64).cpu().numpy()[:, :32]
+            ns[rep - 2, t] = bufs[t].view(G, 64).cpu().numpy()[:, :64]
 print(f"us per step (traced, events): {np.median(tot):.1f}")
 for t in range(C.positions):
     print(f"t={t} positions per CTA: max {int(ns[-1, t, :, 12].max())} median {int(np.median(ns[-1, t, :, 12]))}")
@@ -72,3 +72,23 @@ for t in range(C.positions):
             mx = np.median([np.max(xx[xx > 0]) - tt for xx, tt in zip(x, t0) if (xx > 0).any()]) / 1e3
             line.append(f"{nm}={mx:.2f}")
     print(f"t={t} router: " + " ".join(line))
+
+# few-row router (meta_rows_kernel, all CTAs; slots 24-29), relative to the th kernel's first start
+ln = {24: "mr_start", 25: "mr_wait", 26: "units", 27: "polled", 28: "topk", 29: "union"}
+for t in range(C.positions):
+    a = ns[:, t]
+    t0 = np.where(a[:, :, 0] > 0, a[:, :, 0], np.inf).min(1)
+    line = []
+    for sl, nm in ln.items():
+        x = a[:, :, sl]
+        if (x > 0).any():
+            mx = np.median([np.max(xx[xx > 0]) - tt for xx, tt in zip(x, t0) if (xx > 0).any()]) / 1e3
+            mn = np.median([np.min(xx[xx > 0]) - tt for xx, tt in zip(x, t0) if (xx > 0).any()]) / 1e3
+            line.append(f"{nm}={mn:.2f}..{mx:.2f}")
+    print(f"t={t} few-row router: " + " ".join(line))
+
+# SM-clock cycles between router marks in the row CTAs (CTA b < B): poll->topk, topk->end
+for t in range(C.positions):
+    a = ns[-1, t, :C.B]
+    print(f"t={t} row CTAs cycles: wait->units {np.median(a[:, 58] - a[:, 57]):.0f} units->polled {np.median(a[:, 59] - a[:, 58]):.0f} "
+          f"polled->topk {np.median(a[:, 60] - a[:, 59]):.0f}; union CTA topk?->union: {a[0, 61] - a[0, 60]:.0f}")

@@ -442,7 +442,7 @@ def test_tc_head_random_regime_qwen_full_size(th, monkeypatch):
     C = S.CONFIGS["qwen25"]
     W, rt, tau, part, c, r = _setup(C.V, C.d, C.M, C.h_r, "bf16", "random")
     st = Dy.DraftStep(c, r, C.B, C.k_t, shared=True, z_out=True)
-    assert st.launches == 3
+    assert st.launches == 2  # few-row router (meta_rows.cu) + tree head
     hp, e, hn = S.step_inputs(C.B, C.d, 0, "bf16", sibling_eps=0.1)
     st(hp.to(DEV), e.to(DEV), hn.to(DEV), t=0, k_max=C.k_max, k_min=C.k_min)
     torch.cuda.synchronize()
@@ -553,7 +553,9 @@ def test_tc_batched_draft_step_llama3_b16(gh, monkeypatch):
     B = 16
     W, rt, tau, part, c, r = _setup(C.V, C.d, C.M, C.h_r, "bf16", "random")
     st = Dy.DraftStep(c, r, B, C.k_t)
-    assert st.launches == (5 if gh == "1" else 4)
+    # router: one launch (meta_rows.cu) when the 16 rows' x fit its shared-memory staging, else two;
+    # then gh (3) / union + tc head (2)
+    assert st.launches in ((4, 5) if gh == "1" else (3, 4))
     hp, e, hn = S.step_inputs(B, C.d, 2, "bf16")
     st(hp.to(DEV), e.to(DEV), hn.to(DEV), t=2, k_max=C.k_max, k_min=C.k_min)
     torch.cuda.synchronize()

@@ -29,8 +29,10 @@ def _run_split(Dy, st, hp, e, hn, t, k_max, k_min):
     st.head(h_new, t, k_max, k_min, cur)
 
 
+# bf16 B in 2..16 takes the few-row one-launch router (meta_rows.cu), f32 / B = 1 the split-K pair
 @pytest.mark.parametrize("dtype,shared,B", [("bf16", False, 1), ("f32", False, 1), ("bf16", False, 3),
-                                            ("bf16", True, 3)])
+                                            ("bf16", True, 3), ("bf16", True, 10), ("bf16", False, 16),
+                                            ("f32", True, 10)])
 def test_route_head_exact_regime(dtype, shared, B):
     """Exact regime (every fp32 sum exact): scores, selection, offsets, every logit and the top-k
     are bit-exact against the oracle."""
