@@ -41,6 +41,23 @@ bool use_tc_batched(const ds_clusters* c, int B, int k_t, int shared, bool z_out
   return !shared && !z_out && c->dtype == DS_BF16 && B >= 8 && tc_batched_supported(c, B, k_t);
 }
 
+// A few independent bf16 rows: the union of their clusters streamed once on the balanced tree head
+// with per-row cluster masks (th.cu rows mode).  Measured at Llama-3 (us per draft step, rows mode vs
+// the default): B = 2 56.8 vs 49.2 (fused step), B = 4 77.8 vs 70.7, B = 8 100.0 vs 105.7 (grouped
+// head), B = 16 170.5 vs 134.3 — so by default only for 8 <= B <= 11 (DS_TH_ROWS_MIN / _MAX; "0"
+// in DS_TH_ROWS disables it).
+bool use_th_rows(const ds_clusters* c, int B, int k_t, int shared, bool z_out) {
+  const char* off = getenv("DS_TH_ROWS");
+  if (off && off[0] == '0') return false;
+  const char* tc = getenv("DS_DISABLE_TC");
+  if (tc && tc[0] == '1') return false;
+  const char* lo = getenv("DS_TH_ROWS_MIN");
+  const char* hi = getenv("DS_TH_ROWS_MAX");
+  const int bmin = lo && lo[0] ? std::max(2, atoi(lo)) : 8;
+  const int bmax = hi && hi[0] ? std::min(16, atoi(hi)) : 11;
+  return !shared && !z_out && B >= bmin && B <= bmax && th_supported(c, B, k_t);
+}
+
 // Many independent rows in bf16: the grouped cluster-major head (gh.cu) reads every selected cluster
 // block once for all the rows that chose it.  DS_GH_MIN_ROWS (default 8) is the smallest batch.
 bool use_gh(const ds_clusters* c, int B, int k_t, int shared, bool z_out, int kmax) {
@@ -277,7 +294,12 @@ ds_status dynaspec_head_forward(const ds_clusters* c, const void* h_new, int32_t
   if (!ws || ws_bytes < L.total) return DS_ERR_WORKSPACE;
   uint8_t* w8 = static_cast<uint8_t*>(ws);
   cudaError_t err;
-  if (!use_tc_head(c, B, k_t, shared, max_shortlist) && use_gh(c, B, k_t, shared, z_out != nullptr, c->M)) {
+  if (use_th_rows(c, B, k_t, shared, z_out != nullptr)) {
+    if (ws_bytes < ws_layout(0, tc_head_part_bytes(c, B, k_t)).total) return DS_ERR_WORKSPACE;
+    err = launch_th(c, h_new, B, sel, sel_count, sl_offsets, k_t, max_shortlist, top_ids, top_logits, top_logp, lse,
+                    nullptr, 0, w8 + L.head, reinterpret_cast<unsigned*>(w8 + L.counters), (cudaStream_t)stream,
+                    false, 1);
+  } else if (!use_tc_head(c, B, k_t, shared, max_shortlist) && use_gh(c, B, k_t, shared, z_out != nullptr, c->M)) {
     if (ws_bytes < ws_layout(0, gh_ws_bytes(c, B, k_t, c->M)).total) return DS_ERR_WORKSPACE;
     err = launch_gh(c, h_new, B, sel, sel_count, shared, k_t, c->M, top_ids, top_logits, top_logp, lse, w8 + L.head,
                     (cudaStream_t)stream);
@@ -466,6 +488,7 @@ int32_t dynaspec_draft_step_launches(const ds_clusters* c, const ds_router* r, i
   // router: one launch (few rows, meta_rows.cu; 16-byte aligned inputs assumed) or layer 1 + layer 2
   const int meta = meta_rows_supported(r, B, 1, nullptr) ? 1 : 2;
   if (use_tc_head(c, B, k_t, shared, ms)) return meta + 1;  // router (+union), tcgen05 tree head
+  if (use_th_rows(c, B, k_t, shared, z_out != 0)) return meta + 1;  // router, tree head (rows mode)
   if (use_gh(c, B, k_t, shared, z_out != 0, c->M))  // router, grouping (1 or 3), grouped tcgen05 head, merge
     return meta + (gh_wide_grouping(B, shared) ? 5 : 3);
   if (use_tc_batched(c, B, k_t, shared, z_out != 0))
@@ -482,6 +505,8 @@ const char* dynaspec_draft_step_kernel(const ds_clusters* c, const ds_router* r,
   if (use_tc_head(c, B, k_t, shared, ms))
     return th_supported(c, B, k_t) ? "ds::th_kernel (tcgen05 balanced tree head: one cluster per CTA, 3-D TMA boxes)"
                                    : "ds::tc_head_kernel (tcgen05, shared shortlist)";
+  if (use_th_rows(c, B, k_t, shared, z_out != 0))
+    return "ds::th_kernel (tcgen05 balanced tree head, rows mode: the rows' union once, per-row cluster masks)";
   if (use_gh(c, B, k_t, shared, z_out != 0, c->M))
     return "ds::gh_head_kernel (tcgen05 grouped head: every selected cluster block once for the rows that chose it)";
   if (use_tc_batched(c, B, k_t, shared, z_out != 0))
@@ -526,9 +551,10 @@ ds_status dynaspec_draft_step(const ds_clusters* c, const ds_router* r, const vo
   const char* gt = getenv("DS_GH_TREE");  // "1": tree rows on the grouped head too (A/B)
   const bool gh_tree = gt && gt[0] == '1';
   const bool tc = !gh_tree && use_tc_head(c, B, k_t, shared, ms);
-  const bool gh = !tc && use_gh(c, B, k_t, shared, out->z_out != nullptr, c->M);
-  const bool tcb = !tc && !gh && use_tc_batched(c, B, k_t, shared, out->z_out != nullptr);
-  const bool fused = !tc && !tcb && !gh && !two_streams && step_supported(c, r, B, k_t, shared, ms);
+  const bool thr = !tc && use_th_rows(c, B, k_t, shared, out->z_out != nullptr);
+  const bool gh = !tc && !thr && use_gh(c, B, k_t, shared, out->z_out != nullptr, c->M);
+  const bool tcb = !tc && !thr && !gh && use_tc_batched(c, B, k_t, shared, out->z_out != nullptr);
+  const bool fused = !tc && !thr && !tcb && !gh && !two_streams && step_supported(c, r, B, k_t, shared, ms);
   if (fused) {  // one persistent launch: router + select + head + epilogue (step.cu)
     const size_t need = step_ws_bytes(c, r, B, k_t);
     if (!ws || need == 0 || ws_bytes < need) return DS_ERR_WORKSPACE;
@@ -553,8 +579,8 @@ ds_status dynaspec_draft_step(const ds_clusters* c, const ds_router* r, const vo
   const size_t score_bytes = (size_t)B * r->M * sizeof(float);
   const WsLayout L = ws_layout(align_up(meta_bytes, 256) + align_up(score_bytes, 256), pmax.part_bytes);
   if (!ws || ws_bytes < L.total) return DS_ERR_WORKSPACE;
-  if (tc && ws_bytes < ws_layout(align_up(meta_bytes, 256) + align_up(score_bytes, 256),
-                                 tc_head_part_bytes(c, B, k_t)).total)
+  if ((tc || thr) && ws_bytes < ws_layout(align_up(meta_bytes, 256) + align_up(score_bytes, 256),
+                                          tc_head_part_bytes(c, B, k_t)).total)
     return DS_ERR_WORKSPACE;
   if (gh && ws_bytes < ws_layout(align_up(meta_bytes, 256) + align_up(score_bytes, 256),
                                  gh_ws_bytes(c, B, k_t, k)).total)
@@ -593,6 +619,10 @@ ds_status dynaspec_draft_step(const ds_clusters* c, const ds_router* r, const vo
   } else if (tcb) {
     err = launch_tc_batched(c, h_new, B, out->sel, out->sel_count, k_t, out->top_ids, out->top_logits,
                             out->top_logp, out->lse, w8 + L.head, counters, sd);
+  } else if (thr) {
+    err = launch_th(c, h_new, B, out->sel, out->sel_count, out->sl_offsets, k_t, ms, out->top_ids, out->top_logits,
+                    out->top_logp, out->lse, nullptr, 0, w8 + L.head, counters, sd,
+                    !two_streams && head_begin == nullptr, 1);
   } else if (tc) {
     err = launch_tc_head(c, h_new, B, out->sel, out->sel_count, out->sl_offsets, k_t, ms, out->top_ids,
                          out->top_logits, out->top_logp, out->lse, out->z_out, out->z_stride,

@@ -133,7 +133,9 @@ size_t th_ws_bytes(const ds_clusters* c, int R, int k_t);
 cudaError_t launch_th(const ds_clusters* c, const void* h_new, int R, const int32_t* sel, const int32_t* sel_count,
                       const int32_t* sl_offsets, int k_t, int64_t max_shortlist, int32_t* top_ids,
                       float* top_logits, float* top_logp, float* lse, float* z_out, int64_t z_stride, void* ws,
-                      unsigned* counter, cudaStream_t st, bool pdl);
+                      unsigned* counter, cudaStream_t st, bool pdl, int rows = 0);
+// independent rows (shared = 0) on the tree head: 2 <= B <= 16, no z_out (dispatch in api.cu)
+bool use_th_rows(const ds_clusters* c, int B, int k_t, int shared, bool z_out);
 bool use_tc_head(const ds_clusters* c, int B, int k_t, int shared, int64_t max_shortlist);
 // batched per-row rows (each with its own selection), streamed once as their union on tcgen05
 bool tc_batched_supported(const ds_clusters* c, int B, int k_t);

@@ -54,8 +54,8 @@ struct ThMaps {
 };
 
 struct ThArgs {
-  const int32_t* sel;
-  const int32_t* sel_count;
+  const int32_t* sel;        // shared: [M] union; rows mode: [R][M] per-row selections
+  const int32_t* sel_count;  // shared: [1]; rows mode: [R]
   const int32_t* sl_off;
   const int32_t* offsets;
   const int32_t* perm;
@@ -72,13 +72,15 @@ struct ThArgs {
   unsigned long long* rec;  // [R][G][2 + K] (row stride rstride words)
   unsigned* counter;        // [0] arrivals, [1] finished mergers (both left at 0)
   unsigned* err;            // workspace error word
+  int32_t rows;  // 1: independent rows (R9 shared = 0): stream the union of the rows' clusters once,
+                 // each row's (max, sum, top-k_t) over its OWN clusters only (per-tile row masks)
   int32_t pdl;
   int32_t dbg;  // DS_TH_DBG (timing experiments): 1 = no MMAs
   unsigned long long* trace;
 };
 
 struct ThSmem {
-  uint32_t ring, h, bars, misc, pieces, ppos, sel, slo, off, tok, total;
+  uint32_t ring, h, bars, misc, pieces, ppos, cmask, tmask, rtot, sel, slo, off, tok, total;
 };
 
 __host__ __device__ inline ThSmem th_smem(int S, int kchunks, int cap, int M) {
@@ -98,6 +100,12 @@ __host__ __device__ inline ThSmem th_smem(int S, int kchunks, int cap, int M) {
   o += kThMaxPieces * 16;
   L.ppos = o;
   o += kThMaxPieces * 4;
+  L.cmask = o;  // [M] rows that selected cluster m (rows mode)
+  o += (uint32_t)M * 4;
+  L.tmask = o;  // [kThMaxPieces] row mask of each tile
+  o += kThMaxPieces * 4;
+  L.rtot = o;   // [16] per-row |V_S,r| (rows mode)
+  o += 16 * 4;
   L.sel = o;
   o += (uint32_t)M * 4;
   L.slo = o;
@@ -135,7 +143,7 @@ __device__ __forceinline__ float ord_to_float(uint32_t mk) {
 // The K best of n unique nonzero keys v[0..n) by one warp, written to out[0..K) in descending order
 // (0-padded): T = the K-th largest of the 32 lane maxima (each lane's maximum is a distinct key, so
 // >= K keys are >= T), the keys >= T are compacted to cand[] and each is rank-counted against the
-// others.  No sequential rounds.  Returns min(n, K).
+// others.  No sequential rounds.  Zero keys are ignored.  Returns min(#nonzero keys, K).
 __device__ __forceinline__ int th_warp_topk(const unsigned long long* v, int n, int K, int lane,
                                             unsigned long long* cand, unsigned long long* out) {
   unsigned long long lm = 0ull;
@@ -146,9 +154,13 @@ __device__ __forceinline__ int th_warp_topk(const unsigned long long* v, int n, 
   for (int o = 0; o < 32; ++o) rk += __shfl_sync(0xffffffffu, lm, o) > lm ? 1 : 0;
   const unsigned sel = __ballot_sync(0xffffffffu, lm != 0ull && rk == K - 1);
   const unsigned long long T = sel ? __shfl_sync(0xffffffffu, lm, __ffs(sel) - 1) : 0ull;
-  int c = 0;
+  int c = 0, nz = 0;  // zero keys (positions outside the row's own clusters) never count
 #pragma unroll 4
-  for (int i = lane; i < n; i += 32) c += v[i] >= T ? 1 : 0;
+  for (int i = lane; i < n; i += 32) {
+    c += (v[i] >= T && v[i] != 0ull) ? 1 : 0;
+    nz += v[i] != 0ull ? 1 : 0;
+  }
+  nz = (int)__reduce_add_sync(0xffffffffu, (unsigned)nz);
   int inc = c;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -158,7 +170,7 @@ __device__ __forceinline__ int th_warp_topk(const unsigned long long* v, int n, 
   const int nc = __shfl_sync(0xffffffffu, inc, 31);
   int w = inc - c;
   for (int i = lane; i < n; i += 32)
-    if (v[i] >= T) cand[w++] = v[i];
+    if (v[i] >= T && v[i] != 0ull) cand[w++] = v[i];
   __syncwarp();
   for (int i = lane; i < nc; i += 32) {
     const unsigned long long x = cand[i];
@@ -167,7 +179,7 @@ __device__ __forceinline__ int th_warp_topk(const unsigned long long* v, int n, 
     for (int j = 0; j < nc; ++j) r += cand[j] > x ? 1 : 0;
     if (r < K) out[r] = x;
   }
-  const int nv = min(n, K);
+  const int nv = min(nz, K);
   for (int j = nv + lane; j < K; j += 32) out[j] = 0ull;
   __syncwarp();
   return nv;
@@ -192,6 +204,10 @@ __global__ void __launch_bounds__(kThThreads, 1) th_kernel(const __grid_constant
   int* ssel = reinterpret_cast<int*>(smem + L.sel);
   int* sslo = reinterpret_cast<int*>(smem + L.slo);
   int* soff = reinterpret_cast<int*>(smem + L.off);
+  uint32_t* cmask = reinterpret_cast<uint32_t*>(smem + L.cmask);
+  uint32_t* tmask = reinterpret_cast<uint32_t*>(smem + L.tmask);
+  int* rtot = reinterpret_cast<int*>(smem + L.rtot);
+  int* rcnt = reinterpret_cast<int*>(smem + L.misc) + 32;  // [16]
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int G = gridDim.x, b = blockIdx.x, R = a.R, K = a.K, M = a.M;
 
@@ -217,6 +233,7 @@ __global__ void __launch_bounds__(kThThreads, 1) th_kernel(const __grid_constant
   }
   // cluster offsets are static (not produced upstream): staged before the dependency wait
   for (int i = tid; i <= M; i += kThThreads) soff[i] = __ldg(a.offsets + i);
+  for (int i = tid; i < M; i += kThThreads) cmask[i] = 0u;
   trace_mark(a.trace, 0);
   if (a.pdl) pdl_wait();
   trace_mark(a.trace, 13);  // dependency released
@@ -225,14 +242,58 @@ __global__ void __launch_bounds__(kThThreads, 1) th_kernel(const __grid_constant
     mbar_arrive_expect_tx(hbar, (uint32_t)a.kchunks * kThN * 128);
     tma_load_3d(hs, &tmH, 0, 0, 0, hbar, policy_evict_last());
   }
-  // the selection (count, ids, offsets) in one round of loads, whatever the count
-  if (tid == 32) misc[7] = __ldcg(a.sel_count);
+  if (!a.rows) {
+    // the selection (count, ids, offsets) in one round of loads, whatever the count
+    if (tid == 32) misc[7] = __ldcg(a.sel_count);
 #pragma unroll 4
-  for (int i = tid; i < 2 * M + 1; i += kThThreads) {
-    if (i < M) ssel[i] = __ldcg(a.sel + i);
-    else sslo[i - M] = __ldcg(a.sl_off + (i - M));
+    for (int i = tid; i < 2 * M + 1; i += kThThreads) {
+      if (i < M) ssel[i] = __ldcg(a.sel + i);
+      else sslo[i - M] = __ldcg(a.sl_off + (i - M));
+    }
+    __syncthreads();
+  } else {
+    // independent rows: cluster m -> the rows that selected it; then the union in ascending id
+    // (R8) with its offsets, exactly as a shared selection
+    if (tid < R) {
+      const int cr = __ldcg(a.sel_count + tid);
+      rcnt[tid] = cr;
+      rtot[tid] = cr > 0 ? __ldcg(a.sl_off + (size_t)tid * (M + 1) + cr) : 0;
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int idx = tid; idx < R * M; idx += kThThreads) {
+      const int r = idx / M, i = idx - r * M;
+      if (i < rcnt[r]) atomicOr(&cmask[__ldcg(a.sel + idx)], 1u << r);
+    }
+    __syncthreads();
+    if (warp == 0) {
+      int run = 0, off = 0;
+      for (int m0 = 0; m0 < M; m0 += 32) {
+        const int m = m0 + lane;
+        const bool f = m < M && cmask[m] != 0u;
+        const unsigned bal = __ballot_sync(0xffffffffu, f);
+        const int sz = f ? soff[m + 1] - soff[m] : 0;
+        int inc = sz;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, inc, o);
+          if (lane >= o) inc += y;
+        }
+        if (f) {
+          const int pos = run + __popc(bal & ((1u << lane) - 1u));
+          ssel[pos] = m;
+          sslo[pos] = off + inc - sz;
+        }
+        run += __popc(bal);
+        off += __shfl_sync(0xffffffffu, inc, 31);
+      }
+      if (lane == 0) {
+        misc[7] = run;
+        sslo[run] = off;
+      }
+    }
+    __syncthreads();
   }
-  __syncthreads();
   trace_mark(a.trace, 14);  // selection staged
 
   // ---- plan (warp 0): this CTA's tiles.  Cluster i of the union (positions [so_i, so_i + n_i))
@@ -243,7 +304,8 @@ __global__ void __launch_bounds__(kThThreads, 1) th_kernel(const __grid_constant
   if (warp == 0) {
     const int cnt = misc[7];
     const int total = cnt > 0 ? sslo[cnt] : 0;
-    const bool fits = cnt > 0 && cnt <= M && (a.max_shortlist <= 0 || (long long)total <= a.max_shortlist);
+    const bool fits = cnt > 0 && cnt <= M &&
+                      (a.rows || a.max_shortlist <= 0 || (long long)total <= a.max_shortlist);
     const int ncl = fits ? cnt : 0;
     const unsigned NU = total > 0 ? (unsigned)total : 1u;  // 2 G |V_S| + |V_S| < 2^32 (host: V G < 2^30)
     int nt = 0, p0 = INT_MAX, p1 = 0;
@@ -279,6 +341,7 @@ __global__ void __launch_bounds__(kThThreads, 1) th_kernel(const __grid_constant
         for (int r = r0; r < r1 && slot < kThMaxPieces; r += 128, ++slot) {
           const int len = min(128, r1 - r);
           pc[slot] = make_int4(wbase + r, so + r, (len + 7) & ~7, len);  // (W_perm row, position, rows, valid)
+          tmask[slot] = a.rows ? cmask[m] : 0xffffffffu;
         }
         p0 = min(p0, so + r0);
         p1 = max(p1, so + r1);
@@ -419,24 +482,29 @@ __global__ void __launch_bounds__(kThThreads, 1) th_kernel(const __grid_constant
       for (int base = tid; base < nr * n; base += kB * kThThreads) {
         float z[kB];
         int tok[kB];
+        bool in[kB];
 #pragma unroll
         for (int u = 0; u < kB; ++u) {
           const int idx = base + u * kThThreads;
           z[u] = 0.f;
           tok[u] = 0;
+          in[u] = false;
           if (idx < nr * n) {
             const int rr = idx / n, i = idx - rr * n;
             const int pos = P0 + i;
             int t = 0;  // the CTA's tiles cover [P0, P1) in position order
             while (t + 1 < ntiles && pc[t + 1].y <= pos) ++t;
-            z[u] = __ldcg(a.z + (size_t)(rb0 + rr) * a.z_stride + pos);
-            tok[u] = __ldg(a.perm + pc[t].x + (pos - pc[t].y));
+            in[u] = (tmask[t] >> (rb0 + rr)) & 1u;  // rows mode: only the row's own clusters
+            if (in[u]) {
+              z[u] = __ldcg(a.z + (size_t)(rb0 + rr) * a.z_stride + pos);
+              tok[u] = __ldg(a.perm + pc[t].x + (pos - pc[t].y));
+            }
           }
         }
 #pragma unroll
         for (int u = 0; u < kB; ++u) {
           const int idx = base + u * kThThreads;
-          if (idx < nr * n) keys[idx] = tok_key(z[u], tok[u]);
+          if (idx < nr * n) keys[idx] = in[u] ? tok_key(z[u], tok[u]) : 0ull;
         }
       }
       __syncthreads();
@@ -450,7 +518,8 @@ __global__ void __launch_bounds__(kThThreads, 1) th_kernel(const __grid_constant
         const float mx = ord_to_float(mk);
         float s = 0.f;
 #pragma unroll 4
-        for (int i = lane; i < n; i += 32) s += expf(key_value(kr[i]) - mx);
+        for (int i = lane; i < n; i += 32)
+          if (kr[i] != 0ull) s += expf(key_value(kr[i]) - mx);
         s = warp_sum(s);
         unsigned long long* out = a.rec + (size_t)(rb0 + rr) * rstride + (size_t)b * rec;
         const int nv = (a.dbg & 16) ? 0 : th_warp_topk(kr, n, K, lane, cand + (size_t)warp * n, out + 2);
@@ -496,7 +565,8 @@ __global__ void __launch_bounds__(kThThreads, 1) th_kernel(const __grid_constant
   }
   __syncthreads();
   float* lse_sh = reinterpret_cast<float*>(st + rstride);
-  const bool ok_all = misc[5] != 0 && misc[9] == 0;
+  const bool ok_all = misc[5] != 0 && misc[9] == 0 &&
+                     (!a.rows || a.max_shortlist <= 0 || (long long)rtot[row] <= a.max_shortlist);
   if (warp == 1) {
     // lse: lane l folds records l, l + 32, ... in order, then one fixed xor tree (R19)
     uint32_t mk = 0u;
@@ -639,8 +709,9 @@ size_t th_ws_bytes(const ds_clusters* c, int R, int k_t) {
 cudaError_t launch_th(const ds_clusters* c, const void* h_new, int R, const int32_t* sel, const int32_t* sel_count,
                       const int32_t* sl_offsets, int k_t, int64_t max_shortlist, int32_t* top_ids,
                       float* top_logits, float* top_logp, float* lse, float* z_out, int64_t z_stride, void* ws,
-                      unsigned* counter, cudaStream_t st, bool pdl) {
+                      unsigned* counter, cudaStream_t st, bool pdl, int rows) {
   ThPlan p;
+  if (rows && (z_out || R > 16)) return cudaErrorInvalidValue;  // rows mode: no packed per-row z_out
   if (!th_plan(c, R, k_t, &p)) return cudaErrorInvalidValue;
   ThMaps mw;
   for (int j = 0; j < kThMaps; ++j)
@@ -682,6 +753,7 @@ cudaError_t launch_th(const ds_clusters* c, const void* h_new, int R, const int3
   a.err = reinterpret_cast<unsigned*>(reinterpret_cast<uint8_t*>(counter) + kWsErrorWord);
   const char* np_ = getenv("DS_TH_NOPDL");  // A/B: launch without programmatic dependent launch
   if (np_ && np_[0] == '1') pdl = false;
+  a.rows = rows ? 1 : 0;
   a.pdl = pdl ? 1 : 0;
   const char* dbg = getenv("DS_TH_DBG");
   a.dbg = dbg ? atoi(dbg) : 0;

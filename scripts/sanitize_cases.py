@@ -2,7 +2,8 @@
 case under memcheck, racecheck, synccheck and initcheck).  Usage: sanitize_cases.py CASE
 
 Cases: gstep (B = 1 grid step), gstep_head (head-only grid step), cstep (B = 1 cluster step),
-step (grid-wide fused step, B = 4), head (head_forward B = 3), tc_tree (tcgen05 shared head, 10 rows),
+step (grid-wide fused step, B = 4), head (head_forward B = 3), tc_tree (few-row router + balanced tree
+head, 10 rows; tc_tree_z with z_out; tc_tree_old: the general tcgen05 shared head + split-K router),
 tc_batched (tcgen05 batched head, 16 rows), gh (grouped tcgen05 head, 16 rows), gh_wide (160 rows:
 tcgen05 router layer 1 + grid-wide grouping + grouped head), verify (verify_chain), build (k-means build)."""
 import os
@@ -51,7 +52,14 @@ elif case == "head":
     D.head_forward(c, hn, sel, cnt, off, 8)
     torch.cuda.synchronize()
 elif case == "tc_tree":
-    st = steps(10, shared=True)
+    st = steps(10, shared=True)          # few-row router (meta_rows.cu) + balanced tree head (th.cu)
+    assert st.kernel.startswith("ds::th_kernel"), st.kernel
+elif case == "tc_tree_z":
+    st = steps(10, shared=True, z_out=True)   # tree head writing the caller's z_out
+elif case == "tc_tree_old":
+    os.environ["DS_TH"] = "0"
+    os.environ["DS_META_ROWS"] = "0"
+    st = steps(10, shared=True)          # general tcgen05 shared head + split-K router
 elif case == "tc_batched":
     st = steps(16)
 elif case == "gh":

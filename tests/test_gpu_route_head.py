@@ -102,3 +102,67 @@ def test_route_head_llama3_random(B):
             assert np.max(np.abs(st.z[b, :n].cpu().numpy().astype(np.float64) - rb["z"])) <= 2e-2
             check_topk(st.top_ids[b].cpu().numpy(), st.top_logits[b].cpu().numpy(), st.top_logp[b].cpu().numpy(),
                        st.lse[b].item(), rb["z"], rb["V_S"], C.k_t, torch.bfloat16)
+
+
+@pytest.mark.parametrize("B,split", [(8, False), (8, True), (3, False)])
+def test_th_rows_mode_exact_regime(B, split, monkeypatch):
+    """Independent rows on the balanced tree head (th.cu rows mode: the union of the rows' clusters
+    streamed once, each row reduced over its OWN clusters only): selection, offsets, top-k ids /
+    logits (bit-exact) and lse against the oracle, through draft_step and the route/head split."""
+    from paper_2510_13847_b200 import dynaspec as Dy
+    monkeypatch.setenv("DS_TH_ROWS_MIN", "2")
+    V, d, M, h_r, k_t = 5003, 256, 24, 16, 8
+    W = S.lm_head(V, d, 0, "bf16", "exact")
+    rt = S.router(d, h_r, M, 1, "bf16", "exact")
+    tau = S.random_partition(V, M, 2)
+    perm, off = O.layout(tau, M)
+    part = {"perm": perm, "offsets": off}
+    c = Dy.Clusters.from_tau(W.to(DEV), torch.as_tensor(tau, dtype=torch.int32, device=DEV), M)
+    r = Dy.Router(*[x.to(DEV) for x in rt])
+    st = Dy.DraftStep(c, r, B, k_t)
+    assert st.kernel.startswith("ds::th_kernel"), st.kernel
+    Wo, ro = Rows(W), tuple(f64(x) for x in rt)
+    for t in range(4):
+        hp, e, hn = S.step_inputs(B, d, t, "bf16", "exact", h_r=h_r)
+        if split:
+            _run_split(Dy, st, hp.to(DEV), e.to(DEV), hn.to(DEV), t, 8, 2)
+        else:
+            st(hp.to(DEV), e.to(DEV), hn.to(DEV), t, 8, 2)
+        torch.cuda.synchronize()
+        ref = O.draft_step(part, ro, Wo, f64(hp), f64(e), f64(hn), t, 8, 2, k_t)
+        for b in range(B):
+            cnt = st.sel_count[b].item()
+            assert st.sel[b, :cnt].cpu().tolist() == ref[b]["sel"].tolist()
+            assert st.sl_offsets[b, :cnt + 1].cpu().tolist() == ref[b]["sl_offsets"].tolist()
+            check_topk(st.top_ids[b].cpu().numpy(), st.top_logits[b].cpu().numpy(), st.top_logp[b].cpu().numpy(),
+                       st.lse[b].item(), ref[b]["z"], ref[b]["V_S"], k_t, torch.float32, exact=True)
+
+
+def test_th_rows_mode_llama3_b8_sampled_rows():
+    """Llama-3 at full size, the bench's B = 8 (rows mode is the default there): sampled rows
+    against the oracle (scores, selection, top-k, lse) in the random regime."""
+    from paper_2510_13847_b200 import dynaspec as Dy
+    C = S.CONFIGS["llama3"]
+    B = 8
+    W = S.lm_head(C.V, C.d, 0, "bf16", device=DEV)
+    tau = S.random_partition(C.V, C.M, 2)
+    perm, off = O.layout(tau, C.M)
+    part = {"perm": perm, "offsets": off}
+    c = Dy.Clusters.from_tau(W, torch.as_tensor(tau, dtype=torch.int32, device=DEV), C.M)
+    rt = S.router(C.d, C.h_r, C.M, 1, "bf16")
+    r = Dy.Router(*[x.to(DEV) for x in rt])
+    st = Dy.DraftStep(c, r, B, C.k_t)
+    assert st.kernel.startswith("ds::th_kernel"), st.kernel
+    for t in (0, 3):
+        hp, e, hn = S.step_inputs(B, C.d, t, "bf16")
+        st(hp.to(DEV), e.to(DEV), hn.to(DEV), t=t, k_max=C.k_max, k_min=C.k_min)
+        torch.cuda.synchronize()
+        Wo, ro = Rows(W), tuple(f64(x) for x in rt)
+        for b in (0, 5):
+            cnt = st.sel_count[b].item()
+            sel = np.array(st.sel[b, :cnt].cpu().tolist(), dtype=np.int32)
+            ref = O.draft_step(part, ro, Wo, f64(hp[b:b + 1]), f64(e[b:b + 1]), f64(hn[b:b + 1]), t, C.k_max,
+                               C.k_min, C.k_t, sel_override=[sel])[0]
+            assert np.max(np.abs(st.scores[b].cpu().numpy() - ref["scores"])) <= score_tol(ref["scores"])
+            check_topk(st.top_ids[b].cpu().numpy(), st.top_logits[b].cpu().numpy(), st.top_logp[b].cpu().numpy(),
+                       st.lse[b].item(), ref["z"], ref["V_S"], C.k_t, torch.bfloat16)
