@@ -92,3 +92,12 @@ for t in range(C.positions):
     a = ns[-1, t, :C.B]
     print(f"t={t} row CTAs cycles: wait->units {np.median(a[:, 58] - a[:, 57]):.0f} units->polled {np.median(a[:, 59] - a[:, 58]):.0f} "
           f"polled->topk {np.median(a[:, 60] - a[:, 59]):.0f}; union CTA topk?->union: {a[0, 61] - a[0, 60]:.0f}")
+# effective SM clock in the merger CTAs (clock64 / globaltimer between marks 3 and 4), and cycles per phase
+for t in range(C.positions):
+    a = ns[-1, t]
+    mc = np.where(a[:, 3] > 0)[0]
+    if len(mc):
+        dc = a[mc, 32 + 4] - a[mc, 32 + 3]
+        dt = a[mc, 4] - a[mc, 3]
+        print(f"t={t} mergers: cycles {np.median(dc):.0f} in {np.median(dt):.0f} ns -> {np.median(dc / np.maximum(dt, 1)):.2f} GHz;"
+              f" keys->records cycles (all CTAs) {np.median(a[:, 32 + 9] - a[:, 32 + 10]):.0f}")
