@@ -70,7 +70,7 @@ struct ThArgs {
   float* top_logp;
   float* lse;
   unsigned long long* rec;  // [R][G][2 + K] (row stride rstride words)
-  unsigned* counter;        // [0] arrivals, [1] finished mergers (both left at 0)
+  unsigned* counter;        // 64-bit arrival count (8-byte aligned), never reset: epoch = count / G
   unsigned* err;            // workspace error word
   int32_t rows;  // 1: independent rows (R9 shared = 0): stream the union of the rows' clusters once,
                  // each row's (max, sum, top-k_t) over its OWN clusters only (per-tile row masks)
@@ -146,6 +146,28 @@ __device__ __forceinline__ float ord_to_float(uint32_t mk) {
 // others.  No sequential rounds.  Zero keys are ignored.  Returns min(#nonzero keys, K).
 __device__ __forceinline__ int th_warp_topk(const unsigned long long* v, int n, int K, int lane,
                                             unsigned long long* cand, unsigned long long* out) {
+  if (n <= 96) {  // short lists: every nonzero key rank-counted against all n directly (no threshold)
+    int nz = 0;
+    for (int i = lane; i < n; i += 32) {
+      const unsigned long long x = v[i];
+      nz += x != 0ull;
+      if (x == 0ull) continue;
+      int r0 = 0, r1 = 0;
+      int j = 0;
+#pragma unroll 4
+      for (; j + 1 < n; j += 2) {
+        r0 += v[j] > x ? 1 : 0;
+        r1 += v[j + 1] > x ? 1 : 0;
+      }
+      if (j < n) r0 += v[j] > x ? 1 : 0;
+      if (r0 + r1 < K) out[r0 + r1] = x;
+    }
+    nz = (int)__reduce_add_sync(0xffffffffu, (unsigned)nz);
+    const int nv = min(nz, K);
+    for (int j = nv + lane; j < K; j += 32) out[j] = 0ull;
+    __syncwarp();
+    return nv;
+  }
   unsigned long long lm = 0ull;
 #pragma unroll 4
   for (int i = lane; i < n; i += 32) lm = v[i] > lm ? v[i] : lm;
@@ -533,17 +555,23 @@ __global__ void __launch_bounds__(kThThreads, 1) th_kernel(const __grid_constant
   // ---- ticket: the last R CTAs to arrive merge one row each (row G - 1 - ticket)
   __syncthreads();
   trace_mark(a.trace, 9);  // records written
+  // 64-bit arrival count, never re-armed: launch e sees tickets [e G, (e + 1) G), so its mergers
+  // wait for the count to reach (e + 1) G (no end-of-kernel reset atomics)
+  unsigned long long* ticket = reinterpret_cast<unsigned long long*>(a.counter);
   if (tid == 0) {
     fence_acq_rel_gpu();
-    misc[8] = G - 1 - (int)atomicAdd(a.counter, 1u);
+    const unsigned long long tk = atomicAdd(ticket, 1ull);
+    misc[8] = G - 1 - (int)(tk % (unsigned long long)G);
+    reinterpret_cast<unsigned long long*>(misc + 14)[0] = (tk / (unsigned long long)G + 1ull) * (unsigned long long)G;
   }
   __syncthreads();
   const int row = misc[8];
   if (row >= R) return;
   if (tid == 0) {  // every CTA's records: spin (bounded) until all G have arrived
     const unsigned long long t0 = globaltimer_ns();
+    const unsigned long long target = reinterpret_cast<unsigned long long*>(misc + 14)[0];
     int dead = 0;
-    for (unsigned k = 1; ld_acquire_u32(a.counter) < (unsigned)G; ++k) {
+    for (unsigned k = 1; ld_acquire_u64(ticket) < target; ++k) {
       if ((k & 63u) == 0u && globaltimer_ns() - t0 > kThSpinNs) {
         atomicExch(a.err, (unsigned)DS_ERR_DEVICE_TIMEOUT);
         dead = 1;
@@ -564,10 +592,19 @@ __global__ void __launch_bounds__(kThThreads, 1) th_kernel(const __grid_constant
     for (int i = tid; i < nv4; i += kThThreads) dst[i] = __ldcg(src + i);
   }
   __syncthreads();
+  trace_mark(a.trace, 5);  // merger: records staged
   float* lse_sh = reinterpret_cast<float*>(st + rstride);
   const bool ok_all = misc[5] != 0 && misc[9] == 0 &&
                      (!a.rows || a.max_shortlist <= 0 || (long long)rtot[row] <= a.max_shortlist);
-  if (warp == 1) {
+  // top-K: T = the K-th best record head (the K best heads are distinct keys, so >= K keys are
+  // >= T); every record's keys >= T (a prefix of the sorted record) are candidates; rank-count them.
+  unsigned long long* hd = st + rstride + 2;       // [G] heads
+  unsigned long long* cnd = hd + G;                // [G K] candidates
+  int* ncnd = reinterpret_cast<int*>(cnd + (size_t)G * K);
+  if (tid < G) hd[tid] = st[(size_t)tid * rec + 1] > 0 ? st[(size_t)tid * rec + 2] : 0ull;
+  if (tid == 0) *ncnd = 0;
+  __syncthreads();
+  if (warp == kThThreads / 32 - 1) {  // the last warp (no head: G <= 160), alongside the head ranking
     // lse: lane l folds records l, l + 32, ... in order, then one fixed xor tree (R19)
     uint32_t mk = 0u;
     for (int g = lane; g < G; g += 32) {
@@ -590,14 +627,6 @@ __global__ void __launch_bounds__(kThThreads, 1) th_kernel(const __grid_constant
       a.lse[row] = lse;
     }
   }  // lse_sh is read after the barriers below
-  // top-K: T = the K-th best record head (the K best heads are distinct keys, so >= K keys are
-  // >= T); every record's keys >= T (a prefix of the sorted record) are candidates; rank-count them.
-  unsigned long long* hd = st + rstride + 2;       // [G] heads
-  unsigned long long* cnd = hd + G;                // [G K] candidates
-  int* ncnd = reinterpret_cast<int*>(cnd + (size_t)G * K);
-  if (tid < G) hd[tid] = st[(size_t)tid * rec + 1] > 0 ? st[(size_t)tid * rec + 2] : 0ull;
-  if (tid == 0) *ncnd = 0;
-  __syncthreads();
   if (tid < G) {
     const unsigned long long h = hd[tid];
     int rk0 = 0, rk1 = 0;
@@ -611,6 +640,7 @@ __global__ void __launch_bounds__(kThThreads, 1) th_kernel(const __grid_constant
   }
   // records with a key: >= K of them means misc[10] holds the K-th best head's record
   const int nz = __syncthreads_count(tid < G && hd[tid] != 0ull);
+  trace_mark(a.trace, 6);  // merger: heads ranked
   {
     const unsigned long long T = nz >= K ? hd[misc[10]] : 1ull;
     if (tid < G) {
@@ -624,6 +654,7 @@ __global__ void __launch_bounds__(kThThreads, 1) th_kernel(const __grid_constant
     }
   }
   __syncthreads();
+  trace_mark(a.trace, 7);  // merger: candidates compacted
   {
     const int nc = *ncnd;
     const float lse = *lse_sh;
@@ -644,13 +675,6 @@ __global__ void __launch_bounds__(kThThreads, 1) th_kernel(const __grid_constant
       a.top_ids[(size_t)row * K + j] = -1;
       a.top_logits[(size_t)row * K + j] = -INFINITY;
       a.top_logp[(size_t)row * K + j] = -INFINITY;
-    }
-  }
-  if (tid == 0) {  // the last merger to finish re-arms both counters for the next launch (stream order)
-    fence_acq_rel_gpu();
-    if (atomicAdd(a.counter + 1, 1u) == (unsigned)(R - 1)) {
-      a.counter[0] = 0u;
-      a.counter[1] = 0u;
     }
   }
   trace_mark(a.trace, 4);

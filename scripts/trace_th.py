@@ -101,3 +101,9 @@ for t in range(C.positions):
         dt = a[mc, 4] - a[mc, 3]
         print(f"t={t} mergers: cycles {np.median(dc):.0f} in {np.median(dt):.0f} ns -> {np.median(dc / np.maximum(dt, 1)):.2f} GHz;"
               f" keys->records cycles (all CTAs) {np.median(a[:, 32 + 9] - a[:, 32 + 10]):.0f}")
+for t in range(C.positions):
+    a = ns[-1, t]
+    mc = np.where(a[:, 3] > 0)[0]
+    if len(mc):
+        c = lambda x, y: np.median(a[mc, 32 + y] - a[mc, 32 + x])
+        print(f"t={t} merger cycles: start->staged {c(3, 5):.0f} staged->heads {c(5, 6):.0f} heads->cands {c(6, 7):.0f} cands->done {c(7, 4):.0f}")
