@@ -308,10 +308,17 @@ bool step_supported(const ds_clusters* c, const ds_router* r, int B, int k_t, in
 
 // The cluster step's records live after the grid-wide step's scratch, so the two kernels never
 // alias (the cluster step's merger relies on its record words reading 0 between launches).
+// The workspace of the fused step does not depend on the shortlist bound (only its shared-memory
+// plan does), so size it from any plan that fits: the unbounded one, else the tightest bound
+// (a tree step of few clusters fits where the full-vocabulary bound does not).  Both modes.
 static size_t grid_step_ws(const ds_clusters* c, const ds_router* r, int B, int k_t) {
-  StepPlan p;
-  if (!step_plan(c, r, B, k_t, 0, 0, &p) && !step_plan(c, r, B, k_t, 0, 1, &p)) return 0;
-  return align_up(p.total, 256);
+  size_t need = 0;
+  for (int64_t ms : {(int64_t)0, (int64_t)1})
+    for (int sh = 0; sh < 2; ++sh) {
+      StepPlan p;
+      if (step_plan(c, r, B, k_t, ms, sh, &p)) need = std::max(need, align_up(p.total, 256));
+    }
+  return need;
 }
 
 size_t step_ws_bytes(const ds_clusters* c, const ds_router* r, int B, int k_t) {
