@@ -493,7 +493,8 @@ int32_t dynaspec_draft_step_launches(const ds_clusters* c, const ds_router* r, i
     return meta + (gh_wide_grouping(B, shared) ? 5 : 3);
   if (use_tc_batched(c, B, k_t, shared, z_out != 0))
     return meta + 2 * ((B + 127) / 128);  // router, then (union + tcgen05 head) per 128 rows
-  if (!two_streams && step_supported(c, r, B, k_t, shared, 0)) return 1;  // fused single-stream step
+  if (!two_streams && step_supported(c, r, B, k_t, shared, 0))  // fused single-stream step
+    return step_rows_as_gsteps(c, r, B, k_t, shared) ? B : 1;      // (a couple of rows: a grid step each)
   return meta + p.launches;  // router (+select), head chunks
 }
 
@@ -512,6 +513,8 @@ const char* dynaspec_draft_step_kernel(const ds_clusters* c, const ds_router* r,
   if (use_tc_batched(c, B, k_t, shared, z_out != 0))
     return "ds::tc_head_kernel (tcgen05, batched rows over the union)";
   if (!two_streams && step_supported(c, r, B, k_t, shared, 0)) {
+    if (step_rows_as_gsteps(c, r, B, k_t, shared))
+      return "ds::gstep_kernel (one grid step per row, PDL-chained)";
     if (gstep_supported(c, r, B, k_t, shared))
       return "ds::gstep_kernel (grid step: router units over all CTAs + select + gathered head + epilogue, one launch)";
     if (cstep_supported(c, r, B, k_t, shared, 0))

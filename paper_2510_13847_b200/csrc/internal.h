@@ -85,6 +85,8 @@ cudaError_t launch_head(const ds_clusters* c, const HeadPlan& p, const void* h_n
 // ---- fused one-launch draft step (step.cu): router + select + head + epilogue
 bool step_supported(const ds_clusters* c, const ds_router* r, int B, int k_t, int shared, int64_t max_shortlist);
 size_t step_ws_bytes(const ds_clusters* c, const ds_router* r, int B, int k_t);
+// 2 <= B <= DS_GSTEP_ROWS_MAX (3) independent rows run as one grid step per row (launch_step)
+bool step_rows_as_gsteps(const ds_clusters* c, const ds_router* r, int B, int k_t, int shared);
 cudaError_t launch_step(const ds_clusters* c, const ds_router* r, const void* h_prev, const void* e,
                         const void* h_new, int B, int k, int k_t, int shared, int64_t max_shortlist, float* scores,
                         int32_t* sel, int32_t* sel_count, int32_t* sl_offsets, int32_t* top_ids, float* top_logits,
