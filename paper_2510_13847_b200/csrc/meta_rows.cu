@@ -45,6 +45,7 @@ struct MrArgs {
   const __nv_bfloat16* e;       // [B][d]
   const int32_t* offsets;       // [M + 1]
   int32_t B, d, h_r, M, k, shared;
+  int32_t RB;  // x rows staged per batch
   float* scores;      // [B][M]
   int32_t* sel;       // [B][M] (shared: one row)
   int32_t* sel_count;
@@ -108,16 +109,8 @@ __global__ void __launch_bounds__(kMrThreads, 1) meta_rows_kernel(const __grid_c
   if (a.pdl) pdl_wait();
   trace_mark(a.trace, 25);
   __syncthreads();  // xbar initialised
-  // x rows (produced upstream): 2 B bulk copies (h_prev_b, e_b) into shared memory, one round trip
-  if (g < h_r && tid == 0) {
-    mbar_arrive_expect_tx(&xbar, (uint32_t)(B * dr * 2));
-    for (int b = 0; b < B; ++b) {
-      bulk_g2s(xs + (size_t)b * dr, a.h_prev + (size_t)b * d, (uint32_t)(d * 2), &xbar, policy_evict_last());
-      bulk_g2s(xs + (size_t)b * dr + d, a.e + (size_t)b * d, (uint32_t)(d * 2), &xbar, policy_evict_last());
-    }
-  }
-
-  // ---- layer 1: unit g for every row, x from shared memory
+  // ---- layer 1: unit g for every row.  x rows (produced upstream) staged in shared memory by 2 bulk
+  // copies per row (h_prev_b, e_b), RB rows per batch (one batch when they fit: one round trip)
   if (g < h_r) {
     float acc[kMrMaxRows];
 #pragma unroll
@@ -125,18 +118,29 @@ __global__ void __launch_bounds__(kMrThreads, 1) meta_rows_kernel(const __grid_c
     float wf[kMrW1Chunks][8];
 #pragma unroll
     for (int i = 0; i < kMrW1Chunks; ++i) widen16(w1[i], wf[i], a.W1);
-    mbar_wait(&xbar, 0);
+    for (int b0 = 0, ph = 0; b0 < B; b0 += a.RB, ph ^= 1) {
+      const int nb = min(a.RB, B - b0);
+      if (b0 > 0) __syncthreads();  // the previous batch is consumed
+      if (tid == 0) {
+        mbar_arrive_expect_tx(&xbar, (uint32_t)(nb * dr * 2));
+        for (int q = 0; q < nb; ++q) {
+          bulk_g2s(xs + (size_t)q * dr, a.h_prev + (size_t)(b0 + q) * d, (uint32_t)(d * 2), &xbar, policy_evict_last());
+          bulk_g2s(xs + (size_t)q * dr + d, a.e + (size_t)(b0 + q) * d, (uint32_t)(d * 2), &xbar, policy_evict_last());
+        }
+      }
+      mbar_wait(&xbar, (uint32_t)ph);
 #pragma unroll
-    for (int b = 0; b < kMrMaxRows; ++b) {
-      if (b < B) {
+      for (int b = 0; b < kMrMaxRows; ++b) {
+        if (b >= b0 && b < b0 + nb) {
 #pragma unroll
-        for (int i = 0; i < kMrW1Chunks; ++i) {
-          const int c = tid + i * kMrThreads;
-          if (c < nch) {
-            float xf[8];
-            widen16(*reinterpret_cast<const uint4*>(xs + (size_t)b * dr + c * 8), xf, a.W1);
+          for (int i = 0; i < kMrW1Chunks; ++i) {
+            const int c = tid + i * kMrThreads;
+            if (c < nch) {
+              float xf[8];
+              widen16(*reinterpret_cast<const uint4*>(xs + (size_t)(b - b0) * dr + c * 8), xf, a.W1);
 #pragma unroll
-            for (int j = 0; j < 8; ++j) acc[b] = fmaf(wf[i][j], xf[j], acc[b]);
+              for (int j = 0; j < 8; ++j) acc[b] = fmaf(wf[i][j], xf[j], acc[b]);
+            }
           }
         }
       }
@@ -245,7 +249,7 @@ bool meta_rows_supported(const ds_router* r, int B, int k, const int32_t* k_per_
   return r && r->dtype == DS_BF16 && r->h_r > 0 && B >= 2 && B <= kMrMaxRows && k_per_row == nullptr &&
          r->h_r <= G && r->h_r <= 8 * kMrW2Chunks && r->h_r % 8 == 0 && r->M <= kMrThreads && r->M <= 256 &&
          2 * r->d <= 8 * kMrThreads * kMrW1Chunks && r->d % 8 == 0 && G >= B + 1 && k >= 1 && k <= r->M &&
-         (size_t)B * 4 * r->d + 16 * 1024 <= (size_t)max_smem_optin();  // x rows staged in shared memory
+         (size_t)4 * r->d + 16 * 1024 <= (size_t)max_smem_optin();  // >= one x row staged in shared memory
   // (static arrays < 16 KB: see launch_meta_rows)
 }
 
@@ -276,7 +280,9 @@ cudaError_t launch_meta_rows(const ds_router* r, const void* h_prev, const void*
   a.err = reinterpret_cast<unsigned*>(w8 + kWsErrorWord);
   a.pdl = pdl ? 1 : 0;
   a.trace = debug_trace();
-  const size_t smem = (size_t)B * 2 * r->d * 2;
+  const int rb_fit = (int)(((size_t)max_smem_optin() - 16 * 1024) / ((size_t)4 * r->d));
+  a.RB = std::max(1, std::min(B, rb_fit));
+  const size_t smem = (size_t)a.RB * 2 * r->d * 2;
   static int configured[64] = {0};  // dynamic limit = opt-in maximum minus the static arrays (<= 16 KB)
   int dev = 0;
   cudaGetDevice(&dev);
