@@ -43,9 +43,9 @@ bool use_tc_batched(const ds_clusters* c, int B, int k_t, int shared, bool z_out
 
 // A few independent bf16 rows: the union of their clusters streamed once on the balanced tree head
 // with per-row cluster masks (th.cu rows mode).  Measured at Llama-3 (us per draft step, rows mode vs
-// the default): B = 2 56.8 vs 49.2 (fused step), B = 4 77.8 vs 70.7, B = 8 100.0 vs 105.7 (grouped
-// head), B = 16 170.5 vs 134.3 — so by default only for 8 <= B <= 11 (DS_TH_ROWS_MIN / _MAX; "0"
-// in DS_TH_ROWS disables it).
+// the default; with 8 stored H rows for R <= 8): B = 4 72.6 vs 71.2 (multi-row fused step), B = 6
+// 85.0 vs 92.6, B = 8 92.9 vs 105.4 (grouped head); B = 16 170.5 vs 134.3 (16 H rows) — so by
+// default for 5 <= B <= 11 (DS_TH_ROWS_MIN / _MAX; "0" in DS_TH_ROWS disables it).
 bool use_th_rows(const ds_clusters* c, int B, int k_t, int shared, bool z_out) {
   const char* off = getenv("DS_TH_ROWS");
   if (off && off[0] == '0') return false;
@@ -53,7 +53,7 @@ bool use_th_rows(const ds_clusters* c, int B, int k_t, int shared, bool z_out) {
   if (tc && tc[0] == '1') return false;
   const char* lo = getenv("DS_TH_ROWS_MIN");
   const char* hi = getenv("DS_TH_ROWS_MAX");
-  const int bmin = lo && lo[0] ? std::max(2, atoi(lo)) : 8;
+  const int bmin = lo && lo[0] ? std::max(2, atoi(lo)) : 5;
   const int bmax = hi && hi[0] ? std::min(16, atoi(hi)) : 11;
   return !shared && !z_out && B >= bmin && B <= bmax && th_supported(c, B, k_t);
 }

@@ -60,6 +60,7 @@ struct ThArgs {
   const int32_t* offsets;
   const int32_t* perm;
   int32_t R, kchunks, K, S, cap, M;
+  int32_t hr;  // H rows stored per K chunk (8 when R <= 8, else 16)
   int64_t V;  // cap: union positions per CTA (token-id buffer)
   int32_t rstride;                   // record words per row (G (2 + K), even)
   int64_t max_shortlist;          // > 0: a union longer than this is not computed (dynaspec.h)
@@ -83,13 +84,13 @@ struct ThSmem {
   uint32_t ring, h, bars, misc, pieces, ppos, cmask, tmask, rtot, sel, slo, off, tok, total;
 };
 
-__host__ __device__ inline ThSmem th_smem(int S, int kchunks, int cap, int M) {
+__host__ __device__ inline ThSmem th_smem(int S, int kchunks, int cap, int M, int hr) {
   ThSmem L;
   uint32_t o = 0;
   L.ring = o;
   o += (uint32_t)S * kThSlot;
   L.h = o;  // directly after the ring: the MMA's 128-row reads of a short tile spill into H (harmless)
-  o += (uint32_t)kchunks * kThN * 128;
+  o += (uint32_t)kchunks * hr * 128;  // H rows stored per K chunk: 8 (R <= 8) or 16
   o = (o + 1023u) & ~1023u;
   if (o < L.h + kThSlot) o = L.h + kThSlot;  // the spill window exists even for tiny d
   L.bars = o;
@@ -213,7 +214,7 @@ __global__ void __launch_bounds__(kThThreads, 1) th_kernel(const __grid_constant
                                                            const __grid_constant__ CUtensorMap tmH,
                                                            const __grid_constant__ ThArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  const ThSmem L = th_smem(a.S, a.kchunks, a.cap, a.M);
+  const ThSmem L = th_smem(a.S, a.kchunks, a.cap, a.M, a.hr);
   uint8_t* ring = smem + L.ring;
   uint8_t* hs = smem + L.h;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.bars);
@@ -261,7 +262,7 @@ __global__ void __launch_bounds__(kThThreads, 1) th_kernel(const __grid_constant
   trace_mark(a.trace, 13);  // dependency released
   __syncthreads();  // barriers initialised
   if (tid == 0) {  // H (produced upstream) as soon as the wait is over: ONE 3-D box, all K chunks
-    mbar_arrive_expect_tx(hbar, (uint32_t)a.kchunks * kThN * 128);
+    mbar_arrive_expect_tx(hbar, (uint32_t)a.kchunks * a.hr * 128);
     tma_load_3d(hs, &tmH, 0, 0, 0, hbar, policy_evict_last());
   }
   if (!a.rows) {
@@ -442,7 +443,9 @@ __global__ void __launch_bounds__(kThThreads, 1) th_kernel(const __grid_constant
           }
           for (int j = 0; j < nk; ++j) {
             const uint32_t abase = smem_u32(ring + (size_t)s * kThSlot + (size_t)j * r8 * 128);
-            const uint32_t bbase = smem_u32(hs + (size_t)(kc0 + j) * kThN * 128);
+            // B = 16 H rows at SBO 1024: with 8 stored rows per chunk the upper atom is the next
+            // chunk's (or the region after H): garbage in D columns 8..15, which no row reads
+            const uint32_t bbase = smem_u32(hs + (size_t)(kc0 + j) * a.hr * 128);
 #pragma unroll
             for (int k = 0; k < 4; ++k)
               tc_mma_bf16(d_tmem, sw128_desc(abase + k * 32), sw128_desc(bbase + k * 32), idesc,
@@ -682,7 +685,7 @@ __global__ void __launch_bounds__(kThThreads, 1) th_kernel(const __grid_constant
 
 // ------------------------------------------------------------------ host
 struct ThPlan {
-  int S, cap, rstride;
+  int S, cap, rstride, hr;
   size_t smem;
 };
 
@@ -699,23 +702,25 @@ static bool th_plan(const ds_clusters* c, int R, int k_t, ThPlan* p) {
   // union positions per CTA: a share of its big cluster (< 2 shares) + the small clusters rounded
   // to it (< 1 share) + up to 7 rows of group rounding; a share is |V_S| / G <= V / G
   p->cap = (int)(3 * ((c->V + G - 1) / G) + 64);
+  const char* h8 = getenv("DS_TH_H8");  // "0": always store 16 H rows (A/B)
+  p->hr = (R <= 8 && !(h8 && h8[0] == '0')) ? 8 : 16;
   const int smax = max_smem_optin();
   p->S = 0;
   for (int S = 16; S >= 2; --S)
-    if ((int)th_smem(S, kchunks, p->cap, c->M).total <= smax) {
+    if ((int)th_smem(S, kchunks, p->cap, c->M, p->hr).total <= smax) {
       p->S = S;
       break;
     }
   if (p->S == 0) return false;
   // staging after the stream (ring + H): >= one row of keys + six warps' candidates (cap x 8 B each);
   // one row's G records + heads + candidates
-  const ThSmem L = th_smem(p->S, kchunks, p->cap, c->M);
+  const ThSmem L = th_smem(p->S, kchunks, p->cap, c->M, p->hr);
   const size_t stage = L.bars - L.ring;
   p->rstride = (G * (2 + k_t) + 1) & ~1;
   if ((size_t)p->cap * 8 * 7 > stage ||
       ((size_t)p->rstride + 2 + G + (size_t)G * k_t) * 8 + 16 > stage)
     return false;
-  p->smem = th_smem(p->S, kchunks, p->cap, c->M).total;
+  p->smem = th_smem(p->S, kchunks, p->cap, c->M, p->hr).total;
   return encode_fn() != nullptr;
 }
 
@@ -743,7 +748,7 @@ cudaError_t launch_th(const ds_clusters* c, const void* h_new, int R, const int3
                           (uint32_t)th_cpc(8 * (j + 1))))
       return cudaErrorInvalidValue;
   CUtensorMap mh;  // H as (64, R rows, K chunks): one box {64, 16, kchunks} = the whole [chunk][16][128 B] image
-  if (!make_map_kchunks(&mh, h_new, (uint64_t)R, (uint64_t)c->d, (uint32_t)kThN, (uint32_t)((c->d + 63) / 64)))
+  if (!make_map_kchunks(&mh, h_new, (uint64_t)R, (uint64_t)c->d, (uint32_t)p.hr, (uint32_t)((c->d + 63) / 64)))
     return cudaErrorInvalidValue;
   uint8_t* w8 = static_cast<uint8_t*>(ws);
   ThArgs a;
@@ -757,6 +762,7 @@ cudaError_t launch_th(const ds_clusters* c, const void* h_new, int R, const int3
   a.K = k_t;
   a.S = p.S;
   a.cap = p.cap;
+  a.hr = p.hr;
   a.M = c->M;
   a.V = c->V;
   a.rstride = p.rstride;
