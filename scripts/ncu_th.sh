@@ -7,6 +7,6 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:th_k
   -o gpurun_out/th_full_$tag python bench.py --config qwen25 --steps 2 --warmup 1 --profile --no-graph \
   > gpurun_out/ncu_th_full_$tag.log 2>&1
 timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
-  -k regex:"th_kernel|meta_l" --csv --log-file gpurun_out/launches_qwen_th_$tag.csv \
+  -k regex:"th_kernel|meta_" --csv --log-file gpurun_out/launches_qwen_th_$tag.csv \
   python bench.py --config qwen25 --steps 2 --warmup 1 --profile --no-graph > gpurun_out/launch_th_$tag.log 2>&1
 echo ncu-done
