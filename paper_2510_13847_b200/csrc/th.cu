@@ -331,16 +331,27 @@ __global__ void __launch_bounds__(kThThreads, 1) th_kernel(const __grid_constant
                       (a.rows || a.max_shortlist <= 0 || (long long)total <= a.max_shortlist);
     const int ncl = fits ? cnt : 0;
     const unsigned NU = total > 0 ? (unsigned)total : 1u;  // 2 G |V_S| + |V_S| < 2^32 (host: V G < 2^30)
+    // s(i) is monotone, so this CTA's clusters are a contiguous index range found by one binary
+    // search (lane 0): i* = the last cluster with s(i*) <= b, then back over the clusters with
+    // s(i) = s(i*) = b (small clusters rounded onto b; at b = G - 1 also s(i) = G).
     int nt = 0, p0 = INT_MAX, p1 = 0;
-    for (int i0 = 0; i0 < ncl; i0 += 32) {
-      const int i = i0 + lane;
-      int r0 = 0, r1 = 0, so = 0, m = 0;
-      if (i < ncl) {
-        so = sslo[i];
-        const int n = sslo[i + 1] - so;
-        m = ssel[i];
-        const int si = (int)(((unsigned)G * (unsigned)so * 2u + NU) / (2u * NU));
-        const int sn = i + 1 < ncl ? (int)(((unsigned)G * (unsigned)sslo[i + 1] * 2u + NU) / (2u * NU)) : G;
+    if (lane == 0 && ncl > 0) {
+      auto sidx = [&](int i) -> int {
+        return i >= ncl ? G : (int)(((unsigned)G * (unsigned)sslo[i] * 2u + NU) / (2u * NU));
+      };
+      int lo = 0, hi = ncl - 1;  // s(0) = 0 <= b
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (min(sidx(mid), G - 1) <= b) lo = mid;
+        else hi = mid - 1;
+      }
+      const int istar = lo;
+      int first = istar;
+      while (first > 0 && min(sidx(first - 1), G - 1) == b && min(sidx(first), G - 1) == b) --first;
+      for (int i = first; i <= istar; ++i) {
+        const int so = sslo[i], n = sslo[i + 1] - so, m = ssel[i];
+        const int si = sidx(i), sn = sidx(i + 1);
+        int r0 = 0, r1 = 0;
         if (sn > si) {
           if (b >= si && b < sn) {
             const int c = sn - si, j = b - si, ng = (n + 7) >> 3;
@@ -350,26 +361,17 @@ __global__ void __launch_bounds__(kThThreads, 1) th_kernel(const __grid_constant
         } else if (min(si, G - 1) == b) {
           r1 = n;
         }
-      }
-      const int ntl = r1 > r0 ? (r1 - r0 + 127) >> 7 : 0;
-      int inc = ntl;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, inc, o);
-        if (lane >= o) inc += y;
-      }
-      if (ntl > 0) {
-        int slot = nt + inc - ntl;
-        const int wbase = soff[m];
-        for (int r = r0; r < r1 && slot < kThMaxPieces; r += 128, ++slot) {
-          const int len = min(128, r1 - r);
-          pc[slot] = make_int4(wbase + r, so + r, (len + 7) & ~7, len);  // (W_perm row, position, rows, valid)
-          tmask[slot] = a.rows ? cmask[m] : 0xffffffffu;
+        if (r1 > r0) {
+          const int wbase = soff[m];
+          for (int r = r0; r < r1 && nt < kThMaxPieces; r += 128, ++nt) {
+            const int len = min(128, r1 - r);
+            pc[nt] = make_int4(wbase + r, so + r, (len + 7) & ~7, len);  // (W_perm row, position, rows, valid)
+            tmask[nt] = a.rows ? cmask[m] : 0xffffffffu;
+          }
+          p0 = min(p0, so + r0);
+          p1 = max(p1, so + r1);
         }
-        p0 = min(p0, so + r0);
-        p1 = max(p1, so + r1);
       }
-      nt += __shfl_sync(0xffffffffu, inc, 31);
     }
     const int P0 = (int)__reduce_min_sync(0xffffffffu, (unsigned)p0);
     const int P1 = (int)__reduce_max_sync(0xffffffffu, (unsigned)p1);
