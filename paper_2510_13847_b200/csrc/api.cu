@@ -73,13 +73,20 @@ static bool dtype_ok(int dt) { return dt == DS_BF16 || dt == DS_F32; }
 
 // S1 + S3/S4 for B rows: the few-row one-launch router (meta_rows.cu) when it applies, else the
 // split-K pair (meta.cu).  ws = the workspace base.
-static cudaError_t route_rows(const ds_router* r, const ds_clusters* c, const void* h_prev, const void* e, int B,
-                              float* scores, float* part, unsigned* counter, int k, int shared, int32_t* sel,
-                              int32_t* sel_count, int32_t* sl_offsets, void* ws, cudaStream_t st, bool pdl) {
+static bool rows_router(const ds_router* r, const void* h_prev, const void* e, int B, int k) {
   const bool aligned = ((reinterpret_cast<uintptr_t>(h_prev) | reinterpret_cast<uintptr_t>(e) |
                          reinterpret_cast<uintptr_t>(r->W1) | reinterpret_cast<uintptr_t>(r->W2)) & 15u) == 0;
-  if (aligned && meta_rows_supported(r, B, k, nullptr))
-    return launch_meta_rows(r, h_prev, e, B, scores, c->offsets, k, shared, sel, sel_count, sl_offsets, ws, st, pdl);
+  return aligned && meta_rows_supported(r, B, k, nullptr);
+}
+// defer_union (tree rows + tree head): the router leaves the rows' masks in the workspace and the
+// tree head forms the union (one kernel boundary less on the path)
+static cudaError_t route_rows(const ds_router* r, const ds_clusters* c, const void* h_prev, const void* e, int B,
+                              float* scores, float* part, unsigned* counter, int k, int shared, int32_t* sel,
+                              int32_t* sel_count, int32_t* sl_offsets, void* ws, cudaStream_t st, bool pdl,
+                              bool defer_union = false) {
+  if (rows_router(r, h_prev, e, B, k))
+    return launch_meta_rows(r, h_prev, e, B, scores, c->offsets, k, shared, sel, sel_count, sl_offsets, ws, st, pdl,
+                            defer_union);
   return launch_meta(r, h_prev, e, B, scores, part, counter, c->offsets, k, nullptr, shared, sel, sel_count,
                      sl_offsets, st, pdl);
 }
@@ -602,8 +609,11 @@ ds_status dynaspec_draft_step(const ds_clusters* c, const ds_router* r, const vo
     if (cudaEventRecord((cudaEvent_t)ev_fork, sd) != cudaSuccess) return DS_ERR_CUDA;
     if (cudaStreamWaitEvent(sm, (cudaEvent_t)ev_fork, 0) != cudaSuccess) return DS_ERR_CUDA;
   }
+  const char* du = getenv("DS_DEFER_UNION");  // "0": the router forms the tree union (A/B)
+  const bool defer = tc && shared && !two_streams && !(du && du[0] == '0') && th_supported(c, B, k_t) &&
+                     rows_router(r, h_prev, e, B, k);
   cudaError_t err = route_rows(r, c, h_prev, e, B, scores, meta_part, counters + 1, k, shared ? 1 : 0, out->sel,
-                               out->sel_count, out->sl_offsets, ws, sm, !two_streams);
+                               out->sel_count, out->sl_offsets, ws, sm, !two_streams, defer);
   if (err != cudaSuccess) return DS_ERR_CUDA;
   if (two_streams) {  // Alg. 1 line 10: "sync S_m, S_d"
     if (cudaEventRecord((cudaEvent_t)ev_join, sm) != cudaSuccess) return DS_ERR_CUDA;
@@ -626,6 +636,10 @@ ds_status dynaspec_draft_step(const ds_clusters* c, const ds_router* r, const vo
     err = launch_th(c, h_new, B, out->sel, out->sel_count, out->sl_offsets, k_t, ms, out->top_ids, out->top_logits,
                     out->top_logp, out->lse, nullptr, 0, w8 + L.head, counters, sd,
                     !two_streams && head_begin == nullptr, 1);
+  } else if (defer) {
+    err = launch_th(c, h_new, B, out->sel, out->sel_count, out->sl_offsets, k_t, ms, out->top_ids, out->top_logits,
+                    out->top_logp, out->lse, out->z_out, out->z_stride, w8 + L.head, counters, sd,
+                    head_begin == nullptr, 0, ws);
   } else if (tc) {
     err = launch_tc_head(c, h_new, B, out->sel, out->sel_count, out->sl_offsets, k_t, ms, out->top_ids,
                          out->top_logits, out->top_logp, out->lse, out->z_out, out->z_stride,

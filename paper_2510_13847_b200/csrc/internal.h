@@ -43,7 +43,7 @@ bool meta_tc_plan(const ds_router* r, int B, int* KS, int* kc_per);
 bool meta_rows_supported(const ds_router* r, int B, int k, const int32_t* k_per_row);
 cudaError_t launch_meta_rows(const ds_router* r, const void* h_prev, const void* e, int B, float* scores,
                              const int32_t* offsets, int k, int shared, int32_t* sel, int32_t* sel_count,
-                             int32_t* sl_offsets, void* ws, cudaStream_t st, bool pdl);
+                             int32_t* sl_offsets, void* ws, cudaStream_t st, bool pdl, bool defer_union = false);
 cudaError_t launch_meta_tc_l1(const ds_router* r, const void* h_prev, const void* e, int B, float* part, int KS,
                               int kc_per, cudaStream_t st, bool pdl);
 MetaPlan meta_plan(const ds_router* r, int B);
@@ -135,7 +135,8 @@ size_t th_ws_bytes(const ds_clusters* c, int R, int k_t);
 cudaError_t launch_th(const ds_clusters* c, const void* h_new, int R, const int32_t* sel, const int32_t* sel_count,
                       const int32_t* sl_offsets, int k_t, int64_t max_shortlist, int32_t* top_ids,
                       float* top_logits, float* top_logp, float* lse, float* z_out, int64_t z_stride, void* ws,
-                      unsigned* counter, cudaStream_t st, bool pdl, int rows = 0);
+                      unsigned* counter, cudaStream_t st, bool pdl, int rows = 0,
+                      const void* umask_ws = nullptr /* workspace base: deferred tree union (meta_rows) */);
 // independent rows (shared = 0) on the tree head: 2 <= B <= 16, no z_out (dispatch in api.cu)
 bool use_th_rows(const ds_clusters* c, int B, int k_t, int shared, bool z_out);
 bool use_tc_head(const ds_clusters* c, int B, int k_t, int shared, int64_t max_shortlist);

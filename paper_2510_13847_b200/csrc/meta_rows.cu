@@ -54,6 +54,7 @@ struct MrArgs {
   unsigned long long* masks;  // [B][32] tagged mask words (workspace prefix)
   unsigned* err;              // workspace error word
   int32_t pdl;
+  int32_t defer_union;  // shared mode: the row masks stay in the workspace for the tree head (th.cu)
   unsigned long long* trace;
 };
 
@@ -160,7 +161,7 @@ __global__ void __launch_bounds__(kMrThreads, 1) meta_rows_kernel(const __grid_c
     }
   }
   trace_mark(a.trace, 26);
-  if (!rowcta && !(a.shared && g == B)) return;
+  if (!rowcta && !(a.shared && !a.defer_union && g == B)) return;
 
   const unsigned long long t0 = globaltimer_ns();
   if (rowcta) {
@@ -255,7 +256,7 @@ bool meta_rows_supported(const ds_router* r, int B, int k, const int32_t* k_per_
 
 cudaError_t launch_meta_rows(const ds_router* r, const void* h_prev, const void* e, int B, float* scores,
                              const int32_t* offsets, int k, int shared, int32_t* sel, int32_t* sel_count,
-                             int32_t* sl_offsets, void* ws, cudaStream_t st, bool pdl) {
+                             int32_t* sl_offsets, void* ws, cudaStream_t st, bool pdl, bool defer_union) {
   uint8_t* w8 = static_cast<uint8_t*>(ws);
   MrArgs a;
   a.W1 = static_cast<const __nv_bfloat16*>(r->W1);
@@ -279,6 +280,7 @@ cudaError_t launch_meta_rows(const ds_router* r, const void* h_prev, const void*
   a.masks = reinterpret_cast<unsigned long long*>(w8 + kWsRowsMasks);
   a.err = reinterpret_cast<unsigned*>(w8 + kWsErrorWord);
   a.pdl = pdl ? 1 : 0;
+  a.defer_union = defer_union ? 1 : 0;
   a.trace = debug_trace();
   const int rb_fit = (int)(((size_t)max_smem_optin() - 16 * 1024) / ((size_t)4 * r->d));
   a.RB = std::max(1, std::min(B, rb_fit));

@@ -56,6 +56,12 @@ struct ThMaps {
 struct ThArgs {
   const int32_t* sel;        // shared: [M] union; rows mode: [R][M] per-row selections
   const int32_t* sel_count;  // shared: [1]; rows mode: [R]
+  unsigned long long* umask;        // shared mode, deferred union (nullable): the R rows' TopK masks as
+                                    // published by the few-row router ([R][32] tagged words); the union,
+                                    // sel / sel_count / sl_offsets are then built (and written) here
+  int32_t* usel;                    // deferred union outputs (CTA 0 writes them)
+  int32_t* ucnt;
+  int32_t* usloff;
   const int32_t* sl_off;
   const int32_t* offsets;
   const int32_t* perm;
@@ -265,7 +271,21 @@ __global__ void __launch_bounds__(kThThreads, 1) th_kernel(const __grid_constant
     mbar_arrive_expect_tx(hbar, (uint32_t)a.kchunks * a.hr * 128);
     tma_load_3d(hs, &tmH, 0, 0, 0, hbar, policy_evict_last());
   }
-  if (!a.rows) {
+  if (!a.rows && a.umask) {
+    // tree rows, deferred union: OR the rows' masks (one round of loads), then the union in
+    // ascending id with its offsets — the router's union step, done where it is consumed
+    if (tid < 32) {
+      uint32_t u = 0u;
+      const int words = (M + 31) >> 5;
+      if (tid < words)
+        for (int r = 0; r < R; ++r) u |= (uint32_t)__ldcg(a.umask + (size_t)r * 32 + tid);
+      rcnt[tid] = (int)u;  // scratch: union word tid
+    }
+    __syncthreads();
+    for (int m = tid; m < M; m += kThThreads) cmask[m] = ((uint32_t)rcnt[m >> 5] >> (m & 31)) & 1u ? ~0u : 0u;
+    __syncthreads();
+  }
+  if (!a.rows && !a.umask) {
     // the selection (count, ids, offsets) in one round of loads, whatever the count
     if (tid == 32) misc[7] = __ldcg(a.sel_count);
 #pragma unroll 4
@@ -276,19 +296,21 @@ __global__ void __launch_bounds__(kThThreads, 1) th_kernel(const __grid_constant
     __syncthreads();
   } else {
     // independent rows: cluster m -> the rows that selected it; then the union in ascending id
-    // (R8) with its offsets, exactly as a shared selection
-    if (tid < R) {
+    // (R8) with its offsets, exactly as a shared selection (deferred union: cmask is set above)
+    if (a.rows && tid < R) {
       const int cr = __ldcg(a.sel_count + tid);
       rcnt[tid] = cr;
       rtot[tid] = cr > 0 ? __ldcg(a.sl_off + (size_t)tid * (M + 1) + cr) : 0;
     }
     __syncthreads();
+    if (a.rows) {
 #pragma unroll 4
-    for (int idx = tid; idx < R * M; idx += kThThreads) {
-      const int r = idx / M, i = idx - r * M;
-      if (i < rcnt[r]) atomicOr(&cmask[__ldcg(a.sel + idx)], 1u << r);
+      for (int idx = tid; idx < R * M; idx += kThThreads) {
+        const int r = idx / M, i = idx - r * M;
+        if (i < rcnt[r]) atomicOr(&cmask[__ldcg(a.sel + idx)], 1u << r);
+      }
+      __syncthreads();
     }
-    __syncthreads();
     if (warp == 0) {
       int run = 0, off = 0;
       for (int m0 = 0; m0 < M; m0 += 32) {
@@ -316,6 +338,14 @@ __global__ void __launch_bounds__(kThThreads, 1) th_kernel(const __grid_constant
       }
     }
     __syncthreads();
+    if (!a.rows && b == 0) {  // deferred union: the S3/S4 outputs of the step
+      const int cnt = misc[7];
+      for (int i = tid; i <= cnt; i += kThThreads) {
+        if (i < cnt) a.usel[i] = ssel[i];
+        a.usloff[i] = sslo[i];
+      }
+      if (tid == 0) *a.ucnt = cnt;
+    }
   }
   trace_mark(a.trace, 14);  // selection staged
 
@@ -587,6 +617,10 @@ __global__ void __launch_bounds__(kThThreads, 1) th_kernel(const __grid_constant
     misc[9] = dead;
   }
   __syncthreads();
+  // deferred union: every CTA read the masks before its ticket, so the first merger clears them
+  // (a later router launch that polls for its rows' masks must not see these)
+  if (a.umask && row == 0)
+    for (int i = tid; i < R * 32; i += kThThreads) a.umask[i] = 0ull;
   trace_mark(a.trace, 3);
   unsigned long long* st = reinterpret_cast<unsigned long long*>(ring);  // [G][rec] of this row
   {
@@ -740,7 +774,7 @@ size_t th_ws_bytes(const ds_clusters* c, int R, int k_t) {
 cudaError_t launch_th(const ds_clusters* c, const void* h_new, int R, const int32_t* sel, const int32_t* sel_count,
                       const int32_t* sl_offsets, int k_t, int64_t max_shortlist, int32_t* top_ids,
                       float* top_logits, float* top_logp, float* lse, float* z_out, int64_t z_stride, void* ws,
-                      unsigned* counter, cudaStream_t st, bool pdl, int rows) {
+                      unsigned* counter, cudaStream_t st, bool pdl, int rows, const void* umask_ws) {
   ThPlan p;
   if (rows && (z_out || R > 16)) return cudaErrorInvalidValue;  // rows mode: no packed per-row z_out
   if (!th_plan(c, R, k_t, &p)) return cudaErrorInvalidValue;
@@ -756,6 +790,13 @@ cudaError_t launch_th(const ds_clusters* c, const void* h_new, int R, const int3
   ThArgs a;
   a.sel = sel;
   a.sel_count = sel_count;
+  // deferred union: the few-row router left the rows' masks in the workspace prefix of umask_ws
+  a.umask = (!rows && umask_ws) ? reinterpret_cast<unsigned long long*>(
+                                     const_cast<uint8_t*>(static_cast<const uint8_t*>(umask_ws)) + kWsRowsMasks)
+                                : nullptr;
+  a.usel = const_cast<int32_t*>(sel);
+  a.ucnt = const_cast<int32_t*>(sel_count);
+  a.usloff = const_cast<int32_t*>(sl_offsets);
   a.sl_off = sl_offsets;
   a.offsets = c->offsets;
   a.perm = c->perm;
