@@ -166,3 +166,40 @@ def test_th_rows_mode_llama3_b8_sampled_rows():
             assert np.max(np.abs(st.scores[b].cpu().numpy() - ref["scores"])) <= score_tol(ref["scores"])
             check_topk(st.top_ids[b].cpu().numpy(), st.top_logits[b].cpu().numpy(), st.top_logp[b].cpu().numpy(),
                        st.lse[b].item(), ref["z"], ref["V_S"], C.k_t, torch.bfloat16)
+
+
+@pytest.mark.parametrize("defer", ["1", "0"])
+def test_tree_rows_exact_regime_deferred_union(defer, monkeypatch):
+    """Tree rows (shared, 8 rows) through draft_step on the few-row router + the tree head; with
+    DS_DEFER_UNION=1 the union is formed by the tree head from the rows' published masks.  Scores,
+    the union selection and its offsets, every logit and the top-k are bit-exact against the oracle,
+    several steps in a row on one workspace (the masks must be cleared between steps)."""
+    from paper_2510_13847_b200 import dynaspec as Dy
+    monkeypatch.setenv("DS_DEFER_UNION", defer)
+    V, d, M, h_r, k_t, B = 5003, 256, 24, 16, 8, 8
+    W = S.lm_head(V, d, 0, "bf16", "exact")
+    rt = S.router(d, h_r, M, 1, "bf16", "exact")
+    tau = S.random_partition(V, M, 2)
+    perm, off = O.layout(tau, M)
+    part = {"perm": perm, "offsets": off}
+    c = Dy.Clusters.from_tau(W.to(DEV), torch.as_tensor(tau, dtype=torch.int32, device=DEV), M)
+    r = Dy.Router(*[x.to(DEV) for x in rt])
+    st = Dy.DraftStep(c, r, B, k_t, shared=True, z_out=True)
+    assert st.kernel.startswith("ds::th_kernel"), st.kernel
+    Wo, ro = Rows(W), tuple(f64(x) for x in rt)
+    for t in range(5):
+        hp, e, hn = S.step_inputs(B, d, t, "bf16", "exact", h_r=h_r)
+        st(hp.to(DEV), e.to(DEV), hn.to(DEV), t, 8, 2)
+        torch.cuda.synchronize()
+        ref = O.draft_step(part, ro, Wo, f64(hp), f64(e), f64(hn), t, 8, 2, k_t, shared=True)
+        sc = st.scores.cpu().numpy()
+        for b in range(B):
+            assert np.array_equal(sc[b], ref[b]["scores"].astype(np.float32))
+        cnt = st.sel_count[0].item()
+        assert st.sel[0, :cnt].cpu().tolist() == ref[0]["sel"].tolist()
+        assert st.sl_offsets[0, :cnt + 1].cpu().tolist() == ref[0]["sl_offsets"].tolist()
+        for b in range(B):
+            n = len(ref[b]["V_S"])
+            assert np.array_equal(st.z[b, :n].cpu().numpy(), ref[b]["z"].astype(np.float32))
+            check_topk(st.top_ids[b].cpu().numpy(), st.top_logits[b].cpu().numpy(), st.top_logp[b].cpu().numpy(),
+                       st.lse[b].item(), ref[b]["z"], ref[b]["V_S"], k_t, torch.float32, exact=True)
