@@ -37,7 +37,8 @@
 
 namespace ds {
 
-constexpr int kThThreads = 192;          // 6 warps
+constexpr int kThThreads = 320;          // 10 warps: 0 TMA, 1 MMA, 2-5 epilogue; all 10 in the tail
+constexpr int kThWarps = kThThreads / 32;
 constexpr int kThN = 16;                 // MMA N: rows padded to 16
 constexpr int kThSlot = 32768;           // ring slot bytes
 constexpr int kThMaxPieces = 256;
@@ -490,7 +491,7 @@ __global__ void __launch_bounds__(kThThreads, 1) th_kernel(const __grid_constant
       trace_mark_w(a.trace, 8);  // last MMA issued
     }
     __syncwarp();
-  } else {
+  } else if (warp < 6) {
     // warps 2..5: TMEM lane quarter q = warp % 4 holds rows 32q .. 32q + 31 of a tile
     const int q = warp & 3;
     for (int tile = 0; tile < ntiles; ++tile) {
@@ -530,7 +531,11 @@ __global__ void __launch_bounds__(kThThreads, 1) th_kernel(const __grid_constant
   {
     unsigned long long* keys = reinterpret_cast<unsigned long long*>(ring);
     // rb rows of keys + one candidate buffer of n keys per warp
-    const int rb = n > 0 ? min(R, (int)(((size_t)(L.bars - L.ring) / 8) / (size_t)n) - 6) : R;
+    // one row per warp when the staging holds R rows of keys + a candidate buffer per warp, else
+    // six record warps (the host sizes the staging for rows of keys + 6 candidate buffers)
+    const size_t stage_keys = (size_t)(L.bars - L.ring) / 8;
+    const int nwr = (n > 0 && (size_t)(R + kThWarps) * n > stage_keys) ? 6 : kThWarps;
+    const int rb = n > 0 ? min(R, (int)(stage_keys / (size_t)n) - nwr) : R;
     unsigned long long* cand = keys + (size_t)rb * n;
     for (int rb0 = 0; rb0 < R; rb0 += rb) {
       const int nr = min(rb, R - rb0);
@@ -566,7 +571,7 @@ __global__ void __launch_bounds__(kThThreads, 1) th_kernel(const __grid_constant
       }
       __syncthreads();
       if (rb0 == 0) trace_mark(a.trace, 10);  // keys staged
-      for (int rr = warp; rr < nr; rr += 6) {
+      for (int rr = warp; rr < nr && warp < nwr; rr += nwr) {
         const unsigned long long* kr = keys + (size_t)rr * n;
         uint32_t mk = 0u;
 #pragma unroll 4
