@@ -312,30 +312,47 @@ __global__ void __launch_bounds__(kThThreads, 1) th_kernel(const __grid_constant
       }
       __syncthreads();
     }
-    if (warp == 0) {
-      int run = 0, off = 0;
-      for (int m0 = 0; m0 < M; m0 += 32) {
-        const int m = m0 + lane;
-        const bool f = m < M && cmask[m] != 0u;
-        const unsigned bal = __ballot_sync(0xffffffffu, f);
-        const int sz = f ? soff[m + 1] - soff[m] : 0;
-        int inc = sz;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const int y = __shfl_up_sync(0xffffffffu, inc, o);
-          if (lane >= o) inc += y;
-        }
-        if (f) {
-          const int pos = run + __popc(bal & ((1u << lane) - 1u));
-          ssel[pos] = m;
-          sslo[pos] = off + inc - sz;
-        }
-        run += __popc(bal);
-        off += __shfl_sync(0xffffffffu, inc, 31);
-      }
+    // the union in ascending id with its offsets: 32-cluster chunks over all warps (per-chunk count
+    // and size, then each chunk's base from the chunks before it)
+    int* ccnt = reinterpret_cast<int*>(ring);  // [32] (the ring is idle until the plan)
+    int* csz = ccnt + 32;
+    const int nchunk = (M + 31) >> 5;
+    for (int ch = warp; ch < nchunk; ch += kThWarps) {
+      const int m = ch * 32 + lane;
+      const bool f = m < M && cmask[m] != 0u;
+      const int sz = f ? soff[m + 1] - soff[m] : 0;
+      const unsigned bal = __ballot_sync(0xffffffffu, f);
+      const int tot = (int)__reduce_add_sync(0xffffffffu, (unsigned)sz);
       if (lane == 0) {
-        misc[7] = run;
-        sslo[run] = off;
+        ccnt[ch] = __popc(bal);
+        csz[ch] = tot;
+      }
+    }
+    __syncthreads();
+    for (int ch = warp; ch < nchunk; ch += kThWarps) {
+      int run = 0, off = 0;
+      for (int c2 = 0; c2 < ch; ++c2) {
+        run += ccnt[c2];
+        off += csz[c2];
+      }
+      const int m = ch * 32 + lane;
+      const bool f = m < M && cmask[m] != 0u;
+      const unsigned bal = __ballot_sync(0xffffffffu, f);
+      const int sz = f ? soff[m + 1] - soff[m] : 0;
+      int inc = sz;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+      }
+      if (f) {
+        const int pos = run + __popc(bal & ((1u << lane) - 1u));
+        ssel[pos] = m;
+        sslo[pos] = off + inc - sz;
+      }
+      if (ch == nchunk - 1 && lane == 0) {
+        misc[7] = run + __popc(bal);
+        sslo[run + __popc(bal)] = off + csz[ch];
       }
     }
     __syncthreads();
@@ -370,10 +387,12 @@ __global__ void __launch_bounds__(kThThreads, 1) th_kernel(const __grid_constant
       auto sidx = [&](int i) -> int {
         return i >= ncl ? G : (int)(((unsigned)G * (unsigned)sslo[i] * 2u + NU) / (2u * NU));
       };
+      // min(s(i), G - 1) <= b  <=>  b = G - 1, or 2 G so_i < (2 b + 1) |V_S| (division-free)
+      const unsigned long long lim = (unsigned long long)(2 * b + 1) * NU;
       int lo = 0, hi = ncl - 1;  // s(0) = 0 <= b
       while (lo < hi) {
         const int mid = (lo + hi + 1) >> 1;
-        if (min(sidx(mid), G - 1) <= b) lo = mid;
+        if (b == G - 1 || 2ull * (unsigned long long)G * (unsigned)sslo[mid] < lim) lo = mid;
         else hi = mid - 1;
       }
       const int istar = lo;
