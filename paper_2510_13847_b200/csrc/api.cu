@@ -43,9 +43,10 @@ bool use_tc_batched(const ds_clusters* c, int B, int k_t, int shared, bool z_out
 
 // A few independent bf16 rows: the union of their clusters streamed once on the balanced tree head
 // with per-row cluster masks (th.cu rows mode).  Measured at Llama-3 (us per draft step, rows mode vs
-// the default; with 8 stored H rows for R <= 8): B = 4 72.6 vs 71.2 (multi-row fused step), B = 6
-// 85.0 vs 92.6, B = 8 92.9 vs 105.4 (grouped head); B = 16 170.5 vs 134.3 (16 H rows) — so by
-// default for 5 <= B <= 11 (DS_TH_ROWS_MIN / _MAX; "0" in DS_TH_ROWS disables it).
+// the default; with 8 stored H rows for R <= 8): B = 4 71.8 vs 71.1 (multi-row fused step), B = 5
+// 80.6 vs 82.1, B = 6 85.0 vs 92.6, B = 8 88.8 vs 105.4 (grouped head), B = 9 101.0 vs 108.4,
+// B = 10 114.7 vs 111.4, B = 12 136.0 vs 117.7 — so by default for 5 <= B <= 9 (DS_TH_ROWS_MIN /
+// _MAX; "0" in DS_TH_ROWS disables it).
 bool use_th_rows(const ds_clusters* c, int B, int k_t, int shared, bool z_out) {
   const char* off = getenv("DS_TH_ROWS");
   if (off && off[0] == '0') return false;
@@ -54,7 +55,7 @@ bool use_th_rows(const ds_clusters* c, int B, int k_t, int shared, bool z_out) {
   const char* lo = getenv("DS_TH_ROWS_MIN");
   const char* hi = getenv("DS_TH_ROWS_MAX");
   const int bmin = lo && lo[0] ? std::max(2, atoi(lo)) : 5;
-  const int bmax = hi && hi[0] ? std::min(16, atoi(hi)) : 11;
+  const int bmax = hi && hi[0] ? std::min(16, atoi(hi)) : 9;
   return !shared && !z_out && B >= bmin && B <= bmax && th_supported(c, B, k_t);
 }
 
