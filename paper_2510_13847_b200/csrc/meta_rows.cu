@@ -8,14 +8,14 @@
 // split-K partials through L2, a row-CTA TopK, then a ticketed union) — a third of the Qwen tree
 // step.  Here, as in the grid step (gstep.cu), the hidden units are spread over the grid:
 //   * CTA g owns hidden unit u = g (h_r <= #SMs): its W1 row (2d bf16) is loaded into REGISTERS
-//     before the dependency wait (router weights never depend on the upstream kernel; W2 is
-//     prefetched into L2 then too); after the wait one thread stages the B rows of
+//     before the dependency wait (router weights never depend on the upstream kernel; so is the
+//     W2 row of each thread of the row CTAs); after the wait one thread stages the B rows of
 //     x_b = [h_prev,b ‖ e_b] in shared memory with 2B bulk copies (one round trip), the CTA reduces
 //     B dot products in a fixed order, and publishes a_bu = ReLU(. + b1_u) as ONE 64-bit word
 //     (1 << 32 | bits) — value and "written" land together, no fence, no counter;
 //   * CTA b < B (row CTAs) then polls the h_r unit words of row b (bounded spin), zeroes them
-//     (it is their only reader), evaluates layer 2 (thread m: W2 row m from L2, fp32 a from
-//     shared memory), writes the scores, and takes TopK_k by a rank count of 64-bit keys
+//     (it is their only reader), evaluates layer 2 (thread m: W2 row m from registers, fp32 a
+//     from shared memory), writes the scores, and takes TopK_k by a rank count of 64-bit keys
 //     (ord(score) << 32 | ~id, R7) over the M <= 256 scores; independent rows emit their
 //     selection here;
 //   * shared mode: row CTAs publish their TopK masks as tagged words; CTA B polls the B masks,
@@ -98,10 +98,11 @@ __global__ void __launch_bounds__(kMrThreads, 1) meta_rows_kernel(const __grid_c
                                   : make_uint4(0, 0, 0, 0);
   }
   const bool rowcta = g < B;
-  if (rowcta && tid == 32) {  // W2 (M h_r bf16) into L2, a slice per row CTA
-    const size_t bytes = (size_t)M * h_r * 2, per = ((bytes + B - 1) / B + 15) & ~(size_t)15, lo = (size_t)g * per;
-    if (lo < bytes) bulk_prefetch_l2(reinterpret_cast<const uint8_t*>(a.W2) + lo, (uint32_t)min(per, bytes - lo));
-  }
+  uint4 w2[kMrW2Chunks];  // row CTAs: W2 row m of thread m, in registers before the dependency wait
+#pragma unroll
+  for (int i = 0; i < kMrW2Chunks; ++i)
+    w2[i] = (rowcta && tid < M && i * 8 < h_r) ? __ldg(reinterpret_cast<const uint4*>(a.W2 + (size_t)tid * h_r) + i)
+                                                : make_uint4(0, 0, 0, 0);
   const float b1u = g < h_r ? __ldg(a.b1 + g) : 0.f;
   const float b2m = (rowcta && tid < M) ? __ldg(a.b2 + tid) : 0.f;
   if (rowcta || (a.shared && g == B))
@@ -172,11 +173,6 @@ __global__ void __launch_bounds__(kMrThreads, 1) meta_rows_kernel(const __grid_c
       a1[u] = __uint_as_float((uint32_t)v);
       st_relaxed_u64(a.units + (size_t)b * h_r + u, 0ull);  // its only reader: re-arm for the next launch
     }
-    uint4 w2[kMrW2Chunks];  // W2 row m (L2-resident: prefetched before the wait)
-#pragma unroll
-    for (int i = 0; i < kMrW2Chunks; ++i)
-      w2[i] = (tid < M && i * 8 < h_r) ? __ldg(reinterpret_cast<const uint4*>(a.W2 + (size_t)tid * h_r) + i)
-                                       : make_uint4(0, 0, 0, 0);
     __syncthreads();
     trace_mark(a.trace, 27);
     unsigned long long key = 0ull;
