@@ -224,7 +224,7 @@ def oracle_cycles(C, B, dtype, seconds, W_host, rt_host, part):
     rows, t0, cycles = 0, time.perf_counter(), 0
     while True:
         for t in range(C.positions):
-            hp, e, hn = S.step_inputs(B, C.d, t, dtype)
+            hp, e, hn = S.step_inputs(B, C.d, t, dtype, sibling_eps=0.1 if C.shared else None)
             f = lambda x: x.to(torch.float64).numpy()
             O.draft_step(part, ro, W, f(hp), f(e), f(hn), t, C.k_max, C.k_min, C.k_t, shared=C.shared)
             rows += B
@@ -897,7 +897,8 @@ def e2e_run(D, steppers, clusters, router, C, B, args, dev, flush, ws, rows_all_
     for i in range(2):  # two input sets, alternated: nothing is reused from the previous replay
         h = torch.empty((P, 3, B, C.d), dtype=tdt).pin_memory()
         for t in range(P):
-            for j, x in enumerate(S.step_inputs(B, C.d, P * (100 + i) + t, args.dtype, pool=1 << 20)):
+            for j, x in enumerate(S.step_inputs(B, C.d, P * (100 + i) + t, args.dtype, pool=1 << 20,
+                                                sibling_eps=0.1 if C.shared else None)):  # the timed workload's rows
                 h[t, j].copy_(x)
         host_in.append(h)
     dev_in = torch.empty((P, 3, B, C.d), dtype=tdt, device=dev)
@@ -926,13 +927,18 @@ def e2e_run(D, steppers, clusters, router, C, B, args, dev, flush, ws, rows_all_
         graphs[i % 2].replay()
     torch.cuda.synchronize()
     tot = 0.0
+    dev_ms = []
     for i in range(reps):
         flush.zero_()
         torch.cuda.synchronize()
+        ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         t0 = time.perf_counter()
+        ea.record()
         graphs[i % 2].replay()
+        eb.record()
         torch.cuda.synchronize()   # the host has the step's results
         tot += time.perf_counter() - t0
+        dev_ms.append(ea.elapsed_time(eb))
     tot = max_over_ranks(tot, ws)
     for st, (ids, lp) in zip(steppers, saved):
         st.bind_outputs(top_ids=ids, top_logp=lp)
@@ -941,7 +947,7 @@ def e2e_run(D, steppers, clusters, router, C, B, args, dev, flush, ws, rows_all_
     return {"value": rows_all_ranks * P * reps / tot, "unit": "draft tokens/s", "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h, "timing": "host wall clock around graph replay + synchronize "
             "(one H2D copy of the cycle's inputs, 8 PDL-chained steps, one D2H copy of the results)",
-            "ms_per_step": 1e3 * tot / reps}
+            "ms_per_step": 1e3 * tot / reps, "device_ms_per_step": statistics.median(dev_ms)}
 
 
 def run_cluster_sharded(args, ws, rank, local):
