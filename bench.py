@@ -908,11 +908,8 @@ def e2e_run(D, steppers, clusters, router, C, B, args, dev, flush, ws, rows_all_
     for t, st in enumerate(steppers):
         st.bind_outputs(top_ids=dev_out[t, 0], top_logp=dev_out[t, 1].view(torch.float32))
 
-    graphs = []
-    overlap = P * 3 * B * C.d * bw >= (1 << 20)  # >= 1 MB of inputs per cycle: overlap the copies
-
-    def e2e_body(i, cs):
-        if not overlap:  # small inputs: one copy (the overlapped form's event waits break the PDL chain)
+    def e2e_body(i, cs, overlap):
+        if not overlap:  # one copy of the cycle's inputs, then the PDL-chained steps
             dev_in.copy_(host_in[i], non_blocking=True)
             for t in range(P):
                 steppers[t](dev_in[t, 0], dev_in[t, 1], dev_in[t, 2], t, C.k_max, C.k_min)
@@ -932,35 +929,43 @@ def e2e_run(D, steppers, clusters, router, C, B, args, dev, flush, ws, rows_all_
             cur.wait_stream(cs)
         host_out.copy_(dev_out, non_blocking=True)
 
-    for i in range(2):
-        g = torch.cuda.CUDAGraph()
-        s = torch.cuda.Stream(device=dev)
-        s.wait_stream(torch.cuda.current_stream())
-        with torch.cuda.stream(s):
-            dev_in.copy_(host_in[i], non_blocking=True)
-        torch.cuda.current_stream().wait_stream(s)
+    # both copy schedules are timed; the faster is reported (large inputs gain from overlapping the
+    # copies, small ones lose the PDL chain to the event waits)
+    best = None
+    for overlap in (False, True):
+        graphs = []
+        for i in range(2):
+            g = torch.cuda.CUDAGraph()
+            s = torch.cuda.Stream(device=dev)
+            s.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(s):
+                dev_in.copy_(host_in[i], non_blocking=True)
+            torch.cuda.current_stream().wait_stream(s)
+            torch.cuda.synchronize()
+            cs = torch.cuda.Stream(device=dev)
+            with torch.cuda.graph(g):
+                e2e_body(i, cs, overlap)
+            graphs.append(g)
+        for i in range(4):
+            graphs[i % 2].replay()
         torch.cuda.synchronize()
-        cs = torch.cuda.Stream(device=dev)
-        with torch.cuda.graph(g):
-            e2e_body(i, cs)
-        graphs.append(g)
-    for i in range(4):
-        graphs[i % 2].replay()
-    torch.cuda.synchronize()
-    tot = 0.0
-    dev_ms = []
-    for i in range(reps):
-        flush.zero_()
-        torch.cuda.synchronize()
-        ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        t0 = time.perf_counter()
-        ea.record()
-        graphs[i % 2].replay()
-        eb.record()
-        torch.cuda.synchronize()   # the host has the step's results
-        tot += time.perf_counter() - t0
-        dev_ms.append(ea.elapsed_time(eb))
-    tot = max_over_ranks(tot, ws)
+        tot = 0.0
+        dev_ms = []
+        for i in range(reps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            t0 = time.perf_counter()
+            ea.record()
+            graphs[i % 2].replay()
+            eb.record()
+            torch.cuda.synchronize()   # the host has the step's results
+            tot += time.perf_counter() - t0
+            dev_ms.append(ea.elapsed_time(eb))
+        tot = max_over_ranks(tot, ws)
+        if best is None or tot < best[0]:
+            best = (tot, overlap, statistics.median(dev_ms))
+    tot, overlap, dev_med = best
     for st, (ids, lp) in zip(steppers, saved):
         st.bind_outputs(top_ids=ids, top_logp=lp)
     h2d = P * 3 * B * C.d * bw
@@ -970,7 +975,7 @@ def e2e_run(D, steppers, clusters, router, C, B, args, dev, flush, ws, rows_all_
             + ("(per position one H2D copy of its inputs on a copy stream, position t + 1's copy overlapping "
                "step t; the cycle's steps; one D2H copy of the results)" if overlap else
                "(one H2D copy of the cycle's inputs, the cycle's PDL-chained steps, one D2H copy of the results)"),
-            "ms_per_step": 1e3 * tot / reps, "device_ms_per_step": statistics.median(dev_ms)}
+            "ms_per_step": 1e3 * tot / reps, "device_ms_per_step": dev_med}
 
 
 def run_cluster_sharded(args, ws, rank, local):
