@@ -203,3 +203,71 @@ def test_tree_rows_exact_regime_deferred_union(defer, monkeypatch):
             assert np.array_equal(st.z[b, :n].cpu().numpy(), ref[b]["z"].astype(np.float32))
             check_topk(st.top_ids[b].cpu().numpy(), st.top_logits[b].cpu().numpy(), st.top_logp[b].cpu().numpy(),
                        st.lse[b].item(), ref[b]["z"], ref[b]["V_S"], k_t, torch.float32, exact=True)
+
+
+def test_few_row_router_batched_staging_exact():
+    """The few-row router with the x rows staged in two batches (B = 16 rows of 2d = 8192 bf16 do not
+    fit shared memory at once): scores, selection and offsets bit-exact against the oracle."""
+    from paper_2510_13847_b200 import dynaspec as Dy
+    V, d, M, h_r, k_t, B = 2003, 4096, 24, 16, 8, 16
+    W = S.lm_head(V, d, 0, "bf16", "exact")
+    rt = S.router(d, h_r, M, 1, "bf16", "exact")
+    tau = S.random_partition(V, M, 2)
+    perm, off = O.layout(tau, M)
+    part = {"perm": perm, "offsets": off}
+    c = Dy.Clusters.from_tau(W.to(DEV), torch.as_tensor(tau, dtype=torch.int32, device=DEV), M)
+    r = Dy.Router(*[x.to(DEV) for x in rt])
+    st = Dy.DraftStep(c, r, B, k_t)
+    Wo, ro = Rows(W), tuple(f64(x) for x in rt)
+    for t in (0, 3):
+        hp, e, hn = S.step_inputs(B, d, t, "bf16", "exact", h_r=h_r)
+        st(hp.to(DEV), e.to(DEV), hn.to(DEV), t, 8, 2)
+        torch.cuda.synchronize()
+        ref = O.draft_step(part, ro, Wo, f64(hp), f64(e), f64(hn), t, 8, 2, k_t)
+        sc = st.scores.cpu().numpy()
+        for b in range(B):
+            assert np.array_equal(sc[b], ref[b]["scores"].astype(np.float32)), (t, b)
+            cnt = st.sel_count[b].item()
+            assert st.sel[b, :cnt].cpu().tolist() == ref[b]["sel"].tolist()
+            assert st.sl_offsets[b, :cnt + 1].cpu().tolist() == ref[b]["sl_offsets"].tolist()
+            check_topk(st.top_ids[b].cpu().numpy(), st.top_logits[b].cpu().numpy(), st.top_logp[b].cpu().numpy(),
+                       st.lse[b].item(), ref[b]["z"], ref[b]["V_S"], k_t, torch.float32, exact=True)
+
+
+def test_th_rows_mode_per_row_shortlist_bound(monkeypatch):
+    """Rows mode with a shortlist bound that some rows exceed: those rows get the documented sentinel
+    (ids -1, lse NaN), the others are computed exactly (head_forward on the tree head's rows mode)."""
+    from paper_2510_13847_b200 import dynaspec as Dy
+    monkeypatch.setenv("DS_TH_ROWS_MIN", "2")
+    V, d, M, k_t, B = 3001, 128, 20, 4, 6
+    q = max(1, min(127, int((2 ** 21 / d) ** 0.5)))
+    W = S.lm_head(V, d, 0, "bf16", "exact", q=q)
+    tau = S.random_partition(V, M, 2)
+    perm, off = O.layout(tau, M)
+    c = Dy.Clusters.from_tau(W.to(DEV), torch.as_tensor(tau, dtype=torch.int32, device=DEV), M)
+    hn = S.hidden(B, d, 7, "bf16", "exact", q=q)
+    rng = np.random.default_rng(1)
+    sizes = np.diff(off)
+    ks = [1, 2, 3, 1, 4, 2]
+    sel = torch.zeros((B, M), dtype=torch.int32)
+    cnt = torch.zeros(B, dtype=torch.int32)
+    slo = torch.zeros((B, M + 1), dtype=torch.int32)
+    sels = []
+    for b in range(B):
+        sb = np.sort(rng.choice(M, ks[b], replace=False)).astype(np.int32)
+        sels.append(sb)
+        sel[b, :ks[b]] = torch.as_tensor(sb)
+        cnt[b] = ks[b]
+        slo[b, :ks[b] + 1] = torch.as_tensor(O.shortlist_offsets(sb, off), dtype=torch.int32)
+    tot = [int(sizes[sb].sum()) for sb in sels]
+    bound = sorted(tot)[B // 2]  # about half the rows exceed it
+    out = Dy.head_forward(c, hn.to(DEV), sel.to(DEV), cnt.to(DEV), slo.to(DEV), k_t, max_shortlist=bound)
+    for b in range(B):
+        if tot[b] > bound:
+            assert (out["top_ids"][b].cpu() == -1).all() and np.isnan(out["lse"][b].item())
+        else:
+            V_S = O.shortlist(sels[b], perm, off)
+            zref = O.head(f64(hn[b:b + 1]), f64(W), V_S)[0]
+            check_topk(out["top_ids"][b].cpu().numpy(), out["top_logits"][b].cpu().numpy(),
+                       out["top_logp"][b].cpu().numpy(), out["lse"][b].item(), zref, V_S, k_t, torch.float32,
+                       exact=True)
