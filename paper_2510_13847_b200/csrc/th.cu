@@ -5,26 +5,28 @@
 //   D[128 tokens x 16] (fp32, TMEM, two buffers) += A[128 x 64] (W_perm rows, SW128) B[16 x 64]^T (H).
 //
 // Why a second tree head (tc_head.cu is the general one): at tree depths the union is 6-25k rows,
-// i.e. 40-170 rows per SM, so what costs is not the contraction but everything around it — a
-// per-CTA segment/box setup, an H box per K chunk, and a record merge over L2.  Here:
-//   * work split in 8-row GROUPS of the selected clusters (a cluster of n rows is ceil(n / 8) groups;
-//     union positions are the concatenation of the selected clusters, ascending id, R8): CTA b takes
-//     groups [b Gt / G, (b + 1) Gt / G) — a contiguous range of union positions, balanced to one
-//     group.  A group's rows are contiguous in W_perm, so a run of groups of one cluster is ONE piece,
-//     loaded with <= 5 TMA boxes (heights 128/64/32/16/8) per 64-wide K chunk; only a cluster's last
-//     group reads up to 7 rows past it (masked).
-//   * H (<= 16 rows x d) is loaded ONCE into shared memory (one box per K chunk, rows >= R
-//     zero-filled by the tensor map); the ring holds only W.  A ring slot (16 KB) holds as many K
-//     chunks of the CTA's tile as fit (tile rows r8: floor(16 KB / (r8 x 128 B)) chunks).
+// i.e. 40-200 rows per SM, so what costs is not the contraction but how the rows are fetched and
+// everything around the stream.  Here:
+//   * CTA ranges snapped to clusters: cluster i of the union owns CTAs [s_i, s_(i+1)),
+//     s_i = round(G so_i / |V_S|), its 8-row groups split evenly over them (a cluster too small for a
+//     CTA of its own goes whole to CTA min(s_i, G - 1)); found per CTA by one division-free binary
+//     search.  Every tile (<= 128 rows) is one contiguous W_perm row range, loaded with ONE 3-D TMA
+//     box {64, h, c} per 32 KB ring slot — c K chunks at once (16 maps, h = 8..128); small 2-D boxes
+//     per K chunk measured ~125 ns of fixed cost per op.
+//   * H (<= 16 rows x d) loaded ONCE by one 3-D box and kept in shared memory (8 rows per K chunk
+//     when R <= 8: the MMA's upper 8-row atom is then the next chunk's, garbage in unused D columns).
 //   * roles: warp 0 lane 0 TMA producer; warp 1 lane 0 MMA issuer (4 x K = 16 per chunk,
 //     tcgen05.commit frees the slot / publishes the tile); warps 2-5 drain TMEM (tcgen05.ld
 //     32x32b, one vocabulary row per thread, the R logits in registers) and write z[r][pos]
-//     (z_out, or workspace scratch) and the token id of pos.
-//   * per-CTA record per row (after the stream; the ring is then reused as staging): (max, sum exp),
-//     count, the k_t best keys (logit desc, token id asc — R7/R23, keys.cuh); then ONE atomic
-//     ticket: the last CTA to arrive merges the G records of every row in CTA order (R19) — lse =
-//     M + log sum_g s_g e^{m_g - M}, top-k_t by a k_t-round tournament over the sorted records
-//      — and re-arms the ticket.
+//     (z_out, or workspace scratch); warps 6-9 join the tail.
+//   * tail: keys (logit, token id) staged in the freed ring + H, one warp per row reduces the CTA's
+//     record (max, sum exp, k_t best keys: direct rank count, or a lane-maximum threshold + rank
+//     count); a 64-bit epoch arrival ticket makes the last R CTAs per-row mergers (bounded spin until
+//     all G arrived): lse by a fixed fold over the records in CTA order (R19), top-k_t by a head
+//     threshold + rank count.
+//   * modes: shared (tree rows; the union either staged from the router's selection or formed here
+//     from the rows' published masks — deferred union) and rows (independent rows, R9 shared = 0:
+//     the union of their clusters streamed once, per-tile row masks, each row over its own clusters).
 // Exactness: bf16 x bf16 products are exact in fp32; in the exact regime every partial sum is an
 // integer below 2^24, so the logits equal the oracle's bit for bit whatever the MMA order.
 #include <cuda.h>
