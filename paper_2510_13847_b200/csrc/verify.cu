@@ -62,6 +62,24 @@ __device__ __forceinline__ float ex2(float x) {
   return y;
 }
 
+// 2^x on the FMA pipe for x <= 0 (round-to-nearest split x = j + f, |f| <= 1/2, Taylor degree 6 of
+// 2^f: relative error <= 1.3e-7, about ex2.approx's; x < -126 clamps to ~2^-126).  Moves part of the
+// lse pass's exponentials off the SFU (DS_VERIFY_POLY = how many of each lane's 16 word pairs).
+__device__ __forceinline__ float ex2_fma(float x) {
+  x = fmaxf(x, -126.f);
+  const float t = x + 12582912.f;  // 1.5 * 2^23: the low mantissa bits hold round(x)
+  const int j = __float_as_int(t) - 0x4B400000;
+  const float f = x - (t - 12582912.f);
+  float p = 1.5403530393381606e-4f;
+  p = fmaf(p, f, 1.3333558146428443e-3f);
+  p = fmaf(p, f, 9.6181291076284772e-3f);
+  p = fmaf(p, f, 5.5504108664821580e-2f);
+  p = fmaf(p, f, 2.4022650695910071e-1f);
+  p = fmaf(p, f, 6.9314718055994531e-1f);
+  p = fmaf(p, f, 1.f);
+  return __int_as_float(__float_as_int(p) + (j << 23));
+}
+
 __device__ __forceinline__ float to_f(__nv_bfloat16 v) { return __bfloat162float(v); }
 __device__ __forceinline__ float to_f(float v) { return v; }
 
@@ -138,6 +156,7 @@ __device__ __forceinline__ void stream_segment(const T* __restrict__ l, const fl
 // the next batch's loads in flight; the batch max by packed bf16x2 max (exact), then one
 // exp2 per logit against the running max in two independent sums.  ~4.5 instructions per logit
 // (the generic stream_segment path needs ~13).  Returns the first position it did not cover.
+template <int NP>
 __device__ __forceinline__ int lse_seg_bf16(const __nv_bfloat16* l, int lo, int hi, int lane, float& m, float& s) {
   constexpr int U = 4, STEP = 32 * 8 * U;
   const int nfull = (hi - lo) / STEP;
@@ -169,7 +188,8 @@ __device__ __forceinline__ int lse_seg_bf16(const __nv_bfloat16* l, int lo, int 
 #pragma unroll
       for (int i = 0; i < 4 * U; ++i) {
         acc0 += ex2(fmaf(__uint_as_float(w[i] << 16), kLog2e, -mxl));
-        acc1 += ex2(fmaf(__uint_as_float(w[i] & 0xffff0000u), kLog2e, -mxl));
+        const float xh = fmaf(__uint_as_float(w[i] & 0xffff0000u), kLog2e, -mxl);
+        acc1 += i < NP ? ex2_fma(xh) : ex2(xh);
       }
       s = acc0 + acc1;
       m = mx;
@@ -252,7 +272,7 @@ __device__ void verify_decide(const VerifyArgs& a, int b, int* sh) {
   }
 }
 
-template <typename T>
+template <typename T, int NP>
 __global__ void __launch_bounds__(kVT, 2) verify_lse_kernel(const VerifyArgs a) {
   __shared__ int sh[2];
   const int row = blockIdx.x, cta = blockIdx.y, g1 = a.gamma + 1, b = row / g1, i = row - b * g1;
@@ -265,7 +285,7 @@ __global__ void __launch_bounds__(kVT, 2) verify_lse_kernel(const VerifyArgs a) 
   float m = -INFINITY, s = 0.f;
   int lo2 = lo;  // bf16 rows with 16-byte aligned segments: lean full batches, generic tail
   if (sizeof(T) == 2 && ((reinterpret_cast<uintptr_t>(l + lo) & 15u) == 0))
-    lo2 = lse_seg_bf16(reinterpret_cast<const __nv_bfloat16*>(l), lo, hi, lane, m, s);
+    lo2 = lse_seg_bf16<NP>(reinterpret_cast<const __nv_bfloat16*>(l), lo, hi, lane, m, s);
   stream_segment<T, U, false>(l, nullptr, lo2, hi, lane, [&](float (&v)[U][8], float (&)[U][8]) {
     float mx = m;
 #pragma unroll
@@ -647,10 +667,21 @@ cudaError_t launch_verify(const void* p_logits, int dtype, int64_t V, int B, int
   a.ctr_res = reinterpret_cast<unsigned*>(w + L.ctr_res);
   const dim3 g1(B * (gamma + 1), L.s1), g2(B, L.s3);  // rows in x (no 65535 limit)
   if (dtype == DS_BF16) {
-    verify_lse_kernel<__nv_bfloat16><<<g1, kVT, 0, st>>>(a);
+    const char* ev = getenv("DS_VERIFY_POLY");  // A/B knob: word pairs per lane on the FMA-pipe exp2
+    const int np = ev && ev[0] ? atoi(ev) : 0;
+    if (np >= 8)
+      verify_lse_kernel<__nv_bfloat16, 8><<<g1, kVT, 0, st>>>(a);
+    else if (np >= 6)
+      verify_lse_kernel<__nv_bfloat16, 6><<<g1, kVT, 0, st>>>(a);
+    else if (np >= 4)
+      verify_lse_kernel<__nv_bfloat16, 4><<<g1, kVT, 0, st>>>(a);
+    else if (np >= 2)
+      verify_lse_kernel<__nv_bfloat16, 2><<<g1, kVT, 0, st>>>(a);
+    else
+      verify_lse_kernel<__nv_bfloat16, 0><<<g1, kVT, 0, st>>>(a);
     verify_residual_kernel<__nv_bfloat16><<<g2, kVT, 0, st>>>(a);
   } else {
-    verify_lse_kernel<float><<<g1, kVT, 0, st>>>(a);
+    verify_lse_kernel<float, 0><<<g1, kVT, 0, st>>>(a);
     verify_residual_kernel<float><<<g2, kVT, 0, st>>>(a);
   }
   return cudaGetLastError();

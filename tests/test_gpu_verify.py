@@ -78,9 +78,11 @@ def _run(inp, dtype, q_lse, x, slot, ver=None):
     return acc.cpu().numpy().copy(), com.cpu().numpy().copy()
 
 
-@pytest.mark.parametrize("V,n_short,dtype", [(32000, 4000, "bf16"), (128256, 27000, "bf16"), (128256, 27000, "f32"),
-                                             (4104, 300, "f32")])
-def test_verify_parity(V, n_short, dtype):
+@pytest.mark.parametrize("V,n_short,dtype,poly", [(32000, 4000, "bf16", "0"), (128256, 27000, "bf16", "0"),
+                                                  (128256, 27000, "f32", "0"), (4104, 300, "f32", "0"),
+                                                  (128256, 27000, "bf16", "8"), (32000, 4000, "bf16", "4")])
+def test_verify_parity(V, n_short, dtype, poly, monkeypatch):
+    monkeypatch.setenv("DS_VERIFY_POLY", poly)  # lse pass: word pairs per lane on the FMA-pipe exp2
     B, g = 12, 4
     inp = S.verify_inputs(B, g, V, n_short, seed=V % 97, dtype=dtype)
     q_lse, x, slot = _prepare(inp)
