@@ -52,6 +52,7 @@ struct VerifyArgs {
   unsigned* ctr_row;    // [B (gamma+1)]
   unsigned* ctr_chain;  // [B]
   unsigned* ctr_res;    // [B]
+  int pf;               // lse pass: L2 bulk-prefetch distance in batches (0 off; DS_VERIFY_PF)
 };
 
 constexpr float kLog2e = 1.4426950408889634f;
@@ -157,15 +158,25 @@ __device__ __forceinline__ void stream_segment(const T* __restrict__ l, const fl
 // exp2 per logit against the running max in two independent sums.  ~4.5 instructions per logit
 // (the generic stream_segment path needs ~13).  Returns the first position it did not cover.
 template <int NP>
-__device__ __forceinline__ int lse_seg_bf16(const __nv_bfloat16* l, int lo, int hi, int lane, float& m, float& s) {
+__device__ __forceinline__ int lse_seg_bf16(const __nv_bfloat16* l, int lo, int hi, int lane, float& m, float& s,
+                                            int pf) {
   constexpr int U = 4, STEP = 32 * 8 * U;
   const int nfull = (hi - lo) / STEP;
   if (nfull <= 0) return lo;
   const uint4* base = reinterpret_cast<const uint4*>(l + lo) + lane;
+  if (pf > 0 && lane == 0) {  // batches 1 .. pf into L2 (one 2 KB bulk prefetch each; no registers)
+    for (int q = 1; q <= pf && q < nfull; ++q)
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(l + lo + (size_t)q * STEP), "r"(STEP * 2)
+                   : "memory");
+  }
   uint4 cur[U], nxt[U];
 #pragma unroll
   for (int u = 0; u < U; ++u) cur[u] = __ldcs(base + u * 32);
   for (int bt = 0; bt < nfull; ++bt) {
+    if (pf > 0 && lane == 0 && bt + 1 + pf < nfull)
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(l + lo + (size_t)(bt + 1 + pf) * STEP),
+                   "r"(STEP * 2)
+                   : "memory");
     if (bt + 1 < nfull) {
 #pragma unroll
       for (int u = 0; u < U; ++u) nxt[u] = __ldcs(base + (size_t)(bt + 1) * (STEP / 8) + u * 32);
@@ -285,7 +296,7 @@ __global__ void __launch_bounds__(kVT, 2) verify_lse_kernel(const VerifyArgs a) 
   float m = -INFINITY, s = 0.f;
   int lo2 = lo;  // bf16 rows with 16-byte aligned segments: lean full batches, generic tail
   if (sizeof(T) == 2 && ((reinterpret_cast<uintptr_t>(l + lo) & 15u) == 0))
-    lo2 = lse_seg_bf16<NP>(reinterpret_cast<const __nv_bfloat16*>(l), lo, hi, lane, m, s);
+    lo2 = lse_seg_bf16<NP>(reinterpret_cast<const __nv_bfloat16*>(l), lo, hi, lane, m, s, a.pf);
   stream_segment<T, U, false>(l, nullptr, lo2, hi, lane, [&](float (&v)[U][8], float (&)[U][8]) {
     float mx = m;
 #pragma unroll
@@ -665,6 +676,10 @@ cudaError_t launch_verify(const void* p_logits, int dtype, int64_t V, int B, int
   a.ctr_row = reinterpret_cast<unsigned*>(w + L.ctr_row);
   a.ctr_chain = reinterpret_cast<unsigned*>(w + L.ctr_chain);
   a.ctr_res = reinterpret_cast<unsigned*>(w + L.ctr_res);
+  {
+    const char* ev = getenv("DS_VERIFY_PF");
+    a.pf = ev && ev[0] ? std::max(0, std::min(8, atoi(ev))) : 0;
+  }
   const dim3 g1(B * (gamma + 1), L.s1), g2(B, L.s3);  // rows in x (no 65535 limit)
   if (dtype == DS_BF16) {
     const char* ev = getenv("DS_VERIFY_POLY");  // A/B knob: word pairs per lane on the FMA-pipe exp2

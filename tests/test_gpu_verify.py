@@ -80,9 +80,13 @@ def _run(inp, dtype, q_lse, x, slot, ver=None):
 
 @pytest.mark.parametrize("V,n_short,dtype,poly", [(32000, 4000, "bf16", "0"), (128256, 27000, "bf16", "0"),
                                                   (128256, 27000, "f32", "0"), (4104, 300, "f32", "0"),
-                                                  (128256, 27000, "bf16", "8"), (32000, 4000, "bf16", "4")])
+                                                  (128256, 27000, "bf16", "8"), (32000, 4000, "bf16", "4"),
+                                                  (128256, 27000, "bf16", "pf3")])
 def test_verify_parity(V, n_short, dtype, poly, monkeypatch):
-    monkeypatch.setenv("DS_VERIFY_POLY", poly)  # lse pass: word pairs per lane on the FMA-pipe exp2
+    if poly.startswith("pf"):  # lse pass: L2 bulk-prefetch distance
+        monkeypatch.setenv("DS_VERIFY_PF", poly[2:])
+    else:  # lse pass: word pairs per lane on the FMA-pipe exp2
+        monkeypatch.setenv("DS_VERIFY_POLY", poly)
     B, g = 12, 4
     inp = S.verify_inputs(B, g, V, n_short, seed=V % 97, dtype=dtype)
     q_lse, x, slot = _prepare(inp)
