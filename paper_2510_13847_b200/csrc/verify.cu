@@ -289,6 +289,7 @@ __global__ void __launch_bounds__(kVT, 2) verify_lse_kernel(const VerifyArgs a) 
   const int row = blockIdx.x, cta = blockIdx.y, g1 = a.gamma + 1, b = row / g1, i = row - b * g1;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int seg = cta * kVW + warp;
+  pdl_launch_dependents();  // the residual pass may be scheduled now; it waits for this grid's completion
   const T* l = static_cast<const T*>(a.p_logits) + (size_t)row * a.V;
   const int V = (int)a.V, L1 = (int)a.L1;
   const int lo = (int)min((int64_t)seg * L1, (int64_t)V), hi = min(V, lo + L1);
@@ -377,6 +378,7 @@ __global__ void __launch_bounds__(kVT, 2) verify_residual_kernel(const VerifyArg
   __shared__ float wsum[kVW], fsh[3];
   const int b = blockIdx.x, cta = blockIdx.y, g1 = a.gamma + 1;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  pdl_wait();  // the lse pass (a programmatic dependency when DS_VERIFY_PDL is on; else a no-op)
   const int j = a.jrow[b];
   if (j < 0) return;
   const int row = b * g1 + j;
@@ -681,6 +683,17 @@ cudaError_t launch_verify(const void* p_logits, int dtype, int64_t V, int B, int
     a.pf = ev && ev[0] ? std::max(0, std::min(8, atoi(ev))) : 0;
   }
   const dim3 g1(B * (gamma + 1), L.s1), g2(B, L.s3);  // rows in x (no 65535 limit)
+  const char* evp = getenv("DS_VERIFY_PDL");
+  const bool pdl = evp && evp[0] == '1';  // A/B knob: no measurable gain (profiles/r2_probes), off
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = g2;
+  cfg.blockDim = dim3(kVT);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
   if (dtype == DS_BF16) {
     const char* ev = getenv("DS_VERIFY_POLY");  // A/B knob: word pairs per lane on the FMA-pipe exp2
     const int np = ev && ev[0] ? atoi(ev) : 0;
@@ -694,12 +707,15 @@ cudaError_t launch_verify(const void* p_logits, int dtype, int64_t V, int B, int
       verify_lse_kernel<__nv_bfloat16, 2><<<g1, kVT, 0, st>>>(a);
     else
       verify_lse_kernel<__nv_bfloat16, 0><<<g1, kVT, 0, st>>>(a);
-    verify_residual_kernel<__nv_bfloat16><<<g2, kVT, 0, st>>>(a);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    return cudaLaunchKernelEx(&cfg, verify_residual_kernel<__nv_bfloat16>, a);
   } else {
     verify_lse_kernel<float, 0><<<g1, kVT, 0, st>>>(a);
-    verify_residual_kernel<float><<<g2, kVT, 0, st>>>(a);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    return cudaLaunchKernelEx(&cfg, verify_residual_kernel<float>, a);
   }
-  return cudaGetLastError();
 }
 
 cudaError_t launch_shortlist_ids(const ds_clusters* c, int rows, const int32_t* sel, const int32_t* cnt,

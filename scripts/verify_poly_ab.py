@@ -1,6 +1,7 @@
 """A/B of the lse pass's knobs on the bench's verification workload (Llama-3 vocabulary, 64 chains x
 gamma = 8 and one chain, shortlist 7k): DS_VERIFY_POLY (FMA-pipe exp2 share) or, with --pf, DS_VERIFY_PF
-(L2 bulk-prefetch distance); alternates settings, median of the per-round medians."""
+(L2 bulk-prefetch distance) or, with --pdl, DS_VERIFY_PDL (the residual pass as a programmatic dependent
+launch); alternates settings, median of the per-round medians."""
 import json
 import os
 import statistics
@@ -17,7 +18,8 @@ dev = torch.device("cuda:0")
 C = S.CONFIGS["llama3"]
 flush = bench.L2Flush(dev)
 res = {}
-knob, vals = ("DS_VERIFY_PF", ["0", "1", "2", "3", "5"]) if "--pf" in sys.argv else ("DS_VERIFY_POLY", ["0", "2", "4", "6", "8"])
+knob, vals = (("DS_VERIFY_PF", ["0", "1", "2", "3", "5"]) if "--pf" in sys.argv else
+              ("DS_VERIFY_PDL", ["0", "1"]) if "--pdl" in sys.argv else ("DS_VERIFY_POLY", ["0", "2", "4", "6", "8"]))
 for rnd in range(3):
     for np_ in vals:
         os.environ[knob] = np_

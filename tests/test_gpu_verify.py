@@ -81,9 +81,12 @@ def _run(inp, dtype, q_lse, x, slot, ver=None):
 @pytest.mark.parametrize("V,n_short,dtype,poly", [(32000, 4000, "bf16", "0"), (128256, 27000, "bf16", "0"),
                                                   (128256, 27000, "f32", "0"), (4104, 300, "f32", "0"),
                                                   (128256, 27000, "bf16", "8"), (32000, 4000, "bf16", "4"),
-                                                  (128256, 27000, "bf16", "pf3")])
+                                                  (128256, 27000, "bf16", "pf3"), (128256, 27000, "f32", "pdl"),
+                                                  (32000, 4000, "bf16", "pdl")])
 def test_verify_parity(V, n_short, dtype, poly, monkeypatch):
-    if poly.startswith("pf"):  # lse pass: L2 bulk-prefetch distance
+    if poly == "pdl":  # the residual pass as a programmatic dependent launch
+        monkeypatch.setenv("DS_VERIFY_PDL", "1")
+    elif poly.startswith("pf"):  # lse pass: L2 bulk-prefetch distance
         monkeypatch.setenv("DS_VERIFY_PF", poly[2:])
     else:  # lse pass: word pairs per lane on the FMA-pipe exp2
         monkeypatch.setenv("DS_VERIFY_POLY", poly)
